@@ -1,0 +1,207 @@
+/* apb.h - C ABI of the B200-native ball dot product / block ball matmul.
+ *
+ * This is the drop-in boundary for the hot path of the reference library
+ * `apball` (/root/reference/proj).  Every entry point below replaces one C++
+ * operator of the reference; the replaced interface is cited as file:line
+ * relative to /root/reference/proj.  No C++ or torch types cross this
+ * boundary: plain pointers, sizes and a cudaStream_t passed as void*.
+ *
+ * Data layout ("ball array", SoA, same layout on host and device):
+ *   mant    uint64[count * L]  mantissa limbs of element e at mant[e*L .. e*L+L),
+ *                              little-endian and TOP-ALIGNED: an ApFloat with n
+ *                              limbs occupies slots L-n .. L-1, lower slots are 0.
+ *                              (ApFloat keeps the minimal limb count,
+ *                              include/apball/apfloat.hpp:4-9, so n is recovered
+ *                              exactly as L minus the number of zero low slots.)
+ *   exp     int64[count]       ApFloat exponent e: 2^(e-1) <= |x| < 2^e
+ *   kind    uint8[count]       APB_ZERO/APB_FINITE/APB_PINF/APB_NINF/APB_NAN,
+ *                              bit 7 (APB_SIGN) = negative finite midpoint
+ *   rad_man uint32[count]      Mag mantissa b in [2^29, 2^30) (include/apball/mag.hpp:15-59);
+ *                              0 = exact (zero radius), APB_RAD_INF = infinite radius
+ *   rad_exp int64[count]       Mag exponent f: radius = b * 2^(f-30)
+ *
+ * Status codes map to the reference's exceptions:
+ *   0 ok, 1 std::invalid_argument (dimensions), 2 std::overflow_error
+ *   (exponent range, src/apfloat.cpp:18-22), 3 unsupported, 4 CUDA error.
+ */
+#ifndef APB_H
+#define APB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    APB_ZERO = 0,
+    APB_FINITE = 1,
+    APB_PINF = 2,
+    APB_NINF = 3,
+    APB_NAN = 4,
+    APB_KIND_MASK = 7,
+    APB_SIGN = 0x80
+};
+#define APB_RAD_INF 0xFFFFFFFFu
+
+enum {
+    APB_OK = 0,
+    APB_ERR_INVALID = 1,
+    APB_ERR_OVERFLOW = 2,
+    APB_ERR_UNSUPPORTED = 3,
+    APB_ERR_CUDA = 4
+};
+
+typedef struct apb_balls {
+    uint64_t* mant;
+    int64_t* exp;
+    uint8_t* kind;
+    uint32_t* rad_man;
+    int64_t* rad_exp;
+    int64_t count;
+    int32_t L;
+} apb_balls;
+
+/* Term addressing for a batch of dot products.  Dot b (0 <= b < batch) reads
+ * term i (0 <= i < n) of x at element
+ *     (b / bdiv) * xs1 + (b % bdiv) * xs2 + i * xstep  (+ x_off)
+ * and likewise for y.  A flat batch of contiguous dots uses bdiv = 1,
+ * xs1 = n, xs2 = 0, xstep = 1; a classical matmul C = A B uses bdiv = N,
+ * xs1 = K, xs2 = 0, xstep = 1 and ys1 = 0, ys2 = 1, ystep = N
+ * (src/matmul.cpp:442-451).  Steps may be negative (src/dot.cpp:29-43). */
+typedef struct apb_dot_index {
+    int64_t bdiv;
+    int64_t x_off, xs1, xs2, xstep;
+    int64_t y_off, ys1, ys2, ystep;
+} apb_dot_index;
+
+enum { APB_DOT_BALL = 0, APB_DOT_APPROX = 1 };
+
+/* Dot plan + accumulator as the reference exposes them for parity
+ * (include/apball/dot.hpp:25-43).  One record per dot. */
+typedef struct apb_dot_state {
+    int64_t e_max, e_min, e_rad;
+    uint64_t n_nonzero;
+    int64_t p_eff;
+    int32_t extend, padding;
+    int64_t n_s;
+    int64_t e_s;
+    int32_t status; /* 0 Proceed, 1 Fallback, 2 ZeroResult (DotStatus) */
+    int32_t _pad;
+    uint64_t err;
+    uint64_t srad;
+} apb_dot_state;
+
+/* Device-side tuning knobs mirrored from DotTuning (include/apball/dot.hpp:45-51). */
+typedef struct apb_dot_tuning {
+    int32_t disable_precision_reduction;
+    int32_t force_threeprod;
+    int64_t threeprod_cutoff_limbs;
+} apb_dot_tuning;
+
+/* ------------------------------------------------------------------ dots */
+
+/* Batched real ball / approx dot product, all pointers DEVICE.
+ * Replaces dot_ball (include/apball/dot.hpp:73-74, src/dot.cpp:402-405) and
+ * dot_approx (dot.hpp:77-78) called once per dot.  `initial` (nullable) holds
+ * one ball per dot (element b), `subtract` negates the sum.  out must have
+ * L >= ceil(prec/64) and count >= batch.  mode = APB_DOT_BALL|APB_DOT_APPROX
+ * (approx writes zero radii).  state (nullable, device) receives the plan and
+ * the final accumulator scalars per dot; acc_limbs (nullable, device) receives
+ * n_s two's-complement accumulator limbs per dot at stride acc_stride (the
+ * state BEFORE dot_finalize), for bit-exact parity with dot_setup/dot_init/
+ * dot_accumulate_term (dot.hpp:57-69). */
+int apb_dot_batch(const apb_balls* x, const apb_balls* y, const apb_balls* initial,
+                  int subtract, const apb_dot_index* idx, int64_t n, int64_t batch,
+                  int64_t prec, int mode, const apb_dot_tuning* tuning, apb_balls* out,
+                  apb_dot_state* state, uint64_t* acc_limbs, int64_t acc_stride,
+                  void* stream);
+
+/* Batched complex dot product (re/im as two ball arrays per operand), DEVICE.
+ * Replaces dot_complex_ball / dot_complex_approx (include/apball/dot.hpp:86-89,
+ * src/dot.cpp:549-568).  threeprod_hits (nullable, device uint64[1]) is
+ * incremented like dot_threeprod_hits() (dot.hpp:54). */
+int apb_dot_complex_batch(const apb_balls* xre, const apb_balls* xim, const apb_balls* yre,
+                          const apb_balls* yim, const apb_dot_index* idx, int64_t n,
+                          int64_t batch, int64_t prec, int mode, const apb_dot_tuning* tuning,
+                          apb_balls* out_re, apb_balls* out_im, uint64_t* threeprod_hits,
+                          void* stream);
+
+/* ---------------------------------------------------------------- matmul */
+
+typedef struct apb_mat {
+    apb_balls b; /* rows*cols balls, row-major (include/apball/matmul.hpp:18-26) */
+    int64_t rows, cols;
+} apb_mat;
+
+enum { APB_MM_AUTO = 0, APB_MM_BLOCK = 1, APB_MM_CLASSICAL = 2 };
+
+/* Matmul statistics mirrored from MatmulStats (include/apball/matmul.hpp:98-105);
+ * int_gemm_products counts scaled-integer GEMMs run on the tensor cores
+ * (the reference counts multimodular products instead). */
+typedef struct apb_matmul_stats {
+    uint64_t classical_calls;
+    uint64_t block_calls;
+    uint64_t int_gemm_products;
+    uint64_t last_block_count;
+    uint64_t last_height_a, last_height_b, last_slices_a, last_slices_b;
+} apb_matmul_stats;
+
+/* C = A B over balls, all matrices DEVICE.  Replaces matmul_auto /
+ * block_matmul_ball / classical_matmul_ball (include/apball/matmul.hpp:89-91,
+ * src/matmul.cpp:442-531).  C must have L >= ceil(prec/64). */
+int apb_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, apb_mat* C,
+               void* stream);
+
+/* Complex C = A B (re/im parts), DEVICE.  Replaces complex_matmul_ball
+ * (include/apball/matmul.hpp:92-93, src/matmul.cpp:533-548): four real
+ * products each rounded to prec, then re = AC - BD, im = AD + BC. */
+int apb_matmul_complex(const apb_mat* Are, const apb_mat* Aim, const apb_mat* Bre,
+                       const apb_mat* Bim, int64_t prec, int algo, apb_mat* Cre, apb_mat* Cim,
+                       void* stream);
+
+/* Parity hook: the exact scaled-integer block product of a single block
+ * [lo,hi) (matmul.hpp:77-84: int_matmul(scale_block_rows(A), scale_block_cols(B))).
+ * Writes the row/col scale exponents (int64[M], int64[N], DEVICE) and the
+ * exact product as little-endian two's-complement limbs, `out_limbs` limbs
+ * per entry (DEVICE uint64[M*N*out_limbs]).  Returns APB_ERR_UNSUPPORTED if
+ * out_limbs is too small for the product height. */
+int apb_block_int_product(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi,
+                          int64_t* row_scale, int64_t* col_scale, uint64_t* out,
+                          int64_t out_limbs, void* stream);
+
+/* Parity hook: greedy block plan (include/apball/matmul.hpp:73, src/matmul.cpp:132-161).
+ * steps_out receives up to max_steps triples (lo, hi, basecase); *n_steps the count. */
+int apb_plan_blocks(const apb_mat* A, const apb_mat* B, int64_t prec, int64_t* steps_out,
+                    int64_t max_steps, int64_t* n_steps, void* stream);
+
+/* Parity hook: radius product upper bound of two Mag matrices given as
+ * (rad_man, rad_exp) planes (include/apball/matmul.hpp:87, src/matmul.cpp:368-438). */
+int apb_radius_matmul_upper(const uint32_t* p_man, const int64_t* p_exp, const uint32_t* q_man,
+                            const int64_t* q_exp, int64_t m, int64_t n, int64_t k,
+                            uint32_t* out_man, int64_t* out_exp, void* stream);
+
+/* --------------------------------------------------------- host wrappers */
+
+/* End-to-end variants taking HOST ball arrays: host->device copy, kernels,
+ * device->host copy inside one call (the drop-in path for callers holding
+ * host data). */
+int apb_dot_batch_host(const apb_balls* x, const apb_balls* y, const apb_balls* initial,
+                       int subtract, const apb_dot_index* idx, int64_t n, int64_t batch,
+                       int64_t prec, int mode, apb_balls* out);
+int apb_matmul_host(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, apb_mat* C);
+
+/* ------------------------------------------------------------------ misc */
+
+apb_matmul_stats* apb_matmul_stats_get(void);
+void apb_matmul_stats_reset(void);
+const char* apb_last_error(void);
+/* number of kernel launches issued by this library since load (bench evidence) */
+uint64_t apb_launch_count(void);
+int apb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* APB_H */
