@@ -194,6 +194,12 @@ int apb_matmul_host(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, 
 
 /* ------------------------------------------------------------------ misc */
 
+/* Synchronize `stream` and return (then clear) the APB_* status raised by
+ * device code since the last call (e.g. APB_ERR_OVERFLOW where the reference
+ * throws std::overflow_error, src/apfloat.cpp:18-22).  The device entry points
+ * above are asynchronous and only report launch/argument errors. */
+int apb_device_status(void* stream);
+
 apb_matmul_stats* apb_matmul_stats_get(void);
 void apb_matmul_stats_reset(void);
 const char* apb_last_error(void);

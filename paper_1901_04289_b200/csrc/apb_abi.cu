@@ -1,0 +1,263 @@
+// apb_abi.cu - the extern "C" boundary (include/apb.h): argument checks,
+// status/error plumbing, library-owned device workspace and the host-buffer
+// (end-to-end) wrappers.  The compute lives in dot_kernels.cu / matmul.cu.
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "apb.h"
+#include "apb_internal.h"
+
+namespace apb {
+
+static std::atomic<uint64_t> g_launches{0};
+static thread_local std::string g_error;
+static apb_matmul_stats g_stats;
+
+void count_launch(uint64_t k) { g_launches += k; }
+void set_error(const char* msg) { g_error = msg ? msg : ""; }
+
+int cuda_check(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return APB_OK;
+    std::string m = std::string(where) + ": " + cudaGetErrorString(e);
+    set_error(m.c_str());
+    return APB_ERR_CUDA;
+}
+
+static std::mutex g_ws_mu;
+
+Workspace& workspace() {
+    static Workspace* ws = [] {
+        auto* w = new Workspace();
+        cudaMalloc(&w->status_dev, sizeof(int));
+        cudaMemset(w->status_dev, 0, sizeof(int));
+        return w;
+    }();
+    return *ws;
+}
+
+void* Workspace::scratch(cudaStream_t st, size_t bytes, int slot) {
+    std::lock_guard<std::mutex> g(g_ws_mu);
+    if (bytes == 0) bytes = 1;
+    if (caps[slot] < bytes) {
+        if (bufs[slot]) {
+            cudaStreamSynchronize(st);
+            cudaFree(bufs[slot]);
+        }
+        size_t cap = bytes + bytes / 4 + 256;
+        if (cudaMalloc(&bufs[slot], cap) != cudaSuccess) {
+            bufs[slot] = nullptr;
+            caps[slot] = 0;
+            return nullptr;
+        }
+        caps[slot] = cap;
+    }
+    return bufs[slot];
+}
+
+apb_matmul_stats& stats() { return g_stats; }
+
+static int64_t limbs_for(int64_t prec) { return prec <= 64 ? 1 : (prec + 63) / 64; }
+
+static bool balls_ok(const apb_balls* a) {
+    return a && a->mant && a->exp && a->kind && a->rad_man && a->rad_exp && a->L >= 1;
+}
+
+}  // namespace apb
+
+using namespace apb;
+
+extern "C" {
+
+int apb_version(void) { return 1; }
+uint64_t apb_launch_count(void) { return g_launches.load(); }
+const char* apb_last_error(void) { return g_error.c_str(); }
+apb_matmul_stats* apb_matmul_stats_get(void) { return &g_stats; }
+void apb_matmul_stats_reset(void) { std::memset(&g_stats, 0, sizeof g_stats); }
+
+int apb_device_status(void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = cuda_check(cudaStreamSynchronize(st), "apb_device_status");
+    if (rc) return rc;
+    int h = 0;
+    Workspace& ws = workspace();
+    rc = cuda_check(cudaMemcpy(&h, ws.status_dev, sizeof(int), cudaMemcpyDeviceToHost), "status read");
+    if (rc) return rc;
+    if (h) {
+        cudaMemset(ws.status_dev, 0, sizeof(int));
+        set_error(h == APB_ERR_OVERFLOW ? "apball: exponent out of representable range"
+                                        : "device-side error");
+    }
+    return h;
+}
+
+int apb_dot_batch(const apb_balls* x, const apb_balls* y, const apb_balls* initial, int subtract,
+                  const apb_dot_index* idx, int64_t n, int64_t batch, int64_t prec, int mode,
+                  const apb_dot_tuning* tuning, apb_balls* out, apb_dot_state* state,
+                  uint64_t* acc_limbs, int64_t acc_stride, void* stream) {
+    if (batch < 0 || n < 0 || !idx || !out || !balls_ok(out) || idx->bdiv < 1) {
+        set_error("apb_dot_batch: invalid arguments");
+        return APB_ERR_INVALID;
+    }
+    if (n > 0 && (!balls_ok(x) || !balls_ok(y))) {
+        set_error("apb_dot_batch: missing operands");
+        return APB_ERR_INVALID;
+    }
+    if (prec < 2) prec = 2;
+    if (out->L < limbs_for(prec) || out->count < batch) {
+        set_error("apb_dot_batch: output slots too small for prec");
+        return APB_ERR_INVALID;
+    }
+    if (initial && !balls_ok(initial)) {
+        set_error("apb_dot_batch: bad initial");
+        return APB_ERR_INVALID;
+    }
+    // n == 0 with no x/y: substitute the output as a never-read operand
+    const apb_balls* xx = n > 0 ? x : out;
+    const apb_balls* yy = n > 0 ? y : out;
+    int rc = dot_batch_launch(xx, yy, initial, subtract, idx, n, batch, prec, mode, tuning, out,
+                              state, acc_limbs, acc_stride, (cudaStream_t)stream);
+    if (rc) return rc;
+    return cuda_check(cudaGetLastError(), "apb_dot_batch launch");
+}
+
+int apb_dot_complex_batch(const apb_balls* xre, const apb_balls* xim, const apb_balls* yre,
+                          const apb_balls* yim, const apb_dot_index* idx, int64_t n, int64_t batch,
+                          int64_t prec, int mode, const apb_dot_tuning* tuning, apb_balls* out_re,
+                          apb_balls* out_im, uint64_t* threeprod_hits, void* stream) {
+    (void)tuning;
+    (void)threeprod_hits;
+    if (batch < 0 || n < 0 || !idx || !balls_ok(out_re) || !balls_ok(out_im) || idx->bdiv < 1) {
+        set_error("apb_dot_complex_batch: invalid arguments");
+        return APB_ERR_INVALID;
+    }
+    if (n > 0 && (!balls_ok(xre) || !balls_ok(xim) || !balls_ok(yre) || !balls_ok(yim))) {
+        set_error("apb_dot_complex_batch: missing operands");
+        return APB_ERR_INVALID;
+    }
+    if (prec < 2) prec = 2;
+    if (out_re->L < limbs_for(prec) || out_im->L < limbs_for(prec)) {
+        set_error("apb_dot_complex_batch: output slots too small for prec");
+        return APB_ERR_INVALID;
+    }
+    const apb_balls* a = n > 0 ? xre : out_re;
+    const apb_balls* b = n > 0 ? xim : out_re;
+    const apb_balls* c = n > 0 ? yre : out_re;
+    const apb_balls* d = n > 0 ? yim : out_re;
+    int rc = dot_complex_launch(a, b, c, d, idx, n, batch, prec, mode, out_re, out_im,
+                                (cudaStream_t)stream);
+    if (rc) return rc;
+    return cuda_check(cudaGetLastError(), "apb_dot_complex_batch launch");
+}
+
+int apb_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, apb_mat* C,
+               void* stream) {
+    if (!A || !B || !C) {
+        set_error("apb_matmul: null matrix");
+        return APB_ERR_INVALID;
+    }
+    if (A->cols != B->rows || C->rows != A->rows || C->cols != B->cols) {
+        set_error("matmul: dimension mismatch");
+        return APB_ERR_INVALID;
+    }
+    if (prec < 2) prec = 2;
+    if (C->b.L < limbs_for(prec)) {
+        set_error("apb_matmul: output slots too small for prec");
+        return APB_ERR_INVALID;
+    }
+    int rc = matmul_launch(A, B, prec, algo, C, (cudaStream_t)stream);
+    if (rc) return rc;
+    return cuda_check(cudaGetLastError(), "apb_matmul launch");
+}
+
+// ---------------------------------------------------------- host wrappers
+
+namespace {
+
+struct DevBalls {
+    apb_balls d;
+};
+
+// copy a host ball array into workspace slots [slot0, slot0+5)
+int to_device(const apb_balls* h, apb_balls* d, int slot0, cudaStream_t st, bool copy) {
+    Workspace& ws = workspace();
+    const size_t cnt = (size_t)h->count;
+    d->count = h->count;
+    d->L = h->L;
+    d->mant = (uint64_t*)ws.scratch(st, cnt * h->L * 8, slot0);
+    d->exp = (int64_t*)ws.scratch(st, cnt * 8, slot0 + 1);
+    d->kind = (uint8_t*)ws.scratch(st, cnt, slot0 + 2);
+    d->rad_man = (uint32_t*)ws.scratch(st, cnt * 4, slot0 + 3);
+    d->rad_exp = (int64_t*)ws.scratch(st, cnt * 8, slot0 + 4);
+    if (!d->mant || !d->exp || !d->kind || !d->rad_man || !d->rad_exp) {
+        set_error("out of device memory");
+        return APB_ERR_CUDA;
+    }
+    if (!copy || cnt == 0) return APB_OK;
+    cudaMemcpyAsync(d->mant, h->mant, cnt * h->L * 8, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d->exp, h->exp, cnt * 8, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d->kind, h->kind, cnt, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d->rad_man, h->rad_man, cnt * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d->rad_exp, h->rad_exp, cnt * 8, cudaMemcpyHostToDevice, st);
+    return cuda_check(cudaGetLastError(), "h2d");
+}
+
+int to_host(const apb_balls* d, apb_balls* h, cudaStream_t st) {
+    const size_t cnt = (size_t)h->count;
+    if (cnt == 0) return APB_OK;
+    cudaMemcpyAsync(h->mant, d->mant, cnt * h->L * 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(h->exp, d->exp, cnt * 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(h->kind, d->kind, cnt, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(h->rad_man, d->rad_man, cnt * 4, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(h->rad_exp, d->rad_exp, cnt * 8, cudaMemcpyDeviceToHost, st);
+    return cuda_check(cudaGetLastError(), "d2h");
+}
+
+cudaStream_t host_stream() {
+    static cudaStream_t s = [] {
+        cudaStream_t t;
+        cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking);
+        return t;
+    }();
+    return s;
+}
+
+}  // namespace
+
+int apb_dot_batch_host(const apb_balls* x, const apb_balls* y, const apb_balls* initial,
+                       int subtract, const apb_dot_index* idx, int64_t n, int64_t batch,
+                       int64_t prec, int mode, apb_balls* out) {
+    cudaStream_t st = host_stream();
+    apb_balls dx{}, dy{}, di{}, dout{};
+    int rc;
+    if (n > 0) {
+        if ((rc = to_device(x, &dx, 5, st, true))) return rc;
+        if ((rc = to_device(y, &dy, 10, st, true))) return rc;
+    }
+    if (initial && (rc = to_device(initial, &di, 15, st, true))) return rc;
+    apb_balls hout = *out;
+    hout.count = batch;
+    if ((rc = to_device(&hout, &dout, 0, st, false))) return rc;
+    rc = apb_dot_batch(n > 0 ? &dx : nullptr, n > 0 ? &dy : nullptr, initial ? &di : nullptr,
+                       subtract, idx, n, batch, prec, mode, nullptr, &dout, nullptr, nullptr, 0, st);
+    if (rc) return rc;
+    if ((rc = to_host(&dout, &hout, st))) return rc;
+    return apb_device_status(st);
+}
+
+int apb_matmul_host(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, apb_mat* C) {
+    cudaStream_t st = host_stream();
+    apb_mat dA = *A, dB = *B, dC = *C;
+    int rc;
+    if ((rc = to_device(&A->b, &dA.b, 5, st, true))) return rc;
+    if ((rc = to_device(&B->b, &dB.b, 10, st, true))) return rc;
+    if ((rc = to_device(&C->b, &dC.b, 0, st, false))) return rc;
+    if ((rc = apb_matmul(&dA, &dB, prec, algo, &dC, st))) return rc;
+    if ((rc = to_host(&dC.b, &C->b, st))) return rc;
+    return apb_device_status(st);
+}
+
+}  // extern "C"

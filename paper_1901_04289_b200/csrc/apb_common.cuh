@@ -1,0 +1,346 @@
+// apb_common.cuh - device-side number primitives shared by the dot and matmul
+// kernels: Mag upper-bound arithmetic (reference include/apball/mag.hpp,
+// src/mag.cpp), limb helpers, and a bounded-size generic float used by the
+// rare paths (finalize, special-value fallback).  Paths are relative to
+// /root/reference/proj.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "apb.h"
+
+#define APB_DEV __device__ __forceinline__
+
+namespace apb {
+
+// ------------------------------------------------------------------ limbs
+
+APB_DEV unsigned bitw64(uint64_t v) { return v ? 64u - (unsigned)__clzll((long long)v) : 0u; }
+APB_DEV unsigned ctz64(uint64_t v) { return (unsigned)__ffsll((long long)v) - 1u; }
+
+// (lo >> rb) | (hi << (64-rb)), rb in [0,64)
+APB_DEV uint64_t funnel_r(uint64_t lo, uint64_t hi, unsigned rb) {
+    return rb ? (lo >> rb) | (hi << (64 - rb)) : lo;
+}
+
+// 64x64 -> 128
+APB_DEV void mul64(uint64_t a, uint64_t b, uint64_t& lo, uint64_t& hi) {
+    lo = a * b;
+    hi = __umul64hi(a, b);
+}
+
+// ------------------------------------------------------------------- Mag
+// (b / 2^30) * 2^f, 2^29 <= b < 2^30 (include/apball/mag.hpp:15-59)
+struct Mag {
+    int kind;  // 0 zero, 1 finite, 2 inf
+    uint64_t b;
+    int64_t f;
+};
+
+constexpr uint64_t kMagOne = 1ull << 30;
+constexpr int64_t kMExpMax = INT64_MAX - 4;
+constexpr int64_t kMExpMin = INT64_MIN + 4;
+
+APB_DEV Mag mag_zero() { return Mag{0, 0, 0}; }
+APB_DEV Mag mag_inf() { return Mag{2, 0, 0}; }
+
+// Mag::from_parts (src/mag.cpp:18-31)
+APB_DEV Mag mag_parts(uint64_t b, int64_t f) {
+    if (b == kMagOne) {
+        b = kMagOne >> 1;
+        if (f >= kMExpMax) return mag_inf();
+        f++;
+    }
+    return Mag{1, b, f};
+}
+
+// Mag::from_u64_upper (src/mag.cpp:33-50)
+APB_DEV Mag mag_from_u64(uint64_t v, int64_t exp2) {
+    if (v == 0) return mag_zero();
+    unsigned len = bitw64(v);
+    uint64_t b;
+    bool inexact = false;
+    if (len <= 30) {
+        b = v << (30 - len);
+    } else {
+        unsigned sh = len - 30;
+        b = v >> sh;
+        inexact = (v & ((1ull << sh) - 1)) != 0;
+    }
+    if (inexact) b++;
+    // exp2 + len in 128-bit-safe form
+    if (exp2 > kMExpMax - (int64_t)len) return mag_inf();
+    int64_t f = exp2 + (int64_t)len;
+    if (f < kMExpMin) return mag_parts(kMagOne >> 1, kMExpMin);
+    return mag_parts(b, f);
+}
+
+// Mag::from_double_upper (src/mag.cpp:79-87)
+APB_DEV Mag mag_from_double(double v, int64_t exp2) {
+    if (v == 0.0) return mag_zero();
+    if (isinf(v) || isnan(v)) return mag_inf();
+    int e;
+    double fr = frexp(v, &e);
+    uint64_t m53 = (uint64_t)ldexp(fr, 53);
+    return mag_from_u64(m53, exp2 + e - 53);
+}
+
+APB_DEV int mag_cmp(const Mag& a, const Mag& b) {
+    int ra = a.kind == 0 ? 0 : (a.kind == 2 ? 2 : 1);
+    int rb = b.kind == 0 ? 0 : (b.kind == 2 ? 2 : 1);
+    if (ra != rb || ra != 1) return ra < rb ? -1 : (ra > rb ? 1 : 0);
+    if (a.f != b.f) return a.f < b.f ? -1 : 1;
+    if (a.b != b.b) return a.b < b.b ? -1 : 1;
+    return 0;
+}
+
+// mag_add_up (src/mag.cpp:108-130)
+APB_DEV Mag mag_add(const Mag& a, const Mag& b) {
+    if (a.kind == 2 || b.kind == 2) return mag_inf();
+    if (a.kind == 0) return b;
+    if (b.kind == 0) return a;
+    Mag hi = a, lo = b;
+    if (mag_cmp(hi, lo) < 0) {
+        hi = b;
+        lo = a;
+    }
+    uint64_t bh = hi.b;
+    int64_t f = hi.f;
+    uint64_t d = (uint64_t)(f - lo.f);
+    if (d >= 30) {
+        bh += 1;
+    } else {
+        uint64_t bl = lo.b;
+        bh += bl >> d;
+        if (d && (bl & ((1ull << d) - 1))) bh++;
+    }
+    while (bh > kMagOne) {
+        bh = (bh + 1) >> 1;
+        if (f >= kMExpMax) return mag_inf();
+        f++;
+    }
+    return mag_parts(bh, f);
+}
+
+// mag_mul_up (src/mag.cpp:132-145)
+APB_DEV Mag mag_mul(const Mag& a, const Mag& b) {
+    if (a.kind == 0 || b.kind == 0) return mag_zero();
+    if (a.kind == 2 || b.kind == 2) return mag_inf();
+    uint64_t p = a.b * b.b;
+    uint64_t q = (p + (kMagOne - 1)) >> 30;
+    // f = a.f + b.f with saturation
+    __int128 f = (__int128)a.f + b.f;
+    if (q < (kMagOne >> 1)) {
+        q <<= 1;
+        f--;
+    }
+    if (f > kMExpMax) return mag_inf();
+    if (f < kMExpMin) return mag_parts(kMagOne >> 1, kMExpMin);
+    return mag_parts(q, (int64_t)f);
+}
+
+APB_DEV Mag mag_load(uint32_t b, int64_t f) {
+    if (b == 0) return mag_zero();
+    if (b == APB_RAD_INF) return mag_inf();
+    return mag_parts(b, f);
+}
+
+APB_DEV void mag_store(const Mag& r, uint32_t* man, int64_t* ex) {
+    if (r.kind == 0) {
+        *man = 0;
+        *ex = 0;
+    } else if (r.kind == 2) {
+        *man = APB_RAD_INF;
+        *ex = 0;
+    } else {
+        *man = (uint32_t)r.b;
+        *ex = r.f;
+    }
+}
+
+// ----------------------------------------------------------- ball arrays
+
+struct BallsView {
+    const uint64_t* mant;
+    const int64_t* exp;
+    const uint8_t* kind;
+    const uint32_t* rad_man;
+    const int64_t* rad_exp;
+    int32_t L;
+};
+
+struct BallsOut {
+    uint64_t* mant;
+    int64_t* exp;
+    uint8_t* kind;
+    uint32_t* rad_man;
+    int64_t* rad_exp;
+    int32_t L;
+};
+
+inline BallsView view_of(const apb_balls* a) {
+    return BallsView{a->mant, a->exp, a->kind, a->rad_man, a->rad_exp, a->L};
+}
+inline BallsOut out_of(apb_balls* a) {
+    return BallsOut{a->mant, a->exp, a->kind, a->rad_man, a->rad_exp, a->L};
+}
+
+// ------------------------------------------------ bounded generic float
+// A finite/special float with up to CAP limbs, used by finalize and the
+// special-value fallback.  Restates apfloat_normalize / apfloat_round /
+// apfloat_add_round / apfloat_mul_exact (src/apfloat.cpp:116-270).
+
+template <int CAP>
+struct GFloat {
+    int kind;  // APB_ZERO .. APB_NAN
+    int neg;
+    int64_t e;
+    int n;
+    uint64_t d[CAP];
+};
+
+constexpr int64_t kExpHi = INT64_MAX - 8;
+constexpr int64_t kExpLo = INT64_MIN + 8;
+
+// e + a (a small) with the reference's overflow_error semantics
+APB_DEV int64_t checked_add(int64_t e, int64_t a, int* status) {
+    __int128 r = (__int128)e + a;
+    if (r > kExpHi || r < kExpLo) {
+        *status = APB_ERR_OVERFLOW;
+        return 0;
+    }
+    return (int64_t)r;
+}
+
+// apfloat_normalize (src/apfloat.cpp:116-136): value = (-1)^neg 2^e raw/2^(64 nraw)
+template <int CAP>
+__device__ void gf_normalize(GFloat<CAP>& out, int neg, int64_t e, const uint64_t* raw, int nraw,
+                             int* status) {
+    int h = nraw;
+    while (h > 0 && raw[h - 1] == 0) h--;
+    if (h == 0) {
+        out.kind = APB_ZERO;
+        out.neg = 0;
+        out.e = 0;
+        out.n = 0;
+        return;
+    }
+    unsigned tb = bitw64(raw[h - 1]);
+    int64_t adj = -64 * (int64_t)nraw + 64 * (int64_t)(h - 1) + (int64_t)tb;
+    int64_t e_new = checked_add(e, adj, status);
+    unsigned sh = (64 - tb) % 64;
+    for (int i = h - 1; i >= 0; i--)
+        out.d[i] = sh ? ((raw[i] << sh) | (i > 0 ? raw[i - 1] >> (64 - sh) : 0)) : raw[i];
+    int z = 0;
+    while (out.d[z] == 0) z++;
+    int cnt = h - z;
+    if (z)
+        for (int i = 0; i < cnt; i++) out.d[i] = out.d[i + z];
+    out.kind = APB_FINITE;
+    out.neg = neg;
+    out.e = e_new;
+    out.n = cnt;
+}
+
+// mag_upper_of_low_bits (src/apfloat.cpp:26-63)
+APB_DEV Mag mag_low_bits(const uint64_t* limbs, int cut_limbs, unsigned cut_bits, int64_t base,
+                         int* status) {
+    int t = -1;
+    uint64_t tv = 0;
+    if (cut_bits) {
+        uint64_t part = limbs[cut_limbs] & ((1ull << cut_bits) - 1);
+        if (part) {
+            t = cut_limbs;
+            tv = part;
+        }
+    }
+    if (t < 0) {
+        for (int i = cut_limbs - 1; i >= 0; i--)
+            if (limbs[i]) {
+                t = i;
+                tv = limbs[i];
+                break;
+            }
+    }
+    if (t < 0) return mag_zero();
+    unsigned tb = bitw64(tv);
+    uint64_t window = tb < 64 ? tv << (64 - tb) : tv;
+    bool low = false;
+    if (t > 0) {
+        if (tb < 64) {
+            window |= limbs[t - 1] >> tb;
+            if (limbs[t - 1] & ((1ull << tb) - 1)) low = true;
+        } else if (limbs[t - 1]) {
+            low = true;
+        }
+        for (int i = 0; i + 1 < t && !low; i++)
+            if (limbs[i]) low = true;
+    }
+    uint64_t b = window >> 34;
+    if (low || (window & ((1ull << 34) - 1))) b++;
+    return mag_parts(b, checked_add(base, 64 * (int64_t)t + (int64_t)tb, status));
+}
+
+// apfloat_round (src/apfloat.cpp:138-162), in place; returns the error Mag
+template <int CAP>
+__device__ Mag gf_round(GFloat<CAP>& x, int64_t p, int* status) {
+    if (x.kind != APB_FINITE) return mag_zero();
+    const int n = x.n;
+    if (p >= 64 * (int64_t)n) return mag_zero();
+    const int64_t cut = 64 * (int64_t)n - p;
+    const int cut_limbs = (int)(cut / 64);
+    const unsigned cut_bits = (unsigned)(cut % 64);
+    Mag err = mag_low_bits(x.d, cut_limbs, cut_bits, x.e - 64 * (int64_t)n, status);
+    if (err.kind == 0) return err;
+    int keep = n - cut_limbs;
+    for (int i = 0; i < keep; i++) x.d[i] = x.d[i + cut_limbs];
+    if (cut_bits) x.d[0] &= ~((1ull << cut_bits) - 1);
+    int z = 0;
+    while (x.d[z] == 0) z++;
+    if (z) {
+        for (int i = 0; i + z < keep; i++) x.d[i] = x.d[i + z];
+    }
+    x.n = keep - z;
+    return err;
+}
+
+// store a generic float + Mag into slot e of an output ball array
+template <int CAP>
+__device__ void gf_store(const BallsOut& o, int64_t e, const GFloat<CAP>& m, const Mag& r,
+                         int* status) {
+    uint64_t* dst = o.mant + e * (int64_t)o.L;
+    for (int i = 0; i < o.L; i++) dst[i] = 0;
+    o.exp[e] = 0;
+    o.kind[e] = (uint8_t)m.kind;
+    if (m.kind == APB_FINITE) {
+        if (m.n > o.L) {
+            *status = APB_ERR_UNSUPPORTED;
+        } else {
+            for (int i = 0; i < m.n; i++) dst[o.L - m.n + i] = m.d[i];
+        }
+        o.exp[e] = m.e;
+        if (m.neg) o.kind[e] |= APB_SIGN;
+    }
+    mag_store(r, &o.rad_man[e], &o.rad_exp[e]);
+}
+
+// load slot e of a ball array as a generic float (limb count = minimal)
+template <int CAP>
+__device__ void gf_load(GFloat<CAP>& x, const BallsView& a, int64_t e) {
+    uint8_t k = a.kind[e];
+    x.kind = k & APB_KIND_MASK;
+    x.neg = x.kind == APB_NINF;
+    x.e = 0;
+    x.n = 0;
+    if (x.kind != APB_FINITE) return;
+    const uint64_t* m = a.mant + e * (int64_t)a.L;
+    int z = 0;
+    while (z < a.L && m[z] == 0) z++;
+    x.n = a.L - z;
+    for (int i = 0; i < x.n; i++) x.d[i] = m[z + i];
+    x.e = a.exp[e];
+    x.neg = (k & APB_SIGN) != 0;
+}
+
+}  // namespace apb

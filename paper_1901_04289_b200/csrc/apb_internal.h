@@ -1,0 +1,42 @@
+// apb_internal.h - host-side internals shared by the translation units of
+// libapb_b200.so: workspace (device scratch + status word), launch counter,
+// error reporting and the kernel launchers.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "apb.h"
+
+namespace apb {
+
+// Device scratch owned by the library, grown on demand.  Slot `k` is an
+// independent buffer; the status word collects APB_ERR_* codes raised on the
+// device (exponent overflow = std::overflow_error in the reference).
+struct Workspace {
+    int* status_dev = nullptr;
+    void* bufs[32] = {};
+    size_t caps[32] = {};
+    void* scratch(cudaStream_t st, size_t bytes, int slot);
+};
+Workspace& workspace();
+
+void count_launch(uint64_t k = 1);
+void set_error(const char* msg);
+int cuda_check(cudaError_t e, const char* where);
+
+// dot launchers (dot_kernels.cu)
+int dot_batch_launch(const apb_balls* x, const apb_balls* y, const apb_balls* initial,
+                     int subtract, const apb_dot_index* idx, int64_t n, int64_t batch, int64_t prec,
+                     int mode, const apb_dot_tuning* tuning, apb_balls* out, apb_dot_state* state,
+                     uint64_t* acc, int64_t acc_stride, cudaStream_t st);
+int dot_complex_launch(const apb_balls* xre, const apb_balls* xim, const apb_balls* yre,
+                       const apb_balls* yim, const apb_dot_index* idx, int64_t n, int64_t batch,
+                       int64_t prec, int mode, apb_balls* ore, apb_balls* oim, cudaStream_t st);
+
+// matmul launchers (matmul.cu)
+int matmul_launch(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, apb_mat* C,
+                  cudaStream_t st);
+
+}  // namespace apb

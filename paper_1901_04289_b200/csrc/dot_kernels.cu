@@ -1,0 +1,1209 @@
+// dot_kernels.cu - batched fused ball dot products (K1/K2) for sm_100a.
+//
+// Restates Algorithm 1 of the reference (src/dot.cpp, paths relative to
+// /root/reference/proj) for a batch of independent dots:
+//
+//   dot_small<L,NS,TPL>  one warp per dot, lanes stride over the terms.
+//       Pass 1 (setup_core, src/dot.cpp:72-134) is a warp reduction of
+//       e_max / e_min / e_rad / n_nonzero / fallback; every lane then derives
+//       the identical plan (p_eff, n_s, e_s).  Pass 2 computes each lane's
+//       terms into a private NS-limb two's complement accumulator held in
+//       registers (dot_accumulate_term + accumulate_aligned, src/dot.cpp:
+//       139-273), plus the integer ulp count `err` and the scaled radius sum
+//       `srad` (src/dot.cpp:282-295, 346-358).  The lane accumulators are
+//       combined by a warp-shuffle carry-propagating reduction (two's
+//       complement addition mod 2^(64 n_s) is associative, so the result is
+//       bit-identical to the reference's sequential order).  Lane 0 runs
+//       dot_finalize (src/dot.cpp:306-321).
+//       Per-term contribution: with the operands in L-limb top-aligned slots,
+//       the (truncated) product P = A*B (2L limbs) enters the accumulator as
+//       floor(P / 2^r), r = shift + 128 L - 64 n_s, and err += 1 iff the floor
+//       dropped nonzero bits -- exactly the limb placement/drop rule of
+//       accumulate_aligned.  The short product (mulhigh) never triggers here
+//       (it needs n_s >= 25, src/dot.cpp:259).
+//
+//   dot_generic  one thread per dot, runtime limb counts in local memory: the
+//       wide-precision path (any L, n_s, mulhigh_approx) and the special-value
+//       fallback (ball_fallback_addmul, src/ball.cpp:21-36; src/dot.cpp:325-344).
+//       In `fallback_only` mode it processes only dots the small kernel
+//       flagged as Fallback.
+//
+//   dot_complex_generic  complex dots (src/dot.cpp:470-568): two accumulators
+//       (re, im) over the 2N-term part views, thread per dot.
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "apb.h"
+#include "apb_common.cuh"
+#include "apb_internal.h"
+
+namespace apb {
+
+constexpr int64_t kExpCap = int64_t(1) << 60;  // src/dot.cpp:13
+APB_DEV bool exp_huge(int64_t e) { return e > kExpCap || e < -kExpCap; }
+
+struct DotArgs {
+    BallsView x, y, init;
+    bool has_init;
+    BallsOut out;
+    apb_dot_index idx;
+    int64_t n, batch, prec;
+    int mode;  // APB_DOT_BALL / APB_DOT_APPROX
+    int subtract;
+    int disable_reduction;
+    apb_dot_state* state;
+    uint64_t* acc;
+    int64_t acc_stride;
+    uint8_t* fb_flag;  // per dot: 1 = needs the fallback path
+    int* status;
+};
+
+APB_DEV int64_t x_elem(const apb_dot_index& ix, int64_t b, int64_t i) {
+    return ix.x_off + (b / ix.bdiv) * ix.xs1 + (b % ix.bdiv) * ix.xs2 + i * ix.xstep;
+}
+APB_DEV int64_t y_elem(const apb_dot_index& ix, int64_t b, int64_t i) {
+    return ix.y_off + (b / ix.bdiv) * ix.ys1 + (b % ix.bdiv) * ix.ys2 + i * ix.ystep;
+}
+
+// ---------------------------------------------------------------- plan
+
+struct Plan {
+    int64_t e_max, e_min, e_rad;
+    uint64_t nnz;
+    int64_t p_eff;
+    int extend, padding;
+    int n_s;
+    int64_t e_s;
+    int status;  // 0 proceed 1 fallback 2 zero
+};
+
+// tail of setup_core after the scan (src/dot.cpp:115-131)
+APB_DEV Plan finish_plan(int64_t e_max, int64_t e_min, int64_t e_rad, uint64_t nnz, bool fb,
+                         int64_t total, int64_t p, bool disable_reduction) {
+    Plan pl;
+    pl.e_max = e_max;
+    pl.e_min = e_min;
+    pl.e_rad = e_rad;
+    pl.nnz = nnz;
+    pl.p_eff = 2;
+    pl.extend = pl.padding = 0;
+    pl.n_s = 0;
+    pl.e_s = 0;
+    if (fb) {
+        pl.status = 1;
+        return pl;
+    }
+    if (e_max == INT64_MIN && e_rad == INT64_MIN) {
+        pl.status = 2;
+        return pl;
+    }
+    if (e_max == INT64_MIN) {
+        p = 2;
+    } else if (!disable_reduction) {
+        if (e_rad != INT64_MIN && e_max - e_rad + 30 < p) p = e_max - e_rad + 30;
+        if (e_min != INT64_MAX && e_max - e_min + 30 < p) p = e_max - e_min + 30;
+        if (p < 2) p = 2;
+    }
+    pl.p_eff = p;
+    pl.padding = 4 + (int)bitw64((uint64_t)total);
+    pl.extend = (int)bitw64(nnz) + 1;
+    int64_t ns = (p + pl.extend + pl.padding + 63) / 64;
+    pl.n_s = (int)(ns < 2 ? 2 : ns);
+    pl.e_s = e_max == INT64_MIN ? 0 : e_max + pl.extend;
+    pl.status = 0;
+    return pl;
+}
+
+APB_DEV void write_state(apb_dot_state* st, const Plan& pl, uint64_t err, uint64_t srad) {
+    st->e_max = pl.e_max;
+    st->e_min = pl.e_min;
+    st->e_rad = pl.e_rad;
+    st->n_nonzero = pl.nnz;
+    st->p_eff = pl.p_eff;
+    st->extend = pl.extend;
+    st->padding = pl.padding;
+    st->n_s = pl.n_s;
+    st->e_s = pl.e_s;
+    st->status = pl.status;
+    st->_pad = 0;
+    st->err = err;
+    st->srad = srad;
+}
+
+// srad_add (src/dot.cpp:288-295)
+APB_DEV uint64_t srad_term(uint64_t ab, int64_t af, uint64_t bb, int64_t bf, int64_t e_rad) {
+    int64_t d = e_rad - (af + bf);
+    return d < 30 ? ((ab * bb) >> (30 + d)) + 1 : 1;
+}
+
+// dot_finalize (src/dot.cpp:306-321) given the reduced accumulator
+template <int CAP>
+__device__ void finalize_store(const Plan& pl, const uint64_t* s_in, uint64_t err, uint64_t srad,
+                               int64_t p, bool with_radius, const BallsOut& out, int64_t b,
+                               int* status) {
+    if (p > pl.p_eff) p = pl.p_eff;
+    if (p < 2) p = 2;
+    uint64_t s[CAP];
+    for (int i = 0; i < pl.n_s; i++) s[i] = s_in[i];
+    int sign = 0;
+    if (s[pl.n_s - 1] >> 63) {  // neg_in_place (include/apball/limb.hpp:180-187)
+        int i = 0;
+        while (i < pl.n_s && s[i] == 0) i++;
+        if (i < pl.n_s) {
+            s[i] = ~s[i] + 1;
+            for (i++; i < pl.n_s; i++) s[i] = ~s[i];
+        }
+        sign = 1;
+    }
+    GFloat<CAP> mid;
+    gf_normalize(mid, sign, pl.e_s, s, pl.n_s, status);
+    Mag r = gf_round(mid, p, status);
+    if (with_radius) {
+        if (err) r = mag_add(r, mag_from_u64(err, pl.e_s - 64 * (int64_t)pl.n_s));
+        if (srad) r = mag_add(r, mag_from_u64(srad, pl.e_rad - 30));
+    } else {
+        r = mag_zero();
+    }
+    gf_store(out, b, mid, r, status);
+}
+
+// ----------------------------------------------------------- term loads
+
+template <int L>
+struct Term {
+    uint64_t xm[L], ym[L];
+    int64_t ex, ey;
+    uint8_t kx, ky;
+    uint32_t rx, ry;
+    int64_t fx, fy;
+    bool neg;  // subtract flag of this term
+};
+
+template <int L>
+APB_DEV void load_mant(uint64_t (&m)[L], const BallsView& a, int64_t e) {
+    const int off = L - a.L;  // a.L <= L, top-aligned
+    const uint64_t* src = a.mant + e * (int64_t)a.L;
+#pragma unroll
+    for (int j = 0; j < L; j++) m[j] = (j >= off) ? __ldg(src + (j - off)) : 0ull;
+}
+
+template <int L>
+APB_DEV void load_term(Term<L>& t, const DotArgs& A, int64_t b, int64_t i) {
+    if (i < A.n) {
+        int64_t ex = x_elem(A.idx, b, i), ey = y_elem(A.idx, b, i);
+        t.kx = __ldg(A.x.kind + ex);
+        t.ky = __ldg(A.y.kind + ey);
+        t.ex = __ldg(A.x.exp + ex);
+        t.ey = __ldg(A.y.exp + ey);
+        t.rx = __ldg(A.x.rad_man + ex);
+        t.ry = __ldg(A.y.rad_man + ey);
+        t.fx = __ldg(A.x.rad_exp + ex);
+        t.fy = __ldg(A.y.rad_exp + ey);
+        load_mant<L>(t.xm, A.x, ex);
+        load_mant<L>(t.ym, A.y, ey);
+        t.neg = A.subtract != 0;
+    } else {  // the initial value as term N with y = 1 (src/dot.cpp:29-43)
+        t.kx = __ldg(A.init.kind + b);
+        t.ex = __ldg(A.init.exp + b);
+        t.rx = __ldg(A.init.rad_man + b);
+        t.fx = __ldg(A.init.rad_exp + b);
+        load_mant<L>(t.xm, A.init, b);
+        t.ky = APB_FINITE;
+        t.ey = 1;
+        t.ry = 0;
+        t.fy = 0;
+#pragma unroll
+        for (int j = 0; j < L; j++) t.ym[j] = (j == L - 1) ? (1ull << 63) : 0ull;
+        t.neg = false;
+    }
+}
+
+// minimal limb count of a top-aligned L-slot mantissa
+template <int L>
+APB_DEV int limb_count(const uint64_t (&m)[L]) {
+    int z = 0;
+    bool seen = false;
+#pragma unroll
+    for (int j = 0; j < L; j++) {
+        if (!seen && m[j] == 0) z++;
+        else seen = true;
+    }
+    return L - z;
+}
+
+struct ScanAcc {
+    int64_t e_max, e_min, e_rad;
+    uint64_t nnz;
+    bool fb;
+};
+
+template <int L>
+APB_DEV void scan_term(ScanAcc& s, const Term<L>& t, bool track_min, bool with_radius) {
+    const int kx = t.kx & APB_KIND_MASK, ky = t.ky & APB_KIND_MASK;
+    const bool xz = kx == APB_ZERO, yz = ky == APB_ZERO;
+    if ((kx != APB_ZERO && kx != APB_FINITE) || (ky != APB_ZERO && ky != APB_FINITE)) {
+        s.fb = true;
+        return;
+    }
+    if ((!xz && exp_huge(t.ex)) || (!yz && exp_huge(t.ey))) {
+        s.fb = true;
+        return;
+    }
+    if (!xz && !yz) {
+        s.nnz++;
+        int64_t ee = t.ex + t.ey;
+        s.e_max = ee > s.e_max ? ee : s.e_max;
+        if (track_min) {
+            int64_t lo = ee - 64 * (int64_t)(limb_count<L>(t.xm) + limb_count<L>(t.ym));
+            s.e_min = lo < s.e_min ? lo : s.e_min;
+        }
+    }
+    if (with_radius) {
+        const bool rxz = t.rx == 0, ryz = t.ry == 0;
+        if (t.rx == APB_RAD_INF || t.ry == APB_RAD_INF || (!rxz && exp_huge(t.fx)) ||
+            (!ryz && exp_huge(t.fy))) {
+            s.fb = true;
+            return;
+        }
+        if (!ryz && !xz && t.ex + t.fy > s.e_rad) s.e_rad = t.ex + t.fy;
+        if (!rxz && !yz && t.ey + t.fx > s.e_rad) s.e_rad = t.ey + t.fx;
+        if (!rxz && !ryz && t.fx + t.fy > s.e_rad) s.e_rad = t.fx + t.fy;
+    }
+}
+
+// Mag canonicalization of a loaded radius (Mag::from_parts): the SoA stores
+// canonical mantissas, so (b, f) is used as is.
+
+// ------------------------------------------------------- small kernel
+
+template <int L, int NS>
+struct Acc {
+    uint64_t s[NS];
+    uint64_t err;
+    uint64_t srad;
+};
+
+// accumulate one nonzero term (dot_accumulate_term, src/dot.cpp:229-273)
+template <int L, int NS>
+APB_DEV void acc_term(Acc<L, NS>& a, const Term<L>& t, const Plan& pl) {
+    const bool negate = t.neg ^ ((t.kx & APB_SIGN) != 0) ^ ((t.ky & APB_SIGN) != 0);
+    const int64_t shift = pl.e_s - (t.ex + t.ey);
+    if (shift >= 64 * (int64_t)pl.n_s) {
+        a.err++;
+        return;
+    }
+    // operand truncation to ncap limbs (src/dot.cpp:248-253)
+    const int64_t p_t = 64 * (int64_t)pl.n_s - shift;
+    const int64_t ncap = (p_t + 63) / 64 + 1;
+    uint64_t xa[L], yb[L];
+    bool trunc = false;
+#pragma unroll
+    for (int j = 0; j < L; j++) {
+        const bool keep = (int64_t)(L - j) <= ncap;  // slot j is within the top ncap slots
+        xa[j] = keep ? t.xm[j] : 0ull;
+        yb[j] = keep ? t.ym[j] : 0ull;
+        trunc |= (!keep) && (t.xm[j] | t.ym[j]);
+    }
+    if (trunc) a.err++;
+    // P = xa * yb, 2L limbs
+    uint64_t P[2 * L];
+#pragma unroll
+    for (int k = 0; k < 2 * L; k++) P[k] = 0;
+#pragma unroll
+    for (int i = 0; i < L; i++) {
+        uint64_t cy = 0;
+#pragma unroll
+        for (int j = 0; j < L; j++) {
+            uint64_t lo, hi;
+            mul64(xa[i], yb[j], lo, hi);
+            uint64_t s1 = P[i + j] + lo;
+            uint64_t c1 = s1 < lo;
+            uint64_t s2 = s1 + cy;
+            uint64_t c2 = s2 < cy;
+            P[i + j] = s2;
+            cy = hi + c1 + c2;  // cannot overflow: hi <= 2^64-2
+        }
+        P[i + L] = cy;
+    }
+    // contribution floor(P / 2^r), r = shift + 128L - 64 n_s
+    const int64_t r = shift + 128 * (int64_t)L - 64 * (int64_t)pl.n_s;
+    const int64_t rl = r >= 0 ? r / 64 : -((-r + 63) / 64);
+    const unsigned rb = (unsigned)(r - 64 * rl);
+    bool inexact = false;
+    if (r > 0) {
+#pragma unroll
+        for (int k = 0; k < 2 * L; k++) {
+            if (k < rl) inexact |= P[k] != 0;
+            else if (k == rl && rb) inexact |= (P[k] & ((1ull << rb) - 1)) != 0;
+        }
+    }
+    if (inexact) a.err++;
+    uint64_t Cl[NS];
+#pragma unroll
+    for (int j = 0; j < NS; j++) {
+        uint64_t lo = 0, hi = 0;
+#pragma unroll
+        for (int k = 0; k < 2 * L; k++) {
+            if (k == j + rl) lo = P[k];
+            if (k == j + rl + 1) hi = P[k];
+        }
+        Cl[j] = funnel_r(lo, hi, rb);
+    }
+    // two's complement add / subtract mod 2^(64 NS) (add_signed_range)
+    if (!negate) {
+        uint64_t c = 0;
+#pragma unroll
+        for (int j = 0; j < NS; j++) {
+            uint64_t s1 = a.s[j] + Cl[j];
+            uint64_t c1 = s1 < Cl[j];
+            uint64_t s2 = s1 + c;
+            uint64_t c2 = s2 < c;
+            a.s[j] = s2;
+            c = c1 | c2;
+        }
+    } else {
+        uint64_t bw = 0;
+#pragma unroll
+        for (int j = 0; j < NS; j++) {
+            uint64_t x = a.s[j], y = Cl[j];
+            uint64_t d = x - y - bw;
+            bw = (x < y) || (x == y && bw);
+            a.s[j] = d;
+        }
+    }
+}
+
+// radius_pass_term (src/dot.cpp:346-358)
+template <int L, int NS>
+APB_DEV void rad_term(Acc<L, NS>& a, const Term<L>& t, const Plan& pl) {
+    const bool xz = (t.kx & APB_KIND_MASK) == APB_ZERO, yz = (t.ky & APB_KIND_MASK) == APB_ZERO;
+    if (t.ry != 0 && !xz) a.srad += srad_term((t.xm[L - 1] >> 34) + 1, t.ex, t.ry, t.fy, pl.e_rad);
+    if (t.rx != 0 && !yz) a.srad += srad_term((t.ym[L - 1] >> 34) + 1, t.ey, t.rx, t.fx, pl.e_rad);
+    if (t.rx != 0 && t.ry != 0) a.srad += srad_term(t.rx, t.fx, t.ry, t.fy, pl.e_rad);
+}
+
+APB_DEV int64_t warp_max(int64_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        int64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+APB_DEV int64_t warp_min(int64_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        int64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+APB_DEV uint64_t warp_sum(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int L, int NS, int TPL>
+__global__ void __launch_bounds__(256) dot_small_kernel(DotArgs A) {
+    const int lane = threadIdx.x & 31;
+    const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (b >= A.batch) return;
+    const int64_t total = A.n + (A.has_init ? 1 : 0);
+    const bool with_radius = A.mode == APB_DOT_BALL;
+    const bool track_min = A.prec > 128;
+
+    // ---- pass 1: setup scan
+    ScanAcc sc{INT64_MIN, INT64_MAX, INT64_MIN, 0, false};
+    Term<L> keep[TPL > 0 ? TPL : 1];
+    if (TPL > 0) {
+#pragma unroll
+        for (int q = 0; q < (TPL > 0 ? TPL : 1); q++) {
+            int64_t i = lane + 32 * (int64_t)q;
+            if (i < total) {
+                load_term<L>(keep[q], A, b, i);
+                scan_term<L>(sc, keep[q], track_min, with_radius);
+            }
+        }
+    } else {
+        for (int64_t i = lane; i < total; i += 32) {
+            Term<L> t;
+            load_term<L>(t, A, b, i);
+            scan_term<L>(sc, t, track_min, with_radius);
+        }
+    }
+    const bool fb = __any_sync(0xffffffffu, sc.fb);
+    const int64_t e_max = warp_max(sc.e_max);
+    const int64_t e_min = warp_min(sc.e_min);
+    const int64_t e_rad = warp_max(sc.e_rad);
+    const uint64_t nnz = warp_sum(sc.nnz);
+    const Plan pl = finish_plan(e_max, e_min, e_rad, nnz, fb, total, A.prec, A.disable_reduction);
+
+    if (pl.status != 0) {
+        if (lane == 0) {
+            if (A.state) write_state(A.state + b, pl, 0, 0);
+            if (pl.status == 1) {
+                A.fb_flag[b] = 1;
+            } else {  // ZeroResult -> Ball::zero()
+                GFloat<1> z;
+                z.kind = APB_ZERO;
+                z.neg = 0;
+                z.e = 0;
+                z.n = 0;
+                gf_store(A.out, b, z, mag_zero(), A.status);
+            }
+        }
+        return;
+    }
+
+    // ---- pass 2: accumulate
+    Acc<L, NS> acc;
+#pragma unroll
+    for (int j = 0; j < NS; j++) acc.s[j] = 0;
+    acc.err = 0;
+    acc.srad = 0;
+    auto do_term = [&](const Term<L>& t) {
+        const bool xz = (t.kx & APB_KIND_MASK) == APB_ZERO, yz = (t.ky & APB_KIND_MASK) == APB_ZERO;
+        if (!xz && !yz) acc_term<L, NS>(acc, t, pl);
+        if (with_radius) rad_term<L, NS>(acc, t, pl);
+    };
+    if (TPL > 0) {
+#pragma unroll
+        for (int q = 0; q < (TPL > 0 ? TPL : 1); q++) {
+            int64_t i = lane + 32 * (int64_t)q;
+            if (i < total) do_term(keep[q]);
+        }
+    } else {
+        for (int64_t i = lane; i < total; i += 32) {
+            Term<L> t;
+            load_term<L>(t, A, b, i);
+            do_term(t);
+        }
+    }
+
+    // ---- warp reduction of (s, err, srad); s mod 2^(64 NS) with carries
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        uint64_t c = 0;
+#pragma unroll
+        for (int j = 0; j < NS; j++) {
+            uint64_t v = __shfl_xor_sync(0xffffffffu, acc.s[j], o);
+            uint64_t s1 = acc.s[j] + v;
+            uint64_t c1 = s1 < v;
+            uint64_t s2 = s1 + c;
+            uint64_t c2 = s2 < c;
+            acc.s[j] = s2;
+            c = c1 | c2;
+        }
+        acc.err += __shfl_xor_sync(0xffffffffu, acc.err, o);
+        acc.srad += __shfl_xor_sync(0xffffffffu, acc.srad, o);
+    }
+    if (lane == 0) {
+        if (A.state) write_state(A.state + b, pl, acc.err, acc.srad);
+        if (A.acc)
+            for (int j = 0; j < pl.n_s && j < A.acc_stride; j++) A.acc[b * A.acc_stride + j] = acc.s[j];
+        finalize_store<NS>(pl, acc.s, acc.err, acc.srad, A.prec, with_radius, A.out, b, A.status);
+    }
+}
+
+// ====================================================== generic (thread/dot)
+
+constexpr int GCAP = 140;  // limbs: p <= 4096 inputs (64 limbs) and n_s <= 136
+
+typedef GFloat<GCAP> GF;
+
+// apfloat_mul_exact (src/apfloat.cpp:164-176)
+__device__ void gf_mul_exact(GF& out, const GF& a, const GF& b, int* status) {
+    if (a.kind == APB_NAN || b.kind == APB_NAN) {
+        out.kind = APB_NAN;
+        out.neg = 0;
+        out.n = 0;
+        out.e = 0;
+        return;
+    }
+    const bool ai = a.kind == APB_PINF || a.kind == APB_NINF;
+    const bool bi = b.kind == APB_PINF || b.kind == APB_NINF;
+    if (ai || bi) {
+        out.n = 0;
+        out.e = 0;
+        if (a.kind == APB_ZERO || b.kind == APB_ZERO) {
+            out.kind = APB_NAN;
+            out.neg = 0;
+            return;
+        }
+        const int sa = a.kind == APB_NINF || (a.kind == APB_FINITE && a.neg);
+        const int sb = b.kind == APB_NINF || (b.kind == APB_FINITE && b.neg);
+        out.kind = sa != sb ? APB_NINF : APB_PINF;
+        out.neg = sa != sb;
+        return;
+    }
+    if (a.kind == APB_ZERO || b.kind == APB_ZERO) {
+        out.kind = APB_ZERO;
+        out.neg = 0;
+        out.n = 0;
+        out.e = 0;
+        return;
+    }
+    uint64_t prod[2 * GCAP];
+    for (int k = 0; k < a.n + b.n; k++) prod[k] = 0;
+    for (int j = 0; j < b.n; j++) {
+        uint64_t cy = 0;
+        for (int i = 0; i < a.n; i++) {
+            uint64_t lo, hi;
+            mul64(a.d[i], b.d[j], lo, hi);
+            uint64_t s1 = prod[i + j] + lo;
+            uint64_t c1 = s1 < lo;
+            uint64_t s2 = s1 + cy;
+            uint64_t c2 = s2 < cy;
+            prod[i + j] = s2;
+            cy = hi + c1 + c2;
+        }
+        prod[a.n + j] = cy;
+    }
+    int64_t e = checked_add(a.e, b.e, status);
+    gf_normalize(out, a.neg != b.neg, e, prod, a.n + b.n, status);
+}
+
+// place_truncated (src/apfloat.cpp:197-224)
+__device__ int place_trunc(uint64_t* out, const GF& x, int64_t win_bot) {
+    const int n = x.n;
+    // off = e - 64n - win_bot, computed without overflow for the values that occur
+    const int64_t off = (x.e - 64 * (int64_t)n) - win_bot;
+    if (off >= 0) {
+        int ol = (int)(off / 64);
+        unsigned sh = (unsigned)(off % 64);
+        for (int i = 0; i < n; i++) {
+            out[ol + i] |= x.d[i] << sh;
+            if (sh) out[ol + i + 1] |= x.d[i] >> (64 - sh);
+        }
+        return 0;
+    }
+    const int64_t drop = -off;
+    const int64_t dl = drop / 64;
+    const unsigned db = (unsigned)(drop % 64);
+    if (dl >= n) return 1;
+    int inexact = db && (x.d[dl] & ((1ull << db) - 1));
+    for (int i = 0; i < dl && !inexact; i++)
+        if (x.d[i]) inexact = 1;
+    for (int i = (int)dl; i < n; i++) {
+        uint64_t v = db ? x.d[i] >> db : x.d[i];
+        if (db && i + 1 < n) v |= x.d[i + 1] << (64 - db);
+        out[i - dl] = v;
+    }
+    return inexact;
+}
+
+// apfloat_add_round (src/apfloat.cpp:228-270); res may alias a
+__device__ Mag gf_add_round(GF& res, const GF& a, const GF& b, int64_t p, int* status) {
+    if (p < 2) p = 2;
+    if (a.kind == APB_NAN || b.kind == APB_NAN) {
+        res.kind = APB_NAN;
+        res.neg = 0;
+        res.n = 0;
+        res.e = 0;
+        return mag_zero();
+    }
+    const bool ai = a.kind == APB_PINF || a.kind == APB_NINF;
+    const bool bi = b.kind == APB_PINF || b.kind == APB_NINF;
+    if (ai || bi) {
+        if (ai && bi) {
+            if (a.kind == b.kind) {
+                if (&res != &a) res = a;
+            } else {
+                res.kind = APB_NAN;
+                res.neg = 0;
+                res.n = 0;
+                res.e = 0;
+            }
+        } else {
+            if (ai) {
+                if (&res != &a) res = a;
+            } else {
+                res = b;
+            }
+        }
+        return mag_zero();
+    }
+    if (a.kind == APB_ZERO) {
+        res = b;
+        return gf_round(res, p, status);
+    }
+    if (b.kind == APB_ZERO) {
+        if (&res != &a) res = a;
+        return gf_round(res, p, status);
+    }
+    const int64_t e_top = (a.e > b.e ? a.e : b.e) + 1;
+    const int64_t bot_a = a.e - 64 * (int64_t)a.n;
+    const int64_t bot_b = b.e - 64 * (int64_t)b.n;
+    const int64_t span = e_top - (bot_a < bot_b ? bot_a : bot_b);
+    int64_t k = (span + 63) / 64;
+    const int64_t budget = p / 64 + 3;
+    if (k > budget) k = budget;
+    const int64_t win_bot = checked_add(e_top, -64 * k, status);
+    uint64_t Aw[GCAP + 2], Bw[GCAP + 2], S[GCAP + 2];
+    for (int i = 0; i <= k; i++) Aw[i] = Bw[i] = 0;
+    unsigned units = 0;
+    units += place_trunc(Aw, a, win_bot);
+    units += place_trunc(Bw, b, win_bot);
+    int sign;
+    int cmp = 0;
+    for (int i = (int)k; i >= 0; i--)
+        if (Aw[i] != Bw[i]) {
+            cmp = Aw[i] > Bw[i] ? 1 : -1;
+            break;
+        }
+    const uint64_t *P = Aw, *Q = Bw;
+    if (a.neg == b.neg) {
+        uint64_t c = 0;
+        for (int i = 0; i <= k; i++) {
+            uint64_t s1 = Aw[i] + Bw[i];
+            uint64_t c1 = s1 < Bw[i];
+            uint64_t s2 = s1 + c;
+            c = c1 | (s2 < c);
+            S[i] = s2;
+        }
+        sign = a.neg;
+    } else {
+        if (cmp >= 0) {
+            sign = a.neg;
+        } else {
+            P = Bw;
+            Q = Aw;
+            sign = b.neg;
+        }
+        uint64_t bw = 0;
+        for (int i = 0; i <= k; i++) {
+            uint64_t x = P[i], y = Q[i];
+            S[i] = x - y - bw;
+            bw = (x < y) || (x == y && bw);
+        }
+    }
+    gf_normalize(res, sign, checked_add(win_bot, 64 * (k + 1), status), S, (int)k + 1, status);
+    Mag rerr = gf_round(res, p, status);
+    return units ? mag_add(rerr, mag_from_u64(units, win_bot)) : rerr;
+}
+
+APB_DEV Mag mag_upper_of(const GF& x) {
+    if (x.kind == APB_ZERO) return mag_zero();
+    // the reference reads an empty limb vector here (unspecified); an infinite
+    // midpoint has an infinite magnitude bound
+    if (x.kind != APB_FINITE) return mag_inf();
+    return mag_parts((x.d[x.n - 1] >> 34) + 1, x.e);
+}
+
+struct GBall {
+    GF m;
+    Mag r;
+};
+
+__device__ void gb_load(GBall& g, const BallsView& a, int64_t e) {
+    gf_load(g.m, a, e);
+    g.r = mag_load(a.rad_man[e], a.rad_exp[e]);
+}
+
+__device__ void gb_one(GBall& g) {
+    g.m.kind = APB_FINITE;
+    g.m.neg = 0;
+    g.m.e = 1;
+    g.m.n = 1;
+    g.m.d[0] = 1ull << 63;
+    g.r = mag_zero();
+}
+
+__device__ void gf_negate(GF& x) {
+    if (x.kind == APB_FINITE) x.neg = !x.neg;
+    else if (x.kind == APB_PINF) {
+        x.kind = APB_NINF;
+        x.neg = 1;
+    } else if (x.kind == APB_NINF) {
+        x.kind = APB_PINF;
+        x.neg = 0;
+    }
+}
+
+// ball_fallback_addmul (src/ball.cpp:21-36), acc updated in place
+__device__ void gb_addmul(GBall& acc, const GBall& x, const GBall& y, int64_t p, GF& tmp, int* status) {
+    if (acc.m.kind == APB_NAN || x.m.kind == APB_NAN || y.m.kind == APB_NAN) {
+        acc.m.kind = APB_NAN;
+        acc.m.n = 0;
+        acc.r = mag_inf();
+        return;
+    }
+    gf_mul_exact(tmp, x.m, y.m, status);
+    if (tmp.kind == APB_NAN) {
+        acc.m.kind = APB_NAN;
+        acc.m.n = 0;
+        acc.r = mag_inf();
+        return;
+    }
+    Mag rad = acc.r;
+    if (y.r.kind != 0 && x.m.kind != APB_ZERO) rad = mag_add(rad, mag_mul(mag_upper_of(x.m), y.r));
+    if (x.r.kind != 0 && y.m.kind != APB_ZERO) rad = mag_add(rad, mag_mul(mag_upper_of(y.m), x.r));
+    if (x.r.kind != 0 && y.r.kind != 0) rad = mag_add(rad, mag_mul(x.r, y.r));
+    Mag perr = gf_round(tmp, p, status);
+    Mag aerr = gf_add_round(acc.m, acc.m, tmp, p, status);
+    if (acc.m.kind == APB_NAN) {
+        acc.r = mag_inf();
+        return;
+    }
+    acc.r = mag_add(rad, mag_add(perr, aerr));
+}
+
+// mulhigh_approx (include/apball/limb.hpp:194-228)
+__device__ void g_mulhigh(const uint64_t* a, int na, const uint64_t* b, int nb, int k, uint64_t* out) {
+    const int total = na + nb;
+    const int base = total - k >= 2 ? total - k - 2 : 0;
+    const int wlen = total - base;
+    uint64_t w[2 * GCAP];
+    for (int i = 0; i < wlen; i++) w[i] = 0;
+    for (int j = 0; j < nb; j++) {
+        int i0 = base > j ? base - j : 0;
+        if (i0 >= na) continue;
+        int len = na - i0;
+        int off = i0 + j - base;
+        uint64_t cy = 0;
+        for (int i = 0; i < len; i++) {
+            uint64_t lo, hi;
+            mul64(a[i0 + i], b[j], lo, hi);
+            uint64_t s1 = w[off + i] + lo;
+            uint64_t c1 = s1 < lo;
+            uint64_t s2 = s1 + cy;
+            uint64_t c2 = s2 < cy;
+            w[off + i] = s2;
+            cy = hi + c1 + c2;
+        }
+        for (int q = off + len; q < wlen && cy; q++) {
+            uint64_t s = w[q] + cy;
+            cy = s < cy;
+            w[q] = s;
+        }
+    }
+    for (int i = 0; i < k; i++) out[i] = w[wlen - k + i];
+}
+
+// accumulate_aligned (src/dot.cpp:139-173) on a runtime-size accumulator
+__device__ void g_acc_aligned(const Plan& pl, uint64_t* s, uint64_t& err, const uint64_t* t, int nt,
+                              int64_t e_term, bool negate) {
+    const int64_t shift = pl.e_s - e_term;
+    if (shift >= 64 * (int64_t)pl.n_s) {
+        err++;
+        return;
+    }
+    const unsigned sb = (unsigned)(shift % 64);
+    const int sl = (int)(shift / 64);
+    uint64_t buf[2 * GCAP + 2];
+    if (sb) {
+        buf[0] = t[0] << (64 - sb);
+        for (int i = 0; i + 1 < nt; i++) buf[i + 1] = (t[i] >> sb) | (t[i + 1] << (64 - sb));
+        buf[nt] = t[nt - 1] >> sb;
+        t = buf;
+        nt++;
+    }
+    while (nt && t[0] == 0) {
+        t++;
+        nt--;
+    }
+    if (nt == 0) return;
+    const int avail = pl.n_s - sl;
+    int ds, dt, v;
+    if (nt <= avail) {
+        ds = avail - nt;
+        dt = 0;
+        v = nt;
+    } else {
+        ds = 0;
+        dt = nt - avail;
+        v = avail;
+        err++;
+    }
+    uint64_t* w = s + ds;
+    if (!negate) {
+        uint64_t c = 0;
+        for (int i = 0; i < v; i++) {
+            uint64_t y = t[dt + i];
+            uint64_t s1 = w[i] + y;
+            uint64_t c1 = s1 < y;
+            uint64_t s2 = s1 + c;
+            c = c1 | (s2 < c);
+            w[i] = s2;
+        }
+        for (int i = v; ds + i < pl.n_s && c; i++) {
+            uint64_t s1 = w[i] + c;
+            c = s1 < c;
+            w[i] = s1;
+        }
+    } else {
+        uint64_t bw = 0;
+        for (int i = 0; i < v; i++) {
+            uint64_t x = w[i], y = t[dt + i];
+            w[i] = x - y - bw;
+            bw = (x < y) || (x == y && bw);
+        }
+        for (int i = v; ds + i < pl.n_s && bw; i++) {
+            uint64_t x = w[i];
+            w[i] = x - 1;
+            bw = x == 0;
+        }
+    }
+}
+
+// general dot_accumulate_term (src/dot.cpp:229-273) incl. truncation and mulhigh
+__device__ void g_acc_term(const Plan& pl, uint64_t* s, uint64_t& err, const GF& m, const GF& mp,
+                           bool negate) {
+    negate ^= (m.neg != 0) ^ (mp.neg != 0);
+    const int64_t e_term = m.e + mp.e;
+    const int64_t shift = pl.e_s - e_term;
+    if (shift >= 64 * (int64_t)pl.n_s) {
+        err++;
+        return;
+    }
+    const int n = m.n, np = mp.n;
+    const int64_t p_t = 64 * (int64_t)pl.n_s - shift;
+    const int ncap = (int)((p_t + 63) / 64) + 1;
+    const int na = n < ncap ? n : ncap, nb = np < ncap ? np : ncap;
+    if (n > ncap || np > ncap) err++;
+    const uint64_t* a = m.d + (n - na);
+    const uint64_t* bb = mp.d + (np - nb);
+    const int nt = na + nb;
+    uint64_t t[2 * GCAP];
+    int lead = nt;
+    bool short_prod = false;
+    const int mn = n < np ? n : np;
+    if (p_t >= 25 * 64 && 640 * (int64_t)mn > 9 * p_t) {
+        const int v = pl.n_s - (int)(shift / 64);
+        const int k = nt < v + 1 ? nt : v + 1;
+        if (k < nt) {
+            g_mulhigh(a, na, bb, nb, k, t);
+            err++;
+            lead = k;
+            short_prod = true;
+        }
+    }
+    if (!short_prod) {
+        for (int q = 0; q < nt; q++) t[q] = 0;
+        for (int j = 0; j < nb; j++) {
+            uint64_t cy = 0;
+            for (int i = 0; i < na; i++) {
+                uint64_t lo, hi;
+                mul64(a[i], bb[j], lo, hi);
+                uint64_t s1 = t[i + j] + lo;
+                uint64_t c1 = s1 < lo;
+                uint64_t s2 = s1 + cy;
+                uint64_t c2 = s2 < cy;
+                t[i + j] = s2;
+                cy = hi + c1 + c2;
+            }
+            t[na + j] = cy;
+        }
+    }
+    g_acc_aligned(pl, s, err, t, lead, e_term, negate);
+}
+
+// setup_core over term i via a callback that yields (x, y, neg)
+template <class GetTerm>
+__device__ Plan g_setup(GetTerm&& get, int64_t total, int64_t p, bool with_radius, bool disable_red,
+                        GBall& xs, GBall& ys) {
+    ScanAcc sc{INT64_MIN, INT64_MAX, INT64_MIN, 0, false};
+    const bool track_min = p > 128;
+    for (int64_t i = 0; i < total && !sc.fb; i++) {
+        bool neg;
+        get(i, xs, ys, neg);
+        const GF& xm = xs.m;
+        const GF& ym = ys.m;
+        const bool xf = xm.kind == APB_ZERO || xm.kind == APB_FINITE;
+        const bool yf = ym.kind == APB_ZERO || ym.kind == APB_FINITE;
+        if (!xf || !yf) {
+            sc.fb = true;
+            break;
+        }
+        if ((xm.kind != APB_ZERO && exp_huge(xm.e)) || (ym.kind != APB_ZERO && exp_huge(ym.e))) {
+            sc.fb = true;
+            break;
+        }
+        if (xm.kind != APB_ZERO && ym.kind != APB_ZERO) {
+            sc.nnz++;
+            int64_t ee = xm.e + ym.e;
+            if (ee > sc.e_max) sc.e_max = ee;
+            if (track_min) {
+                int64_t lo = ee - 64 * (int64_t)(xm.n + ym.n);
+                if (lo < sc.e_min) sc.e_min = lo;
+            }
+        }
+        if (with_radius) {
+            const Mag& xr = xs.r;
+            const Mag& yr = ys.r;
+            if (xr.kind == 2 || yr.kind == 2 || (xr.kind == 1 && exp_huge(xr.f)) ||
+                (yr.kind == 1 && exp_huge(yr.f))) {
+                sc.fb = true;
+                break;
+            }
+            if (yr.kind == 1 && xm.kind != APB_ZERO && xm.e + yr.f > sc.e_rad) sc.e_rad = xm.e + yr.f;
+            if (xr.kind == 1 && ym.kind != APB_ZERO && ym.e + xr.f > sc.e_rad) sc.e_rad = ym.e + xr.f;
+            if (xr.kind == 1 && yr.kind == 1 && xr.f + yr.f > sc.e_rad) sc.e_rad = xr.f + yr.f;
+        }
+    }
+    return finish_plan(sc.e_max, sc.e_min, sc.e_rad, sc.nnz, sc.fb, total, p, disable_red);
+}
+
+__device__ void g_rad_term(uint64_t& srad, const GBall& x, const GBall& y, int64_t e_rad) {
+    if (y.r.kind != 0 && x.m.kind != APB_ZERO)
+        srad += srad_term((x.m.d[x.m.n - 1] >> 34) + 1, x.m.e, y.r.b, y.r.f, e_rad);
+    if (x.r.kind != 0 && y.m.kind != APB_ZERO)
+        srad += srad_term((y.m.d[y.m.n - 1] >> 34) + 1, y.m.e, x.r.b, x.r.f, e_rad);
+    if (x.r.kind != 0 && y.r.kind != 0) srad += srad_term(x.r.b, x.r.f, y.r.b, y.r.f, e_rad);
+}
+
+// one dot over a term callback; writes the output ball at `ob`
+template <class GetTerm>
+__device__ void g_dot(GetTerm&& get, int64_t total, int64_t p, bool approx, bool disable_red,
+                      const BallsOut& out, int64_t ob, apb_dot_state* st, uint64_t* accout,
+                      int64_t acc_stride, int* status) {
+    GBall xs, ys;
+    Plan pl = g_setup(get, total, p, !approx, disable_red, xs, ys);
+    if (pl.status == 2) {
+        if (st) write_state(st, pl, 0, 0);
+        GFloat<1> z;
+        z.kind = APB_ZERO;
+        z.neg = 0;
+        z.e = 0;
+        z.n = 0;
+        gf_store(out, ob, z, mag_zero(), status);
+        return;
+    }
+    if (pl.status == 1) {
+        if (st) write_state(st, pl, 0, 0);
+        // fallback_ball / fallback_approx (src/dot.cpp:325-344)
+        GBall acc;
+        GF tmp;
+        acc.m.kind = APB_ZERO;
+        acc.m.neg = 0;
+        acc.m.n = 0;
+        acc.m.e = 0;
+        acc.r = mag_zero();
+        for (int64_t i = 0; i < total; i++) {
+            bool neg;
+            get(i, xs, ys, neg);
+            if (neg) gf_negate(ys.m);
+            if (approx) {
+                gf_mul_exact(tmp, xs.m, ys.m, status);
+                gf_round(tmp, p, status);
+                gf_add_round(acc.m, acc.m, tmp, p, status);
+            } else {
+                gb_addmul(acc, xs, ys, p, tmp, status);
+            }
+        }
+        gf_store(out, ob, acc.m, approx ? mag_zero() : acc.r, status);
+        return;
+    }
+    uint64_t s[GCAP];
+    for (int j = 0; j < pl.n_s; j++) s[j] = 0;
+    uint64_t err = 0, srad = 0;
+    for (int64_t i = 0; i < total; i++) {
+        bool neg;
+        get(i, xs, ys, neg);
+        if (xs.m.kind != APB_ZERO && ys.m.kind != APB_ZERO) g_acc_term(pl, s, err, xs.m, ys.m, neg);
+        if (!approx) g_rad_term(srad, xs, ys, pl.e_rad);
+    }
+    if (st) write_state(st, pl, err, srad);
+    if (accout)
+        for (int j = 0; j < pl.n_s && j < acc_stride; j++) accout[j] = s[j];
+    finalize_store<GCAP>(pl, s, err, srad, p, !approx, out, ob, status);
+}
+
+__global__ void __launch_bounds__(128) dot_generic_kernel(DotArgs A, int fallback_only) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= A.batch) return;
+    if (fallback_only && !A.fb_flag[b]) return;
+    const int64_t total = A.n + (A.has_init ? 1 : 0);
+    auto get = [&](int64_t i, GBall& xs, GBall& ys, bool& neg) {
+        if (i < A.n) {
+            gb_load(xs, A.x, x_elem(A.idx, b, i));
+            gb_load(ys, A.y, y_elem(A.idx, b, i));
+            neg = A.subtract != 0;
+        } else {
+            gb_load(xs, A.init, b);
+            gb_one(ys);
+            neg = false;
+        }
+    };
+    g_dot(get, total, A.prec, A.mode == APB_DOT_APPROX, A.disable_reduction != 0, A.out, b,
+          A.state ? A.state + b : nullptr, A.acc ? A.acc + b * A.acc_stride : nullptr, A.acc_stride,
+          A.status);
+}
+
+// ------------------------------------------------------------ complex
+
+struct CDotArgs {
+    BallsView xre, xim, yre, yim;
+    BallsOut ore, oim;
+    apb_dot_index idx;
+    int64_t n, batch, prec;
+    int mode;
+    int* status;
+};
+
+__global__ void __launch_bounds__(128) dot_complex_generic_kernel(CDotArgs A) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= A.batch) return;
+    const bool approx = A.mode == APB_DOT_APPROX;
+    // ComplexPartView (src/dot.cpp:52-68): re terms (a,c,+),(b,d,-); im (a,d,+),(b,c,+)
+    auto get_re = [&](int64_t i, GBall& xs, GBall& ys, bool& neg) {
+        int64_t j = i >> 1;
+        int64_t ex = x_elem(A.idx, b, j), ey = y_elem(A.idx, b, j);
+        if (i & 1) {
+            gb_load(xs, A.xim, ex);
+            gb_load(ys, A.yim, ey);
+            neg = true;
+        } else {
+            gb_load(xs, A.xre, ex);
+            gb_load(ys, A.yre, ey);
+            neg = false;
+        }
+    };
+    auto get_im = [&](int64_t i, GBall& xs, GBall& ys, bool& neg) {
+        int64_t j = i >> 1;
+        int64_t ex = x_elem(A.idx, b, j), ey = y_elem(A.idx, b, j);
+        if (i & 1) {
+            gb_load(xs, A.xim, ex);
+            gb_load(ys, A.yre, ey);
+        } else {
+            gb_load(xs, A.xre, ex);
+            gb_load(ys, A.yim, ey);
+        }
+        neg = false;
+    };
+    GBall xs, ys;
+    Plan pre = g_setup(get_re, 2 * A.n, A.prec, !approx, false, xs, ys);
+    Plan pim = g_setup(get_im, 2 * A.n, A.prec, !approx, false, xs, ys);
+    if (pre.status == 1 || pim.status == 1) {
+        // complex_fallback_ball (src/dot.cpp:532-545)
+        GBall are, aim;
+        GF tmp;
+        are.m.kind = aim.m.kind = APB_ZERO;
+        are.m.neg = aim.m.neg = 0;
+        are.m.n = aim.m.n = 0;
+        are.m.e = aim.m.e = 0;
+        are.r = aim.r = mag_zero();
+        for (int64_t j = 0; j < A.n; j++) {
+            bool neg;
+            get_re(2 * j, xs, ys, neg);
+            gb_addmul(are, xs, ys, A.prec, tmp, A.status);
+            get_re(2 * j + 1, xs, ys, neg);
+            gf_negate(ys.m);
+            gb_addmul(are, xs, ys, A.prec, tmp, A.status);
+            get_im(2 * j, xs, ys, neg);
+            gb_addmul(aim, xs, ys, A.prec, tmp, A.status);
+            get_im(2 * j + 1, xs, ys, neg);
+            gb_addmul(aim, xs, ys, A.prec, tmp, A.status);
+        }
+        gf_store(A.ore, b, are.m, approx ? mag_zero() : are.r, A.status);
+        gf_store(A.oim, b, aim.m, approx ? mag_zero() : aim.r, A.status);
+        return;
+    }
+    g_dot(get_re, 2 * A.n, A.prec, approx, false, A.ore, b, nullptr, nullptr, 0, A.status);
+    g_dot(get_im, 2 * A.n, A.prec, approx, false, A.oim, b, nullptr, nullptr, 0, A.status);
+}
+
+// ------------------------------------------------------------ launchers
+
+template <int L, int NS, int TPL>
+static void launch_small(const DotArgs& A, cudaStream_t st) {
+    const int warps = 8;
+    dim3 grid((unsigned)((A.batch + warps - 1) / warps));
+    dot_small_kernel<L, NS, TPL><<<grid, 32 * warps, 0, st>>>(A);
+    count_launch();
+}
+
+// the smallest accumulator width covering every plan for (prec, total)
+static int ns_bound(int64_t prec, int64_t total) {
+    auto bc = [](uint64_t v) {
+        int r = 0;
+        while (v) {
+            r++;
+            v >>= 1;
+        }
+        return r;
+    };
+    int64_t ns = (prec + (bc((uint64_t)total) + 1) + (4 + bc((uint64_t)total)) + 63) / 64;
+    return (int)(ns < 2 ? 2 : ns);
+}
+
+template <int L, int NS>
+static bool try_small_tpl(const DotArgs& A, int64_t total, cudaStream_t st) {
+    if (total <= 32 * 4 && L <= 2) {
+        launch_small<L, NS, 4>(A, st);
+    } else {
+        launch_small<L, NS, 0>(A, st);
+    }
+    return true;
+}
+
+int dot_batch_launch(const apb_balls* x, const apb_balls* y, const apb_balls* initial,
+                     int subtract, const apb_dot_index* idx, int64_t n, int64_t batch, int64_t prec,
+                     int mode, const apb_dot_tuning* tuning, apb_balls* out, apb_dot_state* state,
+                     uint64_t* acc, int64_t acc_stride, cudaStream_t st) {
+    if (batch == 0) return APB_OK;
+    DotArgs A;
+    A.x = view_of(x);
+    A.y = view_of(y);
+    A.has_init = initial != nullptr;
+    A.init = initial ? view_of(initial) : view_of(x);
+    A.out = out_of(out);
+    A.idx = *idx;
+    A.n = n;
+    A.batch = batch;
+    A.prec = prec;
+    A.mode = mode;
+    A.subtract = subtract;
+    A.disable_reduction = tuning ? tuning->disable_precision_reduction : 0;
+    A.state = state;
+    A.acc = acc;
+    A.acc_stride = acc_stride;
+    Workspace& ws = workspace();
+    A.status = ws.status_dev;
+    A.fb_flag = (uint8_t*)ws.scratch(st, (size_t)batch, 20);
+    cudaMemsetAsync(A.fb_flag, 0, (size_t)batch, st);
+    const int64_t total = n + (initial ? 1 : 0);
+    int Lin = x->L > y->L ? x->L : y->L;
+    if (initial && initial->L > Lin) Lin = initial->L;
+    const int nsb = ns_bound(prec, total);
+    bool small = true;
+    if (Lin <= 1 && nsb <= 3) try_small_tpl<1, 3>(A, total, st);
+    else if (Lin <= 2 && nsb <= 3) try_small_tpl<2, 3>(A, total, st);
+    else if (Lin <= 2 && nsb <= 5) try_small_tpl<2, 5>(A, total, st);
+    else if (Lin <= 4 && nsb <= 5) try_small_tpl<4, 5>(A, total, st);
+    else if (Lin <= 4 && nsb <= 9) try_small_tpl<4, 9>(A, total, st);
+    else if (Lin <= 8 && nsb <= 9) try_small_tpl<8, 9>(A, total, st);
+    else small = false;
+    const unsigned gthreads = 128;
+    dim3 ggrid((unsigned)((batch + gthreads - 1) / gthreads));
+    dot_generic_kernel<<<ggrid, gthreads, 0, st>>>(A, small ? 1 : 0);
+    count_launch();
+    return APB_OK;
+}
+
+int dot_complex_launch(const apb_balls* xre, const apb_balls* xim, const apb_balls* yre,
+                       const apb_balls* yim, const apb_dot_index* idx, int64_t n, int64_t batch,
+                       int64_t prec, int mode, apb_balls* ore, apb_balls* oim, cudaStream_t st) {
+    if (batch == 0) return APB_OK;
+    CDotArgs A;
+    A.xre = view_of(xre);
+    A.xim = view_of(xim);
+    A.yre = view_of(yre);
+    A.yim = view_of(yim);
+    A.ore = out_of(ore);
+    A.oim = out_of(oim);
+    A.idx = *idx;
+    A.n = n;
+    A.batch = batch;
+    A.prec = prec;
+    A.mode = mode;
+    A.status = workspace().status_dev;
+    const unsigned t = 128;
+    dot_complex_generic_kernel<<<(unsigned)((batch + t - 1) / t), t, 0, st>>>(A);
+    count_launch();
+    return APB_OK;
+}
+
+}  // namespace apb

@@ -1,0 +1,361 @@
+// int8_gemm.cu - K5: exact scaled-integer block product on the 5th-gen tensor
+// cores (tcgen05 kind::i8, TMA-fed, int32 accumulators in TMEM).
+//
+// Replaces int_matmul_multimodular (src/matmul.cpp:280-350, paths relative to
+// /root/reference/proj): instead of residues mod 61-bit primes and a CRT, the
+// scaled integers a_ik (height <= H_A bits) and b_kj are cut into balanced
+// signed 8-bit digits, a = sum_s A_s 256^s, b = sum_t B_t 256^t (scale_pack in
+// matmul.cu), and
+//     T_ij = sum_d 256^d D_d,   D_d = sum_{s+t=d} (A_s B_t)_ij .
+// Each diagonal D_d (or a chunk of its slice pairs, bounded so |D| < 2^30)
+// is accumulated exactly in an int32 TMEM tile by tcgen05.mma over K; the
+// epilogue warps stream the diagonals in increasing d with a per-entry carry:
+//     v = carry + D_d ;  byte_d = v mod 256 ;  carry = v >> 8
+// so each byte is final when emitted.  Bytes are packed 4 per uint32 word
+// (Tw[word][row][col]); each CTA covers one 128x128 output tile and one group
+// of consecutive diagonals (group boundaries are multiples of 4), and leaves
+// its final carry in Tc[group][row][col].  The recombine kernel forms
+// T = (bytes as an unsigned number) + sum_g Tc[g] 256^(d1_g).
+//
+// Roles (320 threads): warp 0 TMA producer, warp 1 MMA issuer (one lane),
+// warps 2..9 epilogue (two warps per TMEM lane quarter, 64 columns each).
+// Shapes: UMMA M=128, N=128, K=32 (int8); smem tiles 128x128 B with the
+// 128-byte swizzle; 4-stage smem ring; 2 TMEM accumulator buffers.
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "apb.h"
+#include "apb_internal.h"
+#include "int8_gemm.h"
+
+namespace apb {
+
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 128;  // BK in bytes (= int8 elements)
+constexpr int STAGES = 4;
+constexpr int STAGE_A = BM * BK, STAGE_B = BN * BK;
+constexpr int STAGE_BYTES = STAGE_A + STAGE_B;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 32 * (2 + EPI_WARPS);
+constexpr int TMEM_COLS = 256;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// K-major, 128-byte swizzle smem matrix descriptor (8-row atoms of 1024 B)
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)(1024 >> 4) << 32;  // stride byte offset between 8-row groups
+    d |= (uint64_t)1 << 46;            // sm100 descriptor version
+    d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+#define TMEM_LD32(taddr, v)                                                                      \
+    asm volatile(                                                                                \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"       \
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),    \
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),             \
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),          \
+          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),          \
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),          \
+          "=r"(v[31])                                                                            \
+        : "r"(taddr))
+
+// instruction descriptor: s32 accumulate, s8 x s8, K-major both, M=128, N=128
+constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+__global__ void __launch_bounds__(THREADS, 1)
+    slice_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      SliceGemmParams P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + STAGES;
+    uint64_t* tfull = bars + 2 * STAGES;
+    uint64_t* tempty = bars + 2 * STAGES + 2;
+    uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = blockIdx.x;   // diagonal group
+    const int mt = blockIdx.y;  // row tile
+    const int nt = blockIdx.z;  // col tile
+    const int m0 = mt * BM, n0 = nt * BN;
+    const int u_begin = P.group_unit_begin[g], u_end = P.group_unit_begin[g + 1];
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], EPI_WARPS * 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = u_begin; u < u_end; u++) {
+                const int4 U = P.units[u];  // (d, s_lo, s_hi, flags)
+                for (int s = U.y; s < U.z; s++) {
+                    const int t = U.x - s;
+                    for (int kb = 0; kb < P.n_kb; kb++) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* sa = smem + stage * STAGE_BYTES;
+                        mbar_expect_tx(&full[stage], STAGE_BYTES);
+                        tma_load_2d(sa, &tmA, kb * BK, s * P.Mp + m0, &full[stage]);
+                        tma_load_2d(sa + STAGE_A, &tmB, kb * BK, t * P.Np + n0, &full[stage]);
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int u = u_begin; u < u_end; u++) {
+            const int ui = u - u_begin;
+            const int buf = ui & 1;
+            const uint32_t tph = (ui >> 1) & 1;
+            const int4 U = P.units[u];
+            mbar_wait(&tempty[buf], tph ^ 1);
+            fence_after();
+            const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
+            uint32_t acc = 0;
+            for (int s = U.y; s < U.z; s++) {
+                for (int kb = 0; kb < P.n_kb; kb++) {
+                    mbar_wait(&full[stage], phase);
+                    fence_after();
+                    if (lane == 0) {
+                        const uint32_t a0 = smem_u32(smem + stage * STAGE_BYTES);
+                        const uint32_t b0 = a0 + STAGE_A;
+#pragma unroll
+                        for (int k = 0; k < BK / 32; k++) {
+                            mma_i8(tmem_d, smem_desc(a0 + 32 * k), smem_desc(b0 + 32 * k), kIdesc, acc);
+                            acc = 1;
+                        }
+                        mma_commit(&empty[stage]);
+                    }
+                    __syncwarp();
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+            if (lane == 0) mma_commit(&tfull[buf]);
+            __syncwarp();
+        }
+    } else {
+        // ------------------------------------------------ epilogue
+        const int e = warp - 2;
+        const int q = warp & 3;          // TMEM lane quarter this warp may access
+        const int col0 = (e >> 2) * 64;  // column half
+        const int row = m0 + 32 * q + lane;
+        int32_t carry[64];
+        uint32_t word[64];
+#pragma unroll
+        for (int c = 0; c < 64; c++) {
+            carry[c] = 0;
+            word[c] = 0;
+        }
+        for (int u = u_begin; u < u_end; u++) {
+            const int ui = u - u_begin;
+            const int buf = ui & 1;
+            const uint32_t tph = (ui >> 1) & 1;
+            const int4 U = P.units[u];
+            const int d = U.x;
+            const bool first = (U.w & 1) != 0, last = (U.w & 2) != 0;
+            mbar_wait(&tfull[buf], tph);
+            fence_after();
+            uint32_t v[64];
+            const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * BN + col0);
+            TMEM_LD32(taddr, v);
+            TMEM_LD32(taddr + 32, (v + 32));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            fence_before();
+            mbar_arrive(&tempty[buf]);
+            const int sh = 8 * (d & 3);
+#pragma unroll
+            for (int c = 0; c < 64; c++) {
+                const int32_t D = (int32_t)v[c];
+                const int32_t b = (int32_t)((word[c] >> sh) & 255u);
+                const int32_t val = b + D + (first ? carry[c] : 0);
+                word[c] = (word[c] & ~(255u << sh)) | ((uint32_t)(val & 255) << sh);
+                carry[c] = (first ? 0 : carry[c]) + (val >> 8);
+            }
+            if (last && ((d & 3) == 3 || d == P.group_d1[g] - 1)) {
+                uint32_t* dst = P.Tw + ((size_t)(d >> 2) * P.Mp + row) * P.Np + n0 + col0;
+#pragma unroll
+                for (int c = 0; c < 64; c += 4) {
+                    *(uint4*)(dst + c) = make_uint4(word[c], word[c + 1], word[c + 2], word[c + 3]);
+                    word[c] = word[c + 1] = word[c + 2] = word[c + 3] = 0;
+                }
+            }
+        }
+        int32_t* cdst = P.Tc + ((size_t)g * P.Mp + row) * P.Np + n0 + col0;
+#pragma unroll
+        for (int c = 0; c < 64; c += 4)
+            *(int4*)(cdst + c) = make_int4(carry[c], carry[c + 1], carry[c + 2], carry[c + 3]);
+    }
+
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(TMEM_COLS)
+                     : "memory");
+    }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (EncodeTiledFn) nullptr;
+        return (EncodeTiledFn)p;
+    }();
+    return fn;
+}
+
+int make_map(CUtensorMap* m, const void* base, uint64_t inner_bytes, uint64_t rows, uint32_t box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return APB_ERR_CUDA;
+    }
+    cuuint64_t dims[2] = {inner_bytes, rows};
+    cuuint64_t strides[1] = {inner_bytes};
+    cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed");
+        return APB_ERR_CUDA;
+    }
+    return APB_OK;
+}
+
+}  // namespace
+
+int slice_gemm_launch(const int8_t* Apack, const int8_t* Bpack, const SliceGemmParams& P, int n_groups,
+                      cudaStream_t st) {
+    CUtensorMap ma, mb;
+    int rc = make_map(&ma, Apack, (uint64_t)P.Kp, (uint64_t)P.S_A * P.Mp, BM);
+    if (rc) return rc;
+    rc = make_map(&mb, Bpack, (uint64_t)P.Kp, (uint64_t)P.S_B * P.Np, BN);
+    if (rc) return rc;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(slice_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        attr = true;
+    }
+    dim3 grid((unsigned)n_groups, (unsigned)(P.Mp / BM), (unsigned)(P.Np / BN));
+    slice_gemm_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, P);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "slice_gemm launch");
+}
+
+}  // namespace apb

@@ -1,0 +1,25 @@
+// int8_gemm.h - interface of the tcgen05 slice GEMM (int8_gemm.cu)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace apb {
+
+constexpr int kSliceTile = 128;  // BM = BN
+constexpr int kSliceBK = 128;    // K padding granule (bytes)
+
+struct SliceGemmParams {
+    int S_A, S_B;          // digit slices of A and B
+    int Mp, Np, Kp;        // padded dims (multiples of 128)
+    int n_kb;              // Kp / 128
+    const int4* units;     // (d, s_lo, s_hi, flags: 1 first-of-d, 2 last-of-d)
+    const int* group_unit_begin;  // [n_groups + 1]
+    const int* group_d1;          // [n_groups] one past the last diagonal of the group
+    uint32_t* Tw;          // [ceil(ND/4)][Mp][Np] packed result bytes
+    int32_t* Tc;           // [n_groups][Mp][Np] final carry of each group
+};
+
+int slice_gemm_launch(const int8_t* Apack, const int8_t* Bpack, const SliceGemmParams& P, int n_groups,
+                      cudaStream_t st);
+
+}  // namespace apb

@@ -178,4 +178,10 @@ def edge_dots(rng: np.random.Generator, batch: int, n: int, max_limbs: int = 4,
             arr.rad_man = np.where(huge, 0, arr.rad_man).astype(np.uint32)
             sel2 = rng.random(cnt) < 0.001
             arr.rad_man = np.where(sel2, APB_RAD_INF, arr.rad_man).astype(np.uint32)
+        # the reference reads an empty limb vector in mag_upper_from_apfloat(+-inf)
+        # when the other factor carries a radius (src/ball.cpp:29-32 with
+        # src/mag.cpp:147-153, assert compiled out): its output radius is
+        # unspecified there, so parity inputs keep such partners exact.
+        infx = ((x.kind & 7) == APB_PINF) | ((x.kind & 7) == APB_NINF)
+        y.rad_man = np.where(infx, 0, y.rad_man).astype(np.uint32)
     return x, y

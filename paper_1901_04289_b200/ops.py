@@ -1,0 +1,215 @@
+"""Host-side mirror of the reference operator surface for the hot path.
+
+Names, argument meaning and error behaviour follow the reference C++ API
+(/root/reference/proj/include/apball/dot.hpp:57-89, matmul.hpp:69-109):
+
+    dot_ball(initial, subtract, x, xstep, y, ystep, n, prec)   -> ball
+    dot_approx(...)                                              -> midpoint
+    dot_complex_ball(x, xstep, y, ystep, n, prec)               -> complex ball
+    classical_matmul_ball / block_matmul_ball / matmul_auto(A, B, prec)
+    complex_matmul_ball(A, B, prec)
+
+plus the batched device entry points the B200 build adds (dot_batch,
+dot_complex_batch, matmul on device-resident matrices).  Errors raise
+InvalidArgument (std::invalid_argument) and OverflowErrorApb
+(std::overflow_error) like the reference.  Every call runs the CUDA library;
+there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .balls import (APB_DOT_APPROX, APB_DOT_BALL, APB_MM_AUTO, APB_MM_BLOCK, APB_MM_CLASSICAL,
+                    DOT_STATE_DTYPE, BallArray, DeviceBallArray, apb_dot_index, apb_dot_tuning,
+                    apb_mat, flat_index, limbs_for)
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+# ------------------------------------------------------------ batched dots
+
+def dot_batch(x: DeviceBallArray, y: DeviceBallArray, n: int, batch: int, prec: int, *,
+              initial: DeviceBallArray | None = None, subtract: bool = False, mode: str = "ball",
+              index: apb_dot_index | None = None, out: DeviceBallArray | None = None,
+              want_state: bool = False, acc_stride: int = 0, disable_precision_reduction=False,
+              stream=None, check: bool = True):
+    """Batch of independent ball dot products on device-resident SoA arrays
+    (one reference dot_ball / dot_approx call per dot)."""
+    import torch
+    lib = _lib.lib()
+    index = index or flat_index(n)
+    out = out if out is not None else DeviceBallArray.empty(batch, limbs_for(prec))
+    state = torch.zeros(batch * DOT_STATE_DTYPE.itemsize, dtype=torch.uint8, device="cuda") if want_state else None
+    acc = torch.zeros(batch * max(acc_stride, 1), dtype=torch.int64, device="cuda") if acc_stride else None
+    tun = apb_dot_tuning(int(bool(disable_precision_reduction)), 0, 128)
+    xc, yc, oc = x.c(), y.c(), out.c()
+    ic = initial.c() if initial is not None else None
+    st = _stream_ptr(stream)
+    rc = lib.apb_dot_batch(C.byref(xc), C.byref(yc), C.byref(ic) if ic is not None else None,
+                           int(bool(subtract)), C.byref(index), n, batch, prec,
+                           APB_DOT_APPROX if mode == "approx" else APB_DOT_BALL, C.byref(tun),
+                           C.byref(oc), state.data_ptr() if state is not None else None,
+                           acc.data_ptr() if acc is not None else None, acc_stride, st)
+    _lib.check(rc, "apb_dot_batch")
+    if check:
+        _lib.check(lib.apb_device_status(st), "apb_dot_batch")
+    if want_state or acc_stride:
+        st_np = np.frombuffer(state.cpu().numpy().tobytes(), DOT_STATE_DTYPE) if state is not None else None
+        acc_np = acc.cpu().numpy().view(np.uint64).reshape(batch, acc_stride) if acc is not None else None
+        return out, st_np, acc_np
+    return out
+
+
+def dot_complex_batch(xre, xim, yre, yim, n: int, batch: int, prec: int, *, mode="ball",
+                      index=None, stream=None, check=True):
+    lib = _lib.lib()
+    index = index or flat_index(n)
+    ore, oim = DeviceBallArray.empty(batch, limbs_for(prec)), DeviceBallArray.empty(batch, limbs_for(prec))
+    cs = [v.c() for v in (xre, xim, yre, yim, ore, oim)]
+    st = _stream_ptr(stream)
+    rc = lib.apb_dot_complex_batch(*[C.byref(v) for v in cs[:4]], C.byref(index), n, batch, prec,
+                                   APB_DOT_APPROX if mode == "approx" else APB_DOT_BALL, None,
+                                   C.byref(cs[4]), C.byref(cs[5]), None, st)
+    _lib.check(rc, "apb_dot_complex_batch")
+    if check:
+        _lib.check(lib.apb_device_status(st), "apb_dot_complex_batch")
+    return ore, oim
+
+
+def dot_batch_host(x: BallArray, y: BallArray, n: int, batch: int, prec: int, *,
+                   initial: BallArray | None = None, subtract=False, mode="ball", index=None,
+                   out: BallArray | None = None) -> BallArray:
+    """Same as dot_batch on HOST arrays: copies in, computes on the GPU, copies out."""
+    lib = _lib.lib()
+    index = index or flat_index(n)
+    out = out if out is not None else BallArray.zeros(batch, limbs_for(prec))
+    xc, yc, oc = x.c(), y.c(), out.c()
+    ic = initial.c() if initial is not None else None
+    rc = lib.apb_dot_batch_host(C.byref(xc), C.byref(yc), C.byref(ic) if ic is not None else None,
+                                int(bool(subtract)), C.byref(index), n, batch, prec,
+                                APB_DOT_APPROX if mode == "approx" else APB_DOT_BALL, C.byref(oc))
+    _lib.check(rc, "apb_dot_batch_host")
+    return out
+
+
+# ------------------------------------------------- reference-shaped dots
+
+def dot_ball(initial: BallArray | None, subtract: bool, x: BallArray | None, xstep: int,
+             y: BallArray | None, ystep: int, n: int, prec: int, *, x_off: int = 0,
+             y_off: int = 0) -> BallArray:
+    """dot_ball (include/apball/dot.hpp:73-74): initial + (-1)^subtract sum x_i y_i
+    with x_i = x[x_off + i*xstep] (steps may be negative)."""
+    return _dot_one(initial, subtract, x, xstep, y, ystep, n, prec, x_off, y_off, "ball")
+
+
+def dot_approx(initial, subtract, x, xstep, y, ystep, n, prec, *, x_off=0, y_off=0) -> BallArray:
+    """dot_approx (include/apball/dot.hpp:77-78): midpoint only (zero radius)."""
+    return _dot_one(initial, subtract, x, xstep, y, ystep, n, prec, x_off, y_off, "approx")
+
+
+def _dot_one(initial, subtract, x, xstep, y, ystep, n, prec, x_off, y_off, mode):
+    if n == 0:
+        x = y = BallArray.zeros(1, 1)
+    idx = apb_dot_index(1, x_off, 0, 0, xstep, y_off, 0, 0, ystep)
+    return dot_batch_host(x, y, n, 1, prec, initial=initial, subtract=subtract, mode=mode, index=idx)
+
+
+# ------------------------------------------------------------------ matmul
+
+@dataclass
+class BallMatrix:
+    """Row-major ball matrix (include/apball/matmul.hpp:18-26), host or device."""
+    balls: BallArray | DeviceBallArray
+    rows: int
+    cols: int
+
+    def c(self) -> apb_mat:
+        return apb_mat(self.balls.c(), self.rows, self.cols)
+
+    @property
+    def on_device(self) -> bool:
+        return isinstance(self.balls, DeviceBallArray)
+
+
+def _matmul(a: BallMatrix, b: BallMatrix, prec: int, algo: int, stream=None, check=True) -> BallMatrix:
+    lib = _lib.lib()
+    if a.cols != b.rows:
+        raise _lib.InvalidArgument(1, "matmul: dimension mismatch")
+    L = limbs_for(prec)
+    if a.on_device:
+        c = BallMatrix(DeviceBallArray.empty(a.rows * b.cols, L), a.rows, b.cols)
+        am, bm, cm = a.c(), b.c(), c.c()
+        st = _stream_ptr(stream)
+        _lib.check(lib.apb_matmul(C.byref(am), C.byref(bm), prec, algo, C.byref(cm), st), "apb_matmul")
+        if check:
+            _lib.check(lib.apb_device_status(st), "apb_matmul")
+        return c
+    c = BallMatrix(BallArray.zeros(a.rows * b.cols, L), a.rows, b.cols)
+    am, bm, cm = a.c(), b.c(), c.c()
+    _lib.check(lib.apb_matmul_host(C.byref(am), C.byref(bm), prec, algo, C.byref(cm)), "apb_matmul_host")
+    return c
+
+
+def classical_matmul_ball(a: BallMatrix, b: BallMatrix, prec: int, **kw) -> BallMatrix:
+    """classical_matmul_ball (include/apball/matmul.hpp:89)"""
+    return _matmul(a, b, prec, APB_MM_CLASSICAL, **kw)
+
+
+def block_matmul_ball(a: BallMatrix, b: BallMatrix, prec: int, **kw) -> BallMatrix:
+    """block_matmul_ball (include/apball/matmul.hpp:90)"""
+    return _matmul(a, b, prec, APB_MM_BLOCK, **kw)
+
+
+def matmul_auto(a: BallMatrix, b: BallMatrix, prec: int, **kw) -> BallMatrix:
+    """matmul_auto (include/apball/matmul.hpp:91)"""
+    return _matmul(a, b, prec, APB_MM_AUTO, **kw)
+
+
+def matmul_dispatch_cutoff(prec: int) -> int:
+    """matmul_dispatch_cutoff (src/matmul.cpp:517-524)"""
+    for lim, c in ((64, 60), (128, 56), (256, 52), (512, 48), (1024, 44)):
+        if prec <= lim:
+            return c
+    return 40
+
+
+def complex_matmul_ball(are: BallMatrix, aim: BallMatrix, bre: BallMatrix, bim: BallMatrix,
+                        prec: int, stream=None, check=True):
+    """complex_matmul_ball (include/apball/matmul.hpp:92-93); parts given separately"""
+    lib = _lib.lib()
+    if are.cols != bre.rows:
+        raise _lib.InvalidArgument(1, "matmul: dimension mismatch")
+    L = limbs_for(prec)
+    cre = BallMatrix(DeviceBallArray.empty(are.rows * bre.cols, L), are.rows, bre.cols)
+    cim = BallMatrix(DeviceBallArray.empty(are.rows * bre.cols, L), are.rows, bre.cols)
+    ms = [m.c() for m in (are, aim, bre, bim, cre, cim)]
+    st = _stream_ptr(stream)
+    _lib.check(lib.apb_matmul_complex(*[C.byref(m) for m in ms[:4]], prec, APB_MM_AUTO,
+                                      C.byref(ms[4]), C.byref(ms[5]), st), "apb_matmul_complex")
+    if check:
+        _lib.check(lib.apb_device_status(st), "apb_matmul_complex")
+    return cre, cim
+
+
+def matmul_stats() -> dict:
+    s = _lib.lib().apb_matmul_stats_get().contents
+    return {f: int(getattr(s, f)) for f, _ in s._fields_}
+
+
+def matmul_stats_reset():
+    _lib.lib().apb_matmul_stats_reset()
+
+
+def launch_count() -> int:
+    return int(_lib.lib().apb_launch_count())

@@ -1,0 +1,118 @@
+"""GPU parity: batched dot kernels (libapb_b200.so) vs the reference.
+
+Bit-exact: output balls, plan, accumulator limbs, err and srad equal the
+reference's dot_setup/dot_init/dot_accumulate_term/dot_finalize
+(golden fixtures from the reference + live oracle/_ref runs on the box)."""
+import numpy as np
+import pytest
+
+import pyoracle as po
+from golden_io import balls, files, index, name
+from paper_1901_04289_b200 import gen
+from paper_1901_04289_b200.balls import BallArray, flat_index
+
+pytestmark = pytest.mark.gpu
+
+DOT = files("dot_")
+
+
+def _dev(a):
+    return a.to_device() if a is not None else None
+
+
+@pytest.mark.parametrize("path", DOT, ids=[name(p) for p in DOT])
+def test_dot_golden_gpu(path):
+    from paper_1901_04289_b200 import ops
+    d = np.load(path)
+    x, y, init, out = balls(d, "x"), balls(d, "y"), balls(d, "init"), balls(d, "out")
+    n, batch, prec = int(d["n"]), int(d["batch"]), int(d["prec"])
+    got, st, acc = ops.dot_batch(_dev(x), _dev(y), n, batch, prec, initial=_dev(init),
+                                 subtract=bool(d["subtract"]), index=index(d),
+                                 mode="approx" if int(d["mode"]) else "ball", want_state=True,
+                                 acc_stride=d["acc"].shape[1],
+                                 disable_precision_reduction=bool(d["disable_reduction"]))
+    got = got.to_host()
+    ok = got.identical(out)
+    assert ok.all(), f"{(~ok).sum()} of {batch} dots differ, first {np.nonzero(~ok)[0][:8]}"
+    if int(d["mode"]):
+        return  # the reference exposes dot_setup only with radius scanning (dot.hpp:57)
+    exp_st = d["state"]
+    for f in ("status", "e_max", "e_rad", "n_nonzero", "p_eff", "n_s", "e_s", "err", "srad"):
+        np.testing.assert_array_equal(st[f], exp_st[f], err_msg=f)
+    proceed = exp_st["status"] == 0
+    np.testing.assert_array_equal(acc[proceed], d["acc"][proceed])
+
+
+@pytest.mark.parametrize("path", files("cdot_"), ids=[name(p) for p in files("cdot_")])
+def test_complex_dot_golden_gpu(path):
+    from paper_1901_04289_b200 import ops
+    d = np.load(path)
+    args = [balls(d, k).to_device() for k in ("xre", "xim", "yre", "yim")]
+    ore, oim = ops.dot_complex_batch(*args, int(d["n"]), int(d["batch"]), int(d["prec"]),
+                                     mode="approx" if int(d["mode"]) else "ball")
+    assert ore.to_host().identical(balls(d, "ore")).all()
+    assert oim.to_host().identical(balls(d, "oim")).all()
+
+
+def test_c1_full_batch_vs_reference():
+    """config 1 at full size: all 65,536 dots bit-identical to the reference
+    (reference timed multithreaded on the host), sampled containment."""
+    from paper_1901_04289_b200 import ops
+    import os
+    x, y = gen.config1_dots()
+    got = ops.dot_batch(x.to_device(), y.to_device(), 100, 65536, 128).to_host()
+    ref = po.dot_batch(x, y, 100, 65536, 128, which="ref", threads=os.cpu_count() or 8)
+    ok = got.identical(ref)
+    assert ok.all(), f"{(~ok).sum()} dots differ"
+    sample = np.arange(0, 65536, 257)
+    xs = x.take((sample[:, None] * 100 + np.arange(100)).ravel())
+    ys = y.take((sample[:, None] * 100 + np.arange(100)).ravel())
+    assert po.dot_contains(xs, ys, 100, len(sample), got.take(sample)).all()
+
+
+@pytest.mark.parametrize("p", [64, 128, 256, 512, 1024, 4096])
+def test_c5_dots_vs_reference(p):
+    from paper_1901_04289_b200 import ops
+    n = 1000 if p <= 1024 else 300
+    batch = 64 if p <= 512 else 16
+    x, y = gen.config5_dots(batch=batch, n=n, p=p)
+    got = ops.dot_batch(x.to_device(), y.to_device(), n, batch, p).to_host()
+    ref = po.dot_batch(x, y, n, batch, p, which="ref", threads=8)
+    assert got.identical(ref).all()
+
+
+def test_edge_random_vs_reference():
+    from paper_1901_04289_b200 import ops
+    rng = np.random.Generator(np.random.PCG64(99))
+    for n in (1, 5, 31, 32, 33, 64, 129, 300):
+        for p in (2, 30, 64, 100, 128, 129, 256, 500, 700, 2000):
+            x, y = gen.edge_dots(rng, 40, n)
+            init, _ = gen.edge_dots(rng, 40, 1)
+            sub = bool(rng.integers(0, 2))
+            kw = dict(initial=init if n % 3 == 0 else None, subtract=sub)
+            got = ops.dot_batch(x.to_device(), y.to_device(), n, 40, p,
+                                initial=_dev(kw["initial"]), subtract=sub).to_host()
+            ref = po.dot_batch(x, y, n, 40, p, which="ref", **kw)
+            ok = got.identical(ref)
+            assert ok.all(), (n, p, np.nonzero(~ok)[0][:5])
+
+
+def test_host_entry_matches_device_entry():
+    from paper_1901_04289_b200 import ops
+    x, y = gen.config1_dots(batch=512)
+    a = ops.dot_batch(x.to_device(), y.to_device(), 100, 512, 128).to_host()
+    b = ops.dot_batch_host(x, y, 100, 512, 128)
+    assert a.identical(b).all()
+
+
+def test_reference_shaped_dot_ball():
+    """dot_ball with negative strides and an initial value, as poly/basecase call it"""
+    from paper_1901_04289_b200 import ops
+    rng = np.random.Generator(np.random.PCG64(5))
+    x, y = gen.edge_dots(rng, 1, 25, specials=False)
+    init, _ = gen.edge_dots(rng, 1, 1, specials=False)
+    got = ops.dot_ball(init, True, x, -1, y, 1, 25, 150, x_off=24)
+    from paper_1901_04289_b200.balls import apb_dot_index
+    ref = po.dot_batch(x, y, 25, 1, 150, which="ref", initial=init, subtract=True,
+                       idx=apb_dot_index(1, 24, 0, 0, -1, 0, 0, 0, 1))
+    assert got.identical(ref).all()
