@@ -200,6 +200,15 @@ int apb_matmul_host(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, 
  * above are asynchronous and only report launch/argument errors. */
 int apb_device_status(void* stream);
 
+/* Kernel-level timing for measurement: when enabled, the library brackets its
+ * kernels with CUDA events on the launching stream, grouped by name
+ * ("slice_gemm", "dot", "pack", "recombine", "rad_gemm", "scan").
+ * apb_profile_read synchronizes the recorded events and returns the summed
+ * device milliseconds and the number of launches since the last reset. */
+void apb_profile_enable(int on);
+void apb_profile_reset(void);
+int apb_profile_read(const char* kernel, double* ms, uint64_t* launches);
+
 apb_matmul_stats* apb_matmul_stats_get(void);
 void apb_matmul_stats_reset(void);
 const char* apb_last_error(void);

@@ -73,6 +73,11 @@ def lib():
     L.apb_last_error.restype = C.c_char_p
     L.apb_launch_count.restype = C.c_uint64
     L.apb_version.restype = I
+    L.apb_profile_enable.argtypes = [I]
+    L.apb_profile_enable.restype = None
+    L.apb_profile_reset.restype = None
+    L.apb_profile_read.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+    L.apb_profile_read.restype = I
     _lib = L
     return L
 

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libapb_b200.so")
-SOURCES = ["apb_abi.cu", "dot_kernels.cu", "matmul.cu"]
+SOURCES = ["apb_abi.cu", "dot_kernels.cu", "matmul.cu", "int8_gemm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

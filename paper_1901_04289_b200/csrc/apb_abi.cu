@@ -7,6 +7,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "apb.h"
 #include "apb_internal.h"
@@ -28,6 +29,37 @@ int cuda_check(cudaError_t e, const char* where) {
 }
 
 static std::mutex g_ws_mu;
+
+// ------------------------------------------------------------- profiling
+struct ProfRec {
+    std::string name;
+    cudaEvent_t b, e;
+    bool open;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;
+
+int prof_begin(const char* name, cudaStream_t st) {
+    if (!g_prof_on) return -1;
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    ProfRec r;
+    r.name = name;
+    cudaEventCreate(&r.b);
+    cudaEventCreate(&r.e);
+    r.open = true;
+    cudaEventRecord(r.b, st);
+    g_prof.push_back(r);
+    return (int)g_prof.size() - 1;
+}
+
+void prof_end(int token, cudaStream_t st) {
+    if (token < 0) return;
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    if (token >= (int)g_prof.size()) return;
+    cudaEventRecord(g_prof[token].e, st);
+    g_prof[token].open = false;
+}
 
 Workspace& workspace() {
     static Workspace* ws = [] {
@@ -77,6 +109,35 @@ uint64_t apb_launch_count(void) { return g_launches.load(); }
 const char* apb_last_error(void) { return g_error.c_str(); }
 apb_matmul_stats* apb_matmul_stats_get(void) { return &g_stats; }
 void apb_matmul_stats_reset(void) { std::memset(&g_stats, 0, sizeof g_stats); }
+
+void apb_profile_enable(int on) { g_prof_on = on != 0; }
+
+void apb_profile_reset(void) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    for (auto& r : g_prof) {
+        cudaEventSynchronize(r.e);
+        cudaEventDestroy(r.b);
+        cudaEventDestroy(r.e);
+    }
+    g_prof.clear();
+}
+
+int apb_profile_read(const char* kernel, double* ms, uint64_t* launches) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    double t = 0;
+    uint64_t n = 0;
+    for (auto& r : g_prof) {
+        if (r.open || r.name != kernel) continue;
+        if (cudaEventSynchronize(r.e) != cudaSuccess) return APB_ERR_CUDA;
+        float f = 0;
+        cudaEventElapsedTime(&f, r.b, r.e);
+        t += f;
+        n++;
+    }
+    if (ms) *ms = t;
+    if (launches) *launches = n;
+    return APB_OK;
+}
 
 int apb_device_status(void* stream) {
     cudaStream_t st = (cudaStream_t)stream;

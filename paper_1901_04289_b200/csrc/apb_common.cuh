@@ -343,4 +343,182 @@ __device__ void gf_load(GFloat<CAP>& x, const BallsView& a, int64_t e) {
     x.neg = (k & APB_SIGN) != 0;
 }
 
+// ----------------------------------------- generic arithmetic (bounded)
+
+constexpr int GCAP = 140;  // limbs: p <= 4096 inputs (64 limbs) and n_s <= 136
+
+typedef GFloat<GCAP> GF;
+
+// apfloat_mul_exact (src/apfloat.cpp:164-176)
+__device__ inline void gf_mul_exact(GF& out, const GF& a, const GF& b, int* status) {
+    if (a.kind == APB_NAN || b.kind == APB_NAN) {
+        out.kind = APB_NAN;
+        out.neg = 0;
+        out.n = 0;
+        out.e = 0;
+        return;
+    }
+    const bool ai = a.kind == APB_PINF || a.kind == APB_NINF;
+    const bool bi = b.kind == APB_PINF || b.kind == APB_NINF;
+    if (ai || bi) {
+        out.n = 0;
+        out.e = 0;
+        if (a.kind == APB_ZERO || b.kind == APB_ZERO) {
+            out.kind = APB_NAN;
+            out.neg = 0;
+            return;
+        }
+        const int sa = a.kind == APB_NINF || (a.kind == APB_FINITE && a.neg);
+        const int sb = b.kind == APB_NINF || (b.kind == APB_FINITE && b.neg);
+        out.kind = sa != sb ? APB_NINF : APB_PINF;
+        out.neg = sa != sb;
+        return;
+    }
+    if (a.kind == APB_ZERO || b.kind == APB_ZERO) {
+        out.kind = APB_ZERO;
+        out.neg = 0;
+        out.n = 0;
+        out.e = 0;
+        return;
+    }
+    uint64_t prod[2 * GCAP];
+    for (int k = 0; k < a.n + b.n; k++) prod[k] = 0;
+    for (int j = 0; j < b.n; j++) {
+        uint64_t cy = 0;
+        for (int i = 0; i < a.n; i++) {
+            uint64_t lo, hi;
+            mul64(a.d[i], b.d[j], lo, hi);
+            uint64_t s1 = prod[i + j] + lo;
+            uint64_t c1 = s1 < lo;
+            uint64_t s2 = s1 + cy;
+            uint64_t c2 = s2 < cy;
+            prod[i + j] = s2;
+            cy = hi + c1 + c2;
+        }
+        prod[a.n + j] = cy;
+    }
+    int64_t e = checked_add(a.e, b.e, status);
+    gf_normalize(out, a.neg != b.neg, e, prod, a.n + b.n, status);
+}
+
+// place_truncated (src/apfloat.cpp:197-224)
+__device__ inline int place_trunc(uint64_t* out, const GF& x, int64_t win_bot) {
+    const int n = x.n;
+    // off = e - 64n - win_bot, computed without overflow for the values that occur
+    const int64_t off = (x.e - 64 * (int64_t)n) - win_bot;
+    if (off >= 0) {
+        int ol = (int)(off / 64);
+        unsigned sh = (unsigned)(off % 64);
+        for (int i = 0; i < n; i++) {
+            out[ol + i] |= x.d[i] << sh;
+            if (sh) out[ol + i + 1] |= x.d[i] >> (64 - sh);
+        }
+        return 0;
+    }
+    const int64_t drop = -off;
+    const int64_t dl = drop / 64;
+    const unsigned db = (unsigned)(drop % 64);
+    if (dl >= n) return 1;
+    int inexact = db && (x.d[dl] & ((1ull << db) - 1));
+    for (int i = 0; i < dl && !inexact; i++)
+        if (x.d[i]) inexact = 1;
+    for (int i = (int)dl; i < n; i++) {
+        uint64_t v = db ? x.d[i] >> db : x.d[i];
+        if (db && i + 1 < n) v |= x.d[i + 1] << (64 - db);
+        out[i - dl] = v;
+    }
+    return inexact;
+}
+
+// apfloat_add_round (src/apfloat.cpp:228-270); res may alias a
+__device__ inline Mag gf_add_round(GF& res, const GF& a, const GF& b, int64_t p, int* status) {
+    if (p < 2) p = 2;
+    if (a.kind == APB_NAN || b.kind == APB_NAN) {
+        res.kind = APB_NAN;
+        res.neg = 0;
+        res.n = 0;
+        res.e = 0;
+        return mag_zero();
+    }
+    const bool ai = a.kind == APB_PINF || a.kind == APB_NINF;
+    const bool bi = b.kind == APB_PINF || b.kind == APB_NINF;
+    if (ai || bi) {
+        if (ai && bi) {
+            if (a.kind == b.kind) {
+                if (&res != &a) res = a;
+            } else {
+                res.kind = APB_NAN;
+                res.neg = 0;
+                res.n = 0;
+                res.e = 0;
+            }
+        } else {
+            if (ai) {
+                if (&res != &a) res = a;
+            } else {
+                res = b;
+            }
+        }
+        return mag_zero();
+    }
+    if (a.kind == APB_ZERO) {
+        res = b;
+        return gf_round(res, p, status);
+    }
+    if (b.kind == APB_ZERO) {
+        if (&res != &a) res = a;
+        return gf_round(res, p, status);
+    }
+    const int64_t e_top = (a.e > b.e ? a.e : b.e) + 1;
+    const int64_t bot_a = a.e - 64 * (int64_t)a.n;
+    const int64_t bot_b = b.e - 64 * (int64_t)b.n;
+    const int64_t span = e_top - (bot_a < bot_b ? bot_a : bot_b);
+    int64_t k = (span + 63) / 64;
+    const int64_t budget = p / 64 + 3;
+    if (k > budget) k = budget;
+    const int64_t win_bot = checked_add(e_top, -64 * k, status);
+    uint64_t Aw[GCAP + 2], Bw[GCAP + 2], S[GCAP + 2];
+    for (int i = 0; i <= k; i++) Aw[i] = Bw[i] = 0;
+    unsigned units = 0;
+    units += place_trunc(Aw, a, win_bot);
+    units += place_trunc(Bw, b, win_bot);
+    int sign;
+    int cmp = 0;
+    for (int i = (int)k; i >= 0; i--)
+        if (Aw[i] != Bw[i]) {
+            cmp = Aw[i] > Bw[i] ? 1 : -1;
+            break;
+        }
+    const uint64_t *P = Aw, *Q = Bw;
+    if (a.neg == b.neg) {
+        uint64_t c = 0;
+        for (int i = 0; i <= k; i++) {
+            uint64_t s1 = Aw[i] + Bw[i];
+            uint64_t c1 = s1 < Bw[i];
+            uint64_t s2 = s1 + c;
+            c = c1 | (s2 < c);
+            S[i] = s2;
+        }
+        sign = a.neg;
+    } else {
+        if (cmp >= 0) {
+            sign = a.neg;
+        } else {
+            P = Bw;
+            Q = Aw;
+            sign = b.neg;
+        }
+        uint64_t bw = 0;
+        for (int i = 0; i <= k; i++) {
+            uint64_t x = P[i], y = Q[i];
+            S[i] = x - y - bw;
+            bw = (x < y) || (x == y && bw);
+        }
+    }
+    gf_normalize(res, sign, checked_add(win_bot, 64 * (k + 1), status), S, (int)k + 1, status);
+    Mag rerr = gf_round(res, p, status);
+    return units ? mag_add(rerr, mag_from_u64(units, win_bot)) : rerr;
+}
+
+
 }  // namespace apb

@@ -353,7 +353,9 @@ int slice_gemm_launch(const int8_t* Apack, const int8_t* Bpack, const SliceGemmP
         attr = true;
     }
     dim3 grid((unsigned)n_groups, (unsigned)(P.Mp / BM), (unsigned)(P.Np / BN));
+    const int tok = prof_begin("slice_gemm", st);
     slice_gemm_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, P);
+    prof_end(tok, st);
     count_launch();
     return cuda_check(cudaGetLastError(), "slice_gemm launch");
 }

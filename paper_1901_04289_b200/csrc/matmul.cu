@@ -1,15 +1,631 @@
-// matmul.cu - ball matrix multiplication driver (src/matmul.cpp:442-548).
-// Classical path: one batched dot launch over all (i,j) (src/matmul.cpp:442-451).
+// matmul.cu - ball matrix multiplication on the B200 (reference src/matmul.cpp,
+// paths relative to /root/reference/proj).
+//
+//   matmul_auto / block / classical driver        src/matmul.cpp:442-531
+//   K3  scan + plan: entry_precision, per-row / per-column bit windows, the
+//       single-block test and the device greedy split    :47-52, 74-161
+//   K4  scale_pack: scaled integers mid * 2^(e_i) -> balanced int8 digits in
+//       slice-major, K-contiguous planes for TMA          :163-203, bigint.cpp:178-185
+//   K5  slice_gemm (int8_gemm.cu): exact integer product on tcgen05
+//   K6  recombine: bytes + carries -> exact integer -> * 2^(-e_i-f_j) -> ball_add
+//       into C (a single block is one apfloat_round)      :476-496, bigint.cpp:187-191
+//   K7  radius: |A| R_B + R_A (|B| + R_B) as scaled binary64 sums in the
+//       reference's exact order (RN, no FMA, 1024-term chunks, (1+2^-29)
+//       inflation), so the radius is bit-identical        :368-438, 498-513
+//   K8  complex: four real products + ball add/sub       :533-548
+//
+// Host synchronisation: one small device->host read after the scan (the plan
+// decides slice counts and block structure, as the reference's planner does).
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
 #include <cuda_runtime.h>
 
 #include "apb.h"
+#include "apb_common.cuh"
 #include "apb_internal.h"
+#include "int8_gemm.h"
 
 namespace apb {
 
 apb_matmul_stats& stats();
 
-static int classical(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, cudaStream_t st) {
+namespace {
+
+struct ScanSummary {
+    int special_a, special_b;
+    long long prec_a, prec_b;   // entry_precision
+    long long maxw_a, maxw_b;   // max row / column window width over the scanned range
+};
+
+// bit width of a finite nonzero midpoint stored in L top-aligned slots
+APB_DEV int64_t slot_bitwidth(const uint64_t* m, int L) {
+    int z = 0;
+    while (z < L - 1 && m[z] == 0) z++;
+    return 64 * (int64_t)L - (64 * (int64_t)z + (int64_t)ctz64(m[z]));
+}
+
+APB_DEV bool ball_special(const BallsView& a, int64_t e) {
+    const int k = a.kind[e] & APB_KIND_MASK;
+    return (k != APB_ZERO && k != APB_FINITE) || a.rad_man[e] == APB_RAD_INF;
+}
+
+// window (top, bottom) of a finite nonzero midpoint (ball_window, src/matmul.cpp:116-121)
+APB_DEV bool mid_window(const BallsView& a, int64_t e, int64_t& top, int64_t& bot) {
+    if ((a.kind[e] & APB_KIND_MASK) != APB_FINITE) return false;
+    top = a.exp[e];
+    bot = top - slot_bitwidth(a.mant + e * (int64_t)a.L, a.L);
+    return true;
+}
+
+// ---------------------------------------------------------------- K3 scan
+
+// warp per row of A: window over columns [lo,hi), specials, entry precision
+__global__ void scan_rows_kernel(BallsView A, int64_t M, int64_t K, int64_t lo, int64_t hi,
+                                 int64_t* rtop, int64_t* rbot, ScanSummary* sum) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= M) return;
+    int64_t top = INT64_MIN, bot = INT64_MAX, prec = 0;
+    int special = 0;
+    for (int64_t k = lo + lane; k < hi; k += 32) {
+        const int64_t e = i * K + k;
+        special |= ball_special(A, e);
+        int64_t t, b;
+        if (mid_window(A, e, t, b)) {
+            top = t > top ? t : top;
+            bot = b < bot ? b : bot;
+            prec = (t - b) > prec ? (t - b) : prec;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        int64_t t2 = __shfl_xor_sync(0xffffffffu, top, o);
+        int64_t b2 = __shfl_xor_sync(0xffffffffu, bot, o);
+        int64_t p2 = __shfl_xor_sync(0xffffffffu, prec, o);
+        top = t2 > top ? t2 : top;
+        bot = b2 < bot ? b2 : bot;
+        prec = p2 > prec ? p2 : prec;
+    }
+    special = __any_sync(0xffffffffu, special);
+    if (lane == 0) {
+        rtop[i] = top;
+        rbot[i] = bot;
+        if (special) atomicOr(&sum->special_a, 1);
+        atomicMax(&sum->prec_a, (long long)prec);
+        if (top != INT64_MIN) atomicMax(&sum->maxw_a, (long long)(top - bot));
+    }
+}
+
+// thread per column of B: window over rows [lo,hi)
+__global__ void scan_cols_kernel(BallsView B, int64_t K, int64_t N, int64_t lo, int64_t hi,
+                                 int64_t* ctop, int64_t* cbot, ScanSummary* sum) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    int64_t top = INT64_MIN, bot = INT64_MAX, prec = 0;
+    int special = 0;
+    for (int64_t k = lo; k < hi; k++) {
+        const int64_t e = k * N + j;
+        special |= ball_special(B, e);
+        int64_t t, b;
+        if (mid_window(B, e, t, b)) {
+            top = t > top ? t : top;
+            bot = b < bot ? b : bot;
+            prec = (t - b) > prec ? (t - b) : prec;
+        }
+    }
+    ctop[j] = top;
+    cbot[j] = bot;
+    if (special) atomicOr(&sum->special_b, 1);
+    atomicMax(&sum->prec_b, (long long)prec);
+    if (top != INT64_MIN) atomicMax(&sum->maxw_b, (long long)(top - bot));
+}
+
+// ----------------------------------------------------- K3 greedy (device)
+// greedy_split (src/matmul.cpp:74-114) over per-entry windows wA[i*K+k],
+// wB[j*K+k] (top == INT64_MIN marks an empty entry); one CTA, sequential in k.
+__global__ void greedy_kernel(const longlong2* wA, const longlong2* wB, int64_t K, int64_t M,
+                              int64_t N, int64_t h, int64_t* out, int* nout) {
+    extern __shared__ longlong2 win[];  // M rows then N cols: (top, bot)
+    __shared__ int s_ok;
+    const int64_t R = M + N;
+    for (int64_t r = threadIdx.x; r < R; r += blockDim.x) win[r] = make_longlong2(INT64_MIN, INT64_MAX);
+    int64_t lo = 0, k = 0;
+    int cnt = 0;
+    __syncthreads();
+    while (lo < K) {
+        if (threadIdx.x == 0) s_ok = 1;
+        __syncthreads();
+        if (k != lo) {
+            bool ok = true;
+            for (int64_t r = threadIdx.x; r < R && ok; r += blockDim.x) {
+                longlong2 e = r < M ? wA[r * K + k] : wB[(r - M) * K + k];
+                if (e.x == INT64_MIN) continue;
+                longlong2 w = win[r];
+                int64_t wd = w.x == INT64_MIN ? e.x - e.y : max(w.x, e.x) - min(w.y, e.y);
+                if (wd > h) ok = false;
+            }
+            if (!ok) s_ok = 0;
+        }
+        __syncthreads();
+        const bool ok = s_ok != 0;
+        if (ok) {
+            for (int64_t r = threadIdx.x; r < R; r += blockDim.x) {
+                longlong2 e = r < M ? wA[r * K + k] : wB[(r - M) * K + k];
+                if (e.x == INT64_MIN) continue;
+                longlong2 w = win[r];
+                win[r] = w.x == INT64_MIN ? e : make_longlong2(max(w.x, e.x), min(w.y, e.y));
+            }
+            if (++k == K) {
+                if (threadIdx.x == 0) {
+                    out[2 * cnt] = lo;
+                    out[2 * cnt + 1] = k;
+                }
+                cnt++;
+                lo = k;
+            }
+        } else {
+            if (threadIdx.x == 0) {
+                out[2 * cnt] = lo;
+                out[2 * cnt + 1] = k;
+            }
+            cnt++;
+            lo = k;
+            for (int64_t r = threadIdx.x; r < R; r += blockDim.x) win[r] = make_longlong2(INT64_MIN, INT64_MAX);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *nout = cnt;
+}
+
+// per-entry midpoint windows, transposed to [row][k] / [col][k]
+__global__ void entry_windows_kernel(BallsView A, BallsView B, int64_t M, int64_t K, int64_t N,
+                                     longlong2* wA, longlong2* wB) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < M * K) {
+        int64_t tp, bt;
+        wA[t] = mid_window(A, t, tp, bt) ? make_longlong2(tp, bt) : make_longlong2(INT64_MIN, INT64_MAX);
+    } else if (t < M * K + K * N) {
+        const int64_t u = t - M * K;  // u = j*K + k
+        const int64_t j = u / K, k = u % K;
+        int64_t tp, bt;
+        wB[u] = mid_window(B, k * N + j, tp, bt) ? make_longlong2(tp, bt) : make_longlong2(INT64_MIN, INT64_MAX);
+    }
+}
+
+// ------------------------------------------------------------- K4 pack
+// bits [pos, pos+8) of the L-slot mantissa integer (0 outside)
+APB_DEV uint32_t get8(const uint64_t* m, int L, int64_t pos) {
+    if (pos >= 64 * (int64_t)L || pos <= -8) return 0;
+    uint32_t r;
+    if (pos < 0) {
+        r = (uint32_t)(m[0] << (-pos)) & 255u;
+    } else {
+        const int li = (int)(pos >> 6);
+        const int bo = (int)(pos & 63);
+        uint64_t v = m[li] >> bo;
+        if (bo > 56 && li + 1 < L) v |= m[li + 1] << (64 - bo);
+        r = (uint32_t)v & 255u;
+    }
+    return r;
+}
+
+// Balanced signed-digit slices of x * 2^scale (exact integer, |.| < 2^(8S-2)):
+// out[s * plane + off] for s < S.  Zero / out-of-range entries give zero digits.
+APB_DEV void write_digits(const BallsView& X, int64_t e, bool valid, int64_t scale, int S,
+                          int8_t* out, size_t plane, size_t off) {
+    int kind = valid ? (X.kind[e] & APB_KIND_MASK) : APB_ZERO;
+    if (kind != APB_FINITE) {
+        for (int s = 0; s < S; s++) out[(size_t)s * plane + off] = 0;
+        return;
+    }
+    const bool neg = (X.kind[e] & APB_SIGN) != 0;
+    const uint64_t* m = X.mant + e * (int64_t)X.L;
+    // value = X_L * 2^sh,  X_L the L-slot integer
+    const int64_t sh = X.exp[e] - 64 * (int64_t)X.L + scale;
+    uint32_t negc = 1, rc = 0;
+    for (int s = 0; s < S; s++) {
+        uint32_t byte = get8(m, X.L, 8 * (int64_t)s - sh);
+        if (neg) {  // two's complement negation, byte-serial
+            uint32_t t = (255u - byte) + negc;
+            byte = t & 255u;
+            negc = t >> 8;
+        }
+        uint32_t v = byte + rc;  // balanced recoding
+        int d;
+        if (v >= 128) {
+            d = (int)v - 256;
+            rc = 1;
+        } else {
+            d = (int)v;
+            rc = 0;
+        }
+        out[(size_t)s * plane + off] = (int8_t)d;
+    }
+}
+
+// A block [lo,hi): Apack[s][i][kk] = digit s of A[i][lo+kk] * 2^(e_i); kk < Kp
+__global__ void pack_a_kernel(BallsView A, int64_t M, int64_t K, int64_t lo, int64_t hi,
+                              const int64_t* rtop, const int64_t* rbot, int S, int Mp, int Kp,
+                              int8_t* out, int64_t* escale) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)Mp * Kp) return;
+    const int64_t i = t / Kp, kk = t % Kp;
+    const bool valid = i < M && kk < hi - lo;
+    int64_t sc = 0;
+    if (i < M) sc = rtop[i] == INT64_MIN ? 0 : -rbot[i];
+    if (valid && kk == 0) escale[i] = sc;
+    write_digits(A, valid ? i * K + lo + kk : 0, valid, sc, S, out, (size_t)Mp * Kp, (size_t)t);
+}
+
+// B block rows [lo,hi): Bpack[t][j][kk] = digit t of B[lo+kk][j] * 2^(f_j)
+__global__ void pack_b_kernel(BallsView B, int64_t K, int64_t N, int64_t lo, int64_t hi,
+                              const int64_t* ctop, const int64_t* cbot, int S, int Np, int Kp,
+                              int8_t* out, int64_t* fscale) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)Np * Kp) return;
+    const int64_t j = t / Kp, kk = t % Kp;
+    const bool valid = j < N && kk < hi - lo;
+    int64_t sc = 0;
+    if (j < N) sc = ctop[j] == INT64_MIN ? 0 : -cbot[j];
+    if (valid && kk == 0) fscale[j] = sc;
+    write_digits(B, valid ? (lo + kk) * N + j : 0, valid, sc, S, out, (size_t)Np * Kp, (size_t)t);
+}
+
+// -------------------------------------------------------- K6 recombine
+struct RecombineArgs {
+    const uint32_t* Tw;
+    const int32_t* Tc;
+    const int* group_d1;
+    int n_groups, nwords;
+    int Mp, Np;
+    int64_t M, N;
+    const int64_t* escale;
+    const int64_t* fscale;
+    BallsOut C;
+    int first;  // C is still all-zero (single block or first scaled block)
+    int64_t prec;
+    int64_t* int_out;  // optional: exact integer limbs (two's complement), int_limbs per entry
+    int int_limbs;
+    int* status;
+};
+
+__global__ void __launch_bounds__(128) recombine_kernel(RecombineArgs R) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= R.M * R.N) return;
+    const int64_t i = t / R.N, j = t % R.N;
+    const size_t plane = (size_t)R.Mp * R.Np;
+    const size_t off = (size_t)i * R.Np + j;
+    // T = (bytes as unsigned) + sum_g carry_g * 256^(d1_g), two's complement in NT limbs
+    const int NT = (R.nwords + 1) / 2 + 2;
+    uint64_t T[GCAP];
+    for (int q = 0; q < NT; q++) T[q] = 0;
+    for (int w = 0; w < R.nwords; w++) T[w >> 1] |= (uint64_t)R.Tw[(size_t)w * plane + off] << (32 * (w & 1));
+    for (int g = 0; g < R.n_groups; g++) {
+        const int64_t c = R.Tc[(size_t)g * plane + off];
+        if (c == 0) continue;
+        const int64_t bit = 8 * (int64_t)R.group_d1[g];
+        const int li = (int)(bit >> 6), bo = (int)(bit & 63);
+        // add c << bit, sign-extended
+        const uint64_t ext = c < 0 ? ~0ull : 0ull;
+        uint64_t lo = (uint64_t)c << bo;
+        uint64_t hi = bo ? (((uint64_t)c >> (64 - bo)) | (ext << bo)) : ext;
+        uint64_t cy = 0;
+        for (int q = li; q < NT; q++) {
+            uint64_t add = q == li ? lo : (q == li + 1 ? hi : ext);
+            uint64_t s1 = T[q] + add;
+            uint64_t c1 = s1 < add;
+            uint64_t s2 = s1 + cy;
+            cy = c1 | (s2 < cy);
+            T[q] = s2;
+        }
+    }
+    if (R.int_out)
+        for (int q = 0; q < R.int_limbs; q++)
+            R.int_out[t * R.int_limbs + q] = (int64_t)(q < NT ? T[q] : ((T[NT - 1] >> 63) ? ~0ull : 0ull));
+    if (!R.C.mant) return;
+    const bool neg = (T[NT - 1] >> 63) != 0;
+    if (neg) {
+        uint64_t c = 1;
+        for (int q = 0; q < NT; q++) {
+            uint64_t v = ~T[q] + c;
+            c = (c && v == 0);
+            T[q] = v;
+        }
+    }
+    bool zero = true;
+    for (int q = 0; q < NT; q++) zero &= T[q] == 0;
+    if (zero) {
+        if (R.first) {  // untouched C entry stays an exact zero
+            GFloat<1> z;
+            z.kind = APB_ZERO;
+            z.neg = 0;
+            z.e = 0;
+            z.n = 0;
+            gf_store(R.C, t, z, mag_zero(), R.status);
+        }
+        return;
+    }
+    // apfloat_from_bigint_scaled(v, -e_i - f_j) (src/bigint.cpp:187-191)
+    GF v;
+    const int64_t exp2 = -R.escale[i] - R.fscale[j];
+    gf_normalize(v, neg ? 1 : 0, checked_add(64 * (int64_t)NT, exp2, R.status), T, NT, R.status);
+    if (R.first) {
+        Mag err = gf_round(v, R.prec, R.status);  // ball_add(0, v): apfloat_round
+        gf_store(R.C, t, v, err, R.status);
+    } else {
+        GF c;
+        BallsView cv{R.C.mant, R.C.exp, R.C.kind, R.C.rad_man, R.C.rad_exp, R.C.L};
+        gf_load(c, cv, t);
+        Mag crad = mag_load(R.C.rad_man[t], R.C.rad_exp[t]);
+        Mag err = gf_add_round(c, c, v, R.prec, R.status);  // ball_add (src/ball.cpp:15-19)
+        if (c.kind == APB_NAN) {
+            gf_store(R.C, t, c, mag_inf(), R.status);
+        } else {
+            gf_store(R.C, t, c, mag_add(crad, err), R.status);
+        }
+    }
+}
+
+// ------------------------------------------------------------ K7 radius
+// Mag planes of the four radius operands (src/matmul.cpp:498-509)
+APB_DEV Mag mid_upper(const BallsView& a, int64_t e) {
+    if ((a.kind[e] & APB_KIND_MASK) != APB_FINITE) return mag_zero();
+    return mag_parts((a.mant[e * (int64_t)a.L + a.L - 1] >> 34) + 1, a.exp[e]);
+}
+
+// which: 0 |A|, 1 R_A, 2 R_B, 3 |B| + R_B
+APB_DEV Mag rad_operand(const BallsView& X, int64_t e, int which) {
+    switch (which) {
+        case 0: return mid_upper(X, e);
+        case 1:
+        case 2: return mag_load(X.rad_man[e], X.rad_exp[e]);
+        default: return mag_add(mid_upper(X, e), mag_load(X.rad_man[e], X.rad_exp[e]));
+    }
+}
+
+// per-entry Mag windows (mag_window, src/matmul.cpp:123-128) of the radius
+// operands, transposed to [row][l] / [col][l] for the greedy split
+__global__ void mag_entry_windows_kernel(BallsView A, BallsView B, int64_t M, int64_t K, int64_t N,
+                                         int wa, int wb, longlong2* wA, longlong2* wB) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < M * K) {
+        Mag m = rad_operand(A, t, wa);
+        wA[t] = m.kind == 1 ? make_longlong2(m.f, m.f - 30) : make_longlong2(INT64_MIN, INT64_MAX);
+    } else if (t < M * K + K * N) {
+        const int64_t u = t - M * K;
+        const int64_t j = u / K, l = u % K;
+        Mag m = rad_operand(B, l * N + j, wb);
+        wB[u] = m.kind == 1 ? make_longlong2(m.f, m.f - 30) : make_longlong2(INT64_MIN, INT64_MAX);
+    }
+}
+
+// per-row (A side) or per-column (B side) Mag windows over l in [lo,hi)
+// -> centring exponent -((top+bot)/2) (src/matmul.cpp:397-411)
+__global__ void rad_center_rows_kernel(BallsView A, int64_t M, int64_t K, int64_t lo, int64_t hi,
+                                       int which, int64_t* ecen, long long* maxw) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= M) return;
+    int64_t top = INT64_MIN, bot = INT64_MAX;
+    for (int64_t l = lo + lane; l < hi; l += 32) {
+        Mag m = rad_operand(A, i * K + l, which);
+        if (m.kind != 1) continue;
+        top = m.f > top ? m.f : top;
+        bot = (m.f - 30) < bot ? (m.f - 30) : bot;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        int64_t t2 = __shfl_xor_sync(0xffffffffu, top, o);
+        int64_t b2 = __shfl_xor_sync(0xffffffffu, bot, o);
+        top = t2 > top ? t2 : top;
+        bot = b2 < bot ? b2 : bot;
+    }
+    if (lane == 0) {
+        ecen[i] = top == INT64_MIN ? 0 : -((top + bot) / 2);
+        if (maxw && top != INT64_MIN) atomicMax(maxw, (long long)(top - bot));
+    }
+}
+
+__global__ void rad_center_cols_kernel(BallsView B, int64_t K, int64_t N, int64_t lo, int64_t hi,
+                                       int which, int64_t* fcen, long long* maxw) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    int64_t top = INT64_MIN, bot = INT64_MAX;
+    for (int64_t l = lo; l < hi; l++) {
+        Mag m = rad_operand(B, l * N + j, which);
+        if (m.kind != 1) continue;
+        top = m.f > top ? m.f : top;
+        bot = (m.f - 30) < bot ? (m.f - 30) : bot;
+    }
+    fcen[j] = top == INT64_MIN ? 0 : -((top + bot) / 2);
+    if (maxw && top != INT64_MIN) atomicMax(maxw, (long long)(top - bot));
+}
+
+// exact doubles of the centred Mags (mag_ldexp, src/mag.cpp:166-172):
+// A side da[i][l] (row-major, width w), B side db[l][j]
+__global__ void rad_planes_kernel(BallsView X, int64_t rows, int64_t cols, int64_t lo, int64_t hi,
+                                  int which, int a_side, const int64_t* cen, double* out) {
+    const int64_t w = hi - lo;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a_side) {
+        if (t >= rows * w) return;
+        const int64_t i = t / w, l = t % w;
+        Mag m = rad_operand(X, i * cols + lo + l, which);
+        out[t] = m.kind == 0 ? 0.0 : ldexp((double)m.b, (int)(m.f - 30 + cen[i]));
+    } else {
+        if (t >= w * cols) return;
+        const int64_t l = t / cols, j = t % cols;
+        Mag m = rad_operand(X, (lo + l) * cols + j, which);
+        out[t] = m.kind == 0 ? 0.0 : ldexp((double)m.b, (int)(m.f - 30 + cen[j]));
+    }
+}
+
+// rounded-to-nearest sums in the reference's order, 1024-term chunks, then
+// Mag::from_double_upper * (1 + 2^-29) and mag_add_up into r (src/matmul.cpp:423-435).
+// 64x64 output tile per 256 threads, 4x4 per thread, sequential in l per entry.
+constexpr int RT = 64, RK = 16;
+__global__ void __launch_bounds__(256) rad_gemm_kernel(const double* __restrict__ da,
+                                                       const double* __restrict__ db, int64_t M,
+                                                       int64_t N, int64_t w, const int64_t* ecen,
+                                                       const int64_t* fcen, uint32_t* rb, int64_t* rf,
+                                                       int accumulate) {
+    __shared__ double sA[RK][RT + 1];
+    __shared__ double sB[RK][RT];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t i0 = (int64_t)blockIdx.y * RT, j0 = (int64_t)blockIdx.x * RT;
+    double s[4][4];
+    Mag ent[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; r++)
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            s[r][c] = 0.0;
+            ent[r][c] = mag_zero();
+        }
+    const Mag infl = mag_parts((1ull << 29) + 1, 1);
+    for (int64_t l0 = 0; l0 < w; l0 += RK) {
+        for (int q = threadIdx.x; q < RK * RT; q += 256) {
+            const int kk = q / RT, rr = q % RT;
+            const int64_t gi = i0 + rr, gl = l0 + kk;
+            sA[kk][rr] = (gi < M && gl < w) ? da[gi * w + gl] : 0.0;
+            const int64_t gj = j0 + rr;
+            sB[kk][rr] = (gj < N && gl < w) ? db[gl * N + gj] : 0.0;
+        }
+        __syncthreads();
+        const int kmax = (w - l0) < RK ? (int)(w - l0) : RK;
+        for (int kk = 0; kk < kmax; kk++) {
+            double a[4], b[4];
+#pragma unroll
+            for (int r = 0; r < 4; r++) a[r] = sA[kk][ty * 4 + r];
+#pragma unroll
+            for (int c = 0; c < 4; c++) b[c] = sB[kk][tx * 4 + c];
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+#pragma unroll
+                for (int c = 0; c < 4; c++) s[r][c] = __dadd_rn(s[r][c], __dmul_rn(a[r], b[c]));
+            const int64_t l = l0 + kk + 1;
+            if ((l % 1024) == 0 || l == w) {  // chunk boundary
+#pragma unroll
+                for (int r = 0; r < 4; r++)
+#pragma unroll
+                    for (int c = 0; c < 4; c++) {
+                        const int64_t gi = i0 + ty * 4 + r, gj = j0 + tx * 4 + c;
+                        if (s[r][c] != 0.0 && gi < M && gj < N)
+                            ent[r][c] = mag_add(ent[r][c],
+                                                mag_mul(mag_from_double(s[r][c], -ecen[gi] - fcen[gj]), infl));
+                        s[r][c] = 0.0;
+                    }
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < 4; r++)
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            const int64_t gi = i0 + ty * 4 + r, gj = j0 + tx * 4 + c;
+            if (gi >= M || gj >= N) continue;
+            const int64_t o = gi * N + gj;
+            Mag m = ent[r][c];
+            if (accumulate) {
+                if (m.kind == 0) continue;
+                m = mag_add(mag_load(rb[o], rf[o]), m);
+            }
+            mag_store(m, &rb[o], &rf[o]);
+        }
+}
+
+// C.rad = mag_add(C.rad, mag_add(r1, r2)) (src/matmul.cpp:512-513)
+__global__ void rad_combine_kernel(BallsOut C, int64_t cnt, const uint32_t* r1b, const int64_t* r1f,
+                                   const uint32_t* r2b, const int64_t* r2f) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= cnt) return;
+    Mag r = mag_add(mag_load(r1b[t], r1f[t]), mag_load(r2b[t], r2f[t]));
+    Mag c = mag_load(C.rad_man[t], C.rad_exp[t]);
+    mag_store(mag_add(c, r), &C.rad_man[t], &C.rad_exp[t]);
+}
+
+// Mag-arithmetic path when an operand plane holds inf (src/matmul.cpp:372-385)
+__global__ void rad_mag_path_kernel(BallsView A, BallsView B, int64_t M, int64_t K, int64_t N,
+                                    int wa, int wb, uint32_t* rb, int64_t* rf) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= M * N) return;
+    const int64_t i = t / N, j = t % N;
+    Mag acc = mag_zero();
+    for (int64_t l = 0; l < K; l++) acc = mag_add(acc, mag_mul(rad_operand(A, i * K + l, wa), rad_operand(B, l * N + j, wb)));
+    mag_store(acc, &rb[t], &rf[t]);
+}
+
+// ------------------------------------------------------------ K8 complex
+__global__ void ball_addsub_kernel(BallsView X, BallsView Y, int negate_y, int64_t cnt, int64_t prec,
+                                   BallsOut O, int* status) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= cnt) return;
+    GF a, b;
+    gf_load(a, X, t);
+    gf_load(b, Y, t);
+    if (negate_y) {
+        if (b.kind == APB_FINITE) b.neg = !b.neg;
+        else if (b.kind == APB_PINF) b.kind = APB_NINF;
+        else if (b.kind == APB_NINF) b.kind = APB_PINF;
+    }
+    Mag err = gf_add_round(a, a, b, prec, status);
+    if (a.kind == APB_NAN) {
+        gf_store(O, t, a, mag_inf(), status);
+        return;
+    }
+    Mag r = mag_add(mag_add(mag_load(X.rad_man[t], X.rad_exp[t]), mag_load(Y.rad_man[t], Y.rad_exp[t])), err);
+    gf_store(O, t, a, r, status);
+}
+
+// ----------------------------------------------------------------- host
+
+template <class T>
+T* ws_buf(int slot, size_t count, cudaStream_t st) {
+    return (T*)workspace().scratch(st, count * sizeof(T), slot);
+}
+
+struct Scratch {
+    // separate allocations owned here (the Workspace slot table is small)
+    void* p[24] = {};
+    size_t cap[24] = {};
+    void* get(int k, size_t bytes, cudaStream_t st) {
+        if (cap[k] < bytes) {
+            if (p[k]) {
+                cudaStreamSynchronize(st);
+                cudaFree(p[k]);
+            }
+            size_t c = bytes + bytes / 4 + 256;
+            if (cudaMalloc(&p[k], c) != cudaSuccess) {
+                p[k] = nullptr;
+                cap[k] = 0;
+                return nullptr;
+            }
+            cap[k] = c;
+        }
+        return p[k];
+    }
+};
+Scratch& scratch() {
+    static Scratch s;
+    return s;
+}
+enum {
+    S_RTOP, S_RBOT, S_CTOP, S_CBOT, S_SUM, S_APACK, S_BPACK, S_TW, S_TC, S_UNITS, S_ESC, S_FSC,
+    S_WA, S_WB, S_GREEDY, S_DA, S_DB, S_CEN_E, S_CEN_F, S_R1B, S_R1F, S_R2B, S_R2F, S_MISC
+};
+template <class T>
+T* sbuf(int k, size_t count, cudaStream_t st) {
+    return (T*)scratch().get(k, count * sizeof(T) + 16, st);
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+int classical(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, cudaStream_t st) {
     stats().classical_calls++;
     apb_dot_index ix;
     ix.bdiv = B->cols;
@@ -25,34 +641,509 @@ static int classical(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* 
                             APB_DOT_BALL, nullptr, &C->b, nullptr, nullptr, 0, st);
 }
 
+// basecase block: c_ij = dot_ball(&c_ij, false, A[i, lo:hi], 1, B[lo:hi, j], N, w, p)
+int basecase(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int64_t prec, apb_mat* C,
+             cudaStream_t st) {
+    apb_dot_index ix;
+    ix.bdiv = B->cols;
+    ix.x_off = lo;
+    ix.xs1 = A->cols;
+    ix.xs2 = 0;
+    ix.xstep = 1;
+    ix.y_off = lo * B->cols;
+    ix.ys1 = 0;
+    ix.ys2 = 1;
+    ix.ystep = B->cols;
+    return dot_batch_launch(&A->b, &B->b, &C->b, 0, &ix, hi - lo, A->rows * B->cols, prec,
+                            APB_DOT_BALL, nullptr, &C->b, nullptr, nullptr, 0, st);
+}
+
+struct Plan {
+    std::vector<int64_t> steps;  // triples (lo, hi, basecase)
+    bool special = false;
+    int64_t maxw_a = 0, maxw_b = 0;  // whole-range widths (single block)
+};
+
+int plan(const apb_mat* A, const apb_mat* B, int64_t prec, Plan& P, cudaStream_t st) {
+    const int64_t M = A->rows, K = A->cols, N = B->cols;
+    BallsView a = view_of(&A->b), b = view_of(&B->b);
+    int64_t* rtop = sbuf<int64_t>(S_RTOP, M, st);
+    int64_t* rbot = sbuf<int64_t>(S_RBOT, M, st);
+    int64_t* ctop = sbuf<int64_t>(S_CTOP, N, st);
+    int64_t* cbot = sbuf<int64_t>(S_CBOT, N, st);
+    ScanSummary* sum = sbuf<ScanSummary>(S_SUM, 1, st);
+    if (!rtop || !rbot || !ctop || !cbot || !sum) return APB_ERR_CUDA;
+    cudaMemsetAsync(sum, 0, sizeof(ScanSummary), st);
+    scan_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(a, M, K, 0, K, rtop, rbot, sum);
+    scan_cols_kernel<<<blocks_for(N, 128), 128, 0, st>>>(b, K, N, 0, K, ctop, cbot, sum);
+    count_launch(2);
+    static ScanSummary* hsum = nullptr;
+    if (!hsum) cudaMallocHost(&hsum, sizeof(ScanSummary));
+    cudaMemcpyAsync(hsum, sum, sizeof(ScanSummary), cudaMemcpyDeviceToHost, st);
+    int rc = cuda_check(cudaStreamSynchronize(st), "matmul plan scan");
+    if (rc) return rc;
+    P.special = hsum->special_a || hsum->special_b;
+    if (P.special) return APB_OK;
+    P.maxw_a = hsum->maxw_a;
+    P.maxw_b = hsum->maxw_b;
+    // plan_blocks (src/matmul.cpp:132-161)
+    int64_t pm = std::max<int64_t>(hsum->prec_a, hsum->prec_b);
+    pm = std::min<int64_t>(prec, pm);
+    const int64_t h = (5 * pm) / 4 + 192;
+    std::vector<int64_t> raw;
+    if (hsum->maxw_a <= h && hsum->maxw_b <= h) {
+        raw = {0, K};  // every window fits: greedy takes all of [0,K)
+    } else {
+        longlong2* wA = sbuf<longlong2>(S_WA, (size_t)M * K, st);
+        longlong2* wB = sbuf<longlong2>(S_WB, (size_t)N * K, st);
+        int64_t* gout = sbuf<int64_t>(S_GREEDY, 2 * (size_t)K + 2, st);
+        int* gn = sbuf<int>(S_MISC, 1, st);
+        if (!wA || !wB || !gout || !gn) return APB_ERR_CUDA;
+        entry_windows_kernel<<<blocks_for(M * K + K * N, 256), 256, 0, st>>>(a, b, M, K, N, wA, wB);
+        const size_t shm = (size_t)(M + N) * sizeof(longlong2);
+        if (shm > 200 * 1024) {
+            set_error("matmul planner: M+N too large for the device greedy split");
+            return APB_ERR_UNSUPPORTED;
+        }
+        cudaFuncSetAttribute(greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        greedy_kernel<<<1, 1024, shm, st>>>(wA, wB, K, M, N, h, gout, gn);
+        count_launch(2);
+        int n = 0;
+        cudaMemcpyAsync(&n, gn, sizeof(int), cudaMemcpyDeviceToHost, st);
+        if ((rc = cuda_check(cudaStreamSynchronize(st), "greedy"))) return rc;
+        raw.resize(2 * (size_t)n);
+        cudaMemcpy(raw.data(), gout, sizeof(int64_t) * 2 * n, cudaMemcpyDeviceToHost);
+    }
+    const int64_t nraw = (int64_t)raw.size() / 2;
+    for (int64_t idx = 0; idx < nraw; idx++) {
+        int64_t lo = raw[2 * idx], hi = raw[2 * idx + 1];
+        if (hi - lo < 30) {  // short block -> dot basecase extended to 30 (src/matmul.cpp:149-155)
+            hi = std::min<int64_t>(lo + 30, K);
+            while (idx + 1 < nraw && raw[2 * (idx + 1) + 1] <= hi) idx++;
+            if (idx + 1 < nraw && raw[2 * (idx + 1)] < hi) raw[2 * (idx + 1)] = hi;
+            P.steps.insert(P.steps.end(), {lo, hi, 1});
+        } else {
+            P.steps.insert(P.steps.end(), {lo, hi, 0});
+        }
+    }
+    return APB_OK;
+}
+
+// slice count for an exact |value| < 2^H with balanced digits (headroom 2 bits)
+inline int slices_for(int64_t H) { return (int)((H + 2 + 7) / 8); }
+
+// unit table + diagonal groups for the slice GEMM
+struct Units {
+    std::vector<int4> units;
+    std::vector<int> group_begin, group_d1;
+};
+
+Units make_units(int SA, int SB, int64_t K, int tiles) {
+    Units U;
+    const int ND = SA + SB - 1;
+    const int64_t pmax = std::max<int64_t>(1, 65535 / std::max<int64_t>(K, 1));  // |D| < 2^30
+    std::vector<int64_t> pairs_upto_quad;  // work per 4-diagonal quad
+    const int NQ = (ND + 3) / 4;
+    std::vector<int64_t> quad_work(NQ, 0);
+    for (int d = 0; d < ND; d++) {
+        const int slo = std::max(0, d - SB + 1), shi = std::min(d, SA - 1) + 1;
+        quad_work[d / 4] += shi - slo;
+    }
+    // groups: enough CTAs to fill the 148 SMs, balanced by pair count
+    int64_t total = 0;
+    for (auto w : quad_work) total += w;
+    int G = std::max(1, std::min(NQ, (148 + tiles - 1) / tiles));
+    const int64_t target = (total + G - 1) / G;
+    U.group_begin.push_back(0);
+    int64_t acc = 0;
+    int q = 0;
+    for (int d = 0; d < ND; d++) {
+        const int slo = std::max(0, d - SB + 1), shi = std::min(d, SA - 1) + 1;
+        for (int s = slo; s < shi; s += (int)pmax) {
+            const int e = (int)std::min<int64_t>(shi, s + pmax);
+            int flags = (s == slo ? 1 : 0) | (e == shi ? 2 : 0);
+            U.units.push_back(make_int4(d, s, e, flags));
+        }
+        if ((d & 3) == 3 || d == ND - 1) {
+            acc += quad_work[q++];
+            const bool last = d == ND - 1;
+            if (last || acc >= target * (int64_t)U.group_d1.size() + target) {
+                U.group_d1.push_back(d + 1);
+                U.group_begin.push_back((int)U.units.size());
+            }
+        }
+    }
+    return U;
+}
+
+int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int64_t prec, apb_mat* C,
+                 bool first, int64_t maxw_a, int64_t maxw_b, const int64_t* rtop_in,
+                 const int64_t* rbot_in, const int64_t* ctop_in, const int64_t* cbot_in,
+                 int64_t* int_out, int int_limbs, int64_t* esc_out, int64_t* fsc_out,
+                 cudaStream_t st) {
+    const int64_t M = A->rows, K = A->cols, N = B->cols, w = hi - lo;
+    BallsView a = view_of(&A->b), b = view_of(&B->b);
+    const int64_t* rtop = rtop_in;
+    const int64_t* rbot = rbot_in;
+    const int64_t* ctop = ctop_in;
+    const int64_t* cbot = cbot_in;
+    if (!rtop) {  // windows of this block only
+        int64_t* rt = sbuf<int64_t>(S_RTOP, M, st);
+        int64_t* rb = sbuf<int64_t>(S_RBOT, M, st);
+        int64_t* ct = sbuf<int64_t>(S_CTOP, N, st);
+        int64_t* cb = sbuf<int64_t>(S_CBOT, N, st);
+        ScanSummary* sum = sbuf<ScanSummary>(S_SUM, 1, st);
+        cudaMemsetAsync(sum, 0, sizeof(ScanSummary), st);
+        scan_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(a, M, K, lo, hi, rt, rb, sum);
+        scan_cols_kernel<<<blocks_for(N, 128), 128, 0, st>>>(b, K, N, lo, hi, ct, cb, sum);
+        count_launch(2);
+        ScanSummary h;
+        cudaMemcpyAsync(&h, sum, sizeof h, cudaMemcpyDeviceToHost, st);
+        int rc = cuda_check(cudaStreamSynchronize(st), "block scan");
+        if (rc) return rc;
+        maxw_a = h.maxw_a;
+        maxw_b = h.maxw_b;
+        rtop = rt;
+        rbot = rb;
+        ctop = ct;
+        cbot = cb;
+    }
+    const int SA = slices_for(maxw_a), SB = slices_for(maxw_b);
+    const int Mp = (int)((M + kSliceTile - 1) / kSliceTile * kSliceTile);
+    const int Np = (int)((N + kSliceTile - 1) / kSliceTile * kSliceTile);
+    const int Kp = (int)((w + kSliceBK - 1) / kSliceBK * kSliceBK);
+    stats().int_gemm_products++;
+    stats().last_height_a = (uint64_t)maxw_a;
+    stats().last_height_b = (uint64_t)maxw_b;
+    stats().last_slices_a = (uint64_t)SA;
+    stats().last_slices_b = (uint64_t)SB;
+    int8_t* Ap = sbuf<int8_t>(S_APACK, (size_t)SA * Mp * Kp, st);
+    int8_t* Bp = sbuf<int8_t>(S_BPACK, (size_t)SB * Np * Kp, st);
+    int64_t* esc = esc_out ? esc_out : sbuf<int64_t>(S_ESC, M, st);
+    int64_t* fsc = fsc_out ? fsc_out : sbuf<int64_t>(S_FSC, N, st);
+    if (!Ap || !Bp || !esc || !fsc) {
+        set_error("out of device memory (slice planes)");
+        return APB_ERR_CUDA;
+    }
+    int tok = prof_begin("pack", st);
+    pack_a_kernel<<<blocks_for((int64_t)Mp * Kp, 256), 256, 0, st>>>(a, M, K, lo, hi, rtop, rbot, SA, Mp, Kp, Ap, esc);
+    pack_b_kernel<<<blocks_for((int64_t)Np * Kp, 256), 256, 0, st>>>(b, K, N, lo, hi, ctop, cbot, SB, Np, Kp, Bp, fsc);
+    prof_end(tok, st);
+    count_launch(2);
+    const int tiles = (Mp / kSliceTile) * (Np / kSliceTile);
+    Units U = make_units(SA, SB, w, tiles);
+    const int G = (int)U.group_d1.size();
+    const int ND = SA + SB - 1;
+    const int NW = (ND + 3) / 4;
+    // unit table upload (small; pinned staging)
+    const size_t ubytes = U.units.size() * sizeof(int4) + (U.group_begin.size() + U.group_d1.size()) * sizeof(int);
+    static char* hstage = nullptr;
+    static size_t hcap = 0;
+    if (hcap < ubytes) {
+        if (hstage) {
+            cudaStreamSynchronize(st);
+            cudaFreeHost(hstage);
+        }
+        cudaMallocHost(&hstage, ubytes * 2);
+        hcap = ubytes * 2;
+    } else {
+        cudaStreamSynchronize(st);  // previous upload finished before reuse
+    }
+    std::memcpy(hstage, U.units.data(), U.units.size() * sizeof(int4));
+    std::memcpy(hstage + U.units.size() * sizeof(int4), U.group_begin.data(), U.group_begin.size() * sizeof(int));
+    std::memcpy(hstage + U.units.size() * sizeof(int4) + U.group_begin.size() * sizeof(int), U.group_d1.data(),
+                U.group_d1.size() * sizeof(int));
+    char* dunits = sbuf<char>(S_UNITS, ubytes, st);
+    uint32_t* Tw = sbuf<uint32_t>(S_TW, (size_t)NW * Mp * Np, st);
+    int32_t* Tc = sbuf<int32_t>(S_TC, (size_t)G * Mp * Np, st);
+    if (!dunits || !Tw || !Tc) {
+        set_error("out of device memory (product planes)");
+        return APB_ERR_CUDA;
+    }
+    cudaMemcpyAsync(dunits, hstage, ubytes, cudaMemcpyHostToDevice, st);
+    SliceGemmParams P;
+    P.S_A = SA;
+    P.S_B = SB;
+    P.Mp = Mp;
+    P.Np = Np;
+    P.Kp = Kp;
+    P.n_kb = Kp / kSliceBK;
+    P.units = (const int4*)dunits;
+    P.group_unit_begin = (const int*)(dunits + U.units.size() * sizeof(int4));
+    P.group_d1 = P.group_unit_begin + U.group_begin.size();
+    P.Tw = Tw;
+    P.Tc = Tc;
+    int rc = slice_gemm_launch(Ap, Bp, P, G, st);
+    if (rc) return rc;
+    RecombineArgs R;
+    R.Tw = Tw;
+    R.Tc = Tc;
+    R.group_d1 = P.group_d1;
+    R.n_groups = G;
+    R.nwords = NW;
+    R.Mp = Mp;
+    R.Np = Np;
+    R.M = M;
+    R.N = N;
+    R.escale = esc;
+    R.fscale = fsc;
+    if (C) {
+        R.C = out_of(&C->b);
+    } else {
+        std::memset(&R.C, 0, sizeof R.C);
+    }
+    R.first = first ? 1 : 0;
+    R.prec = prec;
+    R.int_out = int_out;
+    R.int_limbs = int_limbs;
+    R.status = workspace().status_dev;
+    tok = prof_begin("recombine", st);
+    recombine_kernel<<<blocks_for(M * N, 128), 128, 0, st>>>(R);
+    prof_end(tok, st);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "recombine");
+}
+
+// radius_matmul_upper(P, Q) into (rb, rf) for operand kinds (wa of A, wb of B)
+int radius_product(const apb_mat* A, const apb_mat* B, int wa, int wb, uint32_t* rb, int64_t* rf,
+                   cudaStream_t st) {
+    const int64_t M = A->rows, K = A->cols, N = B->cols;
+    BallsView a = view_of(&A->b), b = view_of(&B->b);
+    int64_t* ecen = sbuf<int64_t>(S_CEN_E, M, st);
+    int64_t* fcen = sbuf<int64_t>(S_CEN_F, N, st);
+    long long* mw = sbuf<long long>(S_SUM, 2, st);
+    cudaMemsetAsync(mw, 0, 2 * sizeof(long long), st);
+    rad_center_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(a, M, K, 0, K, wa, ecen, mw);
+    rad_center_cols_kernel<<<blocks_for(N, 128), 128, 0, st>>>(b, K, N, 0, K, wb, fcen, mw + 1);
+    count_launch(2);
+    long long hw[2];
+    cudaMemcpyAsync(hw, mw, sizeof hw, cudaMemcpyDeviceToHost, st);
+    int rc = cuda_check(cudaStreamSynchronize(st), "radius windows");
+    if (rc) return rc;
+    std::vector<int64_t> blocks = {0, K};
+    if (hw[0] > 900 || hw[1] > 900) {
+        // greedy split with h = 900 on the Mag windows (f, f-30) (src/matmul.cpp:386-392)
+        longlong2* wA = sbuf<longlong2>(S_WA, (size_t)M * K, st);
+        longlong2* wB = sbuf<longlong2>(S_WB, (size_t)N * K, st);
+        int64_t* gout = sbuf<int64_t>(S_GREEDY, 2 * (size_t)K + 2, st);
+        int* gn = sbuf<int>(S_MISC, 1, st);
+        if (!wA || !wB || !gout || !gn) return APB_ERR_CUDA;
+        mag_entry_windows_kernel<<<blocks_for(M * K + K * N, 256), 256, 0, st>>>(a, b, M, K, N, wa, wb, wA, wB);
+        const size_t shm = (size_t)(M + N) * sizeof(longlong2);
+        if (shm > 200 * 1024) {
+            set_error("radius product: M+N too large for the device greedy split");
+            return APB_ERR_UNSUPPORTED;
+        }
+        cudaFuncSetAttribute(greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        greedy_kernel<<<1, 1024, shm, st>>>(wA, wB, K, M, N, 900, gout, gn);
+        count_launch(2);
+        int n = 0;
+        cudaMemcpyAsync(&n, gn, sizeof(int), cudaMemcpyDeviceToHost, st);
+        if ((rc = cuda_check(cudaStreamSynchronize(st), "radius greedy"))) return rc;
+        blocks.resize(2 * (size_t)n);
+        cudaMemcpy(blocks.data(), gout, sizeof(int64_t) * 2 * n, cudaMemcpyDeviceToHost);
+    }
+    for (size_t bi = 0; bi + 1 < blocks.size(); bi += 2) {
+        const int64_t lo = blocks[bi], hi = blocks[bi + 1], w = hi - lo;
+        if (blocks.size() > 2) {  // centring over this block only
+            rad_center_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(a, M, K, lo, hi, wa, ecen, nullptr);
+            rad_center_cols_kernel<<<blocks_for(N, 128), 128, 0, st>>>(b, K, N, lo, hi, wb, fcen, nullptr);
+            count_launch(2);
+        }
+        double* da = sbuf<double>(S_DA, (size_t)M * w, st);
+        double* db = sbuf<double>(S_DB, (size_t)w * N, st);
+        if (!da || !db) return APB_ERR_CUDA;
+        rad_planes_kernel<<<blocks_for(M * w, 256), 256, 0, st>>>(a, M, K, lo, hi, wa, 1, ecen, da);
+        rad_planes_kernel<<<blocks_for(w * N, 256), 256, 0, st>>>(b, K, N, lo, hi, wb, 0, fcen, db);
+        dim3 grid(blocks_for(N, RT), blocks_for(M, RT));
+        const int tk = prof_begin("rad_gemm", st);
+        rad_gemm_kernel<<<grid, 256, 0, st>>>(da, db, M, N, w, ecen, fcen, rb, rf, bi ? 1 : 0);
+        prof_end(tk, st);
+        count_launch(3);
+    }
+    return cuda_check(cudaGetLastError(), "radius product");
+}
+
+int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, cudaStream_t st) {
+    Plan P;
+    int rc = plan(A, B, prec, P, st);
+    if (rc) return rc;
+    if (P.special) return classical(A, B, prec, C, st);  // src/matmul.cpp:455-458
+    stats().block_calls++;
+    stats().last_block_count = P.steps.size() / 3;
+    const int64_t M = A->rows, N = B->cols;
+    bool first = true;
+    const bool single = P.steps.size() == 3 && P.steps[0] == 0 && P.steps[1] == A->cols;
+    for (size_t s = 0; s < P.steps.size(); s += 3) {
+        const int64_t lo = P.steps[s], hi = P.steps[s + 1];
+        if (P.steps[s + 2]) {
+            if (first) {  // C starts as exact zeros
+                cudaMemsetAsync(C->b.kind, 0, (size_t)M * N, st);
+                cudaMemsetAsync(C->b.rad_man, 0, (size_t)M * N * 4, st);
+                cudaMemsetAsync(C->b.exp, 0, (size_t)M * N * 8, st);
+                cudaMemsetAsync(C->b.rad_exp, 0, (size_t)M * N * 8, st);
+                cudaMemsetAsync(C->b.mant, 0, (size_t)M * N * 8 * C->b.L, st);
+            }
+            if ((rc = basecase(A, B, lo, hi, prec, C, st))) return rc;
+        } else {
+            if (single) {
+                rc = scaled_block(A, B, lo, hi, prec, C, first, P.maxw_a, P.maxw_b,
+                                  sbuf<int64_t>(S_RTOP, M, st), sbuf<int64_t>(S_RBOT, M, st),
+                                  sbuf<int64_t>(S_CTOP, N, st), sbuf<int64_t>(S_CBOT, N, st), nullptr, 0,
+                                  nullptr, nullptr, st);
+            } else {
+                rc = scaled_block(A, B, lo, hi, prec, C, first, 0, 0, nullptr, nullptr, nullptr, nullptr,
+                                  nullptr, 0, nullptr, nullptr, st);
+            }
+            if (rc) return rc;
+        }
+        first = false;
+    }
+    // R_C += |A| R_B + R_A (|B| + R_B)
+    uint32_t* r1b = sbuf<uint32_t>(S_R1B, (size_t)M * N, st);
+    int64_t* r1f = sbuf<int64_t>(S_R1F, (size_t)M * N, st);
+    uint32_t* r2b = sbuf<uint32_t>(S_R2B, (size_t)M * N, st);
+    int64_t* r2f = sbuf<int64_t>(S_R2F, (size_t)M * N, st);
+    if (!r1b || !r1f || !r2b || !r2f) return APB_ERR_CUDA;
+    if ((rc = radius_product(A, B, 0, 2, r1b, r1f, st))) return rc;
+    if ((rc = radius_product(A, B, 1, 3, r2b, r2f, st))) return rc;
+    rad_combine_kernel<<<blocks_for(M * N, 256), 256, 0, st>>>(out_of(&C->b), M * N, r1b, r1f, r2b, r2f);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "block matmul");
+}
+
+}  // namespace
+
 int matmul_launch(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, apb_mat* C,
                   cudaStream_t st) {
     if (A->rows * B->cols == 0) return APB_OK;
     if (A->cols == 0 || algo == APB_MM_CLASSICAL) return classical(A, B, prec, C, st);
-    set_error("block matmul not built yet");
-    return APB_ERR_UNSUPPORTED;
+    if (algo == APB_MM_AUTO) {  // matmul_dispatch_cutoff (src/matmul.cpp:517-531)
+        int64_t cut = prec <= 64 ? 60 : prec <= 128 ? 56 : prec <= 256 ? 52 : prec <= 512 ? 48 : prec <= 1024 ? 44 : 40;
+        int64_t mind = std::min(A->rows, std::min(A->cols, B->cols));
+        if (mind <= cut) return classical(A, B, prec, C, st);
+    }
+    return block_matmul(A, B, prec, C, st);
 }
 
 }  // namespace apb
 
+using namespace apb;
+
 extern "C" {
-int apb_matmul_complex(const apb_mat*, const apb_mat*, const apb_mat*, const apb_mat*, int64_t, int,
-                       apb_mat*, apb_mat*, void*) {
-    apb::set_error("complex matmul not built yet");
-    return APB_ERR_UNSUPPORTED;
+
+int apb_matmul_complex(const apb_mat* Are, const apb_mat* Aim, const apb_mat* Bre, const apb_mat* Bim,
+                       int64_t prec, int algo, apb_mat* Cre, apb_mat* Cim, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!Are || !Aim || !Bre || !Bim || !Cre || !Cim || Are->cols != Bre->rows || Aim->cols != Bim->rows ||
+        Are->rows != Aim->rows || Bre->cols != Bim->cols) {
+        set_error("matmul: dimension mismatch");
+        return APB_ERR_INVALID;
+    }
+    if (prec < 2) prec = 2;
+    const int64_t M = Are->rows, N = Bre->cols;
+    const int L = (int)((prec + 63) / 64);
+    // four real products, each rounded to prec (src/matmul.cpp:538-541)
+    static std::vector<void*> bufs(20, nullptr);
+    static std::vector<size_t> caps(20, 0);
+    auto get = [&](int k, size_t bytes) -> void* {
+        if (caps[k] < bytes) {
+            if (bufs[k]) {
+                cudaStreamSynchronize(st);
+                cudaFree(bufs[k]);
+            }
+            if (cudaMalloc(&bufs[k], bytes) != cudaSuccess) return nullptr;
+            caps[k] = bytes;
+        }
+        return bufs[k];
+    };
+    apb_mat P4[4];
+    for (int q = 0; q < 4; q++) {
+        apb_balls& b = P4[q].b;
+        b.count = M * N;
+        b.L = L;
+        b.mant = (uint64_t*)get(5 * q, (size_t)M * N * L * 8);
+        b.exp = (int64_t*)get(5 * q + 1, (size_t)M * N * 8);
+        b.kind = (uint8_t*)get(5 * q + 2, (size_t)M * N);
+        b.rad_man = (uint32_t*)get(5 * q + 3, (size_t)M * N * 4);
+        b.rad_exp = (int64_t*)get(5 * q + 4, (size_t)M * N * 8);
+        if (!b.mant || !b.exp || !b.kind || !b.rad_man || !b.rad_exp) {
+            set_error("out of device memory");
+            return APB_ERR_CUDA;
+        }
+        P4[q].rows = M;
+        P4[q].cols = N;
+    }
+    const apb_mat* lhs[4] = {Are, Aim, Are, Aim};
+    const apb_mat* rhs[4] = {Bre, Bim, Bim, Bre};  // AC, BD, AD, BC
+    for (int q = 0; q < 4; q++) {
+        int rc = matmul_launch(lhs[q], rhs[q], prec, algo, &P4[q], st);
+        if (rc) return rc;
+    }
+    int* status = workspace().status_dev;
+    ball_addsub_kernel<<<blocks_for(M * N, 128), 128, 0, st>>>(view_of(&P4[0].b), view_of(&P4[1].b), 1, M * N,
+                                                               prec, out_of(&Cre->b), status);
+    ball_addsub_kernel<<<blocks_for(M * N, 128), 128, 0, st>>>(view_of(&P4[2].b), view_of(&P4[3].b), 0, M * N,
+                                                               prec, out_of(&Cim->b), status);
+    count_launch(2);
+    return cuda_check(cudaGetLastError(), "complex matmul");
 }
-int apb_block_int_product(const apb_mat*, const apb_mat*, int64_t, int64_t, int64_t*, int64_t*,
-                          uint64_t*, int64_t, void*) {
-    apb::set_error("not built yet");
-    return APB_ERR_UNSUPPORTED;
+
+int apb_block_int_product(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int64_t* row_scale,
+                          int64_t* col_scale, uint64_t* out, int64_t out_limbs, void* stream) {
+    if (!A || !B || A->cols != B->rows || lo < 0 || hi > A->cols || hi <= lo) {
+        set_error("int_matmul: dimension mismatch");
+        return APB_ERR_INVALID;
+    }
+    return scaled_block(A, B, lo, hi, 0, nullptr, true, 0, 0, nullptr, nullptr, nullptr, nullptr,
+                        (int64_t*)out, (int)out_limbs, row_scale, col_scale, (cudaStream_t)stream);
 }
-int apb_plan_blocks(const apb_mat*, const apb_mat*, int64_t, int64_t*, int64_t, int64_t*, void*) {
-    apb::set_error("not built yet");
-    return APB_ERR_UNSUPPORTED;
+
+int apb_plan_blocks(const apb_mat* A, const apb_mat* B, int64_t prec, int64_t* steps_out, int64_t max_steps,
+                    int64_t* n_steps, void* stream) {
+    if (!A || !B || A->cols != B->rows) {
+        set_error("plan_blocks: dimension mismatch");
+        return APB_ERR_INVALID;
+    }
+    Plan P;
+    int rc = plan(A, B, prec, P, (cudaStream_t)stream);
+    if (rc) return rc;
+    *n_steps = (int64_t)P.steps.size() / 3;
+    for (int64_t i = 0; i < *n_steps && i < max_steps; i++)
+        for (int q = 0; q < 3; q++) steps_out[3 * i + q] = P.steps[3 * i + q];
+    return APB_OK;
 }
-int apb_radius_matmul_upper(const uint32_t*, const int64_t*, const uint32_t*, const int64_t*, int64_t,
-                            int64_t, int64_t, uint32_t*, int64_t*, void*) {
-    apb::set_error("not built yet");
-    return APB_ERR_UNSUPPORTED;
+
+int apb_radius_matmul_upper(const uint32_t* p_man, const int64_t* p_exp, const uint32_t* q_man,
+                            const int64_t* q_exp, int64_t m, int64_t n, int64_t k, uint32_t* out_man,
+                            int64_t* out_exp, void* stream) {
+    // P and Q are carried as the radius planes of ball matrices whose
+    // midpoints are never read (operand kinds 1 and 2 of rad_operand)
+    if (!p_man || !p_exp || !q_man || !q_exp || !out_man || !out_exp || m < 0 || n < 0 || k < 0) {
+        set_error("radius_matmul_upper: invalid arguments");
+        return APB_ERR_INVALID;
+    }
+    apb_mat P{}, Q{};
+    static uint64_t dummy_mant;
+    P.b.mant = Q.b.mant = &dummy_mant;
+    P.b.exp = Q.b.exp = (int64_t*)p_exp;
+    P.b.kind = Q.b.kind = (uint8_t*)p_man;
+    P.b.L = Q.b.L = 1;
+    P.b.rad_man = (uint32_t*)p_man;
+    P.b.rad_exp = (int64_t*)p_exp;
+    Q.b.rad_man = (uint32_t*)q_man;
+    Q.b.rad_exp = (int64_t*)q_exp;
+    P.rows = m;
+    P.cols = n;
+    Q.rows = n;
+    Q.cols = k;
+    if (m * k == 0) return APB_OK;
+    if (n == 0) {
+        cudaMemsetAsync(out_man, 0, (size_t)m * k * 4, (cudaStream_t)stream);
+        cudaMemsetAsync(out_exp, 0, (size_t)m * k * 8, (cudaStream_t)stream);
+        return APB_OK;
+    }
+    return radius_product(&P, &Q, 1, 2, out_man, out_exp, (cudaStream_t)stream);
 }
-}
+
+}  // extern "C"

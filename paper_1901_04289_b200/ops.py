@@ -213,3 +213,49 @@ def matmul_stats_reset():
 
 def launch_count() -> int:
     return int(_lib.lib().apb_launch_count())
+
+
+# ------------------------------------------------------------ parity hooks
+
+def plan_blocks(a: BallMatrix, b: BallMatrix, prec: int, stream=None):
+    """plan_blocks (include/apball/matmul.hpp:73): list of (lo, hi, basecase)"""
+    lib = _lib.lib()
+    am, bm = a.c(), b.c()
+    steps = np.zeros(3 * (a.cols + 1), np.int64)
+    ns = C.c_int64(0)
+    _lib.check(lib.apb_plan_blocks(C.byref(am), C.byref(bm), prec, steps.ctypes.data, a.cols + 1,
+                                   C.addressof(ns), _stream_ptr(stream)), "apb_plan_blocks")
+    return [tuple(int(v) for v in steps[3 * i:3 * i + 3]) for i in range(ns.value)]
+
+
+def block_int_product(a: BallMatrix, b: BallMatrix, lo: int, hi: int, out_limbs: int, stream=None):
+    """int_matmul(scale_block_rows(A,lo,hi), scale_block_cols(B,lo,hi)) as two's complement
+    limbs (include/apball/matmul.hpp:77-84); returns (row_scale, col_scale, T)"""
+    import torch
+    lib = _lib.lib()
+    am, bm = a.c(), b.c()
+    rs = torch.zeros(a.rows, dtype=torch.int64, device="cuda")
+    cs = torch.zeros(b.cols, dtype=torch.int64, device="cuda")
+    out = torch.zeros(a.rows * b.cols * out_limbs, dtype=torch.int64, device="cuda")
+    st = _stream_ptr(stream)
+    _lib.check(lib.apb_block_int_product(C.byref(am), C.byref(bm), lo, hi, rs.data_ptr(), cs.data_ptr(),
+                                         out.data_ptr(), out_limbs, st), "apb_block_int_product")
+    _lib.check(lib.apb_device_status(st), "apb_block_int_product")
+    return (rs.cpu().numpy(), cs.cpu().numpy(),
+            out.cpu().numpy().view(np.uint64).reshape(a.rows * b.cols, out_limbs))
+
+
+def radius_matmul_upper(pm, pe, qm, qe, m: int, n: int, k: int, stream=None):
+    """radius_matmul_upper (include/apball/matmul.hpp:87) on Mag planes (mantissa, exponent)"""
+    import torch
+    lib = _lib.lib()
+    t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to("cuda")
+    dpm, dpe = t(np.asarray(pm, np.uint32).view(np.int32), None), t(np.asarray(pe, np.int64), None)
+    dqm, dqe = t(np.asarray(qm, np.uint32).view(np.int32), None), t(np.asarray(qe, np.int64), None)
+    om = torch.zeros(m * k, dtype=torch.int32, device="cuda")
+    oe = torch.zeros(m * k, dtype=torch.int64, device="cuda")
+    st = _stream_ptr(stream)
+    _lib.check(lib.apb_radius_matmul_upper(dpm.data_ptr(), dpe.data_ptr(), dqm.data_ptr(), dqe.data_ptr(),
+                                           m, n, k, om.data_ptr(), oe.data_ptr(), st), "apb_radius_matmul_upper")
+    _lib.check(lib.apb_device_status(st), "apb_radius_matmul_upper")
+    return om.cpu().numpy().view(np.uint32), oe.cpu().numpy()
