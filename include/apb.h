@@ -182,6 +182,20 @@ int apb_radius_matmul_upper(const uint32_t* p_man, const int64_t* p_exp, const u
                             const int64_t* q_exp, int64_t m, int64_t n, int64_t k,
                             uint32_t* out_man, int64_t* out_exp, void* stream);
 
+/* Plan summary of C = A B without computing it (the planner of
+ * src/matmul.cpp:132-161 plus the radius-product windows of :386-392), used
+ * by the row-block sharded driver to verify that every shard's plan is the
+ * global plan (paper_1901_04289_b200/dist.py). */
+typedef struct apb_plan_info {
+    int64_t n_blocks;
+    int64_t entry_prec_a, entry_prec_b;
+    int64_t max_width_a, max_width_b;  /* widest row window of A / column window of B */
+    int32_t special;                   /* non-finite input: block path = classical */
+    int32_t radius_single;             /* both radius products single-block (<= 900 bits) */
+} apb_plan_info;
+int apb_matmul_plan_info(const apb_mat* A, const apb_mat* B, int64_t prec, apb_plan_info* out,
+                         void* stream);
+
 /* --------------------------------------------------------- host wrappers */
 
 /* End-to-end variants taking HOST ball arrays: host->device copy, kernels,

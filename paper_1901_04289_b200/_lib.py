@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 from .balls import (apb_balls, apb_dot_index, apb_dot_state, apb_dot_tuning, apb_mat,
-                    apb_matmul_stats)
+                    apb_matmul_stats, apb_plan_info)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libapb_b200.so")
@@ -73,6 +73,8 @@ def lib():
     L.apb_last_error.restype = C.c_char_p
     L.apb_launch_count.restype = C.c_uint64
     L.apb_version.restype = I
+    L.apb_matmul_plan_info.argtypes = [mp, mp, I64, C.POINTER(apb_plan_info), P]
+    L.apb_matmul_plan_info.restype = I
     L.apb_profile_enable.argtypes = [I]
     L.apb_profile_enable.restype = None
     L.apb_profile_reset.restype = None

@@ -66,6 +66,12 @@ class apb_matmul_stats(C.Structure):
                  "last_height_a", "last_height_b", "last_slices_a", "last_slices_b")]
 
 
+class apb_plan_info(C.Structure):
+    _fields_ = [("n_blocks", C.c_int64), ("entry_prec_a", C.c_int64), ("entry_prec_b", C.c_int64),
+                ("max_width_a", C.c_int64), ("max_width_b", C.c_int64), ("special", C.c_int32),
+                ("radius_single", C.c_int32)]
+
+
 DOT_STATE_DTYPE = np.dtype([
     ("e_max", "<i8"), ("e_min", "<i8"), ("e_rad", "<i8"), ("n_nonzero", "<u8"),
     ("p_eff", "<i8"), ("extend", "<i4"), ("padding", "<i4"), ("n_s", "<i8"), ("e_s", "<i8"),
@@ -153,6 +159,22 @@ class BallArray:
         radfin = (a.rad_man != 0) & (a.rad_man != APB_RAD_INF)
         same &= np.where(radfin, a.rad_exp == b.rad_exp, True)
         return same
+
+    def pinned(self) -> "BallArray":
+        """copy into page-locked host memory (for end-to-end timing of H2D/D2H)"""
+        import torch
+
+        def pin(a):
+            t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+            v = t.numpy().view(a.dtype).reshape(a.shape)
+            v[...] = a
+            return v, t  # the tensor `t` owns the pinned pages; keep it alive with the view
+
+        parts = [pin(a) for a in (self.mant, self.exp, self.kind, self.rad_man, self.rad_exp)]
+        out = BallArray.__new__(BallArray)
+        out.mant, out.exp, out.kind, out.rad_man, out.rad_exp = (p[0] for p in parts)
+        out._pins = [p[1] for p in parts]
+        return out
 
     # ----------------------------------------------------------- device
     def to_device(self, device="cuda") -> "DeviceBallArray":

@@ -301,6 +301,220 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
+
+// ====================================================================
+// Band kernel: 4 consecutive diagonals per pass.  For one output tile and a
+// band d0..d0+3, every A slice s and every B slice t of the band is loaded
+// ONCE per K block and feeds up to 4 MMAs (one per diagonal accumulator),
+// which cuts the L2->SMEM operand traffic ~4x against one diagonal at a time.
+// Sweep per K block: s descending from s_hi to s_lo; the live B slices form a
+// sliding window t in [max(0,d0-s), min(S_B-1,d0+3-s)] that advances by one
+// slice per step (FIFO ring).  Accumulators: 4 x 128 TMEM columns (512).
+// Each (tile, band) work item is independent (carry-in 0, carry-out to
+// Tc[band]); items are LPT-assigned to persistent CTAs on the host.
+// Requires |D_d| < 2^31: pairs(d) * K * 2^14 < 2^31 (checked by the driver).
+constexpr int BAND_W = 4;
+constexpr int A_STAGES = 4, B_STAGES = 8;
+constexpr int TILE_BYTES = 128 * BK;
+constexpr int BAND_SMEM = (A_STAGES + B_STAGES) * TILE_BYTES + 1024 + 512;
+
+__global__ void __launch_bounds__(THREADS, 1)
+    band_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     BandGemmParams P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* smA = smem;
+    uint8_t* smB = smem + A_STAGES * TILE_BYTES;
+    uint64_t* bars = (uint64_t*)(smem + (A_STAGES + B_STAGES) * TILE_BYTES);
+    uint64_t* fullA = bars;
+    uint64_t* emptyA = fullA + A_STAGES;
+    uint64_t* fullB = emptyA + A_STAGES;
+    uint64_t* emptyB = fullB + B_STAGES;
+    uint64_t* tfull = emptyB + B_STAGES;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int it_begin = P.cta_begin[blockIdx.x], it_end = P.cta_begin[blockIdx.x + 1];
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < A_STAGES; i++) {
+            mbar_init(&fullA[i], 1);
+            mbar_init(&emptyA[i], 1);
+        }
+        for (int i = 0; i < B_STAGES; i++) {
+            mbar_init(&fullB[i], 1);
+            mbar_init(&emptyB[i], 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, EPI_WARPS * 32);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+            uint32_t ai = 0, bi = 0;  // sequential ring indices
+            for (int it = it_begin; it < it_end; it++) {
+                const int2 W = P.items[it];
+                const int m0 = (W.x / P.n_tiles_n) * 128, n0 = (W.x % P.n_tiles_n) * 128;
+                const int d0 = BAND_W * W.y;
+                const int s_hi = min(P.S_A - 1, d0 + BAND_W - 1), s_lo = max(0, d0 - (P.S_B - 1));
+                for (int kb = 0; kb < P.n_kb; kb++) {
+                    int tmax_prev = -1;
+                    for (int s = s_hi; s >= s_lo; s--) {
+                        const int tmin = max(0, d0 - s), tmax = min(P.S_B - 1, d0 + BAND_W - 1 - s);
+                        {
+                            const uint32_t st = ai % A_STAGES, ph = (ai / A_STAGES) & 1;
+                            mbar_wait(&emptyA[st], ph ^ 1);
+                            mbar_expect_tx(&fullA[st], TILE_BYTES);
+                            tma_load_2d(smA + st * TILE_BYTES, &tmA, kb * BK, s * P.Mp + m0, &fullA[st]);
+                            ai++;
+                        }
+                        for (int t = max(tmin, tmax_prev + 1); t <= tmax; t++) {
+                            const uint32_t st = bi % B_STAGES, ph = (bi / B_STAGES) & 1;
+                            mbar_wait(&emptyB[st], ph ^ 1);
+                            mbar_expect_tx(&fullB[st], TILE_BYTES);
+                            tma_load_2d(smB + st * TILE_BYTES, &tmB, kb * BK, t * P.Np + n0, &fullB[st]);
+                            bi++;
+                        }
+                        tmax_prev = tmax;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        uint32_t ai = 0, bi = 0;
+        uint32_t tph = 0;
+        for (int it = it_begin; it < it_end; it++) {
+            const int2 W = P.items[it];
+            const int d0 = BAND_W * W.y;
+            const int s_hi = min(P.S_A - 1, d0 + BAND_W - 1), s_lo = max(0, d0 - (P.S_B - 1));
+            mbar_wait(tempty, tph ^ 1);
+            fence_after();
+            uint32_t init_mask = 0;
+            for (int kb = 0; kb < P.n_kb; kb++) {
+                const int t_first = max(0, d0 - s_hi);
+                const uint32_t b_first = bi;  // ring index of B slice t_first in this sweep
+                int tmax_prev = -1;
+                for (int s = s_hi; s >= s_lo; s--) {
+                    const int tmin = max(0, d0 - s), tmax = min(P.S_B - 1, d0 + BAND_W - 1 - s);
+                    const uint32_t ast = ai % A_STAGES, aph = (ai / A_STAGES) & 1;
+                    mbar_wait(&fullA[ast], aph);
+                    for (int t = max(tmin, tmax_prev + 1); t <= tmax; t++) {
+                        const uint32_t bidx = b_first + (uint32_t)(t - t_first);
+                        mbar_wait(&fullB[bidx % B_STAGES], (bidx / B_STAGES) & 1);
+                    }
+                    fence_after();
+                    if (lane == 0) {
+                        const uint32_t a0 = smem_u32(smA + ast * TILE_BYTES);
+                        for (int t = tmin; t <= tmax; t++) {
+                            const int w = s + t - d0;
+                            const uint32_t bidx = b_first + (uint32_t)(t - t_first);
+                            const uint32_t b0 = smem_u32(smB + (bidx % B_STAGES) * TILE_BYTES);
+                            const uint32_t tmem_d = tmem_base + (uint32_t)(w * 128);
+#pragma unroll
+                            for (int k = 0; k < BK / 32; k++) {
+                                const uint32_t acc = ((init_mask >> w) & 1u) | (k > 0 ? 1u : 0u);
+                                mma_i8(tmem_d, smem_desc(a0 + 32 * k), smem_desc(b0 + 32 * k), kIdesc, acc);
+                            }
+                            init_mask |= 1u << w;
+                        }
+                        mma_commit(&emptyA[ast]);
+                        if (s > s_lo) {
+                            const int tr = d0 - s;  // last use of slice tr is at this s
+                            if (tr >= 0) {
+                                const uint32_t bidx = b_first + (uint32_t)(tr - t_first);
+                                mma_commit(&emptyB[bidx % B_STAGES]);
+                            }
+                        } else {
+                            for (int t = tmin; t <= tmax; t++) {
+                                const uint32_t bidx = b_first + (uint32_t)(t - t_first);
+                                mma_commit(&emptyB[bidx % B_STAGES]);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    ai++;
+                    tmax_prev = tmax;
+                }
+                bi = b_first + (uint32_t)(min(P.S_B - 1, d0 + BAND_W - 1 - s_lo) - t_first + 1);
+            }
+            if (lane == 0) mma_commit(tfull);
+            __syncwarp();
+            tph ^= 1;
+        }
+    } else {
+        const int e = warp - 2;
+        const int q = warp & 3;
+        const int col0 = (e >> 2) * 64;
+        uint32_t tph = 0;
+        for (int it = it_begin; it < it_end; it++) {
+            const int2 W = P.items[it];
+            const int m0 = (W.x / P.n_tiles_n) * 128, n0 = (W.x % P.n_tiles_n) * 128;
+            const int d0 = BAND_W * W.y;
+            const int row = m0 + 32 * q + lane;
+            mbar_wait(tfull, tph);
+            fence_after();
+#pragma unroll 1
+            for (int h = 0; h < 2; h++) {
+                int32_t carry[32];
+                uint32_t word[32];
+#pragma unroll
+                for (int c = 0; c < 32; c++) {
+                    carry[c] = 0;
+                    word[c] = 0;
+                }
+#pragma unroll 1
+                for (int w = 0; w < BAND_W; w++) {
+                    if (d0 + w >= P.ND) break;
+                    uint32_t v[32];
+                    const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(w * 128 + col0 + 32 * h);
+                    TMEM_LD32(taddr, v);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int c = 0; c < 32; c++) {
+                        const int64_t val = (int64_t)(int32_t)v[c] + carry[c];
+                        word[c] |= (uint32_t)(val & 255) << (8 * w);
+                        carry[c] = (int32_t)(val >> 8);
+                    }
+                }
+                const size_t off = ((size_t)W.y * P.Mp + row) * P.Np + n0 + col0 + 32 * h;
+                uint32_t* wd = P.Tw + off;
+                int32_t* cd = P.Tc + off;
+#pragma unroll
+                for (int c = 0; c < 32; c += 4) {
+                    *(uint4*)(wd + c) = make_uint4(word[c], word[c + 1], word[c + 2], word[c + 3]);
+                    *(int4*)(cd + c) = make_int4(carry[c], carry[c + 1], carry[c + 2], carry[c + 3]);
+                }
+            }
+            fence_before();
+            mbar_arrive(tempty);
+            tph ^= 1;
+        }
+    }
+
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512)
+                     : "memory");
+    }
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -358,6 +572,29 @@ int slice_gemm_launch(const int8_t* Apack, const int8_t* Bpack, const SliceGemmP
     prof_end(tok, st);
     count_launch();
     return cuda_check(cudaGetLastError(), "slice_gemm launch");
+}
+
+}  // namespace apb
+
+namespace apb {
+
+int band_gemm_launch(const int8_t* Apack, const int8_t* Bpack, const BandGemmParams& P, int n_ctas,
+                     cudaStream_t st) {
+    CUtensorMap ma, mb;
+    int rc = make_map(&ma, Apack, (uint64_t)P.Kp, (uint64_t)P.S_A * P.Mp, BM);
+    if (rc) return rc;
+    rc = make_map(&mb, Bpack, (uint64_t)P.Kp, (uint64_t)P.S_B * P.Np, BN);
+    if (rc) return rc;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(band_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BAND_SMEM);
+        attr = true;
+    }
+    const int tok = prof_begin("slice_gemm", st);
+    band_gemm_kernel<<<n_ctas, THREADS, BAND_SMEM, st>>>(ma, mb, P);
+    prof_end(tok, st);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "band_gemm launch");
 }
 
 }  // namespace apb

@@ -19,6 +19,19 @@ struct SliceGemmParams {
     int32_t* Tc;           // [n_groups][Mp][Np] final carry of each group
 };
 
+// band variant: 4 diagonals per pass, persistent CTAs over (tile, band) items
+struct BandGemmParams {
+    int S_A, S_B, Mp, Np, Kp, n_kb, ND;
+    int n_tiles_n;            // Np / 128
+    const int2* items;        // (tile = mt * n_tiles_n + nt, band)
+    const int* cta_begin;     // [n_ctas + 1] item ranges per CTA
+    uint32_t* Tw;             // [n_bands][Mp][Np] result bytes of diagonals 4b..4b+3
+    int32_t* Tc;              // [n_bands][Mp][Np] carry out of band b
+};
+
+int band_gemm_launch(const int8_t* Apack, const int8_t* Bpack, const BandGemmParams& P, int n_ctas,
+                     cudaStream_t st);
+
 int slice_gemm_launch(const int8_t* Apack, const int8_t* Bpack, const SliceGemmParams& P, int n_groups,
                       cudaStream_t st);
 

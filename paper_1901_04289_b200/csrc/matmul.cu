@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -100,28 +101,63 @@ __global__ void scan_rows_kernel(BallsView A, int64_t M, int64_t K, int64_t lo, 
     }
 }
 
-// thread per column of B: window over rows [lo,hi)
+// column windows of B over rows [lo,hi): grid (column tiles, row chunks),
+// per-column int64 atomics; col_width_kernel finishes the widths
+constexpr int COL_CHUNK = 16;
+
+__global__ void init_minmax_kernel(int64_t* top, int64_t* bot, int64_t n) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) {
+        top[j] = INT64_MIN;
+        bot[j] = INT64_MAX;
+    }
+}
+
 __global__ void scan_cols_kernel(BallsView B, int64_t K, int64_t N, int64_t lo, int64_t hi,
                                  int64_t* ctop, int64_t* cbot, ScanSummary* sum) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= N) return;
+    const int64_t k0 = lo + (int64_t)blockIdx.y * COL_CHUNK;
+    const int64_t k1 = k0 + COL_CHUNK < hi ? k0 + COL_CHUNK : hi;
     int64_t top = INT64_MIN, bot = INT64_MAX, prec = 0;
     int special = 0;
-    for (int64_t k = lo; k < hi; k++) {
-        const int64_t e = k * N + j;
-        special |= ball_special(B, e);
-        int64_t t, b;
-        if (mid_window(B, e, t, b)) {
-            top = t > top ? t : top;
-            bot = b < bot ? b : bot;
-            prec = (t - b) > prec ? (t - b) : prec;
+    if (j < N) {
+        for (int64_t k = k0; k < k1; k++) {
+            const int64_t e = k * N + j;
+            special |= ball_special(B, e);
+            int64_t t, b;
+            if (mid_window(B, e, t, b)) {
+                top = t > top ? t : top;
+                bot = b < bot ? b : bot;
+                prec = (t - b) > prec ? (t - b) : prec;
+            }
+        }
+        if (top != INT64_MIN) {
+            atomicMax((long long*)&ctop[j], (long long)top);
+            atomicMin((long long*)&cbot[j], (long long)bot);
         }
     }
-    ctop[j] = top;
-    cbot[j] = bot;
-    if (special) atomicOr(&sum->special_b, 1);
-    atomicMax(&sum->prec_b, (long long)prec);
-    if (top != INT64_MIN) atomicMax(&sum->maxw_b, (long long)(top - bot));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        int64_t p2 = __shfl_xor_sync(0xffffffffu, prec, o);
+        prec = p2 > prec ? p2 : prec;
+    }
+    special = __any_sync(0xffffffffu, special);
+    if ((threadIdx.x & 31) == 0) {
+        if (special) atomicOr(&sum->special_b, 1);
+        if (prec) atomicMax(&sum->prec_b, (long long)prec);
+    }
+}
+
+__global__ void col_width_kernel(const int64_t* ctop, const int64_t* cbot, int64_t N, long long* maxw) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    long long w = 0;
+    if (j < N && ctop[j] != INT64_MIN) w = (long long)(ctop[j] - cbot[j]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        long long w2 = __shfl_xor_sync(0xffffffffu, w, o);
+        w = w2 > w ? w2 : w;
+    }
+    if ((threadIdx.x & 31) == 0 && w) atomicMax(maxw, w);
 }
 
 // ----------------------------------------------------- K3 greedy (device)
@@ -430,19 +466,40 @@ __global__ void rad_center_rows_kernel(BallsView A, int64_t M, int64_t K, int64_
     }
 }
 
-__global__ void rad_center_cols_kernel(BallsView B, int64_t K, int64_t N, int64_t lo, int64_t hi,
-                                       int which, int64_t* fcen, long long* maxw) {
+__global__ void rad_cols_minmax_kernel(BallsView B, int64_t K, int64_t N, int64_t lo, int64_t hi,
+                                       int which, int64_t* ctop, int64_t* cbot) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t k0 = lo + (int64_t)blockIdx.y * COL_CHUNK;
+    const int64_t k1 = k0 + COL_CHUNK < hi ? k0 + COL_CHUNK : hi;
     if (j >= N) return;
     int64_t top = INT64_MIN, bot = INT64_MAX;
-    for (int64_t l = lo; l < hi; l++) {
+    for (int64_t l = k0; l < k1; l++) {
         Mag m = rad_operand(B, l * N + j, which);
         if (m.kind != 1) continue;
         top = m.f > top ? m.f : top;
         bot = (m.f - 30) < bot ? (m.f - 30) : bot;
     }
-    fcen[j] = top == INT64_MIN ? 0 : -((top + bot) / 2);
-    if (maxw && top != INT64_MIN) atomicMax(maxw, (long long)(top - bot));
+    if (top != INT64_MIN) {
+        atomicMax((long long*)&ctop[j], (long long)top);
+        atomicMin((long long*)&cbot[j], (long long)bot);
+    }
+}
+
+__global__ void rad_cols_center_kernel(const int64_t* ctop, const int64_t* cbot, int64_t N,
+                                       int64_t* fcen, long long* maxw) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    long long w = 0;
+    if (j < N) {
+        const int64_t top = ctop[j], bot = cbot[j];
+        fcen[j] = top == INT64_MIN ? 0 : -((top + bot) / 2);
+        if (top != INT64_MIN) w = (long long)(top - bot);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        long long w2 = __shfl_xor_sync(0xffffffffu, w, o);
+        w = w2 > w ? w2 : w;
+    }
+    if (maxw && (threadIdx.x & 31) == 0 && w) atomicMax(maxw, w);
 }
 
 // exact doubles of the centred Mags (mag_ldexp, src/mag.cpp:166-172):
@@ -467,15 +524,15 @@ __global__ void rad_planes_kernel(BallsView X, int64_t rows, int64_t cols, int64
 // rounded-to-nearest sums in the reference's order, 1024-term chunks, then
 // Mag::from_double_upper * (1 + 2^-29) and mag_add_up into r (src/matmul.cpp:423-435).
 // 64x64 output tile per 256 threads, 4x4 per thread, sequential in l per entry.
-constexpr int RT = 64, RK = 16;
-__global__ void __launch_bounds__(256) rad_gemm_kernel(const double* __restrict__ da,
+constexpr int RT = 32, RK = 32, RTHREADS = 64;
+__global__ void __launch_bounds__(64) rad_gemm_kernel(const double* __restrict__ da,
                                                        const double* __restrict__ db, int64_t M,
                                                        int64_t N, int64_t w, const int64_t* ecen,
                                                        const int64_t* fcen, uint32_t* rb, int64_t* rf,
                                                        int accumulate) {
     __shared__ double sA[RK][RT + 1];
     __shared__ double sB[RK][RT];
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
     const int64_t i0 = (int64_t)blockIdx.y * RT, j0 = (int64_t)blockIdx.x * RT;
     double s[4][4];
     Mag ent[4][4];
@@ -488,7 +545,7 @@ __global__ void __launch_bounds__(256) rad_gemm_kernel(const double* __restrict_
         }
     const Mag infl = mag_parts((1ull << 29) + 1, 1);
     for (int64_t l0 = 0; l0 < w; l0 += RK) {
-        for (int q = threadIdx.x; q < RK * RT; q += 256) {
+        for (int q = threadIdx.x; q < RK * RT; q += RTHREADS) {
             const int kk = q / RT, rr = q % RT;
             const int64_t gi = i0 + rr, gl = l0 + kk;
             sA[kk][rr] = (gi < M && gl < w) ? da[gi * w + gl] : 0.0;
@@ -591,8 +648,8 @@ T* ws_buf(int slot, size_t count, cudaStream_t st) {
 
 struct Scratch {
     // separate allocations owned here (the Workspace slot table is small)
-    void* p[24] = {};
-    size_t cap[24] = {};
+    void* p[32] = {};
+    size_t cap[32] = {};
     void* get(int k, size_t bytes, cudaStream_t st) {
         if (cap[k] < bytes) {
             if (p[k]) {
@@ -616,7 +673,7 @@ Scratch& scratch() {
 }
 enum {
     S_RTOP, S_RBOT, S_CTOP, S_CBOT, S_SUM, S_APACK, S_BPACK, S_TW, S_TC, S_UNITS, S_ESC, S_FSC,
-    S_WA, S_WB, S_GREEDY, S_DA, S_DB, S_CEN_E, S_CEN_F, S_R1B, S_R1F, S_R2B, S_R2F, S_MISC
+    S_WA, S_WB, S_GREEDY, S_DA, S_DB, S_CEN_E, S_CEN_F, S_R1B, S_R1F, S_R2B, S_R2F, S_MISC, S_CTOP2, S_CBOT2
 };
 template <class T>
 T* sbuf(int k, size_t count, cudaStream_t st) {
@@ -624,6 +681,15 @@ T* sbuf(int k, size_t count, cudaStream_t st) {
 }
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+void scan_cols(const BallsView& b, int64_t K, int64_t N, int64_t lo, int64_t hi, int64_t* ctop,
+               int64_t* cbot, ScanSummary* sum, cudaStream_t st) {
+    init_minmax_kernel<<<blocks_for(N, 256), 256, 0, st>>>(ctop, cbot, N);
+    dim3 grid(blocks_for(N, 128), blocks_for(hi - lo, COL_CHUNK));
+    if (hi > lo) scan_cols_kernel<<<grid, 128, 0, st>>>(b, K, N, lo, hi, ctop, cbot, sum);
+    col_width_kernel<<<blocks_for(N, 256), 256, 0, st>>>(ctop, cbot, N, &sum->maxw_b);
+    count_launch(3);
+}
 
 int classical(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, cudaStream_t st) {
     stats().classical_calls++;
@@ -662,6 +728,7 @@ struct Plan {
     std::vector<int64_t> steps;  // triples (lo, hi, basecase)
     bool special = false;
     int64_t maxw_a = 0, maxw_b = 0;  // whole-range widths (single block)
+    int64_t prec_a = 0, prec_b = 0;
 };
 
 int plan(const apb_mat* A, const apb_mat* B, int64_t prec, Plan& P, cudaStream_t st) {
@@ -675,8 +742,8 @@ int plan(const apb_mat* A, const apb_mat* B, int64_t prec, Plan& P, cudaStream_t
     if (!rtop || !rbot || !ctop || !cbot || !sum) return APB_ERR_CUDA;
     cudaMemsetAsync(sum, 0, sizeof(ScanSummary), st);
     scan_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(a, M, K, 0, K, rtop, rbot, sum);
-    scan_cols_kernel<<<blocks_for(N, 128), 128, 0, st>>>(b, K, N, 0, K, ctop, cbot, sum);
-    count_launch(2);
+    scan_cols(b, K, N, 0, K, ctop, cbot, sum, st);
+    count_launch(1);
     static ScanSummary* hsum = nullptr;
     if (!hsum) cudaMallocHost(&hsum, sizeof(ScanSummary));
     cudaMemcpyAsync(hsum, sum, sizeof(ScanSummary), cudaMemcpyDeviceToHost, st);
@@ -686,6 +753,8 @@ int plan(const apb_mat* A, const apb_mat* B, int64_t prec, Plan& P, cudaStream_t
     if (P.special) return APB_OK;
     P.maxw_a = hsum->maxw_a;
     P.maxw_b = hsum->maxw_b;
+    P.prec_a = hsum->prec_a;
+    P.prec_b = hsum->prec_b;
     // plan_blocks (src/matmul.cpp:132-161)
     int64_t pm = std::max<int64_t>(hsum->prec_a, hsum->prec_b);
     pm = std::min<int64_t>(prec, pm);
@@ -795,8 +864,8 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         ScanSummary* sum = sbuf<ScanSummary>(S_SUM, 1, st);
         cudaMemsetAsync(sum, 0, sizeof(ScanSummary), st);
         scan_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(a, M, K, lo, hi, rt, rb, sum);
-        scan_cols_kernel<<<blocks_for(N, 128), 128, 0, st>>>(b, K, N, lo, hi, ct, cb, sum);
-        count_launch(2);
+        scan_cols(b, K, N, lo, hi, ct, cb, sum, st);
+        count_launch(1);
         ScanSummary h;
         cudaMemcpyAsync(&h, sum, sizeof h, cudaMemcpyDeviceToHost, st);
         int rc = cuda_check(cudaStreamSynchronize(st), "block scan");
@@ -821,7 +890,7 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     int8_t* Bp = sbuf<int8_t>(S_BPACK, (size_t)SB * Np * Kp, st);
     int64_t* esc = esc_out ? esc_out : sbuf<int64_t>(S_ESC, M, st);
     int64_t* fsc = fsc_out ? fsc_out : sbuf<int64_t>(S_FSC, N, st);
-    if (!Ap || !Bp || !esc || !fsc) {
+    if (!Ap || !Bp || !esc || !fsc) {  // (slice planes are rewritten in full by the pack kernels)
         set_error("out of device memory (slice planes)");
         return APB_ERR_CUDA;
     }
@@ -831,12 +900,64 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     prof_end(tok, st);
     count_launch(2);
     const int tiles = (Mp / kSliceTile) * (Np / kSliceTile);
-    Units U = make_units(SA, SB, w, tiles);
-    const int G = (int)U.group_d1.size();
     const int ND = SA + SB - 1;
-    const int NW = (ND + 3) / 4;
-    // unit table upload (small; pinned staging)
-    const size_t ubytes = U.units.size() * sizeof(int4) + (U.group_begin.size() + U.group_d1.size()) * sizeof(int);
+    // band kernel when every diagonal fits an int32 accumulator: pairs * w * 2^14 < 2^31
+    static const bool force_unit = std::getenv("APB_FORCE_UNIT_GEMM") != nullptr;  // test hook
+    const bool band = !force_unit && (int64_t)std::min(SA, SB) * w < (int64_t)1 << 17;
+    int G, NW;
+    std::vector<char> host;  // staged tables
+    std::vector<int> group_d1;
+    size_t off_items = 0, off_begin = 0, off_d1 = 0, n_ctas = 0;
+    Units U;
+    if (band) {
+        const int NB = (ND + 3) / 4;
+        std::vector<int64_t> bw(NB, 0);
+        for (int d = 0; d < ND; d++)
+            bw[d / 4] += std::min(d, SA - 1) - std::max(0, d - SB + 1) + 1;
+        std::vector<std::pair<int64_t, int2>> items;
+        for (int t = 0; t < tiles; t++)
+            for (int bnd = 0; bnd < NB; bnd++) items.push_back({bw[bnd], make_int2(t, bnd)});
+        std::stable_sort(items.begin(), items.end(),
+                         [](const std::pair<int64_t, int2>& x, const std::pair<int64_t, int2>& y) { return x.first > y.first; });
+        n_ctas = std::min<size_t>(148, items.size());
+        std::vector<std::vector<int2>> lists(n_ctas);
+        std::vector<int64_t> load(n_ctas, 0);
+        for (auto& it : items) {  // LPT: heaviest item to the least loaded CTA
+            size_t best = 0;
+            for (size_t c = 1; c < n_ctas; c++)
+                if (load[c] < load[best]) best = c;
+            lists[best].push_back(it.second);
+            load[best] += it.first;
+        }
+        std::vector<int2> flat;
+        std::vector<int> begin = {0};
+        for (auto& l : lists) {
+            flat.insert(flat.end(), l.begin(), l.end());
+            begin.push_back((int)flat.size());
+        }
+        for (int bnd = 0; bnd < NB; bnd++) group_d1.push_back(std::min(ND, 4 * bnd + 4));
+        off_items = 0;
+        off_begin = flat.size() * sizeof(int2);
+        off_d1 = off_begin + begin.size() * sizeof(int);
+        host.resize(off_d1 + group_d1.size() * sizeof(int));
+        std::memcpy(host.data(), flat.data(), flat.size() * sizeof(int2));
+        std::memcpy(host.data() + off_begin, begin.data(), begin.size() * sizeof(int));
+        std::memcpy(host.data() + off_d1, group_d1.data(), group_d1.size() * sizeof(int));
+        G = NB;
+        NW = NB;
+    } else {
+        U = make_units(SA, SB, w, tiles);
+        G = (int)U.group_d1.size();
+        NW = (ND + 3) / 4;
+        off_items = 0;
+        off_begin = U.units.size() * sizeof(int4);
+        off_d1 = off_begin + U.group_begin.size() * sizeof(int);
+        host.resize(off_d1 + U.group_d1.size() * sizeof(int));
+        std::memcpy(host.data(), U.units.data(), U.units.size() * sizeof(int4));
+        std::memcpy(host.data() + off_begin, U.group_begin.data(), U.group_begin.size() * sizeof(int));
+        std::memcpy(host.data() + off_d1, U.group_d1.data(), U.group_d1.size() * sizeof(int));
+    }
+    const size_t ubytes = host.size();
     static char* hstage = nullptr;
     static size_t hcap = 0;
     if (hcap < ubytes) {
@@ -849,10 +970,7 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     } else {
         cudaStreamSynchronize(st);  // previous upload finished before reuse
     }
-    std::memcpy(hstage, U.units.data(), U.units.size() * sizeof(int4));
-    std::memcpy(hstage + U.units.size() * sizeof(int4), U.group_begin.data(), U.group_begin.size() * sizeof(int));
-    std::memcpy(hstage + U.units.size() * sizeof(int4) + U.group_begin.size() * sizeof(int), U.group_d1.data(),
-                U.group_d1.size() * sizeof(int));
+    std::memcpy(hstage, host.data(), ubytes);
     char* dunits = sbuf<char>(S_UNITS, ubytes, st);
     uint32_t* Tw = sbuf<uint32_t>(S_TW, (size_t)NW * Mp * Np, st);
     int32_t* Tc = sbuf<int32_t>(S_TC, (size_t)G * Mp * Np, st);
@@ -861,24 +979,43 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         return APB_ERR_CUDA;
     }
     cudaMemcpyAsync(dunits, hstage, ubytes, cudaMemcpyHostToDevice, st);
-    SliceGemmParams P;
-    P.S_A = SA;
-    P.S_B = SB;
-    P.Mp = Mp;
-    P.Np = Np;
-    P.Kp = Kp;
-    P.n_kb = Kp / kSliceBK;
-    P.units = (const int4*)dunits;
-    P.group_unit_begin = (const int*)(dunits + U.units.size() * sizeof(int4));
-    P.group_d1 = P.group_unit_begin + U.group_begin.size();
-    P.Tw = Tw;
-    P.Tc = Tc;
-    int rc = slice_gemm_launch(Ap, Bp, P, G, st);
+    int rc;
+    const int* d_group_d1 = (const int*)(dunits + off_d1);
+    if (band) {
+        BandGemmParams P;
+        P.S_A = SA;
+        P.S_B = SB;
+        P.Mp = Mp;
+        P.Np = Np;
+        P.Kp = Kp;
+        P.n_kb = Kp / kSliceBK;
+        P.ND = ND;
+        P.n_tiles_n = Np / kSliceTile;
+        P.items = (const int2*)(dunits + off_items);
+        P.cta_begin = (const int*)(dunits + off_begin);
+        P.Tw = Tw;
+        P.Tc = Tc;
+        rc = band_gemm_launch(Ap, Bp, P, (int)n_ctas, st);
+    } else {
+        SliceGemmParams P;
+        P.S_A = SA;
+        P.S_B = SB;
+        P.Mp = Mp;
+        P.Np = Np;
+        P.Kp = Kp;
+        P.n_kb = Kp / kSliceBK;
+        P.units = (const int4*)(dunits + off_items);
+        P.group_unit_begin = (const int*)(dunits + off_begin);
+        P.group_d1 = d_group_d1;
+        P.Tw = Tw;
+        P.Tc = Tc;
+        rc = slice_gemm_launch(Ap, Bp, P, G, st);
+    }
     if (rc) return rc;
     RecombineArgs R;
     R.Tw = Tw;
     R.Tc = Tc;
-    R.group_d1 = P.group_d1;
+    R.group_d1 = d_group_d1;
     R.n_groups = G;
     R.nwords = NW;
     R.Mp = Mp;
@@ -904,6 +1041,17 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     return cuda_check(cudaGetLastError(), "recombine");
 }
 
+void rad_center_cols(const BallsView& b, int64_t K, int64_t N, int64_t lo, int64_t hi, int which,
+                     int64_t* fcen, long long* maxw, cudaStream_t st) {
+    int64_t* ct = sbuf<int64_t>(S_CTOP2, N, st);
+    int64_t* cb = sbuf<int64_t>(S_CBOT2, N, st);
+    init_minmax_kernel<<<blocks_for(N, 256), 256, 0, st>>>(ct, cb, N);
+    dim3 grid(blocks_for(N, 128), blocks_for(hi - lo, COL_CHUNK));
+    if (hi > lo) rad_cols_minmax_kernel<<<grid, 128, 0, st>>>(b, K, N, lo, hi, which, ct, cb);
+    rad_cols_center_kernel<<<blocks_for(N, 256), 256, 0, st>>>(ct, cb, N, fcen, maxw);
+    count_launch(3);
+}
+
 // radius_matmul_upper(P, Q) into (rb, rf) for operand kinds (wa of A, wb of B)
 int radius_product(const apb_mat* A, const apb_mat* B, int wa, int wb, uint32_t* rb, int64_t* rf,
                    cudaStream_t st) {
@@ -914,8 +1062,8 @@ int radius_product(const apb_mat* A, const apb_mat* B, int wa, int wb, uint32_t*
     long long* mw = sbuf<long long>(S_SUM, 2, st);
     cudaMemsetAsync(mw, 0, 2 * sizeof(long long), st);
     rad_center_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(a, M, K, 0, K, wa, ecen, mw);
-    rad_center_cols_kernel<<<blocks_for(N, 128), 128, 0, st>>>(b, K, N, 0, K, wb, fcen, mw + 1);
-    count_launch(2);
+    rad_center_cols(b, K, N, 0, K, wb, fcen, mw + 1, st);
+    count_launch(1);
     long long hw[2];
     cudaMemcpyAsync(hw, mw, sizeof hw, cudaMemcpyDeviceToHost, st);
     int rc = cuda_check(cudaStreamSynchronize(st), "radius windows");
@@ -947,8 +1095,8 @@ int radius_product(const apb_mat* A, const apb_mat* B, int wa, int wb, uint32_t*
         const int64_t lo = blocks[bi], hi = blocks[bi + 1], w = hi - lo;
         if (blocks.size() > 2) {  // centring over this block only
             rad_center_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(a, M, K, lo, hi, wa, ecen, nullptr);
-            rad_center_cols_kernel<<<blocks_for(N, 128), 128, 0, st>>>(b, K, N, lo, hi, wb, fcen, nullptr);
-            count_launch(2);
+            rad_center_cols(b, K, N, lo, hi, wb, fcen, nullptr, st);
+            count_launch(1);
         }
         double* da = sbuf<double>(S_DA, (size_t)M * w, st);
         double* db = sbuf<double>(S_DB, (size_t)w * N, st);
@@ -957,7 +1105,7 @@ int radius_product(const apb_mat* A, const apb_mat* B, int wa, int wb, uint32_t*
         rad_planes_kernel<<<blocks_for(w * N, 256), 256, 0, st>>>(b, K, N, lo, hi, wb, 0, fcen, db);
         dim3 grid(blocks_for(N, RT), blocks_for(M, RT));
         const int tk = prof_begin("rad_gemm", st);
-        rad_gemm_kernel<<<grid, 256, 0, st>>>(da, db, M, N, w, ecen, fcen, rb, rf, bi ? 1 : 0);
+        rad_gemm_kernel<<<grid, RTHREADS, 0, st>>>(da, db, M, N, w, ecen, fcen, rb, rf, bi ? 1 : 0);
         prof_end(tk, st);
         count_launch(3);
     }
@@ -1111,6 +1259,41 @@ int apb_plan_blocks(const apb_mat* A, const apb_mat* B, int64_t prec, int64_t* s
     *n_steps = (int64_t)P.steps.size() / 3;
     for (int64_t i = 0; i < *n_steps && i < max_steps; i++)
         for (int q = 0; q < 3; q++) steps_out[3 * i + q] = P.steps[3 * i + q];
+    return APB_OK;
+}
+
+int apb_matmul_plan_info(const apb_mat* A, const apb_mat* B, int64_t prec, apb_plan_info* out,
+                         void* stream) {
+    if (!A || !B || !out || A->cols != B->rows) {
+        set_error("plan_info: dimension mismatch");
+        return APB_ERR_INVALID;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    std::memset(out, 0, sizeof *out);
+    Plan P;
+    int rc = plan(A, B, prec, P, st);
+    if (rc) return rc;
+    out->special = P.special ? 1 : 0;
+    out->n_blocks = (int64_t)P.steps.size() / 3;
+    out->entry_prec_a = P.prec_a;
+    out->entry_prec_b = P.prec_b;
+    out->max_width_a = P.maxw_a;
+    out->max_width_b = P.maxw_b;
+    const int64_t M = A->rows, K = A->cols, N = B->cols;
+    BallsView a = view_of(&A->b), b = view_of(&B->b);
+    int64_t* ecen = sbuf<int64_t>(S_CEN_E, M, st);
+    int64_t* fcen = sbuf<int64_t>(S_CEN_F, N, st);
+    long long* mw = sbuf<long long>(S_SUM, 4, st);
+    cudaMemsetAsync(mw, 0, 4 * sizeof(long long), st);
+    rad_center_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(a, M, K, 0, K, 0, ecen, mw);
+    rad_center_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(a, M, K, 0, K, 1, ecen, mw + 1);
+    rad_center_cols(b, K, N, 0, K, 2, fcen, mw + 2, st);
+    rad_center_cols(b, K, N, 0, K, 3, fcen, mw + 3, st);
+    count_launch(2);
+    long long hw[4];
+    cudaMemcpyAsync(hw, mw, sizeof hw, cudaMemcpyDeviceToHost, st);
+    if ((rc = cuda_check(cudaStreamSynchronize(st), "plan info"))) return rc;
+    out->radius_single = (hw[0] <= 900 && hw[1] <= 900 && hw[2] <= 900 && hw[3] <= 900) ? 1 : 0;
     return APB_OK;
 }
 

@@ -259,3 +259,18 @@ def radius_matmul_upper(pm, pe, qm, qe, m: int, n: int, k: int, stream=None):
                                            m, n, k, om.data_ptr(), oe.data_ptr(), st), "apb_radius_matmul_upper")
     _lib.check(lib.apb_device_status(st), "apb_radius_matmul_upper")
     return om.cpu().numpy().view(np.uint32), oe.cpu().numpy()
+
+
+def plan_info(a: BallMatrix, b: BallMatrix, prec: int, stream=None) -> dict:
+    """planner summary (block count, entry precisions, widths, radius single-block flag)"""
+    from .balls import apb_plan_info
+    lib = _lib.lib()
+    am, bm = a.c(), b.c()
+    out = apb_plan_info()
+    _lib.check(lib.apb_matmul_plan_info(C.byref(am), C.byref(bm), prec, C.byref(out), _stream_ptr(stream)),
+               "apb_matmul_plan_info")
+    return {f: int(getattr(out, f)) for f, _ in out._fields_}
+
+
+def radius_single_block(a: BallMatrix, b: BallMatrix, prec: int = 2) -> bool:
+    return bool(plan_info(a, b, prec)["radius_single"])

@@ -75,3 +75,14 @@ def test_full_config_vs_reference(cfg):
     ref, nb = po.matmul(a, b, n, n, n, p, which="ref", algo=1, threads=os.cpu_count() or 8)
     ok = got.identical(ref)
     assert ok.all(), f"{(~ok).sum()} entries differ"
+
+
+def test_unit_gemm_path_golden():
+    """the one-diagonal-per-pass kernel (used when a diagonal could overflow int32)
+    forced on the golden cases in a subprocess"""
+    import subprocess
+    import sys
+    env = dict(os.environ, APB_FORCE_UNIT_GEMM="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-k", "test_matmul_golden_gpu",
+                        os.path.abspath(__file__)], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:]
