@@ -32,6 +32,7 @@
 //       (re, im) over the 2N-term part views, thread per dot.
 
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "apb.h"
@@ -191,7 +192,10 @@ APB_DEV void load_mant(uint64_t (&m)[L], const BallsView& a, int64_t e) {
 template <int L>
 APB_DEV void load_term(Term<L>& t, const DotArgs& A, int64_t b, int64_t i) {
     if (i < A.n) {
-        int64_t ex = x_elem(A.idx, b, i), ey = y_elem(A.idx, b, i);
+        const int64_t bq = A.idx.bdiv == 1 ? b : b / A.idx.bdiv;
+        const int64_t br = A.idx.bdiv == 1 ? 0 : b - bq * A.idx.bdiv;
+        const int64_t ex = A.idx.x_off + bq * A.idx.xs1 + br * A.idx.xs2 + i * A.idx.xstep;
+        const int64_t ey = A.idx.y_off + bq * A.idx.ys1 + br * A.idx.ys2 + i * A.idx.ystep;
         t.kx = __ldg(A.x.kind + ex);
         t.ky = __ldg(A.y.kind + ey);
         t.ex = __ldg(A.x.exp + ex);
@@ -405,45 +409,112 @@ APB_DEV uint64_t warp_sum(uint64_t v) {
     return v;
 }
 
+// Per-warp batch of up to 32 dots: dot g's reduced accumulator is parked in
+// lane g, and the 32 finalizes (normalize / truncate / Mag error terms) run
+// in parallel at the end instead of serially on lane 0.
 template <int L, int NS, int TPL>
-__global__ void __launch_bounds__(256) dot_small_kernel(DotArgs A) {
+__global__ void __launch_bounds__(128, (TPL > 0 ? 3 : 4)) dot_small_kernel(DotArgs A) {
     const int lane = threadIdx.x & 31;
-    const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (b >= A.batch) return;
+    const int64_t warp_id = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t b0 = warp_id * 32;
+    if (b0 >= A.batch) return;
+    const int nd = (int)(A.batch - b0 < 32 ? A.batch - b0 : 32);
     const int64_t total = A.n + (A.has_init ? 1 : 0);
     const bool with_radius = A.mode == APB_DOT_BALL;
     const bool track_min = A.prec > 128;
 
-    // ---- pass 1: setup scan
-    ScanAcc sc{INT64_MIN, INT64_MAX, INT64_MIN, 0, false};
-    Term<L> keep[TPL > 0 ? TPL : 1];
-    if (TPL > 0) {
+    // lane-parked results of dot b0 + lane
+    Plan my_pl;
+    uint64_t my_s[NS];
+    uint64_t my_err = 0, my_srad = 0;
+    my_pl.status = 2;
+
+    for (int g = 0; g < nd; g++) {
+        const int64_t b = b0 + g;
+        // ---- pass 1: setup scan
+        ScanAcc sc{INT64_MIN, INT64_MAX, INT64_MIN, 0, false};
+        Term<L> keep[TPL > 0 ? TPL : 1];
+        if (TPL > 0) {
 #pragma unroll
-        for (int q = 0; q < (TPL > 0 ? TPL : 1); q++) {
-            int64_t i = lane + 32 * (int64_t)q;
-            if (i < total) {
-                load_term<L>(keep[q], A, b, i);
-                scan_term<L>(sc, keep[q], track_min, with_radius);
+            for (int q = 0; q < (TPL > 0 ? TPL : 1); q++) {
+                int64_t i = lane + 32 * (int64_t)q;
+                if (i < total) {
+                    load_term<L>(keep[q], A, b, i);
+                    scan_term<L>(sc, keep[q], track_min, with_radius);
+                }
+            }
+        } else {
+            for (int64_t i = lane; i < total; i += 32) {
+                Term<L> t;
+                load_term<L>(t, A, b, i);
+                scan_term<L>(sc, t, track_min, with_radius);
             }
         }
-    } else {
-        for (int64_t i = lane; i < total; i += 32) {
-            Term<L> t;
-            load_term<L>(t, A, b, i);
-            scan_term<L>(sc, t, track_min, with_radius);
+        const bool fb = __any_sync(0xffffffffu, sc.fb);
+        const int64_t e_max = warp_max(sc.e_max);
+        const int64_t e_min = warp_min(sc.e_min);
+        const int64_t e_rad = warp_max(sc.e_rad);
+        const uint64_t nnz = warp_sum(sc.nnz);
+        const Plan pl = finish_plan(e_max, e_min, e_rad, nnz, fb, total, A.prec, A.disable_reduction);
+        if (lane == g) my_pl = pl;
+        if (pl.status != 0) continue;
+
+        // ---- pass 2: accumulate
+        Acc<L, NS> acc;
+#pragma unroll
+        for (int j = 0; j < NS; j++) acc.s[j] = 0;
+        acc.err = 0;
+        acc.srad = 0;
+        auto do_term = [&](const Term<L>& t) {
+            const bool xz = (t.kx & APB_KIND_MASK) == APB_ZERO, yz = (t.ky & APB_KIND_MASK) == APB_ZERO;
+            if (!xz && !yz) acc_term<L, NS>(acc, t, pl);
+            if (with_radius) rad_term<L, NS>(acc, t, pl);
+        };
+        if (TPL > 0) {
+#pragma unroll
+            for (int q = 0; q < (TPL > 0 ? TPL : 1); q++) {
+                int64_t i = lane + 32 * (int64_t)q;
+                if (i < total) do_term(keep[q]);
+            }
+        } else {
+            for (int64_t i = lane; i < total; i += 32) {
+                Term<L> t;
+                load_term<L>(t, A, b, i);
+                do_term(t);
+            }
+        }
+
+        // ---- warp reduction of (s, err, srad); s mod 2^(64 NS) with carries
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            uint64_t c = 0;
+#pragma unroll
+            for (int j = 0; j < NS; j++) {
+                uint64_t v = __shfl_xor_sync(0xffffffffu, acc.s[j], o);
+                uint64_t s1 = acc.s[j] + v;
+                uint64_t c1 = s1 < v;
+                uint64_t s2 = s1 + c;
+                uint64_t c2 = s2 < c;
+                acc.s[j] = s2;
+                c = c1 | c2;
+            }
+            acc.err += __shfl_xor_sync(0xffffffffu, acc.err, o);
+            acc.srad += __shfl_xor_sync(0xffffffffu, acc.srad, o);
+        }
+        if (lane == g) {
+#pragma unroll
+            for (int j = 0; j < NS; j++) my_s[j] = acc.s[j];
+            my_err = acc.err;
+            my_srad = acc.srad;
         }
     }
-    const bool fb = __any_sync(0xffffffffu, sc.fb);
-    const int64_t e_max = warp_max(sc.e_max);
-    const int64_t e_min = warp_min(sc.e_min);
-    const int64_t e_rad = warp_max(sc.e_rad);
-    const uint64_t nnz = warp_sum(sc.nnz);
-    const Plan pl = finish_plan(e_max, e_min, e_rad, nnz, fb, total, A.prec, A.disable_reduction);
 
-    if (pl.status != 0) {
-        if (lane == 0) {
-            if (A.state) write_state(A.state + b, pl, 0, 0);
-            if (pl.status == 1) {
+    // ---- parallel finalize: lane g owns dot b0 + g
+    if (lane < nd) {
+        const int64_t b = b0 + lane;
+        if (my_pl.status != 0) {
+            if (A.state) write_state(A.state + b, my_pl, 0, 0);
+            if (my_pl.status == 1) {
                 A.fb_flag[b] = 1;
             } else {  // ZeroResult -> Ball::zero()
                 GFloat<1> z;
@@ -453,57 +524,12 @@ __global__ void __launch_bounds__(256) dot_small_kernel(DotArgs A) {
                 z.n = 0;
                 gf_store(A.out, b, z, mag_zero(), A.status);
             }
+        } else {
+            if (A.state) write_state(A.state + b, my_pl, my_err, my_srad);
+            if (A.acc)
+                for (int j = 0; j < my_pl.n_s && j < A.acc_stride; j++) A.acc[b * A.acc_stride + j] = my_s[j];
+            finalize_store<NS>(my_pl, my_s, my_err, my_srad, A.prec, with_radius, A.out, b, A.status);
         }
-        return;
-    }
-
-    // ---- pass 2: accumulate
-    Acc<L, NS> acc;
-#pragma unroll
-    for (int j = 0; j < NS; j++) acc.s[j] = 0;
-    acc.err = 0;
-    acc.srad = 0;
-    auto do_term = [&](const Term<L>& t) {
-        const bool xz = (t.kx & APB_KIND_MASK) == APB_ZERO, yz = (t.ky & APB_KIND_MASK) == APB_ZERO;
-        if (!xz && !yz) acc_term<L, NS>(acc, t, pl);
-        if (with_radius) rad_term<L, NS>(acc, t, pl);
-    };
-    if (TPL > 0) {
-#pragma unroll
-        for (int q = 0; q < (TPL > 0 ? TPL : 1); q++) {
-            int64_t i = lane + 32 * (int64_t)q;
-            if (i < total) do_term(keep[q]);
-        }
-    } else {
-        for (int64_t i = lane; i < total; i += 32) {
-            Term<L> t;
-            load_term<L>(t, A, b, i);
-            do_term(t);
-        }
-    }
-
-    // ---- warp reduction of (s, err, srad); s mod 2^(64 NS) with carries
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        uint64_t c = 0;
-#pragma unroll
-        for (int j = 0; j < NS; j++) {
-            uint64_t v = __shfl_xor_sync(0xffffffffu, acc.s[j], o);
-            uint64_t s1 = acc.s[j] + v;
-            uint64_t c1 = s1 < v;
-            uint64_t s2 = s1 + c;
-            uint64_t c2 = s2 < c;
-            acc.s[j] = s2;
-            c = c1 | c2;
-        }
-        acc.err += __shfl_xor_sync(0xffffffffu, acc.err, o);
-        acc.srad += __shfl_xor_sync(0xffffffffu, acc.srad, o);
-    }
-    if (lane == 0) {
-        if (A.state) write_state(A.state + b, pl, acc.err, acc.srad);
-        if (A.acc)
-            for (int j = 0; j < pl.n_s && j < A.acc_stride; j++) A.acc[b * A.acc_stride + j] = acc.s[j];
-        finalize_store<NS>(pl, acc.s, acc.err, acc.srad, A.prec, with_radius, A.out, b, A.status);
     }
 }
 
@@ -934,8 +960,9 @@ __global__ void __launch_bounds__(128) dot_complex_generic_kernel(CDotArgs A) {
 
 template <int L, int NS, int TPL>
 static void launch_small(const DotArgs& A, cudaStream_t st) {
-    const int warps = 8;
-    dim3 grid((unsigned)((A.batch + warps - 1) / warps));
+    const int warps = 4;  // each warp: 32 consecutive dots
+    const int64_t nwarps = (A.batch + 31) / 32;
+    dim3 grid((unsigned)((nwarps + warps - 1) / warps));
     dot_small_kernel<L, NS, TPL><<<grid, 32 * warps, 0, st>>>(A);
     count_launch();
 }
@@ -956,7 +983,8 @@ static int ns_bound(int64_t prec, int64_t total) {
 
 template <int L, int NS>
 static bool try_small_tpl(const DotArgs& A, int64_t total, cudaStream_t st) {
-    if (total <= 32 * 4 && L <= 2) {
+    static const bool no_keep = std::getenv("APB_DOT_RELOAD") != nullptr;  // tuning hook
+    if (total <= 32 * 4 && L <= 2 && !no_keep) {
         launch_small<L, NS, 4>(A, st);
     } else {
         launch_small<L, NS, 0>(A, st);

@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -233,82 +234,94 @@ __global__ void entry_windows_kernel(BallsView A, BallsView B, int64_t M, int64_
 }
 
 // ------------------------------------------------------------- K4 pack
-// bits [pos, pos+8) of the L-slot mantissa integer (0 outside)
-APB_DEV uint32_t get8(const uint64_t* m, int L, int64_t pos) {
-    if (pos >= 64 * (int64_t)L || pos <= -8) return 0;
-    uint32_t r;
-    if (pos < 0) {
-        r = (uint32_t)(m[0] << (-pos)) & 255u;
-    } else {
-        const int li = (int)(pos >> 6);
-        const int bo = (int)(pos & 63);
-        uint64_t v = m[li] >> bo;
-        if (bo > 56 && li + 1 < L) v |= m[li + 1] << (64 - bo);
-        r = (uint32_t)v & 255u;
-    }
-    return r;
+// Digit state of one scaled entry, streamed 8 digits at a time: the
+// magnitude bits come from two neighbouring mantissa limbs (funnel shift),
+// two's complement negation and balanced recoding run byte-serially.
+struct DigitStream {
+    const uint64_t* m;  // L top-aligned limbs (global, L1-cached)
+    int L;
+    int64_t sh;         // value = X_L * 2^sh
+    uint32_t negc, rc;
+    bool neg, live;
+};
+
+APB_DEV void ds_init(DigitStream& d, const BallsView& X, int64_t e, bool valid, int64_t scale) {
+    d.live = valid && (X.kind[e] & APB_KIND_MASK) == APB_FINITE;
+    d.negc = 1;
+    d.rc = 0;
+    d.L = X.L;
+    d.m = X.mant + e * (int64_t)X.L;
+    d.neg = d.live && (X.kind[e] & APB_SIGN) != 0;
+    d.sh = d.live ? X.exp[e] - 64 * (int64_t)X.L + scale : 0;
 }
 
-// Balanced signed-digit slices of x * 2^scale (exact integer, |.| < 2^(8S-2)):
-// out[s * plane + off] for s < S.  Zero / out-of-range entries give zero digits.
-APB_DEV void write_digits(const BallsView& X, int64_t e, bool valid, int64_t scale, int S,
-                          int8_t* out, size_t plane, size_t off) {
-    int kind = valid ? (X.kind[e] & APB_KIND_MASK) : APB_ZERO;
-    if (kind != APB_FINITE) {
-        for (int s = 0; s < S; s++) out[(size_t)s * plane + off] = 0;
-        return;
-    }
-    const bool neg = (X.kind[e] & APB_SIGN) != 0;
-    const uint64_t* m = X.mant + e * (int64_t)X.L;
-    // value = X_L * 2^sh,  X_L the L-slot integer
-    const int64_t sh = X.exp[e] - 64 * (int64_t)X.L + scale;
-    uint32_t negc = 1, rc = 0;
-    for (int s = 0; s < S; s++) {
-        uint32_t byte = get8(m, X.L, 8 * (int64_t)s - sh);
-        if (neg) {  // two's complement negation, byte-serial
-            uint32_t t = (255u - byte) + negc;
+// 64 bits of X_L starting at bit position q (zeros outside)
+APB_DEV uint64_t ds_word(const DigitStream& d, int64_t q) {
+    if (q >= 64 * (int64_t)d.L || q <= -64) return 0;
+    if (q < 0) return __ldg(d.m) << (-q);
+    const int li = (int)(q >> 6), bo = (int)(q & 63);
+    uint64_t v = __ldg(d.m + li) >> bo;
+    if (bo && li + 1 < d.L) v |= __ldg(d.m + li + 1) << (64 - bo);
+    return v;
+}
+
+// the next 8 balanced digits (bytes 8c .. 8c+7) packed little-endian
+APB_DEV uint64_t ds_next8(DigitStream& d, int c) {
+    if (!d.live) return 0;
+    uint64_t w = ds_word(d, 64 * (int64_t)c - d.sh);
+    uint64_t out = 0;
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        uint32_t byte = (uint32_t)(w >> (8 * b)) & 255u;
+        if (d.neg) {
+            const uint32_t t = (255u - byte) + d.negc;
             byte = t & 255u;
-            negc = t >> 8;
+            d.negc = t >> 8;
         }
-        uint32_t v = byte + rc;  // balanced recoding
-        int d;
-        if (v >= 128) {
-            d = (int)v - 256;
-            rc = 1;
-        } else {
-            d = (int)v;
-            rc = 0;
-        }
-        out[(size_t)s * plane + off] = (int8_t)d;
+        const uint32_t v = byte + d.rc;
+        d.rc = v >= 128 ? 1u : 0u;
+        out |= (uint64_t)(v & 255u) << (8 * b);  // (v - 256) as a byte == v & 255
     }
+    return out;
 }
 
-// A block [lo,hi): Apack[s][i][kk] = digit s of A[i][lo+kk] * 2^(e_i); kk < Kp
-__global__ void pack_a_kernel(BallsView A, int64_t M, int64_t K, int64_t lo, int64_t hi,
-                              const int64_t* rtop, const int64_t* rbot, int S, int Mp, int Kp,
-                              int8_t* out, int64_t* escale) {
+// Pack 4 consecutive inner indices per thread: plane[s][row][kk..kk+3] (one
+// 32-bit store per plane).  IS_B: entry (lo+kk, row) of B with column scale.
+template <bool IS_B>
+__global__ void __launch_bounds__(256) pack_kernel(BallsView X, int64_t rows, int64_t ld, int64_t lo,
+                                                   int64_t hi, const int64_t* top, const int64_t* bot, int S,
+                                                   int Rp, int Kp, int8_t* out, int64_t* scale_out) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= (int64_t)Mp * Kp) return;
-    const int64_t i = t / Kp, kk = t % Kp;
-    const bool valid = i < M && kk < hi - lo;
+    const int64_t kq = Kp / 4;
+    if (t >= (int64_t)Rp * kq) return;
+    const int64_t r = t / kq, kk0 = 4 * (t % kq);
     int64_t sc = 0;
-    if (i < M) sc = rtop[i] == INT64_MIN ? 0 : -rbot[i];
-    if (valid && kk == 0) escale[i] = sc;
-    write_digits(A, valid ? i * K + lo + kk : 0, valid, sc, S, out, (size_t)Mp * Kp, (size_t)t);
-}
-
-// B block rows [lo,hi): Bpack[t][j][kk] = digit t of B[lo+kk][j] * 2^(f_j)
-__global__ void pack_b_kernel(BallsView B, int64_t K, int64_t N, int64_t lo, int64_t hi,
-                              const int64_t* ctop, const int64_t* cbot, int S, int Np, int Kp,
-                              int8_t* out, int64_t* fscale) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= (int64_t)Np * Kp) return;
-    const int64_t j = t / Kp, kk = t % Kp;
-    const bool valid = j < N && kk < hi - lo;
-    int64_t sc = 0;
-    if (j < N) sc = ctop[j] == INT64_MIN ? 0 : -cbot[j];
-    if (valid && kk == 0) fscale[j] = sc;
-    write_digits(B, valid ? (lo + kk) * N + j : 0, valid, sc, S, out, (size_t)Np * Kp, (size_t)t);
+    if (r < rows) sc = top[r] == INT64_MIN ? 0 : -bot[r];
+    if (r < rows && kk0 == 0) scale_out[r] = sc;
+    DigitStream ds[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int64_t kk = kk0 + q;
+        const bool valid = r < rows && kk < hi - lo;
+        const int64_t e = valid ? (IS_B ? (lo + kk) * ld + r : r * ld + lo + kk) : 0;
+        ds_init(ds[q], X, e, valid, sc);
+    }
+    const size_t plane = (size_t)Rp * Kp;
+    uint32_t* dst = (uint32_t*)(out + (size_t)r * Kp + kk0);
+    for (int c = 0; c * 8 < S; c++) {
+        uint64_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) w[q] = ds_next8(ds[q], c);
+#pragma unroll
+        for (int b = 0; b < 8; b++) {
+            const int s = 8 * c + b;
+            if (s >= S) break;
+            const uint32_t word = ((uint32_t)(w[0] >> (8 * b)) & 255u) | (((uint32_t)(w[1] >> (8 * b)) & 255u) << 8) |
+                                  (((uint32_t)(w[2] >> (8 * b)) & 255u) << 16) |
+                                  (((uint32_t)(w[3] >> (8 * b)) & 255u) << 24);
+            dst[(size_t)s * plane / 4] = word;
+        }
+    }
 }
 
 // -------------------------------------------------------- K6 recombine
@@ -329,6 +342,7 @@ struct RecombineArgs {
     int* status;
 };
 
+template <int CAP>
 __global__ void __launch_bounds__(128) recombine_kernel(RecombineArgs R) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= R.M * R.N) return;
@@ -337,7 +351,7 @@ __global__ void __launch_bounds__(128) recombine_kernel(RecombineArgs R) {
     const size_t off = (size_t)i * R.Np + j;
     // T = (bytes as unsigned) + sum_g carry_g * 256^(d1_g), two's complement in NT limbs
     const int NT = (R.nwords + 1) / 2 + 2;
-    uint64_t T[GCAP];
+    uint64_t T[CAP];
     for (int q = 0; q < NT; q++) T[q] = 0;
     for (int w = 0; w < R.nwords; w++) T[w >> 1] |= (uint64_t)R.Tw[(size_t)w * plane + off] << (32 * (w & 1));
     for (int g = 0; g < R.n_groups; g++) {
@@ -386,18 +400,23 @@ __global__ void __launch_bounds__(128) recombine_kernel(RecombineArgs R) {
         return;
     }
     // apfloat_from_bigint_scaled(v, -e_i - f_j) (src/bigint.cpp:187-191)
-    GF v;
+    GFloat<CAP> v;
     const int64_t exp2 = -R.escale[i] - R.fscale[j];
     gf_normalize(v, neg ? 1 : 0, checked_add(64 * (int64_t)NT, exp2, R.status), T, NT, R.status);
     if (R.first) {
         Mag err = gf_round(v, R.prec, R.status);  // ball_add(0, v): apfloat_round
         gf_store(R.C, t, v, err, R.status);
     } else {
-        GF c;
+        GF c, vv;
+        vv.kind = v.kind;
+        vv.neg = v.neg;
+        vv.e = v.e;
+        vv.n = v.n;
+        for (int q = 0; q < v.n; q++) vv.d[q] = v.d[q];
         BallsView cv{R.C.mant, R.C.exp, R.C.kind, R.C.rad_man, R.C.rad_exp, R.C.L};
         gf_load(c, cv, t);
         Mag crad = mag_load(R.C.rad_man[t], R.C.rad_exp[t]);
-        Mag err = gf_add_round(c, c, v, R.prec, R.status);  // ball_add (src/ball.cpp:15-19)
+        Mag err = gf_add_round(c, c, vv, R.prec, R.status);  // ball_add (src/ball.cpp:15-19)
         if (c.kind == APB_NAN) {
             gf_store(R.C, t, c, mag_inf(), R.status);
         } else {
@@ -596,6 +615,111 @@ __global__ void __launch_bounds__(64) rad_gemm_kernel(const double* __restrict__
         }
 }
 
+
+// ---- sparse radius products (bit-exact: skipping exact zero terms leaves every
+// RN partial sum unchanged since s + (+0.0) == s for s >= 0)
+// ordered nonzero lists of a plane: columns of db (w x N) / rows of da (M x w)
+__global__ void col_lists_kernel(const double* __restrict__ db, int64_t w, int64_t N, int* cnt, int* idx,
+                                 double* val) {
+    const int lane = threadIdx.x & 31;
+    const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (j >= N) return;
+    int base = 0;
+    for (int64_t l0 = 0; l0 < w; l0 += 32) {
+        const int64_t l = l0 + lane;
+        const double v = l < w ? db[l * N + j] : 0.0;
+        const unsigned m = __ballot_sync(0xffffffffu, v != 0.0);
+        if (v != 0.0) {
+            const int pos = base + __popc(m & ((1u << lane) - 1u));
+            idx[j * w + pos] = (int)l;
+            val[j * w + pos] = v;
+        }
+        base += __popc(m);
+    }
+    if (lane == 0) cnt[j] = base;
+}
+
+__global__ void row_lists_kernel(const double* __restrict__ da, int64_t M, int64_t w, int* cnt, int* idx,
+                                 double* val) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= M) return;
+    int base = 0;
+    for (int64_t l0 = 0; l0 < w; l0 += 32) {
+        const int64_t l = l0 + lane;
+        const double v = l < w ? da[i * w + l] : 0.0;
+        const unsigned m = __ballot_sync(0xffffffffu, v != 0.0);
+        if (v != 0.0) {
+            const int pos = base + __popc(m & ((1u << lane) - 1u));
+            idx[i * w + pos] = (int)l;
+            val[i * w + pos] = v;
+        }
+        base += __popc(m);
+    }
+    if (lane == 0) cnt[i] = base;
+}
+
+APB_DEV void rad_fold(Mag& ent, double& s, int64_t e_i, int64_t f_j) {
+    if (s != 0.0) ent = mag_add(ent, mag_mul(mag_from_double(s, -e_i - f_j), mag_parts((1ull << 29) + 1, 1)));
+    s = 0.0;
+}
+
+// out(i,j) over the nonzero list of column j of db; thread per (i, j)
+__global__ void __launch_bounds__(256) rad_spcol_kernel(const double* __restrict__ da, int64_t M, int64_t N,
+                                                        int64_t w, const int* cnt, const int* idx,
+                                                        const double* val, const int64_t* ecen,
+                                                        const int64_t* fcen, uint32_t* rb, int64_t* rf) {
+    const int64_t j = (int64_t)blockIdx.x * 32 + (threadIdx.x & 31);
+    const int64_t i = (int64_t)blockIdx.y * 8 + (threadIdx.x >> 5);
+    if (i >= M || j >= N) return;
+    double s = 0.0;
+    Mag ent = mag_zero();
+    int64_t chunk_end = 1024;
+    const int n = cnt[j];
+    const double* arow = da + i * w;
+    for (int p = 0; p < n; p++) {
+        const int l = idx[j * w + p];
+        if (l >= chunk_end) {
+            rad_fold(ent, s, ecen[i], fcen[j]);
+            chunk_end = ((int64_t)l / 1024 + 1) * 1024;
+        }
+        s = __dadd_rn(s, __dmul_rn(arow[l], val[j * w + p]));
+    }
+    rad_fold(ent, s, ecen[i], fcen[j]);
+    mag_store(ent, &rb[i * N + j], &rf[i * N + j]);
+}
+
+// out(i,j) over the nonzero list of row i of da; thread per (i, j)
+__global__ void __launch_bounds__(256) rad_sprow_kernel(const double* __restrict__ db, int64_t M, int64_t N,
+                                                        int64_t w, const int* cnt, const int* idx,
+                                                        const double* val, const int64_t* ecen,
+                                                        const int64_t* fcen, uint32_t* rb, int64_t* rf) {
+    const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    const int64_t i = blockIdx.y;
+    if (j >= N) return;
+    double s = 0.0;
+    Mag ent = mag_zero();
+    int64_t chunk_end = 1024;
+    const int n = cnt[i];
+    for (int p = 0; p < n; p++) {
+        const int l = idx[i * w + p];
+        if (l >= chunk_end) {
+            rad_fold(ent, s, ecen[i], fcen[j]);
+            chunk_end = ((int64_t)l / 1024 + 1) * 1024;
+        }
+        s = __dadd_rn(s, __dmul_rn(val[i * w + p], db[(int64_t)l * N + j]));
+    }
+    rad_fold(ent, s, ecen[i], fcen[j]);
+    mag_store(ent, &rb[i * N + j], &rf[i * N + j]);
+}
+
+__global__ void count_nonzero_kernel(const double* p, int64_t n, unsigned long long* cnt) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool nz = t < n && p[t] != 0.0;
+    const unsigned m = __ballot_sync(0xffffffffu, nz);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(cnt, (unsigned long long)__popc(m));
+}
+
 // C.rad = mag_add(C.rad, mag_add(r1, r2)) (src/matmul.cpp:512-513)
 __global__ void rad_combine_kernel(BallsOut C, int64_t cnt, const uint32_t* r1b, const int64_t* r1f,
                                    const uint32_t* r2b, const int64_t* r2f) {
@@ -648,8 +772,8 @@ T* ws_buf(int slot, size_t count, cudaStream_t st) {
 
 struct Scratch {
     // separate allocations owned here (the Workspace slot table is small)
-    void* p[32] = {};
-    size_t cap[32] = {};
+    void* p[48] = {};
+    size_t cap[48] = {};
     void* get(int k, size_t bytes, cudaStream_t st) {
         if (cap[k] < bytes) {
             if (p[k]) {
@@ -673,7 +797,7 @@ Scratch& scratch() {
 }
 enum {
     S_RTOP, S_RBOT, S_CTOP, S_CBOT, S_SUM, S_APACK, S_BPACK, S_TW, S_TC, S_UNITS, S_ESC, S_FSC,
-    S_WA, S_WB, S_GREEDY, S_DA, S_DB, S_CEN_E, S_CEN_F, S_R1B, S_R1F, S_R2B, S_R2F, S_MISC, S_CTOP2, S_CBOT2
+    S_WA, S_WB, S_GREEDY, S_DA, S_DB, S_CEN_E, S_CEN_F, S_R1B, S_R1F, S_R2B, S_R2F, S_MISC, S_CTOP2, S_CBOT2, S_LCNT, S_LIDX, S_LVAL, S_DA2, S_DB2, S_CEN_E2, S_CEN_F2, S_RW1, S_RW2, S_LCNT2, S_LIDX2, S_LVAL2
 };
 template <class T>
 T* sbuf(int k, size_t count, cudaStream_t st) {
@@ -731,36 +855,39 @@ struct Plan {
     int64_t prec_a = 0, prec_b = 0;
 };
 
-int plan(const apb_mat* A, const apb_mat* B, int64_t prec, Plan& P, cudaStream_t st) {
+// K3 launch: midpoint windows, specials and entry precision into `sum` (no sync)
+int plan_launch(const apb_mat* A, const apb_mat* B, ScanSummary* sum, cudaStream_t st) {
     const int64_t M = A->rows, K = A->cols, N = B->cols;
     BallsView a = view_of(&A->b), b = view_of(&B->b);
     int64_t* rtop = sbuf<int64_t>(S_RTOP, M, st);
     int64_t* rbot = sbuf<int64_t>(S_RBOT, M, st);
     int64_t* ctop = sbuf<int64_t>(S_CTOP, N, st);
     int64_t* cbot = sbuf<int64_t>(S_CBOT, N, st);
-    ScanSummary* sum = sbuf<ScanSummary>(S_SUM, 1, st);
     if (!rtop || !rbot || !ctop || !cbot || !sum) return APB_ERR_CUDA;
     cudaMemsetAsync(sum, 0, sizeof(ScanSummary), st);
     scan_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(a, M, K, 0, K, rtop, rbot, sum);
     scan_cols(b, K, N, 0, K, ctop, cbot, sum, st);
     count_launch(1);
-    static ScanSummary* hsum = nullptr;
-    if (!hsum) cudaMallocHost(&hsum, sizeof(ScanSummary));
-    cudaMemcpyAsync(hsum, sum, sizeof(ScanSummary), cudaMemcpyDeviceToHost, st);
-    int rc = cuda_check(cudaStreamSynchronize(st), "matmul plan scan");
-    if (rc) return rc;
-    P.special = hsum->special_a || hsum->special_b;
+    return APB_OK;
+}
+
+// K3 finish (host, after the sync): plan_blocks (src/matmul.cpp:132-161)
+int plan_finish(const apb_mat* A, const apb_mat* B, int64_t prec, const ScanSummary& hs, Plan& P,
+                cudaStream_t st) {
+    const int64_t M = A->rows, K = A->cols, N = B->cols;
+    BallsView a = view_of(&A->b), b = view_of(&B->b);
+    int rc;
+    P.special = hs.special_a || hs.special_b;
     if (P.special) return APB_OK;
-    P.maxw_a = hsum->maxw_a;
-    P.maxw_b = hsum->maxw_b;
-    P.prec_a = hsum->prec_a;
-    P.prec_b = hsum->prec_b;
-    // plan_blocks (src/matmul.cpp:132-161)
-    int64_t pm = std::max<int64_t>(hsum->prec_a, hsum->prec_b);
+    P.maxw_a = hs.maxw_a;
+    P.maxw_b = hs.maxw_b;
+    P.prec_a = hs.prec_a;
+    P.prec_b = hs.prec_b;
+    int64_t pm = std::max<int64_t>(hs.prec_a, hs.prec_b);
     pm = std::min<int64_t>(prec, pm);
     const int64_t h = (5 * pm) / 4 + 192;
     std::vector<int64_t> raw;
-    if (hsum->maxw_a <= h && hsum->maxw_b <= h) {
+    if (hs.maxw_a <= h && hs.maxw_b <= h) {
         raw = {0, K};  // every window fits: greedy takes all of [0,K)
     } else {
         longlong2* wA = sbuf<longlong2>(S_WA, (size_t)M * K, st);
@@ -796,6 +923,22 @@ int plan(const apb_mat* A, const apb_mat* B, int64_t prec, Plan& P, cudaStream_t
         }
     }
     return APB_OK;
+}
+
+ScanSummary* pinned_summary() {
+    static ScanSummary* h = nullptr;
+    if (!h) cudaMallocHost(&h, sizeof(ScanSummary) + 8 * sizeof(long long));
+    return h;
+}
+
+int plan(const apb_mat* A, const apb_mat* B, int64_t prec, Plan& P, cudaStream_t st) {
+    ScanSummary* sum = sbuf<ScanSummary>(S_SUM, 1, st);
+    int rc = plan_launch(A, B, sum, st);
+    if (rc) return rc;
+    ScanSummary* hs = pinned_summary();
+    cudaMemcpyAsync(hs, sum, sizeof(ScanSummary), cudaMemcpyDeviceToHost, st);
+    if ((rc = cuda_check(cudaStreamSynchronize(st), "matmul plan scan"))) return rc;
+    return plan_finish(A, B, prec, *hs, P, st);
 }
 
 // slice count for an exact |value| < 2^H with balanced digits (headroom 2 bits)
@@ -895,8 +1038,8 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         return APB_ERR_CUDA;
     }
     int tok = prof_begin("pack", st);
-    pack_a_kernel<<<blocks_for((int64_t)Mp * Kp, 256), 256, 0, st>>>(a, M, K, lo, hi, rtop, rbot, SA, Mp, Kp, Ap, esc);
-    pack_b_kernel<<<blocks_for((int64_t)Np * Kp, 256), 256, 0, st>>>(b, K, N, lo, hi, ctop, cbot, SB, Np, Kp, Bp, fsc);
+    pack_kernel<false><<<blocks_for((int64_t)Mp * Kp / 4, 256), 256, 0, st>>>(a, M, K, lo, hi, rtop, rbot, SA, Mp, Kp, Ap, esc);
+    pack_kernel<true><<<blocks_for((int64_t)Np * Kp / 4, 256), 256, 0, st>>>(b, N, N, lo, hi, ctop, cbot, SB, Np, Kp, Bp, fsc);
     prof_end(tok, st);
     count_launch(2);
     const int tiles = (Mp / kSliceTile) * (Np / kSliceTile);
@@ -958,27 +1101,32 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         std::memcpy(host.data() + off_d1, U.group_d1.data(), U.group_d1.size() * sizeof(int));
     }
     const size_t ubytes = host.size();
-    static char* hstage = nullptr;
-    static size_t hcap = 0;
-    if (hcap < ubytes) {
-        if (hstage) {
-            cudaStreamSynchronize(st);
-            cudaFreeHost(hstage);
-        }
-        cudaMallocHost(&hstage, ubytes * 2);
-        hcap = ubytes * 2;
+    // the tables depend only on (band, S_A, S_B, w, tile grid): cache device copies
+    static std::map<std::vector<int64_t>, char*> table_cache;
+    const std::vector<int64_t> key = {band ? 1 : 0, SA, SB, w, Mp, Np};
+    char* dunits;
+    auto hit = table_cache.find(key);
+    if (hit != table_cache.end()) {
+        dunits = hit->second;
     } else {
-        cudaStreamSynchronize(st);  // previous upload finished before reuse
+        if (cudaMalloc(&dunits, ubytes) != cudaSuccess) {
+            set_error("out of device memory (unit tables)");
+            return APB_ERR_CUDA;
+        }
+        cudaMemcpy(dunits, host.data(), ubytes, cudaMemcpyHostToDevice);
+        if (table_cache.size() > 256) {  // bounded cache
+            cudaDeviceSynchronize();
+            for (auto& kv : table_cache) cudaFree(kv.second);
+            table_cache.clear();
+        }
+        table_cache[key] = dunits;
     }
-    std::memcpy(hstage, host.data(), ubytes);
-    char* dunits = sbuf<char>(S_UNITS, ubytes, st);
     uint32_t* Tw = sbuf<uint32_t>(S_TW, (size_t)NW * Mp * Np, st);
     int32_t* Tc = sbuf<int32_t>(S_TC, (size_t)G * Mp * Np, st);
-    if (!dunits || !Tw || !Tc) {
+    if (!Tw || !Tc) {
         set_error("out of device memory (product planes)");
         return APB_ERR_CUDA;
     }
-    cudaMemcpyAsync(dunits, hstage, ubytes, cudaMemcpyHostToDevice, st);
     int rc;
     const int* d_group_d1 = (const int*)(dunits + off_d1);
     if (band) {
@@ -1035,7 +1183,14 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     R.int_limbs = int_limbs;
     R.status = workspace().status_dev;
     tok = prof_begin("recombine", st);
-    recombine_kernel<<<blocks_for(M * N, 128), 128, 0, st>>>(R);
+    {
+        const int NT = (NW + 1) / 2 + 2;
+        const unsigned gb = blocks_for(M * N, 128);
+        if (NT <= 8) recombine_kernel<8><<<gb, 128, 0, st>>>(R);
+        else if (NT <= 16) recombine_kernel<16><<<gb, 128, 0, st>>>(R);
+        else if (NT <= 40) recombine_kernel<40><<<gb, 128, 0, st>>>(R);
+        else recombine_kernel<GCAP><<<gb, 128, 0, st>>>(R);
+    }
     prof_end(tok, st);
     count_launch();
     return cuda_check(cudaGetLastError(), "recombine");
@@ -1053,24 +1208,74 @@ void rad_center_cols(const BallsView& b, int64_t K, int64_t N, int64_t lo, int64
 }
 
 // radius_matmul_upper(P, Q) into (rb, rf) for operand kinds (wa of A, wb of B)
-int radius_product(const apb_mat* A, const apb_mat* B, int wa, int wb, uint32_t* rb, int64_t* rf,
-                   cudaStream_t st) {
+struct RadSlots {
+    int da, db, ce, cf, mw, lcnt, lidx, lval;
+};
+const RadSlots kRad[2] = {{S_DA, S_DB, S_CEN_E, S_CEN_F, S_RW1, S_LCNT, S_LIDX, S_LVAL},
+                          {S_DA2, S_DB2, S_CEN_E2, S_CEN_F2, S_RW2, S_LCNT2, S_LIDX2, S_LVAL2}};
+
+// radius_matmul_upper phase 1 (no sync): single-block centring, exact double
+// planes, window widths and nonzero counts into mw[0..3]
+int radius_prepare(const apb_mat* A, const apb_mat* B, int wa, int wb, int slot, cudaStream_t st) {
+    const RadSlots& R = kRad[slot];
     const int64_t M = A->rows, K = A->cols, N = B->cols;
     BallsView a = view_of(&A->b), b = view_of(&B->b);
-    int64_t* ecen = sbuf<int64_t>(S_CEN_E, M, st);
-    int64_t* fcen = sbuf<int64_t>(S_CEN_F, N, st);
-    long long* mw = sbuf<long long>(S_SUM, 2, st);
-    cudaMemsetAsync(mw, 0, 2 * sizeof(long long), st);
+    int64_t* ecen = sbuf<int64_t>(R.ce, M, st);
+    int64_t* fcen = sbuf<int64_t>(R.cf, N, st);
+    long long* mw = sbuf<long long>(R.mw, 4, st);
+    double* da = sbuf<double>(R.da, (size_t)M * K, st);
+    double* db = sbuf<double>(R.db, (size_t)K * N, st);
+    if (!ecen || !fcen || !mw || !da || !db) return APB_ERR_CUDA;
+    cudaMemsetAsync(mw, 0, 4 * sizeof(long long), st);
     rad_center_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(a, M, K, 0, K, wa, ecen, mw);
     rad_center_cols(b, K, N, 0, K, wb, fcen, mw + 1, st);
-    count_launch(1);
-    long long hw[2];
-    cudaMemcpyAsync(hw, mw, sizeof hw, cudaMemcpyDeviceToHost, st);
-    int rc = cuda_check(cudaStreamSynchronize(st), "radius windows");
-    if (rc) return rc;
-    std::vector<int64_t> blocks = {0, K};
-    if (hw[0] > 900 || hw[1] > 900) {
-        // greedy split with h = 900 on the Mag windows (f, f-30) (src/matmul.cpp:386-392)
+    rad_planes_kernel<<<blocks_for(M * K, 256), 256, 0, st>>>(a, M, K, 0, K, wa, 1, ecen, da);
+    rad_planes_kernel<<<blocks_for(K * N, 256), 256, 0, st>>>(b, K, N, 0, K, wb, 0, fcen, db);
+    count_nonzero_kernel<<<blocks_for(M * K, 256), 256, 0, st>>>(da, M * K, (unsigned long long*)(mw + 2));
+    count_nonzero_kernel<<<blocks_for(K * N, 256), 256, 0, st>>>(db, K * N, (unsigned long long*)(mw + 3));
+    count_launch(5);
+    return APB_OK;
+}
+
+// phase 2, given hw = mw copied to the host: sparse / dense single block, or the
+// multi-block greedy path (which synchronizes `st` itself)
+int radius_compute(const apb_mat* A, const apb_mat* B, int wa, int wb, int slot, const long long* hw,
+                   uint32_t* rb, int64_t* rf, cudaStream_t st) {
+    const RadSlots& R = kRad[slot];
+    const int64_t M = A->rows, K = A->cols, N = B->cols;
+    BallsView a = view_of(&A->b), b = view_of(&B->b);
+    int64_t* ecen = sbuf<int64_t>(R.ce, M, st);
+    int64_t* fcen = sbuf<int64_t>(R.cf, N, st);
+    double* da = sbuf<double>(R.da, (size_t)M * K, st);
+    double* db = sbuf<double>(R.db, (size_t)K * N, st);
+    int rc;
+    if (hw[0] <= 900 && hw[1] <= 900) {
+        // sparse products when one radius side is mostly exact (config 3: 95% of entries)
+        const double dens_a = M * K ? (double)hw[2] / (double)(M * K) : 1.0;
+        const double dens_b = K * N ? (double)hw[3] / (double)(K * N) : 1.0;
+        int* lcnt = sbuf<int>(R.lcnt, (size_t)std::max(M, N), st);
+        int* lidx = sbuf<int>(R.lidx, (size_t)K * std::max(M, N), st);
+        double* lval = sbuf<double>(R.lval, (size_t)K * std::max(M, N), st);
+        const int tk = prof_begin("rad_gemm", st);
+        if (dens_b <= 0.25 && dens_b <= dens_a && lcnt && lidx && lval) {
+            col_lists_kernel<<<blocks_for(N, 8), 256, 0, st>>>(db, K, N, lcnt, lidx, lval);
+            dim3 grid(blocks_for(N, 32), blocks_for(M, 8));
+            rad_spcol_kernel<<<grid, 256, 0, st>>>(da, M, N, K, lcnt, lidx, lval, ecen, fcen, rb, rf);
+        } else if (dens_a <= 0.25 && lcnt && lidx && lval) {
+            row_lists_kernel<<<blocks_for(M, 8), 256, 0, st>>>(da, M, K, lcnt, lidx, lval);
+            dim3 grid(blocks_for(N, 256), (unsigned)M);
+            rad_sprow_kernel<<<grid, 256, 0, st>>>(db, M, N, K, lcnt, lidx, lval, ecen, fcen, rb, rf);
+        } else {
+            dim3 grid(blocks_for(N, RT), blocks_for(M, RT));
+            rad_gemm_kernel<<<grid, RTHREADS, 0, st>>>(da, db, M, N, K, ecen, fcen, rb, rf, 0);
+        }
+        prof_end(tk, st);
+        count_launch(2);
+        return cuda_check(cudaGetLastError(), "radius product");
+    }
+    // greedy split with h = 900 on the Mag windows (f, f-30) (src/matmul.cpp:386-392)
+    std::vector<int64_t> blocks;
+    {
         longlong2* wA = sbuf<longlong2>(S_WA, (size_t)M * K, st);
         longlong2* wB = sbuf<longlong2>(S_WB, (size_t)N * K, st);
         int64_t* gout = sbuf<int64_t>(S_GREEDY, 2 * (size_t)K + 2, st);
@@ -1093,14 +1298,10 @@ int radius_product(const apb_mat* A, const apb_mat* B, int wa, int wb, uint32_t*
     }
     for (size_t bi = 0; bi + 1 < blocks.size(); bi += 2) {
         const int64_t lo = blocks[bi], hi = blocks[bi + 1], w = hi - lo;
-        if (blocks.size() > 2) {  // centring over this block only
-            rad_center_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(a, M, K, lo, hi, wa, ecen, nullptr);
-            rad_center_cols(b, K, N, lo, hi, wb, fcen, nullptr, st);
-            count_launch(1);
-        }
-        double* da = sbuf<double>(S_DA, (size_t)M * w, st);
-        double* db = sbuf<double>(S_DB, (size_t)w * N, st);
-        if (!da || !db) return APB_ERR_CUDA;
+        // centring over this block only
+        rad_center_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(a, M, K, lo, hi, wa, ecen, nullptr);
+        rad_center_cols(b, K, N, lo, hi, wb, fcen, nullptr, st);
+        count_launch(1);
         rad_planes_kernel<<<blocks_for(M * w, 256), 256, 0, st>>>(a, M, K, lo, hi, wa, 1, ecen, da);
         rad_planes_kernel<<<blocks_for(w * N, 256), 256, 0, st>>>(b, K, N, lo, hi, wb, 0, fcen, db);
         dim3 grid(blocks_for(N, RT), blocks_for(M, RT));
@@ -1112,14 +1313,69 @@ int radius_product(const apb_mat* A, const apb_mat* B, int wa, int wb, uint32_t*
     return cuda_check(cudaGetLastError(), "radius product");
 }
 
-int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, cudaStream_t st) {
-    Plan P;
-    int rc = plan(A, B, prec, P, st);
+// radius_matmul_upper(P, Q) for operand kinds (wa of A, wb of B), synchronous planning
+int radius_product(const apb_mat* A, const apb_mat* B, int wa, int wb, uint32_t* rb, int64_t* rf,
+                   cudaStream_t st) {
+    int rc = radius_prepare(A, B, wa, wb, 0, st);
     if (rc) return rc;
+    long long* hw = (long long*)(pinned_summary() + 1);
+    cudaMemcpyAsync(hw, sbuf<long long>(kRad[0].mw, 4, st), 4 * sizeof(long long), cudaMemcpyDeviceToHost, st);
+    if ((rc = cuda_check(cudaStreamSynchronize(st), "radius windows"))) return rc;
+    long long h[4] = {hw[0], hw[1], hw[2], hw[3]};
+    return radius_compute(A, B, wa, wb, 0, h, rb, rf, st);
+}
+
+cudaStream_t side_stream() {
+    static cudaStream_t s = [] {
+        cudaStream_t t;
+        cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking);
+        return t;
+    }();
+    return s;
+}
+
+int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, cudaStream_t st) {
+    // one host synchronisation: midpoint plan scans + both radius products' windows
+    ScanSummary* sum = sbuf<ScanSummary>(S_SUM, 1, st);
+    int rc = plan_launch(A, B, sum, st);
+    if (rc) return rc;
+    if ((rc = radius_prepare(A, B, 0, 2, 0, st))) return rc;  // |A| R_B
+    if ((rc = radius_prepare(A, B, 1, 3, 1, st))) return rc;  // R_A (|B| + R_B)
+    ScanSummary* hs = pinned_summary();
+    long long* hw = (long long*)(hs + 1);
+    cudaMemcpyAsync(hs, sum, sizeof(ScanSummary), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hw, sbuf<long long>(kRad[0].mw, 4, st), 4 * sizeof(long long), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hw + 4, sbuf<long long>(kRad[1].mw, 4, st), 4 * sizeof(long long), cudaMemcpyDeviceToHost, st);
+    if ((rc = cuda_check(cudaStreamSynchronize(st), "matmul plan"))) return rc;
+    const ScanSummary hsum = *hs;
+    long long hw1[4], hw2[4];
+    for (int q = 0; q < 4; q++) {
+        hw1[q] = hw[q];
+        hw2[q] = hw[4 + q];
+    }
+    Plan P;
+    if ((rc = plan_finish(A, B, prec, hsum, P, st))) return rc;
     if (P.special) return classical(A, B, prec, C, st);  // src/matmul.cpp:455-458
     stats().block_calls++;
     stats().last_block_count = P.steps.size() / 3;
     const int64_t M = A->rows, N = B->cols;
+    // R_C += |A| R_B + R_A (|B| + R_B): FP64 work on a side stream, overlapping the
+    // tensor-core midpoint product (independent inputs)
+    uint32_t* r1b = sbuf<uint32_t>(S_R1B, (size_t)M * N, st);
+    int64_t* r1f = sbuf<int64_t>(S_R1F, (size_t)M * N, st);
+    uint32_t* r2b = sbuf<uint32_t>(S_R2B, (size_t)M * N, st);
+    int64_t* r2f = sbuf<int64_t>(S_R2F, (size_t)M * N, st);
+    if (!r1b || !r1f || !r2b || !r2f) return APB_ERR_CUDA;
+    const bool rad_multi = hw1[0] > 900 || hw1[1] > 900 || hw2[0] > 900 || hw2[1] > 900;
+    cudaStream_t rs = rad_multi ? st : side_stream();  // the multi-block radius path syncs its stream
+    static cudaEvent_t ev_join = [] {
+        cudaEvent_t e;
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        return e;
+    }();
+    if ((rc = radius_compute(A, B, 0, 2, 0, hw1, r1b, r1f, rs))) return rc;
+    if ((rc = radius_compute(A, B, 1, 3, 1, hw2, r2b, r2f, rs))) return rc;
+    if (rs != st) cudaEventRecord(ev_join, rs);
     bool first = true;
     const bool single = P.steps.size() == 3 && P.steps[0] == 0 && P.steps[1] == A->cols;
     for (size_t s = 0; s < P.steps.size(); s += 3) {
@@ -1147,14 +1403,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         }
         first = false;
     }
-    // R_C += |A| R_B + R_A (|B| + R_B)
-    uint32_t* r1b = sbuf<uint32_t>(S_R1B, (size_t)M * N, st);
-    int64_t* r1f = sbuf<int64_t>(S_R1F, (size_t)M * N, st);
-    uint32_t* r2b = sbuf<uint32_t>(S_R2B, (size_t)M * N, st);
-    int64_t* r2f = sbuf<int64_t>(S_R2F, (size_t)M * N, st);
-    if (!r1b || !r1f || !r2b || !r2f) return APB_ERR_CUDA;
-    if ((rc = radius_product(A, B, 0, 2, r1b, r1f, st))) return rc;
-    if ((rc = radius_product(A, B, 1, 3, r2b, r2f, st))) return rc;
+    if (rs != st) cudaStreamWaitEvent(st, ev_join, 0);
     rad_combine_kernel<<<blocks_for(M * N, 256), 256, 0, st>>>(out_of(&C->b), M * N, r1b, r1f, r2b, r2f);
     count_launch();
     return cuda_check(cudaGetLastError(), "block matmul");
