@@ -205,6 +205,8 @@ int apb_dot_batch_host(const apb_balls* x, const apb_balls* y, const apb_balls* 
                        int subtract, const apb_dot_index* idx, int64_t n, int64_t batch,
                        int64_t prec, int mode, apb_balls* out);
 int apb_matmul_host(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, apb_mat* C);
+int apb_matmul_complex_host(const apb_mat* Are, const apb_mat* Aim, const apb_mat* Bre,
+                            const apb_mat* Bim, int64_t prec, int algo, apb_mat* Cre, apb_mat* Cim);
 
 /* ------------------------------------------------------------------ misc */
 

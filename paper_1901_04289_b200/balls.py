@@ -204,11 +204,12 @@ class DeviceBallArray:
     @staticmethod
     def empty(count: int, L: int, device="cuda") -> "DeviceBallArray":
         import torch
-        return DeviceBallArray(torch.zeros((count, L), dtype=torch.int64, device=device),
-                               torch.zeros(count, dtype=torch.int64, device=device),
-                               torch.zeros(count, dtype=torch.uint8, device=device),
-                               torch.zeros(count, dtype=torch.int32, device=device),
-                               torch.zeros(count, dtype=torch.int64, device=device))
+        # every entry is written by the kernels; no fill launches
+        return DeviceBallArray(torch.empty((count, L), dtype=torch.int64, device=device),
+                               torch.empty(count, dtype=torch.int64, device=device),
+                               torch.empty(count, dtype=torch.uint8, device=device),
+                               torch.empty(count, dtype=torch.int32, device=device),
+                               torch.empty(count, dtype=torch.int64, device=device))
 
     def c(self) -> apb_balls:
         return apb_balls(self.mant.data_ptr(), self.exp.data_ptr(), self.kind.data_ptr(),

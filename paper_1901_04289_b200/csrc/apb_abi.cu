@@ -321,4 +321,18 @@ int apb_matmul_host(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, 
     return apb_device_status(st);
 }
 
+int apb_matmul_complex_host(const apb_mat* Are, const apb_mat* Aim, const apb_mat* Bre,
+                            const apb_mat* Bim, int64_t prec, int algo, apb_mat* Cre, apb_mat* Cim) {
+    cudaStream_t st = host_stream();
+    apb_mat d[6] = {*Are, *Aim, *Bre, *Bim, *Cre, *Cim};
+    const apb_mat* h[6] = {Are, Aim, Bre, Bim, Cre, Cim};
+    int rc;
+    for (int q = 0; q < 6; q++)  // workspace slots 32..61
+        if ((rc = to_device(&h[q]->b, &d[q].b, 32 + 5 * q, st, q < 4))) return rc;
+    if ((rc = apb_matmul_complex(&d[0], &d[1], &d[2], &d[3], prec, algo, &d[4], &d[5], st))) return rc;
+    if ((rc = to_host(&d[4].b, &Cre->b, st))) return rc;
+    if ((rc = to_host(&d[5].b, &Cim->b, st))) return rc;
+    return apb_device_status(st);
+}
+
 }  // extern "C"

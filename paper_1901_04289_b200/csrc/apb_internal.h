@@ -16,8 +16,8 @@ namespace apb {
 // device (exponent overflow = std::overflow_error in the reference).
 struct Workspace {
     int* status_dev = nullptr;
-    void* bufs[32] = {};
-    size_t caps[32] = {};
+    void* bufs[64] = {};
+    size_t caps[64] = {};
     void* scratch(cudaStream_t st, size_t bytes, int slot);
 };
 Workspace& workspace();

@@ -458,6 +458,195 @@ __global__ void mag_entry_windows_kernel(BallsView A, BallsView B, int64_t M, in
     }
 }
 
+
+// ------------------------------------------------- fused plan scan (K3 + K7)
+// One pass over A (rows) and one over B (columns) collects, per line, three
+// bit windows with int64 atomics: the midpoint window (planner, scaling) and
+// the Mag windows of the two radius operands on that side (|A|, R_A for rows;
+// R_B, |B|+R_B for columns), plus specials and entry precision.
+struct LineWins {
+    int64_t* top[3];
+    int64_t* bot[3];
+};
+
+__global__ void init_wins_kernel(LineWins W, int64_t n) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        W.top[q][t] = INT64_MIN;
+        W.bot[q][t] = INT64_MAX;
+    }
+}
+
+APB_DEV void win_merge(int64_t& top, int64_t& bot, int64_t t, int64_t b) {
+    top = t > top ? t : top;
+    bot = b < bot ? b : bot;
+}
+
+APB_DEV void win_atomic(int64_t* top, int64_t* bot, int64_t t, int64_t b) {
+    if (t == INT64_MIN) return;
+    atomicMax((long long*)top, (long long)t);
+    atomicMin((long long*)bot, (long long)b);
+}
+
+// rows of A: warp per (row, 32*CH chunk of k), lanes over k (coalesced)
+constexpr int ROW_CH = 4;
+__global__ void __launch_bounds__(256) fused_rows_kernel(BallsView A, int64_t M, int64_t K, LineWins W,
+                                                         ScanSummary* sum) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= M) return;
+    const int64_t k0 = (int64_t)blockIdx.y * 32 * ROW_CH;
+    int64_t t0 = INT64_MIN, b0 = INT64_MAX, t1 = INT64_MIN, b1 = INT64_MAX, t2 = INT64_MIN, b2 = INT64_MAX;
+    int64_t prec = 0;
+    int special = 0;
+#pragma unroll
+    for (int c = 0; c < ROW_CH; c++) {
+        const int64_t k = k0 + 32 * c + lane;
+        if (k >= K) break;
+        const int64_t e = i * K + k;
+        special |= ball_special(A, e);
+        int64_t t, b;
+        if (mid_window(A, e, t, b)) {
+            win_merge(t0, b0, t, b);
+            prec = (t - b) > prec ? (t - b) : prec;
+        }
+        const Mag m1 = mid_upper(A, e);
+        if (m1.kind == 1) win_merge(t1, b1, m1.f, m1.f - 30);
+        const uint32_t rb = A.rad_man[e];
+        if (rb != 0 && rb != APB_RAD_INF) {
+            const Mag m2 = mag_parts(rb, A.rad_exp[e]);
+            win_merge(t2, b2, m2.f, m2.f - 30);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        int64_t x;
+        x = __shfl_xor_sync(0xffffffffu, t0, o); t0 = x > t0 ? x : t0;
+        x = __shfl_xor_sync(0xffffffffu, b0, o); b0 = x < b0 ? x : b0;
+        x = __shfl_xor_sync(0xffffffffu, t1, o); t1 = x > t1 ? x : t1;
+        x = __shfl_xor_sync(0xffffffffu, b1, o); b1 = x < b1 ? x : b1;
+        x = __shfl_xor_sync(0xffffffffu, t2, o); t2 = x > t2 ? x : t2;
+        x = __shfl_xor_sync(0xffffffffu, b2, o); b2 = x < b2 ? x : b2;
+        x = __shfl_xor_sync(0xffffffffu, prec, o); prec = x > prec ? x : prec;
+    }
+    special = __any_sync(0xffffffffu, special);
+    if (lane == 0) {
+        win_atomic(&W.top[0][i], &W.bot[0][i], t0, b0);
+        win_atomic(&W.top[1][i], &W.bot[1][i], t1, b1);
+        win_atomic(&W.top[2][i], &W.bot[2][i], t2, b2);
+        if (special) atomicOr(&sum->special_a, 1);
+        if (prec) atomicMax(&sum->prec_a, (long long)prec);
+    }
+}
+
+// columns of B: thread per (column, COL_CHUNK rows), coalesced across threads
+__global__ void __launch_bounds__(128) fused_cols_kernel(BallsView B, int64_t K, int64_t N, LineWins W,
+                                                         ScanSummary* sum) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t k0 = (int64_t)blockIdx.y * COL_CHUNK;
+    const int64_t k1 = k0 + COL_CHUNK < K ? k0 + COL_CHUNK : K;
+    int64_t t0 = INT64_MIN, b0 = INT64_MAX, t1 = INT64_MIN, b1 = INT64_MAX, t2 = INT64_MIN, b2 = INT64_MAX;
+    int64_t prec = 0;
+    int special = 0;
+    if (j < N) {
+        for (int64_t k = k0; k < k1; k++) {
+            const int64_t e = k * N + j;
+            special |= ball_special(B, e);
+            int64_t t, b;
+            if (mid_window(B, e, t, b)) {
+                win_merge(t0, b0, t, b);
+                prec = (t - b) > prec ? (t - b) : prec;
+            }
+            const uint32_t rb = B.rad_man[e];
+            const Mag r = (rb != 0 && rb != APB_RAD_INF) ? mag_parts(rb, B.rad_exp[e]) : mag_zero();
+            if (r.kind == 1) win_merge(t1, b1, r.f, r.f - 30);
+            const Mag s = mag_add(mid_upper(B, e), r);
+            if (s.kind == 1) win_merge(t2, b2, s.f, s.f - 30);
+        }
+        win_atomic(&W.top[0][j], &W.bot[0][j], t0, b0);
+        win_atomic(&W.top[1][j], &W.bot[1][j], t1, b1);
+        win_atomic(&W.top[2][j], &W.bot[2][j], t2, b2);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        int64_t x = __shfl_xor_sync(0xffffffffu, prec, o);
+        prec = x > prec ? x : prec;
+    }
+    special = __any_sync(0xffffffffu, special);
+    if ((threadIdx.x & 31) == 0) {
+        if (special) atomicOr(&sum->special_b, 1);
+        if (prec) atomicMax(&sum->prec_b, (long long)prec);
+    }
+}
+
+// widths, centring exponents: rows -> maxw_a, ecen1/ecen2 and radius widths
+// (mw1[0], mw2[0]); columns -> maxw_b, fcen1/fcen2 (mw1[1], mw2[1])
+__global__ void fused_finish_kernel(LineWins R, LineWins C, int64_t M, int64_t N, int64_t* ecen1,
+                                    int64_t* ecen2, int64_t* fcen1, int64_t* fcen2, ScanSummary* sum,
+                                    long long* mw1, long long* mw2) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    long long wa = 0, wb = 0, r1 = 0, r2 = 0, c1 = 0, c2 = 0;
+    if (t < M) {
+        if (R.top[0][t] != INT64_MIN) wa = R.top[0][t] - R.bot[0][t];
+        const int64_t t1 = R.top[1][t], b1 = R.bot[1][t], t2 = R.top[2][t], b2 = R.bot[2][t];
+        ecen1[t] = t1 == INT64_MIN ? 0 : -((t1 + b1) / 2);
+        ecen2[t] = t2 == INT64_MIN ? 0 : -((t2 + b2) / 2);
+        if (t1 != INT64_MIN) r1 = t1 - b1;
+        if (t2 != INT64_MIN) r2 = t2 - b2;
+    }
+    if (t < N) {
+        if (C.top[0][t] != INT64_MIN) wb = C.top[0][t] - C.bot[0][t];
+        const int64_t t1 = C.top[1][t], b1 = C.bot[1][t], t2 = C.top[2][t], b2 = C.bot[2][t];
+        fcen1[t] = t1 == INT64_MIN ? 0 : -((t1 + b1) / 2);
+        fcen2[t] = t2 == INT64_MIN ? 0 : -((t2 + b2) / 2);
+        if (t1 != INT64_MIN) c1 = t1 - b1;
+        if (t2 != INT64_MIN) c2 = t2 - b2;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        long long x;
+        x = __shfl_xor_sync(0xffffffffu, wa, o); wa = x > wa ? x : wa;
+        x = __shfl_xor_sync(0xffffffffu, wb, o); wb = x > wb ? x : wb;
+        x = __shfl_xor_sync(0xffffffffu, r1, o); r1 = x > r1 ? x : r1;
+        x = __shfl_xor_sync(0xffffffffu, r2, o); r2 = x > r2 ? x : r2;
+        x = __shfl_xor_sync(0xffffffffu, c1, o); c1 = x > c1 ? x : c1;
+        x = __shfl_xor_sync(0xffffffffu, c2, o); c2 = x > c2 ? x : c2;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (wa) atomicMax(&sum->maxw_a, wa);
+        if (wb) atomicMax(&sum->maxw_b, wb);
+        if (r1) atomicMax(&mw1[0], r1);
+        if (r2) atomicMax(&mw2[0], r2);
+        if (c1) atomicMax(&mw1[1], c1);
+        if (c2) atomicMax(&mw2[1], c2);
+    }
+}
+
+// exact double planes of both radius products + nonzero counts, one pass per side
+// A side: p1 = |A| (ecen1), p2 = R_A (ecen2);  B side: p1 = R_B (fcen1), p2 = |B|+R_B (fcen2)
+__global__ void fused_planes_kernel(BallsView X, int64_t rows, int64_t cols, int a_side, const int64_t* cen1,
+                                    const int64_t* cen2, double* p1, double* p2, long long* nz1,
+                                    long long* nz2) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double v1 = 0.0, v2 = 0.0;
+    if (t < rows * cols) {
+        const int64_t line = a_side ? t / cols : t % cols;  // A: row i; B: column j
+        Mag m1 = rad_operand(X, t, a_side ? 0 : 2);
+        Mag m2 = rad_operand(X, t, a_side ? 1 : 3);
+        if (m1.kind == 1) v1 = ldexp((double)m1.b, (int)(m1.f - 30 + cen1[line]));
+        if (m2.kind == 1) v2 = ldexp((double)m2.b, (int)(m2.f - 30 + cen2[line]));
+        p1[t] = v1;
+        p2[t] = v2;
+    }
+    const unsigned a1 = __ballot_sync(0xffffffffu, v1 != 0.0), a2 = __ballot_sync(0xffffffffu, v2 != 0.0);
+    if ((threadIdx.x & 31) == 0) {
+        if (a1) atomicAdd((unsigned long long*)nz1, (unsigned long long)__popc(a1));
+        if (a2) atomicAdd((unsigned long long*)nz2, (unsigned long long)__popc(a2));
+    }
+}
+
 // per-row (A side) or per-column (B side) Mag windows over l in [lo,hi)
 // -> centring exponent -((top+bot)/2) (src/matmul.cpp:397-411)
 __global__ void rad_center_rows_kernel(BallsView A, int64_t M, int64_t K, int64_t lo, int64_t hi,
@@ -629,10 +818,10 @@ __global__ void col_lists_kernel(const double* __restrict__ db, int64_t w, int64
         const int64_t l = l0 + lane;
         const double v = l < w ? db[l * N + j] : 0.0;
         const unsigned m = __ballot_sync(0xffffffffu, v != 0.0);
-        if (v != 0.0) {
+        if (v != 0.0) {  // list entry p of column j lives at [p][j] (coalesced reads later)
             const int pos = base + __popc(m & ((1u << lane) - 1u));
-            idx[j * w + pos] = (int)l;
-            val[j * w + pos] = v;
+            idx[(int64_t)pos * N + j] = (int)l;
+            val[(int64_t)pos * N + j] = v;
         }
         base += __popc(m);
     }
@@ -678,12 +867,12 @@ __global__ void __launch_bounds__(256) rad_spcol_kernel(const double* __restrict
     const int n = cnt[j];
     const double* arow = da + i * w;
     for (int p = 0; p < n; p++) {
-        const int l = idx[j * w + p];
+        const int l = idx[(int64_t)p * N + j];
         if (l >= chunk_end) {
             rad_fold(ent, s, ecen[i], fcen[j]);
             chunk_end = ((int64_t)l / 1024 + 1) * 1024;
         }
-        s = __dadd_rn(s, __dmul_rn(arow[l], val[j * w + p]));
+        s = __dadd_rn(s, __dmul_rn(arow[l], val[(int64_t)p * N + j]));
     }
     rad_fold(ent, s, ecen[i], fcen[j]);
     mag_store(ent, &rb[i * N + j], &rf[i * N + j]);
@@ -772,8 +961,8 @@ T* ws_buf(int slot, size_t count, cudaStream_t st) {
 
 struct Scratch {
     // separate allocations owned here (the Workspace slot table is small)
-    void* p[48] = {};
-    size_t cap[48] = {};
+    void* p[64] = {};
+    size_t cap[64] = {};
     void* get(int k, size_t bytes, cudaStream_t st) {
         if (cap[k] < bytes) {
             if (p[k]) {
@@ -797,7 +986,7 @@ Scratch& scratch() {
 }
 enum {
     S_RTOP, S_RBOT, S_CTOP, S_CBOT, S_SUM, S_APACK, S_BPACK, S_TW, S_TC, S_UNITS, S_ESC, S_FSC,
-    S_WA, S_WB, S_GREEDY, S_DA, S_DB, S_CEN_E, S_CEN_F, S_R1B, S_R1F, S_R2B, S_R2F, S_MISC, S_CTOP2, S_CBOT2, S_LCNT, S_LIDX, S_LVAL, S_DA2, S_DB2, S_CEN_E2, S_CEN_F2, S_RW1, S_RW2, S_LCNT2, S_LIDX2, S_LVAL2
+    S_WA, S_WB, S_GREEDY, S_DA, S_DB, S_CEN_E, S_CEN_F, S_R1B, S_R1F, S_R2B, S_R2F, S_MISC, S_CTOP2, S_CBOT2, S_LCNT, S_LIDX, S_LVAL, S_DA2, S_DB2, S_CEN_E2, S_CEN_F2, S_RW1, S_RW2, S_LCNT2, S_LIDX2, S_LVAL2, S_RW1T, S_RW1B, S_RW2T, S_RW2B, S_CW1T, S_CW1B, S_CW2T, S_CW2B
 };
 template <class T>
 T* sbuf(int k, size_t count, cudaStream_t st) {
@@ -1335,17 +1524,53 @@ cudaStream_t side_stream() {
 }
 
 int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, cudaStream_t st) {
-    // one host synchronisation: midpoint plan scans + both radius products' windows
+    // one host synchronisation: fused scans of A and B (planner windows and both
+    // radius products' windows), centring, exact double planes and nonzero counts
+    const int64_t M = A->rows, K = A->cols, N = B->cols;
+    BallsView av = view_of(&A->b), bv = view_of(&B->b);
     ScanSummary* sum = sbuf<ScanSummary>(S_SUM, 1, st);
-    int rc = plan_launch(A, B, sum, st);
-    if (rc) return rc;
-    if ((rc = radius_prepare(A, B, 0, 2, 0, st))) return rc;  // |A| R_B
-    if ((rc = radius_prepare(A, B, 1, 3, 1, st))) return rc;  // R_A (|B| + R_B)
+    LineWins RW, CW;
+    const int rslot[6] = {S_RTOP, S_RBOT, S_RW1T, S_RW1B, S_RW2T, S_RW2B};
+    const int cslot[6] = {S_CTOP, S_CBOT, S_CW1T, S_CW1B, S_CW2T, S_CW2B};
+    for (int q = 0; q < 3; q++) {
+        RW.top[q] = sbuf<int64_t>(rslot[2 * q], M, st);
+        RW.bot[q] = sbuf<int64_t>(rslot[2 * q + 1], M, st);
+        CW.top[q] = sbuf<int64_t>(cslot[2 * q], N, st);
+        CW.bot[q] = sbuf<int64_t>(cslot[2 * q + 1], N, st);
+    }
+    long long* mw1 = sbuf<long long>(kRad[0].mw, 4, st);
+    long long* mw2 = sbuf<long long>(kRad[1].mw, 4, st);
+    int64_t* ec1 = sbuf<int64_t>(kRad[0].ce, M, st);
+    int64_t* ec2 = sbuf<int64_t>(kRad[1].ce, M, st);
+    int64_t* fc1 = sbuf<int64_t>(kRad[0].cf, N, st);
+    int64_t* fc2 = sbuf<int64_t>(kRad[1].cf, N, st);
+    double* da1 = sbuf<double>(kRad[0].da, (size_t)M * K, st);
+    double* db1 = sbuf<double>(kRad[0].db, (size_t)K * N, st);
+    double* da2 = sbuf<double>(kRad[1].da, (size_t)M * K, st);
+    double* db2 = sbuf<double>(kRad[1].db, (size_t)K * N, st);
+    if (!sum || !mw1 || !mw2 || !ec1 || !ec2 || !fc1 || !fc2 || !da1 || !db1 || !da2 || !db2) return APB_ERR_CUDA;
+    cudaMemsetAsync(sum, 0, sizeof(ScanSummary), st);
+    cudaMemsetAsync(mw1, 0, 4 * sizeof(long long), st);
+    cudaMemsetAsync(mw2, 0, 4 * sizeof(long long), st);
+    init_wins_kernel<<<blocks_for(M, 256), 256, 0, st>>>(RW, M);
+    init_wins_kernel<<<blocks_for(N, 256), 256, 0, st>>>(CW, N);
+    {
+        dim3 gr(blocks_for(M, 8), blocks_for(K, 32 * ROW_CH));
+        fused_rows_kernel<<<gr, 256, 0, st>>>(av, M, K, RW, sum);
+        dim3 gc(blocks_for(N, 128), blocks_for(K, COL_CHUNK));
+        fused_cols_kernel<<<gc, 128, 0, st>>>(bv, K, N, CW, sum);
+        fused_finish_kernel<<<blocks_for(std::max(M, N), 256), 256, 0, st>>>(RW, CW, M, N, ec1, ec2, fc1, fc2, sum,
+                                                                            mw1, mw2);
+        fused_planes_kernel<<<blocks_for(M * K, 256), 256, 0, st>>>(av, M, K, 1, ec1, ec2, da1, da2, mw1 + 2, mw2 + 2);
+        fused_planes_kernel<<<blocks_for(K * N, 256), 256, 0, st>>>(bv, K, N, 0, fc1, fc2, db1, db2, mw1 + 3, mw2 + 3);
+        count_launch(7);
+    }
     ScanSummary* hs = pinned_summary();
     long long* hw = (long long*)(hs + 1);
     cudaMemcpyAsync(hs, sum, sizeof(ScanSummary), cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(hw, sbuf<long long>(kRad[0].mw, 4, st), 4 * sizeof(long long), cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(hw + 4, sbuf<long long>(kRad[1].mw, 4, st), 4 * sizeof(long long), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hw, mw1, 4 * sizeof(long long), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hw + 4, mw2, 4 * sizeof(long long), cudaMemcpyDeviceToHost, st);
+    int rc;
     if ((rc = cuda_check(cudaStreamSynchronize(st), "matmul plan"))) return rc;
     const ScanSummary hsum = *hs;
     long long hw1[4], hw2[4];
@@ -1358,7 +1583,6 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     if (P.special) return classical(A, B, prec, C, st);  // src/matmul.cpp:455-458
     stats().block_calls++;
     stats().last_block_count = P.steps.size() / 3;
-    const int64_t M = A->rows, N = B->cols;
     // R_C += |A| R_B + R_A (|B| + R_B): FP64 work on a side stream, overlapping the
     // tensor-core midpoint product (independent inputs)
     uint32_t* r1b = sbuf<uint32_t>(S_R1B, (size_t)M * N, st);
