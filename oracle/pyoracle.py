@@ -45,7 +45,7 @@ def ref_lib():
         for name in ("ref_dot_batch", "ref_dot_state", "ref_dot_complex_batch", "ref_matmul",
                      "ref_matmul_complex", "ref_plan_blocks", "ref_block_int_product",
                      "ref_radius_matmul_upper", "ref_dot_contains", "ref_abs_dot_upper",
-                     "ref_run_verify_suite"):
+                     "ref_run_verify_suite", "ref_ball_addsub"):
             getattr(_ref, name).restype = I
     return _ref
 
@@ -263,3 +263,26 @@ def run_verify_suite(name: str, trials: int, seed: int) -> int:
     _check(lib.ref_run_verify_suite(name.encode(), C.c_uint64(trials), C.c_uint64(seed), _p(f)), lib,
            "ref_run_verify_suite")
     return int(f.value)
+
+
+def ball_addsub(x: BallArray, y: BallArray, prec: int, subtract=False) -> BallArray:
+    """reference ball_add / ball_sub elementwise"""
+    from paper_1901_04289_b200.balls import limbs_for
+    out = BallArray.zeros(x.count, limbs_for(prec))
+    xc, yc, oc = x.c(), y.c(), out.c()
+    lib = ref_lib()
+    _check(lib.ref_ball_addsub(_p(xc), _p(yc), I(subtract), I64(x.count), I64(prec), _p(oc)), lib,
+           "ref_ball_addsub")
+    return out
+
+
+def matmul_complex_rows(are, aim, bre, bim, rows, K, N, prec, threads=1):
+    """complex_matmul_ball on the first `rows` rows of A when the full product takes
+    the block path: the four real products with block_matmul_ball (row-split,
+    bit-identical for single-block plans) + ball_sub / ball_add"""
+    sub = lambda a: a.take(np.arange(rows * K))
+    ac, _ = matmul(sub(are), bre, rows, K, N, prec, which="ref", algo=1, threads=threads)
+    bd, _ = matmul(sub(aim), bim, rows, K, N, prec, which="ref", algo=1, threads=threads)
+    ad, _ = matmul(sub(are), bim, rows, K, N, prec, which="ref", algo=1, threads=threads)
+    bc, _ = matmul(sub(aim), bre, rows, K, N, prec, which="ref", algo=1, threads=threads)
+    return ball_addsub(ac, bd, prec, subtract=True), ball_addsub(ad, bc, prec)

@@ -477,6 +477,17 @@ int ref_abs_dot_upper(const apb_balls* x, const apb_balls* y, const apb_dot_inde
     });
 }
 
+// elementwise ball_add / ball_sub (src/ball.cpp:15-19, include/apball/ball.hpp:50-52)
+int ref_ball_addsub(const apb_balls* x, const apb_balls* y, int subtract, int64_t count, int64_t prec,
+                    apb_balls* out) {
+    return guarded([&] {
+        for (int64_t i = 0; i < count; i++) {
+            Ball a = load_ball(x, i), b = load_ball(y, i);
+            store_ball(out, i, subtract ? ball_sub(a, b, prec) : ball_add(a, b, prec));
+        }
+    });
+}
+
 // the reference's own verify suites (src/bench.cpp:486-731), for pinning
 int ref_run_verify_suite(const char* name, uint64_t trials, uint64_t seed, uint64_t* failures) {
     return guarded([&] {

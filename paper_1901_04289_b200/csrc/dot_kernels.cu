@@ -533,6 +533,220 @@ __global__ void __launch_bounds__(128, (TPL > 0 ? 3 : 4)) dot_small_kernel(DotAr
     }
 }
 
+
+// ------------------------------------------------- staged small kernel
+// For dots of <= 128 terms with <= 2-limb operands (config 1): the warp's 32
+// dots are software-pipelined through shared memory -- while dot g is
+// scanned and accumulated from its stage, cp.async copies of dot g+1's
+// mantissas, exponents and radii land in the other stage (kind bytes are
+// prefetched into registers).  Each lane only touches its own term slots, so
+// no barrier is needed beyond cp.async.wait_group.
+constexpr int STG_T = 128;  // term slots per stage (4 per lane)
+
+template <int L>
+struct StageBuf {
+    uint64_t xm[L][STG_T], ym[L][STG_T];
+    int64_t xe[STG_T], ye[STG_T], xf[STG_T], yf[STG_T];
+    uint32_t xr[STG_T], yr[STG_T];
+};
+
+APB_DEV void cp_async(void* sdst, const void* gsrc, int bytes) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(sdst);
+    if (bytes == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+    else if (bytes == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gsrc) : "memory");
+}
+APB_DEV void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+APB_DEV void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// issue the copies of dot b's terms (this lane's slots) into stage buf; return kinds
+template <int L>
+APB_DEV void stage_dot(StageBuf<L>& sb, uint32_t (&kinds)[4], const DotArgs& A, int64_t b, int64_t total,
+                       int lane) {
+    const int64_t bq = A.idx.bdiv == 1 ? b : b / A.idx.bdiv;
+    const int64_t br = A.idx.bdiv == 1 ? 0 : b - bq * A.idx.bdiv;
+    const int64_t xb = A.idx.x_off + bq * A.idx.xs1 + br * A.idx.xs2;
+    const int64_t yb = A.idx.y_off + bq * A.idx.ys1 + br * A.idx.ys2;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int64_t i = lane + 32 * q;
+        const int slot = lane + 32 * q;
+        kinds[q] = 0;
+        if (i >= total) continue;
+        const BallsView& X = i < A.n ? A.x : A.init;
+        const int64_t ex = i < A.n ? xb + i * A.idx.xstep : b;
+        // x operand (or the initial value)
+        const int offx = L - X.L;
+#pragma unroll
+        for (int j = 0; j < L; j++) {
+            if (j >= offx) cp_async(&sb.xm[j][slot], X.mant + ex * X.L + (j - offx), 8);
+            else sb.xm[j][slot] = 0;
+        }
+        cp_async(&sb.xe[slot], X.exp + ex, 8);
+        cp_async(&sb.xf[slot], X.rad_exp + ex, 8);
+        cp_async(&sb.xr[slot], X.rad_man + ex, 4);
+        uint32_t kx = __ldg(X.kind + ex), ky = APB_FINITE;
+        if (i < A.n) {
+            const int64_t ey = yb + i * A.idx.ystep;
+            const int offy = L - A.y.L;
+#pragma unroll
+            for (int j = 0; j < L; j++) {
+                if (j >= offy) cp_async(&sb.ym[j][slot], A.y.mant + ey * A.y.L + (j - offy), 8);
+                else sb.ym[j][slot] = 0;
+            }
+            cp_async(&sb.ye[slot], A.y.exp + ey, 8);
+            cp_async(&sb.yf[slot], A.y.rad_exp + ey, 8);
+            cp_async(&sb.yr[slot], A.y.rad_man + ey, 4);
+            ky = __ldg(A.y.kind + ey);
+        } else {  // y = 1 for the initial term
+#pragma unroll
+            for (int j = 0; j < L; j++) sb.ym[j][slot] = (j == L - 1) ? (1ull << 63) : 0ull;
+            sb.ye[slot] = 1;
+            sb.yf[slot] = 0;
+            sb.yr[slot] = 0;
+        }
+        kinds[q] = kx | (ky << 8);
+    }
+}
+
+template <int L>
+APB_DEV void read_term(Term<L>& t, const StageBuf<L>& sb, int slot, uint32_t kinds, bool sub) {
+#pragma unroll
+    for (int j = 0; j < L; j++) {
+        t.xm[j] = sb.xm[j][slot];
+        t.ym[j] = sb.ym[j][slot];
+    }
+    t.ex = sb.xe[slot];
+    t.ey = sb.ye[slot];
+    t.fx = sb.xf[slot];
+    t.fy = sb.yf[slot];
+    t.rx = sb.xr[slot];
+    t.ry = sb.yr[slot];
+    t.kx = (uint8_t)(kinds & 255u);
+    t.ky = (uint8_t)(kinds >> 8);
+    t.neg = sub;
+}
+
+template <int L, int NS>
+__global__ void __launch_bounds__(128, 3) dot_staged_kernel(DotArgs A) {
+    extern __shared__ __align__(16) uint8_t stg_raw[];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    StageBuf<L>* bufs = reinterpret_cast<StageBuf<L>*>(stg_raw) + 2 * wl;
+    const int64_t warp_id = (int64_t)blockIdx.x * (blockDim.x >> 5) + wl;
+    const int64_t b0 = warp_id * 32;
+    if (b0 >= A.batch) return;
+    const int nd = (int)(A.batch - b0 < 32 ? A.batch - b0 : 32);
+    const int64_t total = A.n + (A.has_init ? 1 : 0);
+    const bool with_radius = A.mode == APB_DOT_BALL;
+    const bool track_min = A.prec > 128;
+
+    Plan my_pl;
+    uint64_t my_s[NS];
+    uint64_t my_err = 0, my_srad = 0;
+    my_pl.status = 2;
+
+    uint32_t kinds[4], kinds_next[4];
+    stage_dot<L>(bufs[0], kinds, A, b0, total, lane);
+    cp_commit();
+    for (int g = 0; g < nd; g++) {
+        const int64_t b = b0 + g;
+        if (g + 1 < nd) {
+            stage_dot<L>(bufs[(g + 1) & 1], kinds_next, A, b + 1, total, lane);
+            cp_commit();
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        const StageBuf<L>& sb = bufs[g & 1];
+        // ---- pass 1: setup scan from the stage
+        ScanAcc sc{INT64_MIN, INT64_MAX, INT64_MIN, 0, false};
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int64_t i = lane + 32 * q;
+            if (i < total) {
+                Term<L> t;
+                read_term<L>(t, sb, lane + 32 * q, kinds[q], (i < A.n) && A.subtract);
+                scan_term<L>(sc, t, track_min, with_radius);
+            }
+        }
+        const bool fb = __any_sync(0xffffffffu, sc.fb);
+        const int64_t e_max = warp_max(sc.e_max);
+        const int64_t e_min = warp_min(sc.e_min);
+        const int64_t e_rad = warp_max(sc.e_rad);
+        const uint64_t nnz = warp_sum(sc.nnz);
+        const Plan pl = finish_plan(e_max, e_min, e_rad, nnz, fb, total, A.prec, A.disable_reduction);
+        if (lane == g) my_pl = pl;
+        if (pl.status == 0) {
+            Acc<L, NS> acc;
+#pragma unroll
+            for (int j = 0; j < NS; j++) acc.s[j] = 0;
+            acc.err = 0;
+            acc.srad = 0;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int64_t i = lane + 32 * q;
+                if (i < total) {
+                    Term<L> t;
+                    read_term<L>(t, sb, lane + 32 * q, kinds[q], (i < A.n) && A.subtract);
+                    const bool xz = (t.kx & APB_KIND_MASK) == APB_ZERO, yz = (t.ky & APB_KIND_MASK) == APB_ZERO;
+                    if (!xz && !yz) acc_term<L, NS>(acc, t, pl);
+                    if (with_radius) rad_term<L, NS>(acc, t, pl);
+                }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                uint64_t c = 0;
+#pragma unroll
+                for (int j = 0; j < NS; j++) {
+                    uint64_t v = __shfl_xor_sync(0xffffffffu, acc.s[j], o);
+                    uint64_t s1 = acc.s[j] + v;
+                    uint64_t c1 = s1 < v;
+                    uint64_t s2 = s1 + c;
+                    uint64_t c2 = s2 < c;
+                    acc.s[j] = s2;
+                    c = c1 | c2;
+                }
+                acc.err += __shfl_xor_sync(0xffffffffu, acc.err, o);
+                acc.srad += __shfl_xor_sync(0xffffffffu, acc.srad, o);
+            }
+            if (lane == g) {
+#pragma unroll
+                for (int j = 0; j < NS; j++) my_s[j] = acc.s[j];
+                my_err = acc.err;
+                my_srad = acc.srad;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) kinds[q] = kinds_next[q];
+    }
+
+    if (lane < nd) {
+        const int64_t b = b0 + lane;
+        if (my_pl.status != 0) {
+            if (A.state) write_state(A.state + b, my_pl, 0, 0);
+            if (my_pl.status == 1) {
+                A.fb_flag[b] = 1;
+            } else {
+                GFloat<1> z;
+                z.kind = APB_ZERO;
+                z.neg = 0;
+                z.e = 0;
+                z.n = 0;
+                gf_store(A.out, b, z, mag_zero(), A.status);
+            }
+        } else {
+            if (A.state) write_state(A.state + b, my_pl, my_err, my_srad);
+            if (A.acc)
+                for (int j = 0; j < my_pl.n_s && j < A.acc_stride; j++) A.acc[b * A.acc_stride + j] = my_s[j];
+            finalize_store<NS>(my_pl, my_s, my_err, my_srad, A.prec, with_radius, A.out, b, A.status);
+        }
+    }
+}
+
 // ====================================================== generic (thread/dot)
 
 APB_DEV Mag mag_upper_of(const GF& x) {
@@ -981,10 +1195,37 @@ static int ns_bound(int64_t prec, int64_t total) {
     return (int)(ns < 2 ? 2 : ns);
 }
 
+static bool staged_ok(const DotArgs& A) {
+    auto al = [](const void* p, size_t a) { return ((uintptr_t)p % a) == 0; };
+    bool ok = al(A.x.mant, 8) && al(A.x.exp, 8) && al(A.x.rad_exp, 8) && al(A.x.rad_man, 4) &&
+              al(A.y.mant, 8) && al(A.y.exp, 8) && al(A.y.rad_exp, 8) && al(A.y.rad_man, 4);
+    if (A.has_init)
+        ok = ok && al(A.init.mant, 8) && al(A.init.exp, 8) && al(A.init.rad_exp, 8) && al(A.init.rad_man, 4);
+    return ok;
+}
+
+template <int L, int NS>
+static void launch_staged(const DotArgs& A, cudaStream_t st) {
+    const int warps = 4;
+    const size_t shm = (size_t)warps * 2 * sizeof(StageBuf<L>);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(dot_staged_kernel<L, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        attr = true;
+    }
+    const int64_t nwarps = (A.batch + 31) / 32;
+    dim3 grid((unsigned)((nwarps + warps - 1) / warps));
+    dot_staged_kernel<L, NS><<<grid, 32 * warps, shm, st>>>(A);
+    count_launch();
+}
+
 template <int L, int NS>
 static bool try_small_tpl(const DotArgs& A, int64_t total, cudaStream_t st) {
-    static const bool no_keep = std::getenv("APB_DOT_RELOAD") != nullptr;  // tuning hook
-    if (total <= 32 * 4 && L <= 2 && !no_keep) {
+    static const bool no_keep = std::getenv("APB_DOT_RELOAD") != nullptr;  // tuning hooks
+    static const bool no_stage = std::getenv("APB_DOT_NOSTAGE") != nullptr;
+    if (total <= STG_T && L <= 2 && !no_stage && staged_ok(A)) {
+        launch_staged<L, NS>(A, st);
+    } else if (total <= 32 * 4 && L <= 2 && !no_keep) {
         launch_small<L, NS, 4>(A, st);
     } else {
         launch_small<L, NS, 0>(A, st);

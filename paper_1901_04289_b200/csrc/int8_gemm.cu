@@ -479,11 +479,17 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
 #pragma unroll 1
                 for (int w = 0; w < BAND_W; w++) {
-                    if (d0 + w >= P.ND) break;
+                    // diagonals past the last one contribute D = 0, so every band's
+                    // carry leaves at bit 32 (b + 1) (word aligned for the recombine)
                     uint32_t v[32];
-                    const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(w * 128 + col0 + 32 * h);
-                    TMEM_LD32(taddr, v);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (d0 + w < P.ND) {
+                        const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(w * 128 + col0 + 32 * h);
+                        TMEM_LD32(taddr, v);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 32; c++) v[c] = 0;
+                    }
 #pragma unroll
                     for (int c = 0; c < 32; c++) {
                         const int64_t val = (int64_t)(int32_t)v[c] + carry[c];

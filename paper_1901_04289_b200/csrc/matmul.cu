@@ -265,10 +265,9 @@ APB_DEV uint64_t ds_word(const DigitStream& d, int64_t q) {
     return v;
 }
 
-// the next 8 balanced digits (bytes 8c .. 8c+7) packed little-endian
-APB_DEV uint64_t ds_next8(DigitStream& d, int c) {
+// 8 balanced digits (bytes 8c .. 8c+7) from the 64 source bits w, packed little-endian
+APB_DEV uint64_t ds_digits8(DigitStream& d, uint64_t w) {
     if (!d.live) return 0;
-    uint64_t w = ds_word(d, 64 * (int64_t)c - d.sh);
     uint64_t out = 0;
 #pragma unroll
     for (int b = 0; b < 8; b++) {
@@ -308,18 +307,30 @@ __global__ void __launch_bounds__(256) pack_kernel(BallsView X, int64_t rows, in
     }
     const size_t plane = (size_t)Rp * Kp;
     uint32_t* dst = (uint32_t*)(out + (size_t)r * Kp + kk0);
-    for (int c = 0; c * 8 < S; c++) {
-        uint64_t w[4];
+    const int nch = (S + 7) / 8;
+    for (int c0 = 0; c0 < nch; c0 += 4) {
+        uint64_t src[4][4];  // [chunk][entry] source words, all loads issued up front
 #pragma unroll
-        for (int q = 0; q < 4; q++) w[q] = ds_next8(ds[q], c);
+        for (int cc = 0; cc < 4; cc++)
 #pragma unroll
-        for (int b = 0; b < 8; b++) {
-            const int s = 8 * c + b;
-            if (s >= S) break;
-            const uint32_t word = ((uint32_t)(w[0] >> (8 * b)) & 255u) | (((uint32_t)(w[1] >> (8 * b)) & 255u) << 8) |
-                                  (((uint32_t)(w[2] >> (8 * b)) & 255u) << 16) |
-                                  (((uint32_t)(w[3] >> (8 * b)) & 255u) << 24);
-            dst[(size_t)s * plane / 4] = word;
+            for (int q = 0; q < 4; q++)
+                src[cc][q] = (c0 + cc < nch && ds[q].live) ? ds_word(ds[q], 64 * (int64_t)(c0 + cc) - ds[q].sh) : 0;
+#pragma unroll
+        for (int cc = 0; cc < 4; cc++) {
+            const int c = c0 + cc;
+            if (c >= nch) break;
+            uint64_t w[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) w[q] = ds_digits8(ds[q], src[cc][q]);
+#pragma unroll
+            for (int b = 0; b < 8; b++) {
+                const int s = 8 * c + b;
+                if (s >= S) break;
+                const uint32_t word = ((uint32_t)(w[0] >> (8 * b)) & 255u) | (((uint32_t)(w[1] >> (8 * b)) & 255u) << 8) |
+                                      (((uint32_t)(w[2] >> (8 * b)) & 255u) << 16) |
+                                      (((uint32_t)(w[3] >> (8 * b)) & 255u) << 24);
+                dst[(size_t)s * plane / 4] = word;
+            }
         }
     }
 }
@@ -423,6 +434,134 @@ __global__ void __launch_bounds__(128) recombine_kernel(RecombineArgs R) {
             gf_store(R.C, t, c, mag_add(crad, err), R.status);
         }
     }
+}
+
+
+// Register-resident recombine for the band GEMM output of a single (first)
+// block: T = sum_b (word_b + carry_b 2^32) 2^(32 b) in base-2^32 digits, then
+// sign, normalize and truncate to p bits with the apfloat_round error term
+// (src/apfloat.cpp:26-63, 138-162), all with compile-time array bounds.
+template <int NBC>
+__global__ void __launch_bounds__(128) recombine_fast_kernel(RecombineArgs R) {
+    constexpr int ND32 = NBC + 2;          // 32-bit digits
+    constexpr int NL = (ND32 + 1) / 2;     // 64-bit limbs
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= R.M * R.N) return;
+    const int64_t i = t / R.N, j = t % R.N;
+    const size_t plane = (size_t)R.Mp * R.Np;
+    const size_t off = (size_t)i * R.Np + j;
+    const int NB = R.nwords;
+    int64_t D[ND32];
+#pragma unroll
+    for (int k = 0; k < ND32; k++) D[k] = 0;
+#pragma unroll
+    for (int b = 0; b < NBC; b++) {
+        if (b < NB) {
+            D[b] += (int64_t)R.Tw[(size_t)b * plane + off];
+            D[b + 1] += (int64_t)R.Tc[(size_t)b * plane + off];
+        }
+    }
+    // carry-propagate base 2^32 (arithmetic shifts keep the sign in the top digit)
+#pragma unroll
+    for (int k = 0; k + 1 < ND32; k++) {
+        D[k + 1] += D[k] >> 32;
+        D[k] &= 0xFFFFFFFFll;
+    }
+    const bool neg = D[ND32 - 1] < 0;
+    uint64_t T[NL];
+#pragma unroll
+    for (int q = 0; q < NL; q++) {
+        const uint64_t lo = (uint64_t)(uint32_t)D[2 * q];
+        const uint64_t hi = 2 * q + 1 < ND32 ? (uint64_t)(uint32_t)D[2 * q + 1] : (neg ? 0xFFFFFFFFull : 0ull);
+        T[q] = lo | (hi << 32);
+    }
+    if (neg) {  // magnitude
+        uint64_t c = 1;
+#pragma unroll
+        for (int q = 0; q < NL; q++) {
+            const uint64_t v = ~T[q] + c;
+            c = (c && v == 0) ? 1 : 0;
+            T[q] = v;
+        }
+    }
+    // bit length B of the magnitude
+    int64_t B = 0;
+#pragma unroll
+    for (int q = 0; q < NL; q++)
+        if (T[q]) B = 64 * (int64_t)q + (int64_t)bitw64(T[q]);
+    BallsOut& O = R.C;
+    uint64_t* dst = O.mant + t * (int64_t)O.L;
+    if (B == 0) {  // exact zero: C stays Ball::zero()
+        for (int q = 0; q < O.L; q++) dst[q] = 0;
+        O.exp[t] = 0;
+        O.kind[t] = APB_ZERO;
+        O.rad_man[t] = 0;
+        O.rad_exp[t] = 0;
+        return;
+    }
+    const int64_t exp2 = -R.escale[i] - R.fscale[j];
+    int st = 0;
+    const int64_t e = checked_add(exp2, B, &st);  // apfloat_from_bigint_scaled exponent
+    const int64_t p = R.prec;
+    const int64_t cut = B > p ? B - p : 0;        // bits [0, cut) are truncated
+    // bits [pos, pos + 64) of the magnitude (0 outside), static-index selects
+    auto bits64 = [&](int64_t pos) -> uint64_t {
+        if (pos >= 64 * (int64_t)NL || pos <= -64) return 0;
+        const int64_t li = pos >= 0 ? pos >> 6 : -1;
+        const int bo = (int)(pos - 64 * li);
+        uint64_t lo = 0, hi = 0;
+#pragma unroll
+        for (int q = 0; q < NL; q++) {
+            if (q == li) lo = T[q];
+            if (q == li + 1) hi = T[q];
+        }
+        return bo ? (lo >> bo) | (hi << (64 - bo)) : lo;
+    };
+    // output mantissa: bits [B - 64 (r + 1), B - 64 r) for r = 0..L-1, cleared below `cut`
+    for (int r = 0; r < O.L; r++) {
+        const int64_t lo_bit = B - 64 * (int64_t)(r + 1);
+        uint64_t v = bits64(lo_bit);
+        if (lo_bit < cut) {
+            const int64_t k = cut - lo_bit;  // low k bits of v are below the cut
+            v = k >= 64 ? 0 : (v & ~((1ull << k) - 1));
+        }
+        dst[O.L - 1 - r] = v;
+    }
+    O.exp[t] = e;
+    O.kind[t] = (uint8_t)(APB_FINITE | (neg ? APB_SIGN : 0));
+    // error of the truncation: Mag upper bound of the discarded bits
+    Mag err = mag_zero();
+    if (cut > 0) {
+        // highest set bit below the cut
+        int64_t top = -1;
+#pragma unroll
+        for (int q = 0; q < NL; q++) {
+            uint64_t v = T[q];
+            const int64_t base = 64 * (int64_t)q;
+            if (base >= cut) v = 0;
+            else if (cut - base < 64) v &= (1ull << (cut - base)) - 1;
+            if (v) top = base + (int64_t)bitw64(v) - 1;
+        }
+        if (top >= 0) {
+            // 64-bit window starting at the top set bit, and sticky of everything below it
+            const uint64_t window = bits64(top - 63);
+            bool low = (window & ((1ull << 34) - 1)) != 0;
+            const int64_t below = top - 63;  // bits [0, below) not in the window
+#pragma unroll
+            for (int q = 0; q < NL; q++) {
+                uint64_t v = T[q];
+                const int64_t base = 64 * (int64_t)q;
+                if (base >= below) v = 0;
+                else if (below - base < 64) v &= (1ull << (below - base)) - 1;
+                low |= v != 0;
+            }
+            uint64_t bm = window >> 34;
+            if (low) bm++;
+            err = mag_parts(bm, checked_add(exp2, top + 1, &st));
+        }
+    }
+    mag_store(err, &O.rad_man[t], &O.rad_exp[t]);
+    if (st) *R.status = st;
 }
 
 // ------------------------------------------------------------ K7 radius
@@ -541,12 +680,13 @@ __global__ void __launch_bounds__(256) fused_rows_kernel(BallsView A, int64_t M,
     }
 }
 
-// columns of B: thread per (column, COL_CHUNK rows), coalesced across threads
+constexpr int FCOL_CHUNK = 4;
+// columns of B: thread per (column, FCOL_CHUNK rows), coalesced across threads
 __global__ void __launch_bounds__(128) fused_cols_kernel(BallsView B, int64_t K, int64_t N, LineWins W,
                                                          ScanSummary* sum) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t k0 = (int64_t)blockIdx.y * COL_CHUNK;
-    const int64_t k1 = k0 + COL_CHUNK < K ? k0 + COL_CHUNK : K;
+    const int64_t k0 = (int64_t)blockIdx.y * FCOL_CHUNK;
+    const int64_t k1 = k0 + FCOL_CHUNK < K ? k0 + FCOL_CHUNK : K;
     int64_t t0 = INT64_MIN, b0 = INT64_MAX, t1 = INT64_MIN, b1 = INT64_MAX, t2 = INT64_MIN, b2 = INT64_MAX;
     int64_t prec = 0;
     int special = 0;
@@ -637,7 +777,9 @@ __global__ void fused_planes_kernel(BallsView X, int64_t rows, int64_t cols, int
         Mag m2 = rad_operand(X, t, a_side ? 1 : 3);
         if (m1.kind == 1) v1 = ldexp((double)m1.b, (int)(m1.f - 30 + cen1[line]));
         if (m2.kind == 1) v2 = ldexp((double)m2.b, (int)(m2.f - 30 + cen2[line]));
-        p1[t] = v1;
+        // A side: |A| plane stored transposed ([l][i]) for coalesced column-list products
+        if (a_side) p1[(t % cols) * rows + t / cols] = v1;
+        else p1[t] = v1;
         p2[t] = v2;
     }
     const unsigned a1 = __ballot_sync(0xffffffffu, v1 != 0.0), a2 = __ballot_sync(0xffffffffu, v2 != 0.0);
@@ -737,7 +879,7 @@ __global__ void __launch_bounds__(64) rad_gemm_kernel(const double* __restrict__
                                                        const double* __restrict__ db, int64_t M,
                                                        int64_t N, int64_t w, const int64_t* ecen,
                                                        const int64_t* fcen, uint32_t* rb, int64_t* rf,
-                                                       int accumulate) {
+                                                       int accumulate, int a_trans) {
     __shared__ double sA[RK][RT + 1];
     __shared__ double sB[RK][RT];
     const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
@@ -756,7 +898,7 @@ __global__ void __launch_bounds__(64) rad_gemm_kernel(const double* __restrict__
         for (int q = threadIdx.x; q < RK * RT; q += RTHREADS) {
             const int kk = q / RT, rr = q % RT;
             const int64_t gi = i0 + rr, gl = l0 + kk;
-            sA[kk][rr] = (gi < M && gl < w) ? da[gi * w + gl] : 0.0;
+            sA[kk][rr] = (gi < M && gl < w) ? (a_trans ? da[gl * M + gi] : da[gi * w + gl]) : 0.0;
             const int64_t gj = j0 + rr;
             sB[kk][rr] = (gj < N && gl < w) ? db[gl * N + gj] : 0.0;
         }
@@ -829,14 +971,14 @@ __global__ void col_lists_kernel(const double* __restrict__ db, int64_t w, int64
 }
 
 __global__ void row_lists_kernel(const double* __restrict__ da, int64_t M, int64_t w, int* cnt, int* idx,
-                                 double* val) {
+                                 double* val, int a_trans) {
     const int lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= M) return;
     int base = 0;
     for (int64_t l0 = 0; l0 < w; l0 += 32) {
         const int64_t l = l0 + lane;
-        const double v = l < w ? da[i * w + l] : 0.0;
+        const double v = l < w ? (a_trans ? da[l * M + i] : da[i * w + l]) : 0.0;
         const unsigned m = __ballot_sync(0xffffffffu, v != 0.0);
         if (v != 0.0) {
             const int pos = base + __popc(m & ((1u << lane) - 1u));
@@ -853,27 +995,31 @@ APB_DEV void rad_fold(Mag& ent, double& s, int64_t e_i, int64_t f_j) {
     s = 0.0;
 }
 
-// out(i,j) over the nonzero list of column j of db; thread per (i, j)
-__global__ void __launch_bounds__(256) rad_spcol_kernel(const double* __restrict__ da, int64_t M, int64_t N,
+// out(i,j) over the nonzero list of column j of db; warp per (32 rows i, column j):
+// list entries are warp-uniform (broadcast), the |A| plane is read transposed
+// (daT[l][i], coalesced across the warp)
+__global__ void __launch_bounds__(256) rad_spcol_kernel(const double* __restrict__ daT, int64_t M, int64_t N,
                                                         int64_t w, const int* cnt, const int* idx,
                                                         const double* val, const int64_t* ecen,
                                                         const int64_t* fcen, uint32_t* rb, int64_t* rf) {
-    const int64_t j = (int64_t)blockIdx.x * 32 + (threadIdx.x & 31);
-    const int64_t i = (int64_t)blockIdx.y * 8 + (threadIdx.x >> 5);
-    if (i >= M || j >= N) return;
+    const int64_t i = (int64_t)blockIdx.x * 32 + (threadIdx.x & 31);
+    const int64_t j = (int64_t)blockIdx.y * 8 + (threadIdx.x >> 5);
+    if (j >= N) return;
     double s = 0.0;
     Mag ent = mag_zero();
     int64_t chunk_end = 1024;
     const int n = cnt[j];
-    const double* arow = da + i * w;
+    const int64_t ii = i < M ? i : 0;
     for (int p = 0; p < n; p++) {
         const int l = idx[(int64_t)p * N + j];
+        const double v = val[(int64_t)p * N + j];
         if (l >= chunk_end) {
-            rad_fold(ent, s, ecen[i], fcen[j]);
+            rad_fold(ent, s, ecen[ii], fcen[j]);
             chunk_end = ((int64_t)l / 1024 + 1) * 1024;
         }
-        s = __dadd_rn(s, __dmul_rn(arow[l], val[(int64_t)p * N + j]));
+        s = __dadd_rn(s, __dmul_rn(daT[(int64_t)l * M + ii], v));
     }
+    if (i >= M) return;
     rad_fold(ent, s, ecen[i], fcen[j]);
     mag_store(ent, &rb[i * N + j], &rf[i * N + j]);
 }
@@ -1267,7 +1413,7 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
             flat.insert(flat.end(), l.begin(), l.end());
             begin.push_back((int)flat.size());
         }
-        for (int bnd = 0; bnd < NB; bnd++) group_d1.push_back(std::min(ND, 4 * bnd + 4));
+        for (int bnd = 0; bnd < NB; bnd++) group_d1.push_back(4 * bnd + 4);
         off_items = 0;
         off_begin = flat.size() * sizeof(int2);
         off_d1 = off_begin + begin.size() * sizeof(int);
@@ -1375,7 +1521,12 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     {
         const int NT = (NW + 1) / 2 + 2;
         const unsigned gb = blocks_for(M * N, 128);
-        if (NT <= 8) recombine_kernel<8><<<gb, 128, 0, st>>>(R);
+        static const bool slow = std::getenv("APB_SLOW_RECOMBINE") != nullptr;  // test hook
+        const bool fast = band && first && !int_out && R.C.mant && !slow;
+        if (fast && NW <= 20) recombine_fast_kernel<20><<<gb, 128, 0, st>>>(R);
+        else if (fast && NW <= 40) recombine_fast_kernel<40><<<gb, 128, 0, st>>>(R);
+        else if (fast && NW <= 72) recombine_fast_kernel<72><<<gb, 128, 0, st>>>(R);
+        else if (NT <= 8) recombine_kernel<8><<<gb, 128, 0, st>>>(R);
         else if (NT <= 16) recombine_kernel<16><<<gb, 128, 0, st>>>(R);
         else if (NT <= 40) recombine_kernel<40><<<gb, 128, 0, st>>>(R);
         else recombine_kernel<GCAP><<<gb, 128, 0, st>>>(R);
@@ -1429,7 +1580,7 @@ int radius_prepare(const apb_mat* A, const apb_mat* B, int wa, int wb, int slot,
 // phase 2, given hw = mw copied to the host: sparse / dense single block, or the
 // multi-block greedy path (which synchronizes `st` itself)
 int radius_compute(const apb_mat* A, const apb_mat* B, int wa, int wb, int slot, const long long* hw,
-                   uint32_t* rb, int64_t* rf, cudaStream_t st) {
+                   uint32_t* rb, int64_t* rf, cudaStream_t st, int a_trans = 0) {
     const RadSlots& R = kRad[slot];
     const int64_t M = A->rows, K = A->cols, N = B->cols;
     BallsView a = view_of(&A->b), b = view_of(&B->b);
@@ -1446,17 +1597,17 @@ int radius_compute(const apb_mat* A, const apb_mat* B, int wa, int wb, int slot,
         int* lidx = sbuf<int>(R.lidx, (size_t)K * std::max(M, N), st);
         double* lval = sbuf<double>(R.lval, (size_t)K * std::max(M, N), st);
         const int tk = prof_begin("rad_gemm", st);
-        if (dens_b <= 0.25 && dens_b <= dens_a && lcnt && lidx && lval) {
+        if (a_trans && dens_b <= 0.25 && dens_b <= dens_a && lcnt && lidx && lval) {
             col_lists_kernel<<<blocks_for(N, 8), 256, 0, st>>>(db, K, N, lcnt, lidx, lval);
-            dim3 grid(blocks_for(N, 32), blocks_for(M, 8));
+            dim3 grid(blocks_for(M, 32), blocks_for(N, 8));
             rad_spcol_kernel<<<grid, 256, 0, st>>>(da, M, N, K, lcnt, lidx, lval, ecen, fcen, rb, rf);
         } else if (dens_a <= 0.25 && lcnt && lidx && lval) {
-            row_lists_kernel<<<blocks_for(M, 8), 256, 0, st>>>(da, M, K, lcnt, lidx, lval);
+            row_lists_kernel<<<blocks_for(M, 8), 256, 0, st>>>(da, M, K, lcnt, lidx, lval, a_trans);
             dim3 grid(blocks_for(N, 256), (unsigned)M);
             rad_sprow_kernel<<<grid, 256, 0, st>>>(db, M, N, K, lcnt, lidx, lval, ecen, fcen, rb, rf);
         } else {
             dim3 grid(blocks_for(N, RT), blocks_for(M, RT));
-            rad_gemm_kernel<<<grid, RTHREADS, 0, st>>>(da, db, M, N, K, ecen, fcen, rb, rf, 0);
+            rad_gemm_kernel<<<grid, RTHREADS, 0, st>>>(da, db, M, N, K, ecen, fcen, rb, rf, 0, a_trans);
         }
         prof_end(tk, st);
         count_launch(2);
@@ -1495,7 +1646,7 @@ int radius_compute(const apb_mat* A, const apb_mat* B, int wa, int wb, int slot,
         rad_planes_kernel<<<blocks_for(w * N, 256), 256, 0, st>>>(b, K, N, lo, hi, wb, 0, fcen, db);
         dim3 grid(blocks_for(N, RT), blocks_for(M, RT));
         const int tk = prof_begin("rad_gemm", st);
-        rad_gemm_kernel<<<grid, RTHREADS, 0, st>>>(da, db, M, N, w, ecen, fcen, rb, rf, bi ? 1 : 0);
+        rad_gemm_kernel<<<grid, RTHREADS, 0, st>>>(da, db, M, N, w, ecen, fcen, rb, rf, bi ? 1 : 0, 0);
         prof_end(tk, st);
         count_launch(3);
     }
@@ -1557,7 +1708,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     {
         dim3 gr(blocks_for(M, 8), blocks_for(K, 32 * ROW_CH));
         fused_rows_kernel<<<gr, 256, 0, st>>>(av, M, K, RW, sum);
-        dim3 gc(blocks_for(N, 128), blocks_for(K, COL_CHUNK));
+        dim3 gc(blocks_for(N, 128), blocks_for(K, FCOL_CHUNK));
         fused_cols_kernel<<<gc, 128, 0, st>>>(bv, K, N, CW, sum);
         fused_finish_kernel<<<blocks_for(std::max(M, N), 256), 256, 0, st>>>(RW, CW, M, N, ec1, ec2, fc1, fc2, sum,
                                                                             mw1, mw2);
@@ -1597,7 +1748,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
         return e;
     }();
-    if ((rc = radius_compute(A, B, 0, 2, 0, hw1, r1b, r1f, rs))) return rc;
+    if ((rc = radius_compute(A, B, 0, 2, 0, hw1, r1b, r1f, rs, 1))) return rc;  // |A| plane transposed
     if ((rc = radius_compute(A, B, 1, 3, 1, hw2, r2b, r2f, rs))) return rc;
     if (rs != st) cudaEventRecord(ev_join, rs);
     bool first = true;
