@@ -224,6 +224,10 @@ int apb_device_status(void* stream);
 void apb_profile_enable(int on);
 void apb_profile_reset(void);
 int apb_profile_read(const char* kernel, double* ms, uint64_t* launches);
+/* timeline of every recorded region as "name<TAB>begin_ms<TAB>end_ms" lines,
+ * relative to the first region's begin (regions on all streams); returns the
+ * full text length (buf may be NULL to query it) */
+int apb_profile_dump(char* buf, size_t cap);
 
 apb_matmul_stats* apb_matmul_stats_get(void);
 void apb_matmul_stats_reset(void);

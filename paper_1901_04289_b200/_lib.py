@@ -80,6 +80,8 @@ def lib():
     L.apb_profile_reset.restype = None
     L.apb_profile_read.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
     L.apb_profile_read.restype = I
+    L.apb_profile_dump.argtypes = [C.c_char_p, C.c_size_t]
+    L.apb_profile_dump.restype = I
     _lib = L
     return L
 

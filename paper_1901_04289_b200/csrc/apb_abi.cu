@@ -139,6 +139,29 @@ int apb_profile_read(const char* kernel, double* ms, uint64_t* launches) {
     return APB_OK;
 }
 
+int apb_profile_dump(char* buf, size_t cap) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    std::string out;
+    cudaEvent_t t0 = nullptr;
+    for (auto& r : g_prof) {
+        if (r.open) continue;
+        if (cudaEventSynchronize(r.e) != cudaSuccess) return APB_ERR_CUDA;
+        if (!t0) t0 = r.b;
+        float b = 0, e = 0;
+        cudaEventElapsedTime(&b, t0, r.b);
+        cudaEventElapsedTime(&e, t0, r.e);
+        char line[160];
+        std::snprintf(line, sizeof line, "%s\t%.4f\t%.4f\n", r.name.c_str(), (double)b, (double)e);
+        out += line;
+    }
+    if (buf && cap) {
+        const size_t n = std::min(cap - 1, out.size());
+        std::memcpy(buf, out.data(), n);
+        buf[n] = 0;
+    }
+    return (int)out.size();
+}
+
 int apb_device_status(void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     int rc = cuda_check(cudaStreamSynchronize(st), "apb_device_status");

@@ -313,19 +313,30 @@ __global__ void __launch_bounds__(THREADS, 1)
 // Each (tile, band) work item is independent (carry-in 0, carry-out to
 // Tc[band]); items are LPT-assigned to persistent CTAs on the host.
 // Requires |D_d| < 2^31: pairs(d) * K * 2^14 < 2^31 (checked by the driver).
-constexpr int BAND_W = 4;
-constexpr int A_STAGES = 4, B_STAGES = 8;
-constexpr int TILE_BYTES = 128 * BK;
-constexpr int BAND_SMEM = (A_STAGES + B_STAGES) * TILE_BYTES + 1024 + 512;
+// variants: <BNT=128, W=4> (4 diagonals, N=128 MMAs) and <BNT=256, W=2>
+// (2 diagonals, N=256 MMAs: half the MMA issues per unit of work)
+template <int BNT, int W>
+struct BandCfg {
+    static constexpr int A_STAGES = 4;
+    static constexpr int TILE_A = 128 * BK;
+    static constexpr int TILE_B = BNT * BK;
+    static constexpr int B_STAGES = BNT == 128 ? 8 : 5;
+    static constexpr int SMEM = A_STAGES * TILE_A + B_STAGES * TILE_B + 1024 + 512;
+    static constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BNT >> 3) << 17) |
+                                      ((uint32_t)(BM >> 4) << 24);
+};
 
+template <int BNT, int BAND_W>
 __global__ void __launch_bounds__(THREADS, 1)
     band_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      BandGemmParams P) {
+    using Cfg = BandCfg<BNT, BAND_W>;
+    constexpr int A_STAGES = Cfg::A_STAGES, B_STAGES = Cfg::B_STAGES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* smA = smem;
-    uint8_t* smB = smem + A_STAGES * TILE_BYTES;
-    uint64_t* bars = (uint64_t*)(smem + (A_STAGES + B_STAGES) * TILE_BYTES);
+    uint8_t* smB = smem + A_STAGES * Cfg::TILE_A;
+    uint64_t* bars = (uint64_t*)(smem + A_STAGES * Cfg::TILE_A + B_STAGES * Cfg::TILE_B);
     uint64_t* fullA = bars;
     uint64_t* emptyA = fullA + A_STAGES;
     uint64_t* fullB = emptyA + A_STAGES;
@@ -369,7 +380,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             uint32_t ai = 0, bi = 0;  // sequential ring indices
             for (int it = it_begin; it < it_end; it++) {
                 const int2 W = P.items[it];
-                const int m0 = (W.x / P.n_tiles_n) * 128, n0 = (W.x % P.n_tiles_n) * 128;
+                const int m0 = (W.x / P.n_tiles_n) * 128, n0 = (W.x % P.n_tiles_n) * BNT;
                 const int d0 = BAND_W * W.y;
                 const int s_hi = min(P.S_A - 1, d0 + BAND_W - 1), s_lo = max(0, d0 - (P.S_B - 1));
                 for (int kb = 0; kb < P.n_kb; kb++) {
@@ -379,15 +390,15 @@ __global__ void __launch_bounds__(THREADS, 1)
                         {
                             const uint32_t st = ai % A_STAGES, ph = (ai / A_STAGES) & 1;
                             mbar_wait(&emptyA[st], ph ^ 1);
-                            mbar_expect_tx(&fullA[st], TILE_BYTES);
-                            tma_load_2d(smA + st * TILE_BYTES, &tmA, kb * BK, s * P.Mp + m0, &fullA[st]);
+                            mbar_expect_tx(&fullA[st], Cfg::TILE_A);
+                            tma_load_2d(smA + st * Cfg::TILE_A, &tmA, kb * BK, s * P.Mp + m0, &fullA[st]);
                             ai++;
                         }
                         for (int t = max(tmin, tmax_prev + 1); t <= tmax; t++) {
                             const uint32_t st = bi % B_STAGES, ph = (bi / B_STAGES) & 1;
                             mbar_wait(&emptyB[st], ph ^ 1);
-                            mbar_expect_tx(&fullB[st], TILE_BYTES);
-                            tma_load_2d(smB + st * TILE_BYTES, &tmB, kb * BK, t * P.Np + n0, &fullB[st]);
+                            mbar_expect_tx(&fullB[st], Cfg::TILE_B);
+                            tma_load_2d(smB + st * Cfg::TILE_B, &tmB, kb * BK, t * P.Np + n0, &fullB[st]);
                             bi++;
                         }
                         tmax_prev = tmax;
@@ -419,16 +430,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                     fence_after();
                     if (lane == 0) {
-                        const uint32_t a0 = smem_u32(smA + ast * TILE_BYTES);
+                        const uint32_t a0 = smem_u32(smA + ast * Cfg::TILE_A);
                         for (int t = tmin; t <= tmax; t++) {
                             const int w = s + t - d0;
                             const uint32_t bidx = b_first + (uint32_t)(t - t_first);
-                            const uint32_t b0 = smem_u32(smB + (bidx % B_STAGES) * TILE_BYTES);
-                            const uint32_t tmem_d = tmem_base + (uint32_t)(w * 128);
+                            const uint32_t b0 = smem_u32(smB + (bidx % B_STAGES) * Cfg::TILE_B);
+                            const uint32_t tmem_d = tmem_base + (uint32_t)(w * BNT);
 #pragma unroll
                             for (int k = 0; k < BK / 32; k++) {
                                 const uint32_t acc = ((init_mask >> w) & 1u) | (k > 0 ? 1u : 0u);
-                                mma_i8(tmem_d, smem_desc(a0 + 32 * k), smem_desc(b0 + 32 * k), kIdesc, acc);
+                                mma_i8(tmem_d, smem_desc(a0 + 32 * k), smem_desc(b0 + 32 * k), Cfg::IDESC, acc);
                             }
                             init_mask |= 1u << w;
                         }
@@ -459,17 +470,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     } else {
         const int e = warp - 2;
         const int q = warp & 3;
-        const int col0 = (e >> 2) * 64;
+        const int col0 = (e >> 2) * (BNT / 2);
         uint32_t tph = 0;
         for (int it = it_begin; it < it_end; it++) {
             const int2 W = P.items[it];
-            const int m0 = (W.x / P.n_tiles_n) * 128, n0 = (W.x % P.n_tiles_n) * 128;
+            const int m0 = (W.x / P.n_tiles_n) * 128, n0 = (W.x % P.n_tiles_n) * BNT;
             const int d0 = BAND_W * W.y;
             const int row = m0 + 32 * q + lane;
             mbar_wait(tfull, tph);
             fence_after();
 #pragma unroll 1
-            for (int h = 0; h < 2; h++) {
+            for (int h = 0; h < BNT / 64; h++) {
                 int32_t carry[32];
                 uint32_t word[32];
 #pragma unroll
@@ -483,7 +494,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     // carry leaves at bit 32 (b + 1) (word aligned for the recombine)
                     uint32_t v[32];
                     if (d0 + w < P.ND) {
-                        const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(w * 128 + col0 + 32 * h);
+                        const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(w * BNT + col0 + 32 * h);
                         TMEM_LD32(taddr, v);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     } else {
@@ -584,20 +595,29 @@ int slice_gemm_launch(const int8_t* Apack, const int8_t* Bpack, const SliceGemmP
 
 namespace apb {
 
+template <int BNT, int W>
+static int band_launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const BandGemmParams& P, int n_ctas,
+                         cudaStream_t st) {
+    using Cfg = BandCfg<BNT, W>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(band_gemm_kernel<BNT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        attr = true;
+    }
+    band_gemm_kernel<BNT, W><<<n_ctas, THREADS, Cfg::SMEM, st>>>(ma, mb, P);
+    return APB_OK;
+}
+
 int band_gemm_launch(const int8_t* Apack, const int8_t* Bpack, const BandGemmParams& P, int n_ctas,
                      cudaStream_t st) {
     CUtensorMap ma, mb;
     int rc = make_map(&ma, Apack, (uint64_t)P.Kp, (uint64_t)P.S_A * P.Mp, BM);
     if (rc) return rc;
-    rc = make_map(&mb, Bpack, (uint64_t)P.Kp, (uint64_t)P.S_B * P.Np, BN);
+    rc = make_map(&mb, Bpack, (uint64_t)P.Kp, (uint64_t)P.S_B * P.Np, (uint32_t)P.bn);
     if (rc) return rc;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(band_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BAND_SMEM);
-        attr = true;
-    }
     const int tok = prof_begin("slice_gemm", st);
-    band_gemm_kernel<<<n_ctas, THREADS, BAND_SMEM, st>>>(ma, mb, P);
+    if (P.bn == 256) band_launch_t<256, 2>(ma, mb, P, n_ctas, st);
+    else band_launch_t<128, 4>(ma, mb, P, n_ctas, st);
     prof_end(tok, st);
     count_launch();
     return cuda_check(cudaGetLastError(), "band_gemm launch");

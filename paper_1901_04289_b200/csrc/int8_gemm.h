@@ -22,6 +22,7 @@ struct SliceGemmParams {
 // band variant: 4 diagonals per pass, persistent CTAs over (tile, band) items
 struct BandGemmParams {
     int S_A, S_B, Mp, Np, Kp, n_kb, ND;
+    int bn, band_w;           // (128, 4) or (256, 2): output tile width / diagonals per item
     int n_tiles_n;            // Np / 128
     const int2* items;        // (tile = mt * n_tiles_n + nt, band)
     const int* cta_begin;     // [n_ctas + 1] item ranges per CTA

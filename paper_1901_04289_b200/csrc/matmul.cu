@@ -335,6 +335,53 @@ __global__ void __launch_bounds__(256) pack_kernel(BallsView X, int64_t rows, in
     }
 }
 
+
+// B-side pack with coalesced reads: a 32 (columns j) x 32 (inner kk) tile per
+// 256 threads; lanes run over consecutive j (contiguous in row-major B), the
+// digits are transposed through shared memory so each plane row (fixed j,
+// contiguous kk) is written with 32-byte segments.
+__global__ void __launch_bounds__(256) pack_b_tiled_kernel(BallsView X, int64_t N, int64_t lo, int64_t hi,
+                                                           const int64_t* top, const int64_t* bot, int S,
+                                                           int Np, int Kp, int8_t* out, int64_t* scale_out) {
+    __shared__ uint32_t tile[8][32][9];  // [digit in chunk][j][kk word], padded
+    const int jl = threadIdx.x & 31, kq = threadIdx.x >> 5;
+    const int64_t j = (int64_t)blockIdx.x * 32 + jl;
+    const int64_t kk0 = (int64_t)blockIdx.y * 32 + 4 * kq;
+    int64_t sc = 0;
+    if (j < N) sc = top[j] == INT64_MIN ? 0 : -bot[j];
+    if (j < N && blockIdx.y == 0 && kq == 0) scale_out[j] = sc;
+    DigitStream ds[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int64_t kk = kk0 + q;
+        const bool valid = j < N && kk < hi - lo;
+        ds_init(ds[q], X, valid ? (lo + kk) * N + j : 0, valid, sc);
+    }
+    const size_t plane = (size_t)Np * Kp;
+    const int nch = (S + 7) / 8;
+    for (int c = 0; c < nch; c++) {
+        uint64_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) w[q] = ds_digits8(ds[q], ds[q].live ? ds_word(ds[q], 64 * (int64_t)c - ds[q].sh) : 0);
+#pragma unroll
+        for (int b = 0; b < 8; b++)
+            tile[b][jl][kq] = ((uint32_t)(w[0] >> (8 * b)) & 255u) | (((uint32_t)(w[1] >> (8 * b)) & 255u) << 8) |
+                              (((uint32_t)(w[2] >> (8 * b)) & 255u) << 16) | (((uint32_t)(w[3] >> (8 * b)) & 255u) << 24);
+        __syncthreads();
+        // 8 digits x 32 rows x 8 words: thread -> (digit b, row r, word m)
+#pragma unroll
+        for (int it = 0; it < 8; it++) {
+            const int idx = it * 256 + threadIdx.x;
+            const int m = idx & 7, r = (idx >> 3) & 31, b = idx >> 8;
+            const int s = 8 * c + b;
+            const int64_t jj = (int64_t)blockIdx.x * 32 + r;
+            if (s < S && jj < Np)
+                *(uint32_t*)(out + (size_t)s * plane + (size_t)jj * Kp + (size_t)blockIdx.y * 32 + 4 * m) = tile[b][r][m];
+        }
+        __syncthreads();
+    }
+}
+
 // -------------------------------------------------------- K6 recombine
 struct RecombineArgs {
     const uint32_t* Tw;
@@ -438,49 +485,64 @@ __global__ void __launch_bounds__(128) recombine_kernel(RecombineArgs R) {
 
 
 // Register-resident recombine for the band GEMM output of a single (first)
-// block: T = sum_b (word_b + carry_b 2^32) 2^(32 b) in base-2^32 digits, then
+// block: T = sum_b (word_b + carry_b 2^DB) 2^(DB b) in base-2^DB digits, then
 // sign, normalize and truncate to p bits with the apfloat_round error term
 // (src/apfloat.cpp:26-63, 138-162), all with compile-time array bounds.
-template <int NBC>
+template <int NBC, int DB>
 __global__ void __launch_bounds__(128) recombine_fast_kernel(RecombineArgs R) {
-    constexpr int ND32 = NBC + 2;          // 32-bit digits
-    constexpr int NL = (ND32 + 1) / 2;     // 64-bit limbs
+    // digits of DB = 8 * (diagonals per band) bits: band b's word is digit b, its carry digit b+1
+    constexpr int ND32 = NBC + 2;               // digits
+    constexpr int PER = 64 / DB;                // digits per 64-bit limb
+    constexpr int NL = (ND32 + PER - 1) / PER;  // 64-bit limbs
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= R.M * R.N) return;
     const int64_t i = t / R.N, j = t % R.N;
     const size_t plane = (size_t)R.Mp * R.Np;
     const size_t off = (size_t)i * R.Np + j;
     const int NB = R.nwords;
-    int64_t D[ND32];
-#pragma unroll
-    for (int k = 0; k < ND32; k++) D[k] = 0;
-#pragma unroll
-    for (int b = 0; b < NBC; b++) {
-        if (b < NB) {
-            D[b] += (int64_t)R.Tw[(size_t)b * plane + off];
-            D[b + 1] += (int64_t)R.Tc[(size_t)b * plane + off];
-        }
-    }
-    // carry-propagate base 2^32 (arithmetic shifts keep the sign in the top digit)
-#pragma unroll
-    for (int k = 0; k + 1 < ND32; k++) {
-        D[k + 1] += D[k] >> 32;
-        D[k] &= 0xFFFFFFFFll;
-    }
-    const bool neg = D[ND32 - 1] < 0;
+    // one streaming pass over the digits, base 2^DB: digit k = word_k + carry_{k-1}
+    // + the running carry; batches of RB bands are loaded before they are
+    // consumed so RB * 2 loads are in flight per thread with few live registers
+    constexpr int RB = 8;
     uint64_t T[NL];
 #pragma unroll
-    for (int q = 0; q < NL; q++) {
-        const uint64_t lo = (uint64_t)(uint32_t)D[2 * q];
-        const uint64_t hi = 2 * q + 1 < ND32 ? (uint64_t)(uint32_t)D[2 * q + 1] : (neg ? 0xFFFFFFFFull : 0ull);
-        T[q] = lo | (hi << 32);
+    for (int q = 0; q < NL; q++) T[q] = 0;
+    int64_t run = 0, prev_c = 0;
+    bool neg = false;
+#pragma unroll
+    for (int kb = 0; kb < ND32; kb += RB) {
+        uint32_t w[RB];
+        int32_t c[RB];
+#pragma unroll
+        for (int u = 0; u < RB; u++) {
+            const int b = kb + u;
+            w[u] = (b < NBC && b < NB) ? __ldcs(R.Tw + (size_t)b * plane + off) : 0u;
+            c[u] = (b < NBC && b < NB) ? __ldcs(R.Tc + (size_t)b * plane + off) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < RB; u++) {
+            const int k = kb + u;
+            if (k < ND32) {
+                const int64_t d = run + (int64_t)w[u] + prev_c;
+                prev_c = c[u];
+                const uint64_t dg = (uint64_t)d & ((1ull << DB) - 1);
+                if (k == ND32 - 1) {
+                    neg = d < 0;  // the arithmetic top digit carries the sign
+                } else {
+                    run = d >> DB;
+                }
+                T[k / PER] |= dg << (DB * (k % PER));
+            }
+        }
     }
-    if (neg) {  // magnitude
-        uint64_t c = 1;
+    if (neg) {  // sign-fill the digits above the top one, then take the magnitude
+#pragma unroll
+        for (int k = ND32; k < NL * PER; k++) T[k / PER] |= ((1ull << DB) - 1) << (DB * (k % PER));
+        uint64_t cc = 1;
 #pragma unroll
         for (int q = 0; q < NL; q++) {
-            const uint64_t v = ~T[q] + c;
-            c = (c && v == 0) ? 1 : 0;
+            const uint64_t v = ~T[q] + cc;
+            cc = (cc && v == 0) ? 1 : 0;
             T[q] = v;
         }
     }
@@ -632,7 +694,7 @@ APB_DEV void win_atomic(int64_t* top, int64_t* bot, int64_t t, int64_t b) {
 // rows of A: warp per (row, 32*CH chunk of k), lanes over k (coalesced)
 constexpr int ROW_CH = 4;
 __global__ void __launch_bounds__(256) fused_rows_kernel(BallsView A, int64_t M, int64_t K, LineWins W,
-                                                         ScanSummary* sum) {
+                                                         ScanSummary* sum, long long* nz1, long long* nz2) {
     const int lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (i >= M) return;
@@ -640,6 +702,7 @@ __global__ void __launch_bounds__(256) fused_rows_kernel(BallsView A, int64_t M,
     int64_t t0 = INT64_MIN, b0 = INT64_MAX, t1 = INT64_MIN, b1 = INT64_MAX, t2 = INT64_MIN, b2 = INT64_MAX;
     int64_t prec = 0;
     int special = 0;
+    int c1 = 0, c2 = 0;  // nonzero |A| and R_A entries (radius sparsity)
 #pragma unroll
     for (int c = 0; c < ROW_CH; c++) {
         const int64_t k = k0 + 32 * c + lane;
@@ -652,11 +715,15 @@ __global__ void __launch_bounds__(256) fused_rows_kernel(BallsView A, int64_t M,
             prec = (t - b) > prec ? (t - b) : prec;
         }
         const Mag m1 = mid_upper(A, e);
-        if (m1.kind == 1) win_merge(t1, b1, m1.f, m1.f - 30);
+        if (m1.kind == 1) {
+            win_merge(t1, b1, m1.f, m1.f - 30);
+            c1++;
+        }
         const uint32_t rb = A.rad_man[e];
         if (rb != 0 && rb != APB_RAD_INF) {
             const Mag m2 = mag_parts(rb, A.rad_exp[e]);
             win_merge(t2, b2, m2.f, m2.f - 30);
+            c2++;
         }
     }
 #pragma unroll
@@ -669,9 +736,13 @@ __global__ void __launch_bounds__(256) fused_rows_kernel(BallsView A, int64_t M,
         x = __shfl_xor_sync(0xffffffffu, t2, o); t2 = x > t2 ? x : t2;
         x = __shfl_xor_sync(0xffffffffu, b2, o); b2 = x < b2 ? x : b2;
         x = __shfl_xor_sync(0xffffffffu, prec, o); prec = x > prec ? x : prec;
+        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+        c2 += __shfl_xor_sync(0xffffffffu, c2, o);
     }
     special = __any_sync(0xffffffffu, special);
     if (lane == 0) {
+        if (c1) atomicAdd((unsigned long long*)nz1, (unsigned long long)c1);
+        if (c2) atomicAdd((unsigned long long*)nz2, (unsigned long long)c2);
         win_atomic(&W.top[0][i], &W.bot[0][i], t0, b0);
         win_atomic(&W.top[1][i], &W.bot[1][i], t1, b1);
         win_atomic(&W.top[2][i], &W.bot[2][i], t2, b2);
@@ -683,13 +754,14 @@ __global__ void __launch_bounds__(256) fused_rows_kernel(BallsView A, int64_t M,
 constexpr int FCOL_CHUNK = 4;
 // columns of B: thread per (column, FCOL_CHUNK rows), coalesced across threads
 __global__ void __launch_bounds__(128) fused_cols_kernel(BallsView B, int64_t K, int64_t N, LineWins W,
-                                                         ScanSummary* sum) {
+                                                         ScanSummary* sum, long long* nz1, long long* nz2) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t k0 = (int64_t)blockIdx.y * FCOL_CHUNK;
     const int64_t k1 = k0 + FCOL_CHUNK < K ? k0 + FCOL_CHUNK : K;
     int64_t t0 = INT64_MIN, b0 = INT64_MAX, t1 = INT64_MIN, b1 = INT64_MAX, t2 = INT64_MIN, b2 = INT64_MAX;
     int64_t prec = 0;
     int special = 0;
+    int c1 = 0, c2 = 0;  // nonzero R_B and |B| + R_B entries
     if (j < N) {
         for (int64_t k = k0; k < k1; k++) {
             const int64_t e = k * N + j;
@@ -701,9 +773,15 @@ __global__ void __launch_bounds__(128) fused_cols_kernel(BallsView B, int64_t K,
             }
             const uint32_t rb = B.rad_man[e];
             const Mag r = (rb != 0 && rb != APB_RAD_INF) ? mag_parts(rb, B.rad_exp[e]) : mag_zero();
-            if (r.kind == 1) win_merge(t1, b1, r.f, r.f - 30);
+            if (r.kind == 1) {
+                win_merge(t1, b1, r.f, r.f - 30);
+                c1++;
+            }
             const Mag s = mag_add(mid_upper(B, e), r);
-            if (s.kind == 1) win_merge(t2, b2, s.f, s.f - 30);
+            if (s.kind == 1) {
+                win_merge(t2, b2, s.f, s.f - 30);
+                c2++;
+            }
         }
         win_atomic(&W.top[0][j], &W.bot[0][j], t0, b0);
         win_atomic(&W.top[1][j], &W.bot[1][j], t1, b1);
@@ -713,11 +791,15 @@ __global__ void __launch_bounds__(128) fused_cols_kernel(BallsView B, int64_t K,
     for (int o = 16; o; o >>= 1) {
         int64_t x = __shfl_xor_sync(0xffffffffu, prec, o);
         prec = x > prec ? x : prec;
+        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+        c2 += __shfl_xor_sync(0xffffffffu, c2, o);
     }
     special = __any_sync(0xffffffffu, special);
     if ((threadIdx.x & 31) == 0) {
         if (special) atomicOr(&sum->special_b, 1);
         if (prec) atomicMax(&sum->prec_b, (long long)prec);
+        if (c1) atomicAdd((unsigned long long*)nz1, (unsigned long long)c1);
+        if (c2) atomicAdd((unsigned long long*)nz2, (unsigned long long)c2);
     }
 }
 
@@ -782,10 +864,12 @@ __global__ void fused_planes_kernel(BallsView X, int64_t rows, int64_t cols, int
         else p1[t] = v1;
         p2[t] = v2;
     }
-    const unsigned a1 = __ballot_sync(0xffffffffu, v1 != 0.0), a2 = __ballot_sync(0xffffffffu, v2 != 0.0);
-    if ((threadIdx.x & 31) == 0) {
-        if (a1) atomicAdd((unsigned long long*)nz1, (unsigned long long)__popc(a1));
-        if (a2) atomicAdd((unsigned long long*)nz2, (unsigned long long)__popc(a2));
+    if (nz1) {
+        const unsigned a1 = __ballot_sync(0xffffffffu, v1 != 0.0), a2 = __ballot_sync(0xffffffffu, v2 != 0.0);
+        if ((threadIdx.x & 31) == 0) {
+            if (a1) atomicAdd((unsigned long long*)nz1, (unsigned long long)__popc(a1));
+            if (a2) atomicAdd((unsigned long long*)nz2, (unsigned long long)__popc(a2));
+        }
     }
 }
 
@@ -1356,8 +1440,13 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         cbot = cb;
     }
     const int SA = slices_for(maxw_a), SB = slices_for(maxw_b);
+    // band tile: 128 x 256 outputs with 2 diagonals per pass (N=256 MMAs) when the
+    // matrix is wide enough, else 128 x 128 with 4 diagonals (APB_BAND_BN overrides)
+    static const int bn_env = std::getenv("APB_BAND_BN") ? std::atoi(std::getenv("APB_BAND_BN")) : 0;
+    const int bn = bn_env == 128 || bn_env == 256 ? bn_env : (N >= 256 ? 256 : 128);
+    const int band_w = bn == 256 ? 2 : 4;
     const int Mp = (int)((M + kSliceTile - 1) / kSliceTile * kSliceTile);
-    const int Np = (int)((N + kSliceTile - 1) / kSliceTile * kSliceTile);
+    const int Np = (int)((N + bn - 1) / bn * bn);
     const int Kp = (int)((w + kSliceBK - 1) / kSliceBK * kSliceBK);
     stats().int_gemm_products++;
     stats().last_height_a = (uint64_t)maxw_a;
@@ -1374,88 +1463,96 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     }
     int tok = prof_begin("pack", st);
     pack_kernel<false><<<blocks_for((int64_t)Mp * Kp / 4, 256), 256, 0, st>>>(a, M, K, lo, hi, rtop, rbot, SA, Mp, Kp, Ap, esc);
-    pack_kernel<true><<<blocks_for((int64_t)Np * Kp / 4, 256), 256, 0, st>>>(b, N, N, lo, hi, ctop, cbot, SB, Np, Kp, Bp, fsc);
+    {
+        dim3 gb((unsigned)(Np / 32), (unsigned)(Kp / 32));
+        pack_b_tiled_kernel<<<gb, 256, 0, st>>>(b, N, lo, hi, ctop, cbot, SB, Np, Kp, Bp, fsc);
+    }
     prof_end(tok, st);
     count_launch(2);
-    const int tiles = (Mp / kSliceTile) * (Np / kSliceTile);
+    const int tiles = (Mp / kSliceTile) * (Np / bn);
     const int ND = SA + SB - 1;
     // band kernel when every diagonal fits an int32 accumulator: pairs * w * 2^14 < 2^31
     static const bool force_unit = std::getenv("APB_FORCE_UNIT_GEMM") != nullptr;  // test hook
     const bool band = !force_unit && (int64_t)std::min(SA, SB) * w < (int64_t)1 << 17;
-    int G, NW;
-    std::vector<char> host;  // staged tables
-    std::vector<int> group_d1;
-    size_t off_items = 0, off_begin = 0, off_d1 = 0, n_ctas = 0;
-    Units U;
-    if (band) {
-        const int NB = (ND + 3) / 4;
-        std::vector<int64_t> bw(NB, 0);
-        for (int d = 0; d < ND; d++)
-            bw[d / 4] += std::min(d, SA - 1) - std::max(0, d - SB + 1) + 1;
-        std::vector<std::pair<int64_t, int2>> items;
-        for (int t = 0; t < tiles; t++)
-            for (int bnd = 0; bnd < NB; bnd++) items.push_back({bw[bnd], make_int2(t, bnd)});
-        std::stable_sort(items.begin(), items.end(),
-                         [](const std::pair<int64_t, int2>& x, const std::pair<int64_t, int2>& y) { return x.first > y.first; });
-        n_ctas = std::min<size_t>(148, items.size());
-        std::vector<std::vector<int2>> lists(n_ctas);
-        std::vector<int64_t> load(n_ctas, 0);
-        for (auto& it : items) {  // LPT: heaviest item to the least loaded CTA
-            size_t best = 0;
-            for (size_t c = 1; c < n_ctas; c++)
-                if (load[c] < load[best]) best = c;
-            lists[best].push_back(it.second);
-            load[best] += it.first;
-        }
-        std::vector<int2> flat;
-        std::vector<int> begin = {0};
-        for (auto& l : lists) {
-            flat.insert(flat.end(), l.begin(), l.end());
-            begin.push_back((int)flat.size());
-        }
-        for (int bnd = 0; bnd < NB; bnd++) group_d1.push_back(4 * bnd + 4);
-        off_items = 0;
-        off_begin = flat.size() * sizeof(int2);
-        off_d1 = off_begin + begin.size() * sizeof(int);
-        host.resize(off_d1 + group_d1.size() * sizeof(int));
-        std::memcpy(host.data(), flat.data(), flat.size() * sizeof(int2));
-        std::memcpy(host.data() + off_begin, begin.data(), begin.size() * sizeof(int));
-        std::memcpy(host.data() + off_d1, group_d1.data(), group_d1.size() * sizeof(int));
-        G = NB;
-        NW = NB;
-    } else {
-        U = make_units(SA, SB, w, tiles);
-        G = (int)U.group_d1.size();
-        NW = (ND + 3) / 4;
-        off_items = 0;
-        off_begin = U.units.size() * sizeof(int4);
-        off_d1 = off_begin + U.group_begin.size() * sizeof(int);
-        host.resize(off_d1 + U.group_d1.size() * sizeof(int));
-        std::memcpy(host.data(), U.units.data(), U.units.size() * sizeof(int4));
-        std::memcpy(host.data() + off_begin, U.group_begin.data(), U.group_begin.size() * sizeof(int));
-        std::memcpy(host.data() + off_d1, U.group_d1.data(), U.group_d1.size() * sizeof(int));
-    }
-    const size_t ubytes = host.size();
-    // the tables depend only on (band, S_A, S_B, w, tile grid): cache device copies
-    static std::map<std::vector<int64_t>, char*> table_cache;
-    const std::vector<int64_t> key = {band ? 1 : 0, SA, SB, w, Mp, Np};
-    char* dunits;
+    // work tables depend only on (band, S_A, S_B, w, tile grid): built once on the
+    // host (LPT item assignment / unit groups), cached as device copies
+    struct Tables {
+        char* dev;
+        int G, NW;
+        size_t off_items, off_begin, off_d1, n_ctas;
+    };
+    static std::map<std::vector<int64_t>, Tables> table_cache;
+    const std::vector<int64_t> key = {band ? bn : 0, SA, SB, w, Mp, Np};
     auto hit = table_cache.find(key);
-    if (hit != table_cache.end()) {
-        dunits = hit->second;
-    } else {
-        if (cudaMalloc(&dunits, ubytes) != cudaSuccess) {
+    if (hit == table_cache.end()) {
+        Tables T{};
+        std::vector<char> host;
+        if (band) {
+            const int NB = (ND + band_w - 1) / band_w;
+            std::vector<int64_t> bw(NB, 0);
+            for (int d = 0; d < ND; d++)
+                bw[d / band_w] += std::min(d, SA - 1) - std::max(0, d - SB + 1) + 1;
+            std::vector<std::pair<int64_t, int2>> items;
+            for (int t = 0; t < tiles; t++)
+                for (int bnd = 0; bnd < NB; bnd++) items.push_back({bw[bnd], make_int2(t, bnd)});
+            std::stable_sort(items.begin(), items.end(),
+                             [](const std::pair<int64_t, int2>& x, const std::pair<int64_t, int2>& y) {
+                                 return x.first > y.first;
+                             });
+            T.n_ctas = std::min<size_t>(148, items.size());
+            std::vector<std::vector<int2>> lists(T.n_ctas);
+            std::vector<int64_t> load(T.n_ctas, 0);
+            for (auto& it : items) {  // LPT: heaviest item to the least loaded CTA
+                size_t best = 0;
+                for (size_t c = 1; c < T.n_ctas; c++)
+                    if (load[c] < load[best]) best = c;
+                lists[best].push_back(it.second);
+                load[best] += it.first;
+            }
+            std::vector<int2> flat;
+            std::vector<int> begin = {0}, group_d1;
+            for (auto& l : lists) {
+                flat.insert(flat.end(), l.begin(), l.end());
+                begin.push_back((int)flat.size());
+            }
+            for (int bnd = 0; bnd < NB; bnd++) group_d1.push_back(band_w * bnd + band_w);
+            T.off_items = 0;
+            T.off_begin = flat.size() * sizeof(int2);
+            T.off_d1 = T.off_begin + begin.size() * sizeof(int);
+            host.resize(T.off_d1 + group_d1.size() * sizeof(int));
+            std::memcpy(host.data(), flat.data(), flat.size() * sizeof(int2));
+            std::memcpy(host.data() + T.off_begin, begin.data(), begin.size() * sizeof(int));
+            std::memcpy(host.data() + T.off_d1, group_d1.data(), group_d1.size() * sizeof(int));
+            T.G = NB;
+            T.NW = NB;
+        } else {
+            Units U = make_units(SA, SB, w, tiles);
+            T.G = (int)U.group_d1.size();
+            T.NW = (ND + 3) / 4;
+            T.off_items = 0;
+            T.off_begin = U.units.size() * sizeof(int4);
+            T.off_d1 = T.off_begin + U.group_begin.size() * sizeof(int);
+            host.resize(T.off_d1 + U.group_d1.size() * sizeof(int));
+            std::memcpy(host.data(), U.units.data(), U.units.size() * sizeof(int4));
+            std::memcpy(host.data() + T.off_begin, U.group_begin.data(), U.group_begin.size() * sizeof(int));
+            std::memcpy(host.data() + T.off_d1, U.group_d1.data(), U.group_d1.size() * sizeof(int));
+        }
+        if (cudaMalloc(&T.dev, host.size()) != cudaSuccess) {
             set_error("out of device memory (unit tables)");
             return APB_ERR_CUDA;
         }
-        cudaMemcpy(dunits, host.data(), ubytes, cudaMemcpyHostToDevice);
+        cudaMemcpy(T.dev, host.data(), host.size(), cudaMemcpyHostToDevice);
         if (table_cache.size() > 256) {  // bounded cache
             cudaDeviceSynchronize();
-            for (auto& kv : table_cache) cudaFree(kv.second);
+            for (auto& kv : table_cache) cudaFree(kv.second.dev);
             table_cache.clear();
         }
-        table_cache[key] = dunits;
+        hit = table_cache.emplace(key, T).first;
     }
+    const Tables& TB = hit->second;
+    const int G = TB.G, NW = TB.NW;
+    char* dunits = TB.dev;
+    const size_t off_items = TB.off_items, off_begin = TB.off_begin, off_d1 = TB.off_d1, n_ctas = TB.n_ctas;
     uint32_t* Tw = sbuf<uint32_t>(S_TW, (size_t)NW * Mp * Np, st);
     int32_t* Tc = sbuf<int32_t>(S_TC, (size_t)G * Mp * Np, st);
     if (!Tw || !Tc) {
@@ -1473,7 +1570,9 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         P.Kp = Kp;
         P.n_kb = Kp / kSliceBK;
         P.ND = ND;
-        P.n_tiles_n = Np / kSliceTile;
+        P.n_tiles_n = Np / bn;
+        P.bn = bn;
+        P.band_w = band_w;
         P.items = (const int2*)(dunits + off_items);
         P.cta_begin = (const int*)(dunits + off_begin);
         P.Tw = Tw;
@@ -1523,9 +1622,12 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         const unsigned gb = blocks_for(M * N, 128);
         static const bool slow = std::getenv("APB_SLOW_RECOMBINE") != nullptr;  // test hook
         const bool fast = band && first && !int_out && R.C.mant && !slow;
-        if (fast && NW <= 20) recombine_fast_kernel<20><<<gb, 128, 0, st>>>(R);
-        else if (fast && NW <= 40) recombine_fast_kernel<40><<<gb, 128, 0, st>>>(R);
-        else if (fast && NW <= 72) recombine_fast_kernel<72><<<gb, 128, 0, st>>>(R);
+        if (fast && band_w == 4 && NW <= 20) recombine_fast_kernel<20, 32><<<gb, 128, 0, st>>>(R);
+        else if (fast && band_w == 4 && NW <= 40) recombine_fast_kernel<40, 32><<<gb, 128, 0, st>>>(R);
+        else if (fast && band_w == 4 && NW <= 72) recombine_fast_kernel<72, 32><<<gb, 128, 0, st>>>(R);
+        else if (fast && band_w == 2 && NW <= 40) recombine_fast_kernel<40, 16><<<gb, 128, 0, st>>>(R);
+        else if (fast && band_w == 2 && NW <= 80) recombine_fast_kernel<80, 16><<<gb, 128, 0, st>>>(R);
+        else if (fast && band_w == 2 && NW <= 144) recombine_fast_kernel<144, 16><<<gb, 128, 0, st>>>(R);
         else if (NT <= 8) recombine_kernel<8><<<gb, 128, 0, st>>>(R);
         else if (NT <= 16) recombine_kernel<16><<<gb, 128, 0, st>>>(R);
         else if (NT <= 40) recombine_kernel<40><<<gb, 128, 0, st>>>(R);
@@ -1703,19 +1805,19 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     cudaMemsetAsync(sum, 0, sizeof(ScanSummary), st);
     cudaMemsetAsync(mw1, 0, 4 * sizeof(long long), st);
     cudaMemsetAsync(mw2, 0, 4 * sizeof(long long), st);
+    const int tk_scan = prof_begin("scan", st);
     init_wins_kernel<<<blocks_for(M, 256), 256, 0, st>>>(RW, M);
     init_wins_kernel<<<blocks_for(N, 256), 256, 0, st>>>(CW, N);
     {
         dim3 gr(blocks_for(M, 8), blocks_for(K, 32 * ROW_CH));
-        fused_rows_kernel<<<gr, 256, 0, st>>>(av, M, K, RW, sum);
+        fused_rows_kernel<<<gr, 256, 0, st>>>(av, M, K, RW, sum, mw1 + 2, mw2 + 2);
         dim3 gc(blocks_for(N, 128), blocks_for(K, FCOL_CHUNK));
-        fused_cols_kernel<<<gc, 128, 0, st>>>(bv, K, N, CW, sum);
+        fused_cols_kernel<<<gc, 128, 0, st>>>(bv, K, N, CW, sum, mw1 + 3, mw2 + 3);
         fused_finish_kernel<<<blocks_for(std::max(M, N), 256), 256, 0, st>>>(RW, CW, M, N, ec1, ec2, fc1, fc2, sum,
                                                                             mw1, mw2);
-        fused_planes_kernel<<<blocks_for(M * K, 256), 256, 0, st>>>(av, M, K, 1, ec1, ec2, da1, da2, mw1 + 2, mw2 + 2);
-        fused_planes_kernel<<<blocks_for(K * N, 256), 256, 0, st>>>(bv, K, N, 0, fc1, fc2, db1, db2, mw1 + 3, mw2 + 3);
-        count_launch(7);
+        count_launch(5);
     }
+    prof_end(tk_scan, st);
     ScanSummary* hs = pinned_summary();
     long long* hw = (long long*)(hs + 1);
     cudaMemcpyAsync(hs, sum, sizeof(ScanSummary), cudaMemcpyDeviceToHost, st);
@@ -1743,6 +1845,12 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     if (!r1b || !r1f || !r2b || !r2f) return APB_ERR_CUDA;
     const bool rad_multi = hw1[0] > 900 || hw1[1] > 900 || hw2[0] > 900 || hw2[1] > 900;
     cudaStream_t rs = rad_multi ? st : side_stream();  // the multi-block radius path syncs its stream
+    const int tk_rad = prof_begin("radius", rs);
+    if (!rad_multi) {  // exact double planes of both radius products, off the critical path
+        fused_planes_kernel<<<blocks_for(M * K, 256), 256, 0, rs>>>(av, M, K, 1, ec1, ec2, da1, da2, nullptr, nullptr);
+        fused_planes_kernel<<<blocks_for(K * N, 256), 256, 0, rs>>>(bv, K, N, 0, fc1, fc2, db1, db2, nullptr, nullptr);
+        count_launch(2);
+    }
     static cudaEvent_t ev_join = [] {
         cudaEvent_t e;
         cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
@@ -1750,6 +1858,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     }();
     if ((rc = radius_compute(A, B, 0, 2, 0, hw1, r1b, r1f, rs, 1))) return rc;  // |A| plane transposed
     if ((rc = radius_compute(A, B, 1, 3, 1, hw2, r2b, r2f, rs))) return rc;
+    prof_end(tk_rad, rs);
     if (rs != st) cudaEventRecord(ev_join, rs);
     bool first = true;
     const bool single = P.steps.size() == 3 && P.steps[0] == 0 && P.steps[1] == A->cols;
@@ -1779,7 +1888,9 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         first = false;
     }
     if (rs != st) cudaStreamWaitEvent(st, ev_join, 0);
+    const int tk_comb = prof_begin("combine", st);
     rad_combine_kernel<<<blocks_for(M * N, 256), 256, 0, st>>>(out_of(&C->b), M * N, r1b, r1f, r2b, r2f);
+    prof_end(tk_comb, st);
     count_launch();
     return cuda_check(cudaGetLastError(), "block matmul");
 }

@@ -116,3 +116,17 @@ def test_reference_shaped_dot_ball():
     ref = po.dot_batch(x, y, 25, 1, 150, which="ref", initial=init, subtract=True,
                        idx=apb_dot_index(1, 24, 0, 0, -1, 0, 0, 0, 1))
     assert got.identical(ref).all()
+
+
+@pytest.mark.parametrize("hook", ["APB_DOT_KEEP", "APB_DOT_STAGE"])
+def test_dot_kernel_variants(hook):
+    """the register-resident (KEEP) and cp.async-staged (STAGE) dot kernels,
+    selected by their tuning hooks in a subprocess, on the golden and edge cases"""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, **{hook: "1"})
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-k",
+                        "test_dot_golden_gpu or test_edge_random or test_host_entry",
+                        os.path.abspath(__file__)], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:]
