@@ -336,11 +336,15 @@ int apb_matmul_host(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, 
     cudaStream_t st = host_stream();
     apb_mat dA = *A, dB = *B, dC = *C;
     int rc;
+    int tk = prof_begin("h2d", st);
     if ((rc = to_device(&A->b, &dA.b, 5, st, true))) return rc;
     if ((rc = to_device(&B->b, &dB.b, 10, st, true))) return rc;
     if ((rc = to_device(&C->b, &dC.b, 0, st, false))) return rc;
+    prof_end(tk, st);
     if ((rc = apb_matmul(&dA, &dB, prec, algo, &dC, st))) return rc;
+    tk = prof_begin("d2h", st);
     if ((rc = to_host(&dC.b, &C->b, st))) return rc;
+    prof_end(tk, st);
     return apb_device_status(st);
 }
 

@@ -25,6 +25,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "apb.h"
 #include "apb_internal.h"
@@ -347,6 +348,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int it_begin = P.cta_begin[blockIdx.x], it_end = P.cta_begin[blockIdx.x + 1];
+    if (P.dbg_ts && threadIdx.x == 0) P.dbg_ts[blockIdx.x * 32 + 31] = clock64();
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < A_STAGES; i++) {
@@ -390,15 +392,23 @@ __global__ void __launch_bounds__(THREADS, 1)
                         {
                             const uint32_t st = ai % A_STAGES, ph = (ai / A_STAGES) & 1;
                             mbar_wait(&emptyA[st], ph ^ 1);
-                            mbar_expect_tx(&fullA[st], Cfg::TILE_A);
-                            tma_load_2d(smA + st * Cfg::TILE_A, &tmA, kb * BK, s * P.Mp + m0, &fullA[st]);
+                            if ((P.debug & 1) && ai >= (uint32_t)A_STAGES) {
+                                mbar_arrive(&fullA[st]);
+                            } else {
+                                mbar_expect_tx(&fullA[st], Cfg::TILE_A);
+                                tma_load_2d(smA + st * Cfg::TILE_A, &tmA, kb * BK, s * P.Mp + m0, &fullA[st]);
+                            }
                             ai++;
                         }
                         for (int t = max(tmin, tmax_prev + 1); t <= tmax; t++) {
                             const uint32_t st = bi % B_STAGES, ph = (bi / B_STAGES) & 1;
                             mbar_wait(&emptyB[st], ph ^ 1);
-                            mbar_expect_tx(&fullB[st], Cfg::TILE_B);
-                            tma_load_2d(smB + st * Cfg::TILE_B, &tmB, kb * BK, t * P.Np + n0, &fullB[st]);
+                            if ((P.debug & 1) && bi >= (uint32_t)B_STAGES) {
+                                mbar_arrive(&fullB[st]);
+                            } else {
+                                mbar_expect_tx(&fullB[st], Cfg::TILE_B);
+                                tma_load_2d(smB + st * Cfg::TILE_B, &tmB, kb * BK, t * P.Np + n0, &fullB[st]);
+                            }
                             bi++;
                         }
                         tmax_prev = tmax;
@@ -413,8 +423,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int2 W = P.items[it];
             const int d0 = BAND_W * W.y;
             const int s_hi = min(P.S_A - 1, d0 + BAND_W - 1), s_lo = max(0, d0 - (P.S_B - 1));
+            if (P.dbg_ts && lane == 0 && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 0] = clock64();
             mbar_wait(tempty, tph ^ 1);
             fence_after();
+            if (P.dbg_ts && lane == 0 && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 1] = clock64();
             uint32_t init_mask = 0;
             for (int kb = 0; kb < P.n_kb; kb++) {
                 const int t_first = max(0, d0 - s_hi);
@@ -464,6 +476,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 bi = b_first + (uint32_t)(min(P.S_B - 1, d0 + BAND_W - 1 - s_lo) - t_first + 1);
             }
             if (lane == 0) mma_commit(tfull);
+            if (P.dbg_ts && lane == 0 && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 2] = clock64();
             __syncwarp();
             tph ^= 1;
         }
@@ -479,6 +492,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int row = m0 + 32 * q + lane;
             mbar_wait(tfull, tph);
             fence_after();
+            if (P.dbg_ts && warp == 2 && lane == 0 && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 3] = clock64();
 #pragma unroll 1
             for (int h = 0; h < BNT / 64; h++) {
                 int32_t carry[32];
@@ -508,16 +522,244 @@ __global__ void __launch_bounds__(THREADS, 1)
                         carry[c] = (int32_t)(val >> 8);
                     }
                 }
-                const size_t off = ((size_t)W.y * P.Mp + row) * P.Np + n0 + col0 + 32 * h;
-                uint32_t* wd = P.Tw + off;
-                int32_t* cd = P.Tc + off;
+                // quad layout plane[band][col/4][row][col%4]: the 32 lanes (rows) of a
+                // warp store 512 contiguous bytes per instruction
+                const size_t q0 = (size_t)W.y * (P.Np >> 2) + ((size_t)(n0 + col0 + 32 * h) >> 2);
+                if (!(P.debug & 2)) {
 #pragma unroll
-                for (int c = 0; c < 32; c += 4) {
-                    *(uint4*)(wd + c) = make_uint4(word[c], word[c + 1], word[c + 2], word[c + 3]);
-                    *(int4*)(cd + c) = make_int4(carry[c], carry[c + 1], carry[c + 2], carry[c + 3]);
+                    for (int c = 0; c < 32; c += 4) {
+                        const size_t off = (((q0 + (c >> 2)) * P.Mp + row) << 2);
+                        *(uint4*)(P.Tw + off) = make_uint4(word[c], word[c + 1], word[c + 2], word[c + 3]);
+                        *(int4*)(P.Tc + off) = make_int4(carry[c], carry[c + 1], carry[c + 2], carry[c + 3]);
+                    }
                 }
             }
             fence_before();
+            if (P.dbg_ts && warp == 2 && lane == 0 && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 4] = clock64();
+            mbar_arrive(tempty);
+            tph ^= 1;
+        }
+    }
+
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512)
+                     : "memory");
+    }
+}
+
+// ====================================================================
+// Band kernel v3: same work decomposition and output as band_gemm_kernel, with
+// a leaner MMA issue path (the v2 profile showed the single MMA thread, not the
+// tensor pipe, setting the pace: ~270 warp instructions and 3-4 mbarrier waits
+// per sweep step).
+//  * one "step" barrier pair per A-ring slot: the producer posts the A tile
+//    and every new B tile of step j on full[j % RA] (one expect_tx), the MMA
+//    thread commits step j to empty[j % RA]; a B slot is recycled once the
+//    last step that read its previous tile has completed (tracked by the
+//    producer, which waits on that step's empty barrier);
+//  * the MMA loop runs on one thread with smem descriptors advanced by adds;
+//  * the epilogue issues all of a column chunk's TMEM loads before one wait.
+template <int BNT, int BAND_W>
+__global__ void __launch_bounds__(THREADS, 1)
+    band3_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      BandGemmParams P) {
+    using Cfg = BandCfg<BNT, BAND_W>;
+    constexpr int RA = Cfg::A_STAGES, RB = Cfg::B_STAGES;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* smA = smem;
+    uint8_t* smB = smem + RA * Cfg::TILE_A;
+    uint64_t* bars = (uint64_t*)(smem + RA * Cfg::TILE_A + RB * Cfg::TILE_B);
+    uint64_t* full = bars;
+    uint64_t* empty = full + RA;
+    uint64_t* tfull = empty + RA;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int it_begin = P.cta_begin[blockIdx.x], it_end = P.cta_begin[blockIdx.x + 1];
+    if (P.dbg_ts && threadIdx.x == 0) P.dbg_ts[blockIdx.x * 32 + 31] = clock64();
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < RA; i++) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, EPI_WARPS * 32);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+            int lastuse[RB];
+#pragma unroll
+            for (int q = 0; q < RB; q++) lastuse[q] = -1;
+            int j = 0;        // step counter
+            uint32_t bi = 0;  // B ring sequence index
+            for (int it = it_begin; it < it_end; it++) {
+                const int2 W = P.items[it];
+                const int m0 = (W.x / P.n_tiles_n) * 128, n0 = (W.x % P.n_tiles_n) * BNT;
+                const int d0 = BAND_W * W.y;
+                const int s_hi = min(P.S_A - 1, d0 + BAND_W - 1), s_lo = max(0, d0 - (P.S_B - 1));
+                for (int kb = 0; kb < P.n_kb; kb++) {
+                    const int t_first = max(0, d0 - s_hi);
+                    const uint32_t b_first = bi;
+                    int tmax_prev = -1;
+                    for (int s = s_hi; s >= s_lo; s--, j++) {
+                        const int tmin = max(0, d0 - s), tmax = min(P.S_B - 1, d0 + BAND_W - 1 - s);
+                        const int slot = j % RA;
+                        if (j >= RA) mbar_wait(&empty[slot], ((j / RA) & 1) ^ 1);  // step j - RA done
+                        const int tnew = max(tmin, tmax_prev + 1);
+                        // recycled B slots: the step that last read the old tile must be done
+                        for (int t = tnew; t <= tmax; t++) {
+                            const int bs = (int)((b_first + (uint32_t)(t - t_first)) % RB);
+                            int L = -1;
+#pragma unroll
+                            for (int q = 0; q < RB; q++)
+                                if (q == bs) L = lastuse[q];
+                            if (L >= 0 && L > j - RA) mbar_wait(&empty[L % RA], (L / RA) & 1);
+                        }
+                        mbar_expect_tx(&full[slot], Cfg::TILE_A + (uint32_t)(tmax - tnew + 1) * Cfg::TILE_B);
+                        tma_load_2d(smA + slot * Cfg::TILE_A, &tmA, kb * BK, s * P.Mp + m0, &full[slot]);
+                        for (int t = tnew; t <= tmax; t++) {
+                            const int bs = (int)((b_first + (uint32_t)(t - t_first)) % RB);
+                            tma_load_2d(smB + bs * Cfg::TILE_B, &tmB, kb * BK, t * P.Np + n0, &full[slot]);
+                        }
+                        for (int t = tmin; t <= tmax; t++) {
+                            const int bs = (int)((b_first + (uint32_t)(t - t_first)) % RB);
+#pragma unroll
+                            for (int q = 0; q < RB; q++)
+                                if (q == bs) lastuse[q] = j;
+                        }
+                        tmax_prev = tmax;
+                    }
+                    bi = b_first + (uint32_t)(min(P.S_B - 1, d0 + BAND_W - 1 - s_lo) - t_first + 1);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint64_t a_desc0 = smem_desc(smem_u32(smA)), b_desc0 = smem_desc(smem_u32(smB));
+            int j = 0;
+            uint32_t bi = 0, tph = 0;
+            for (int it = it_begin; it < it_end; it++) {
+                const int2 W = P.items[it];
+                const int d0 = BAND_W * W.y;
+                const int s_hi = min(P.S_A - 1, d0 + BAND_W - 1), s_lo = max(0, d0 - (P.S_B - 1));
+                if (P.dbg_ts && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 0] = clock64();
+                mbar_wait(tempty, tph ^ 1);
+                fence_after();
+                if (P.dbg_ts && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 1] = clock64();
+                uint32_t init_mask = 0;
+                for (int kb = 0; kb < P.n_kb; kb++) {
+                    const int t_first = max(0, d0 - s_hi);
+                    const uint32_t b_first = bi;
+                    for (int s = s_hi; s >= s_lo; s--, j++) {
+                        const int tmin = max(0, d0 - s), tmax = min(P.S_B - 1, d0 + BAND_W - 1 - s);
+                        const int slot = j % RA;
+                        mbar_wait(&full[slot], (j / RA) & 1);
+                        fence_after();
+                        const uint64_t ad = a_desc0 + (uint64_t)((slot * Cfg::TILE_A) >> 4);
+                        for (int t = tmin; t <= tmax; t++) {
+                            const int w = s + t - d0;
+                            const int bs = (int)((b_first + (uint32_t)(t - t_first)) % RB);
+                            const uint64_t bd = b_desc0 + (uint64_t)((bs * Cfg::TILE_B) >> 4);
+                            const uint32_t td = tmem_base + (uint32_t)(w * BNT);
+                            const uint32_t acc0 = (init_mask >> w) & 1u;
+                            mma_i8(td, ad, bd, Cfg::IDESC, acc0);
+#pragma unroll
+                            for (int k = 1; k < BK / 32; k++) mma_i8(td, ad + 2 * k, bd + 2 * k, Cfg::IDESC, 1u);
+                            init_mask |= 1u << w;
+                        }
+                        mma_commit(&empty[slot]);
+                    }
+                    bi = b_first + (uint32_t)(min(P.S_B - 1, d0 + BAND_W - 1 - s_lo) - t_first + 1);
+                }
+                mma_commit(tfull);
+                if (P.dbg_ts && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 2] = clock64();
+                tph ^= 1;
+            }
+        }
+    } else {
+        const int e = warp - 2;
+        const int q = warp & 3;
+        const int col0 = (e >> 2) * (BNT / 2);
+        uint32_t tph = 0;
+        for (int it = it_begin; it < it_end; it++) {
+            const int2 W = P.items[it];
+            const int m0 = (W.x / P.n_tiles_n) * 128, n0 = (W.x % P.n_tiles_n) * BNT;
+            const int d0 = BAND_W * W.y;
+            const int row = m0 + 32 * q + lane;
+            mbar_wait(tfull, tph);
+            fence_after();
+            if (P.dbg_ts && warp == 2 && lane == 0 && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 3] = clock64();
+            constexpr int WB = BAND_W == 2 ? 2 : 1;  // TMEM loads in flight per wait
+#pragma unroll 1
+            for (int h = 0; h < BNT / 64; h++) {
+                int32_t carry[32];
+                uint32_t word[32];
+#pragma unroll
+                for (int c = 0; c < 32; c++) {
+                    carry[c] = 0;
+                    word[c] = 0;
+                }
+#pragma unroll
+                for (int w0 = 0; w0 < BAND_W; w0 += WB) {
+                    uint32_t v[WB][32];
+#pragma unroll
+                    for (int u = 0; u < WB; u++) {
+                        // diagonals past the last one contribute D = 0, so every band's
+                        // carry leaves at the band boundary (word aligned for the recombine)
+                        if (d0 + w0 + u < P.ND) {
+                            const uint32_t taddr =
+                                tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)((w0 + u) * BNT + col0 + 32 * h);
+                            TMEM_LD32(taddr, v[u]);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < 32; c++) v[u][c] = 0;
+                        }
+                    }
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int u = 0; u < WB; u++)
+#pragma unroll
+                        for (int c = 0; c < 32; c++) {
+                            const int64_t val = (int64_t)(int32_t)v[u][c] + carry[c];
+                            word[c] |= (uint32_t)(val & 255) << (8 * (w0 + u));
+                            carry[c] = (int32_t)(val >> 8);
+                        }
+                }
+                // quad layout plane[band][col/4][row][col%4]: the 32 lanes (rows) of a
+                // warp store 512 contiguous bytes per instruction
+                const size_t q0 = (size_t)W.y * (P.Np >> 2) + ((size_t)(n0 + col0 + 32 * h) >> 2);
+                if (!(P.debug & 2)) {
+#pragma unroll
+                    for (int c = 0; c < 32; c += 4) {
+                        const size_t off = (((q0 + (c >> 2)) * P.Mp + row) << 2);
+                        *(uint4*)(P.Tw + off) = make_uint4(word[c], word[c + 1], word[c + 2], word[c + 3]);
+                        *(int4*)(P.Tc + off) = make_int4(carry[c], carry[c + 1], carry[c + 2], carry[c + 3]);
+                    }
+                }
+            }
+            fence_before();
+            if (P.dbg_ts && warp == 2 && lane == 0 && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 4] = clock64();
             mbar_arrive(tempty);
             tph ^= 1;
         }
@@ -602,9 +844,12 @@ static int band_launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const Ban
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(band_gemm_kernel<BNT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        cudaFuncSetAttribute(band3_gemm_kernel<BNT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         attr = true;
     }
-    band_gemm_kernel<BNT, W><<<n_ctas, THREADS, Cfg::SMEM, st>>>(ma, mb, P);
+    static const bool v2 = std::getenv("APB_BAND_V2") != nullptr;  // previous issue loop (A/B timing)
+    if (v2) band_gemm_kernel<BNT, W><<<n_ctas, THREADS, Cfg::SMEM, st>>>(ma, mb, P);
+    else band3_gemm_kernel<BNT, W><<<n_ctas, THREADS, Cfg::SMEM, st>>>(ma, mb, P);
     return APB_OK;
 }
 

@@ -28,6 +28,8 @@ struct BandGemmParams {
     const int* cta_begin;     // [n_ctas + 1] item ranges per CTA
     uint32_t* Tw;             // [n_bands][Mp][Np] result bytes of diagonals 4b..4b+3
     int32_t* Tc;              // [n_bands][Mp][Np] carry out of band b
+    int debug = 0;            // timing experiments only: 1 skip TMA refills, 2 skip epilogue stores
+    long long* dbg_ts = nullptr;  // optional per-CTA clock64 trace (timing experiments)
 };
 
 int band_gemm_launch(const int8_t* Apack, const int8_t* Bpack, const BandGemmParams& P, int n_ctas,

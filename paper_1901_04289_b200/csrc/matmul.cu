@@ -21,6 +21,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
+#include <functional>
 #include <map>
 #include <vector>
 
@@ -336,6 +338,127 @@ __global__ void __launch_bounds__(256) pack_kernel(BallsView X, int64_t rows, in
 }
 
 
+// ---- pack v2.  Balanced digits by one multi-word addition: with X the S-byte
+// two's complement of the scaled entry, Y = X + 0x8080...80 makes the carry out
+// of every byte exactly the balanced-recoding carry (byte + c >= 128), and
+// Y ^ 0x8080...80 are the digit bytes -- the same bytes as the byte-serial
+// recoding of ds_digits8, in a handful of 64-bit ops per 8 digits.
+// Up to NCW 64-bit digit words (S <= 8 NCW); magnitude bits come straight
+// from the entry's limbs (loaded once, up front).
+template <int NCW>
+APB_DEV void digit_words(const BallsView& X, int64_t e, bool valid, int64_t scale, uint64_t (&d)[NCW]) {
+    const uint8_t kd = valid ? X.kind[e] : (uint8_t)APB_ZERO;
+    const bool live = (kd & APB_KIND_MASK) == APB_FINITE;
+    const bool neg = live && (kd & APB_SIGN);
+    const int L = X.L;
+    const int64_t sh = live ? X.exp[e] - 64 * (int64_t)L + scale : 0;
+    // word c = magnitude bits [64c, 64c + 64) = limbs li = c + lq (shifted right by bo)
+    const int64_t lq = (-sh) >> 6;  // floor
+    const int bo = (int)((-sh) & 63);
+    const uint64_t* m = X.mant + e * (int64_t)L;
+    uint64_t g[NCW + 1];
+#pragma unroll
+    for (int c = 0; c <= NCW; c++) {
+        const int64_t li = c + lq;
+        g[c] = (live && li >= 0 && li < L) ? __ldg(m + li) : 0ull;
+    }
+    uint64_t cy = neg ? 1ull : 0ull;
+    constexpr uint64_t K80 = 0x8080808080808080ull;
+#pragma unroll
+    for (int c = 0; c < NCW; c++) {
+        uint64_t w = bo ? (g[c] >> bo) | (g[c + 1] << (64 - bo)) : g[c];
+        if (neg) w = ~w;
+        const uint64_t s1 = w + K80;
+        const uint64_t c1 = s1 < w ? 1ull : 0ull;
+        const uint64_t s2 = s1 + cy;
+        cy = c1 | (s2 < s1 ? 1ull : 0ull);
+        d[c] = s2 ^ K80;
+    }
+}
+
+// A side: thread per entry (row r, inner kk), plane[s][r][kk] byte stores --
+// a warp writes one 32-byte segment per plane
+template <int NCW>
+__global__ void __launch_bounds__(256) pack_a_v2_kernel(BallsView X, int64_t rows, int64_t ld, int64_t lo, int64_t hi,
+                                                        const int64_t* top, const int64_t* bot, int S, int Rp, int Kp,
+                                                        int8_t* out, int64_t* scale_out) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)Rp * Kp) return;
+    const int64_t r = t / Kp, kk = t % Kp;
+    int64_t sc = 0;
+    if (r < rows) sc = top[r] == INT64_MIN ? 0 : -bot[r];
+    if (r < rows && kk == 0) scale_out[r] = sc;
+    const bool valid = r < rows && kk < hi - lo;
+    uint64_t d[NCW];
+    digit_words<NCW>(X, valid ? r * ld + lo + kk : 0, valid, sc, d);
+    const size_t plane = (size_t)Rp * Kp;
+    int8_t* dst = out + (size_t)r * Kp + kk;
+#pragma unroll
+    for (int q = 0; q < 8 * NCW; q++) {
+        if (q < S) dst[(size_t)q * plane] = (int8_t)(uint8_t)(d[q >> 3] >> (8 * (q & 7)));
+    }
+}
+
+// B side: 32 columns x 32 inner indices per 256 threads (4 consecutive kk per
+// thread, reads coalesced over columns j); digit bytes of 4 entries are merged
+// with byte permutes and transposed through shared memory so plane rows (fixed
+// j, contiguous kk) leave as 32-byte segments.
+template <int NCW>
+__global__ void __launch_bounds__(256) pack_b_v2_kernel(BallsView X, int64_t N, int64_t lo, int64_t hi,
+                                                        const int64_t* top, const int64_t* bot, int S, int Np, int Kp,
+                                                        int8_t* out, int64_t* scale_out) {
+    __shared__ uint32_t tile[8][32][9];  // [digit in chunk][j][kk word], padded
+    const int jl = threadIdx.x & 31, kq = threadIdx.x >> 5;
+    const int64_t j = (int64_t)blockIdx.x * 32 + jl;
+    const int64_t kk0 = (int64_t)blockIdx.y * 32 + 4 * kq;
+    int64_t sc = 0;
+    if (j < N) sc = top[j] == INT64_MIN ? 0 : -bot[j];
+    if (j < N && blockIdx.y == 0 && kq == 0) scale_out[j] = sc;
+    uint64_t d[4][NCW];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int64_t kk = kk0 + q;
+        const bool valid = j < N && kk < hi - lo;
+        digit_words<NCW>(X, valid ? (lo + kk) * N + j : 0, valid, sc, d[q]);
+    }
+    const size_t plane = (size_t)Np * Kp;
+#pragma unroll
+    for (int c = 0; c < NCW; c++) {
+        if (8 * c >= S) break;
+        const uint64_t w0 = d[0][c], w1 = d[1][c], w2 = d[2][c], w3 = d[3][c];
+        // byte b of (w0, w1, w2, w3) -> the word of digit 8c + b
+        const uint32_t lo01 = __byte_perm((uint32_t)w0, (uint32_t)w1, 0x5140);  // w0.b0 w1.b0 w0.b1 w1.b1
+        const uint32_t lo23 = __byte_perm((uint32_t)w2, (uint32_t)w3, 0x5140);
+        const uint32_t hi01 = __byte_perm((uint32_t)w0, (uint32_t)w1, 0x7362);  // w0.b2 w1.b2 w0.b3 w1.b3
+        const uint32_t hi23 = __byte_perm((uint32_t)w2, (uint32_t)w3, 0x7362);
+        const uint32_t lo01b = __byte_perm((uint32_t)(w0 >> 32), (uint32_t)(w1 >> 32), 0x5140);
+        const uint32_t lo23b = __byte_perm((uint32_t)(w2 >> 32), (uint32_t)(w3 >> 32), 0x5140);
+        const uint32_t hi01b = __byte_perm((uint32_t)(w0 >> 32), (uint32_t)(w1 >> 32), 0x7362);
+        const uint32_t hi23b = __byte_perm((uint32_t)(w2 >> 32), (uint32_t)(w3 >> 32), 0x7362);
+        tile[0][jl][kq] = __byte_perm(lo01, lo23, 0x5410);
+        tile[1][jl][kq] = __byte_perm(lo01, lo23, 0x7632);
+        tile[2][jl][kq] = __byte_perm(hi01, hi23, 0x5410);
+        tile[3][jl][kq] = __byte_perm(hi01, hi23, 0x7632);
+        tile[4][jl][kq] = __byte_perm(lo01b, lo23b, 0x5410);
+        tile[5][jl][kq] = __byte_perm(lo01b, lo23b, 0x7632);
+        tile[6][jl][kq] = __byte_perm(hi01b, hi23b, 0x5410);
+        tile[7][jl][kq] = __byte_perm(hi01b, hi23b, 0x7632);
+        __syncthreads();
+        // 8 digits x 32 rows x 8 words: thread -> (digit b, row r, word m)
+#pragma unroll
+        for (int it = 0; it < 8; it++) {
+            const int idx = it * 256 + threadIdx.x;
+            const int m = idx & 7, r = (idx >> 3) & 31, b = idx >> 8;
+            const int sdig = 8 * c + b;
+            const int64_t jj = (int64_t)blockIdx.x * 32 + r;
+            if (sdig < S && jj < Np)
+                *(uint32_t*)(out + (size_t)sdig * plane + (size_t)jj * Kp + (size_t)blockIdx.y * 32 + 4 * m) =
+                    tile[b][r][m];
+        }
+        __syncthreads();
+    }
+}
+
 // B-side pack with coalesced reads: a 32 (columns j) x 32 (inner kk) tile per
 // 256 threads; lanes run over consecutive j (contiguous in row-major B), the
 // digits are transposed through shared memory so each plane row (fixed j,
@@ -398,7 +521,12 @@ struct RecombineArgs {
     int64_t* int_out;  // optional: exact integer limbs (two's complement), int_limbs per entry
     int int_limbs;
     int* status;
+    int quad;  // band GEMM layout: plane[(j/4)][i][j%4] (coalesced epilogue stores), else [i][j]
 };
+
+APB_DEV size_t rc_off(const RecombineArgs& R, int64_t i, int64_t j) {
+    return R.quad ? (((size_t)(j >> 2) * R.Mp + (size_t)i) << 2) + (size_t)(j & 3) : (size_t)i * R.Np + (size_t)j;
+}
 
 template <int CAP>
 __global__ void __launch_bounds__(128) recombine_kernel(RecombineArgs R) {
@@ -406,7 +534,7 @@ __global__ void __launch_bounds__(128) recombine_kernel(RecombineArgs R) {
     if (t >= R.M * R.N) return;
     const int64_t i = t / R.N, j = t % R.N;
     const size_t plane = (size_t)R.Mp * R.Np;
-    const size_t off = (size_t)i * R.Np + j;
+    const size_t off = rc_off(R, i, j);
     // T = (bytes as unsigned) + sum_g carry_g * 256^(d1_g), two's complement in NT limbs
     const int NT = (R.nwords + 1) / 2 + 2;
     uint64_t T[CAP];
@@ -494,11 +622,14 @@ __global__ void __launch_bounds__(128) recombine_fast_kernel(RecombineArgs R) {
     constexpr int ND32 = NBC + 2;               // digits
     constexpr int PER = 64 / DB;                // digits per 64-bit limb
     constexpr int NL = (ND32 + PER - 1) / PER;  // 64-bit limbs
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= R.M * R.N) return;
-    const int64_t i = t / R.N, j = t % R.N;
+    // threads walk the quad layout: t -> (j/4, i, j%4), so plane reads are contiguous
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t jr = u & 3, i = (u >> 2) % R.M, jq = (u >> 2) / R.M;
+    const int64_t j = 4 * jq + jr;
+    if (jq * 4 >= R.N || j >= R.N) return;
+    const int64_t t = i * R.N + j;
     const size_t plane = (size_t)R.Mp * R.Np;
-    const size_t off = (size_t)i * R.Np + j;
+    const size_t off = rc_off(R, i, j);
     const int NB = R.nwords;
     // one streaming pass over the digits, base 2^DB: digit k = word_k + carry_{k-1}
     // + the running carry; batches of RB bands are loaded before they are
@@ -846,6 +977,228 @@ __global__ void fused_finish_kernel(LineWins R, LineWins C, int64_t M, int64_t N
     }
 }
 
+// ---- one-pass plan scan, v2: thread per entry, every field loaded up front,
+// block reductions into per-(line, chunk) partials (no atomics, no init pass);
+// scan_finish_kernel reduces the partials per line.  Same results as
+// fused_rows/cols + fused_finish above (kept for the multi-block path).
+struct ScanAcc {
+    int64_t t[3], b[3], prec, cnt, special;  // cnt = c1 | c2 << 32
+};
+constexpr int SCAN_FIELDS = 9;
+
+APB_DEV void sacc_init(ScanAcc& a) {
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        a.t[q] = INT64_MIN;
+        a.b[q] = INT64_MAX;
+    }
+    a.prec = 0;
+    a.cnt = 0;
+    a.special = 0;
+}
+
+APB_DEV void sacc_merge(ScanAcc& a, const ScanAcc& o) {
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        a.t[q] = o.t[q] > a.t[q] ? o.t[q] : a.t[q];
+        a.b[q] = o.b[q] < a.b[q] ? o.b[q] : a.b[q];
+    }
+    a.prec = o.prec > a.prec ? o.prec : a.prec;
+    a.cnt += o.cnt;
+    a.special |= o.special;
+}
+
+APB_DEV void sacc_shfl(ScanAcc& a, int o) {
+    ScanAcc x;
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        x.t[q] = __shfl_xor_sync(0xffffffffu, a.t[q], o);
+        x.b[q] = __shfl_xor_sync(0xffffffffu, a.b[q], o);
+    }
+    x.prec = __shfl_xor_sync(0xffffffffu, a.prec, o);
+    x.cnt = __shfl_xor_sync(0xffffffffu, a.cnt, o);
+    x.special = __shfl_xor_sync(0xffffffffu, a.special, o);
+    sacc_merge(a, x);
+}
+
+APB_DEV int64_t sacc_get(const ScanAcc& a, int f) {
+    switch (f) {
+        case 0: return a.t[0];
+        case 1: return a.b[0];
+        case 2: return a.t[1];
+        case 3: return a.b[1];
+        case 4: return a.t[2];
+        case 5: return a.b[2];
+        case 6: return a.prec;
+        case 7: return a.cnt;
+        default: return a.special;
+    }
+}
+
+APB_DEV void sacc_set(ScanAcc& a, int f, int64_t v) {
+    switch (f) {
+        case 0: a.t[0] = v; break;
+        case 1: a.b[0] = v; break;
+        case 2: a.t[1] = v; break;
+        case 3: a.b[1] = v; break;
+        case 4: a.t[2] = v; break;
+        case 5: a.b[2] = v; break;
+        case 6: a.prec = v; break;
+        case 7: a.cnt = v; break;
+        default: a.special = v;
+    }
+}
+
+// one entry: midpoint window + entry precision, the two radius-operand Mag
+// windows of this side with nonzero counts, specials.  A side: |A|, R_A;
+// B side: R_B, |B| + R_B (the operands of src/matmul.cpp:498-509)
+APB_DEV void scan_entry(const BallsView& X, int64_t e, bool a_side, ScanAcc& acc) {
+    const uint8_t kd = X.kind[e];
+    const int64_t ex = X.exp[e];
+    const uint32_t rb = X.rad_man[e];
+    const int64_t rexp = X.rad_exp[e];
+    const uint64_t* m = X.mant + e * (int64_t)X.L;
+    const uint64_t mtop = m[X.L - 1];
+    const uint64_t m0 = m[0];
+    const int k = kd & APB_KIND_MASK;
+    acc.special |= ((k != APB_ZERO && k != APB_FINITE) || rb == APB_RAD_INF) ? 1 : 0;
+    Mag mu = mag_zero();
+    if (k == APB_FINITE) {
+        int64_t bw;
+        if (m0 != 0 || X.L == 1) {
+            bw = 64 * (int64_t)X.L - (int64_t)ctz64(m0);
+        } else {
+            bw = slot_bitwidth(m, X.L);
+        }
+        const int64_t t = ex, b = ex - bw;
+        win_merge(acc.t[0], acc.b[0], t, b);
+        acc.prec = bw > acc.prec ? bw : acc.prec;
+        mu = mag_parts((mtop >> 34) + 1, ex);
+    }
+    const Mag r = (rb != 0 && rb != APB_RAD_INF) ? mag_parts(rb, rexp) : mag_zero();
+    const Mag o1 = a_side ? mu : r;
+    const Mag o2 = a_side ? r : mag_add(mu, r);
+    if (o1.kind == 1) {
+        win_merge(acc.t[1], acc.b[1], o1.f, o1.f - 30);
+        acc.cnt += 1;
+    }
+    if (o2.kind == 1) {
+        win_merge(acc.t[2], acc.b[2], o2.f, o2.f - 30);
+        acc.cnt += 1ll << 32;
+    }
+}
+
+constexpr int SCAN_A_COLS = 256;  // entries of a row per A block (one per thread)
+constexpr int SCAN_B_ROWS = 32;   // rows per B block: 32 columns x 8 warps x 4 rows
+
+// blocks [0, nbA): A rows; [nbA, nbA + nbB): B column tiles.  Partials land in
+// pa[f][c][i] (A, cA chunks per row) and pb[f][c][j] (B, cB chunks per column).
+__global__ void __launch_bounds__(256) scan_v2_kernel(BallsView A, BallsView B, int64_t M, int64_t K, int64_t N,
+                                                      int cA, int cB, int64_t* pa, int64_t* pb, ScanSummary* sum,
+                                                      long long* mw1, long long* mw2) {
+    __shared__ int64_t red[8][32][SCAN_FIELDS + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // the finish kernel accumulates into these
+        *sum = ScanSummary{};
+        for (int q = 0; q < 4; q++) mw1[q] = mw2[q] = 0;
+    }
+    const int64_t nbA = M * cA;
+    ScanAcc acc;
+    sacc_init(acc);
+    if ((int64_t)blockIdx.x < nbA) {
+        const int64_t i = blockIdx.x / cA;
+        const int c = (int)(blockIdx.x % cA);
+        const int64_t k = (int64_t)c * SCAN_A_COLS + threadIdx.x;
+        if (k < K) scan_entry(A, i * K + k, true, acc);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sacc_shfl(acc, o);
+        if (lane == 0)
+            for (int f = 0; f < SCAN_FIELDS; f++) red[warp][0][f] = sacc_get(acc, f);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < 8; w++) {
+                ScanAcc o;
+                for (int f = 0; f < SCAN_FIELDS; f++) sacc_set(o, f, red[w][0][f]);
+                sacc_merge(acc, o);
+            }
+            const int64_t stride = (int64_t)cA * M;
+            for (int f = 0; f < SCAN_FIELDS; f++) pa[f * stride + (int64_t)c * M + i] = sacc_get(acc, f);
+        }
+    } else {
+        const int64_t bb = (int64_t)blockIdx.x - nbA;
+        const int64_t nct = (N + 31) / 32;
+        const int64_t jt = bb % nct;
+        const int c = (int)(bb / nct);
+        const int64_t j = jt * 32 + lane;
+        if (j < N) {
+#pragma unroll
+            for (int u = 0; u < SCAN_B_ROWS / 8; u++) {
+                const int64_t k = (int64_t)c * SCAN_B_ROWS + warp + 8 * u;
+                if (k < K) scan_entry(B, k * N + j, false, acc);
+            }
+        }
+        for (int f = 0; f < SCAN_FIELDS; f++) red[warp][lane][f] = sacc_get(acc, f);
+        __syncthreads();
+        if (warp == 0 && j < N) {
+            for (int w = 1; w < 8; w++) {
+                ScanAcc o;
+                for (int f = 0; f < SCAN_FIELDS; f++) sacc_set(o, f, red[w][lane][f]);
+                sacc_merge(acc, o);
+            }
+            const int64_t stride = (int64_t)cB * N;
+            for (int f = 0; f < SCAN_FIELDS; f++) pb[f * stride + (int64_t)c * N + j] = sacc_get(acc, f);
+        }
+    }
+}
+
+// per line: reduce the chunk partials; rows -> rtop/rbot, centring exponents of
+// the two radius operands, maxw_a / special_a / prec_a, radius window widths
+// (mw1[0], mw2[0]) and nonzero counts (mw1[2], mw2[2]); columns likewise with
+// index 1 / 3.  Threads [0, Mpad) take rows, the rest columns (warp-uniform side).
+__global__ void scan_v2_finish_kernel(const int64_t* pa, const int64_t* pb, int64_t M, int64_t N, int cA, int cB,
+                                      int64_t* rtop, int64_t* rbot, int64_t* ctop, int64_t* cbot,
+                                      int64_t* ecen1, int64_t* ecen2, int64_t* fcen1, int64_t* fcen2,
+                                      ScanSummary* sum, long long* mw1, long long* mw2) {
+    // warp per line (rows of A first, then columns of B), lanes over the chunk partials
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wid >= M + N) return;
+    const bool a_side = wid < M;
+    const int64_t line = a_side ? wid : wid - M;
+    const int64_t n = a_side ? M : N;
+    const int nc = a_side ? cA : cB;
+    const int64_t* P = a_side ? pa : pb;
+    const int64_t stride = (int64_t)nc * n;
+    ScanAcc acc;
+    sacc_init(acc);
+    for (int c = lane; c < nc; c += 32) {
+        ScanAcc o;
+#pragma unroll
+        for (int f = 0; f < SCAN_FIELDS; f++) sacc_set(o, f, P[f * stride + (int64_t)c * n + line]);
+        sacc_merge(acc, o);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sacc_shfl(acc, o);
+    if (lane != 0) return;
+    (a_side ? rtop : ctop)[line] = acc.t[0];
+    (a_side ? rbot : cbot)[line] = acc.b[0];
+    (a_side ? ecen1 : fcen1)[line] = acc.t[1] == INT64_MIN ? 0 : -((acc.t[1] + acc.b[1]) / 2);
+    (a_side ? ecen2 : fcen2)[line] = acc.t[2] == INT64_MIN ? 0 : -((acc.t[2] + acc.b[2]) / 2);
+    const long long w0 = acc.t[0] == INT64_MIN ? 0 : acc.t[0] - acc.b[0];
+    const long long w1 = acc.t[1] == INT64_MIN ? 0 : acc.t[1] - acc.b[1];
+    const long long w2 = acc.t[2] == INT64_MIN ? 0 : acc.t[2] - acc.b[2];
+    const unsigned long long n1 = (unsigned long long)(acc.cnt & 0xffffffffll);
+    const unsigned long long n2 = (unsigned long long)(acc.cnt >> 32);
+    const int s = a_side ? 0 : 1;
+    if (acc.special) atomicOr(a_side ? &sum->special_a : &sum->special_b, 1);
+    if (acc.prec) atomicMax(a_side ? &sum->prec_a : &sum->prec_b, (long long)acc.prec);
+    if (w0) atomicMax(a_side ? &sum->maxw_a : &sum->maxw_b, w0);
+    if (w1) atomicMax(&mw1[s], w1);
+    if (w2) atomicMax(&mw2[s], w2);
+    if (n1) atomicAdd((unsigned long long*)&mw1[2 + s], n1);
+    if (n2) atomicAdd((unsigned long long*)&mw2[2 + s], n2);
+}
+
 // exact double planes of both radius products + nonzero counts, one pass per side
 // A side: p1 = |A| (ecen1), p2 = R_A (ecen2);  B side: p1 = R_B (fcen1), p2 = |B|+R_B (fcen2)
 __global__ void fused_planes_kernel(BallsView X, int64_t rows, int64_t cols, int a_side, const int64_t* cen1,
@@ -1132,6 +1485,129 @@ __global__ void __launch_bounds__(256) rad_sprow_kernel(const double* __restrict
     mag_store(ent, &rb[i * N + j], &rf[i * N + j]);
 }
 
+// ---- fused list + product, v2: one CTA per column j (spcol) / row i (sprow)
+// compacts that line's nonzeros of a 1024-term chunk into shared memory in
+// l order (block ballot prefix), then every thread runs its own RN sum over
+// the list with the operand loads issued 8 at a time.  Same term order and
+// chunk folds as rad_spcol/rad_sprow (bit-identical results).
+constexpr int RCH = 1024;
+
+// ordered compaction of v[u] (term l = c0 + 256 u + tid) into (sl, sv); returns count
+APB_DEV int block_compact(const double (&v)[4], int64_t c0, int* sl, double* sv, int* cnt) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned bal[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+        bal[u] = __ballot_sync(0xffffffffu, v[u] != 0.0);
+        if (lane == 0) cnt[u * 8 + warp] = __popc(bal[u]);
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the 32 (u, warp) counts in l order
+        const int c = cnt[lane];
+        int x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        cnt[32 + lane] = x - c;
+        if (lane == 31) cnt[64] = x;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+        if (v[u] != 0.0) {
+            const int pos = cnt[32 + u * 8 + warp] + __popc(bal[u] & ((1u << lane) - 1u));
+            sl[pos] = (int)(c0 + 256 * u + tid);
+            sv[pos] = v[u];
+        }
+    }
+    __syncthreads();
+    return cnt[64];
+}
+
+// |A| R_B with R_B sparse: CTA per column j of db (w x N); |A| plane transposed daT[l][i]
+__global__ void __launch_bounds__(256) rad_spcol_v2_kernel(const double* __restrict__ daT, const double* __restrict__ db,
+                                                           int64_t M, int64_t N, int64_t w, const int64_t* ecen,
+                                                           const int64_t* fcen, uint32_t* rb, int64_t* rf) {
+    __shared__ int sl[RCH];
+    __shared__ double sv[RCH];
+    __shared__ int cnt[65];
+    const int64_t j = blockIdx.x;
+    const int64_t nch = (w + RCH - 1) / RCH;
+    const int64_t fj = fcen[j];
+    int n = 0;
+    for (int64_t pass = 0; pass * 256 < M; pass++) {
+        const int64_t i = pass * 256 + threadIdx.x;
+        const int64_t ii = i < M ? i : 0;
+        double s = 0.0;
+        Mag ent = mag_zero();
+        for (int64_t c0 = 0; c0 < w; c0 += RCH) {
+            if (nch > 1 || pass == 0) {
+                if (nch > 1) __syncthreads();  // previous chunk's list fully consumed
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int64_t l = c0 + 256 * u + threadIdx.x;
+                    v[u] = l < w ? db[l * N + j] : 0.0;
+                }
+                n = block_compact(v, c0, sl, sv, cnt);
+            }
+            for (int p0 = 0; p0 < n; p0 += 8) {
+                double a[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) a[u] = p0 + u < n ? daT[(int64_t)sl[p0 + u] * M + ii] : 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; u++)
+                    if (p0 + u < n) s = __dadd_rn(s, __dmul_rn(a[u], sv[p0 + u]));
+            }
+            rad_fold(ent, s, ecen[ii], fj);
+        }
+        if (i < M) mag_store(ent, &rb[i * N + j], &rf[i * N + j]);
+    }
+}
+
+// R_A (|B| + R_B) with R_A sparse: CTA per row i of da (M x w, row-major)
+__global__ void __launch_bounds__(256) rad_sprow_v2_kernel(const double* __restrict__ da, const double* __restrict__ db,
+                                                           int64_t M, int64_t N, int64_t w, const int64_t* ecen,
+                                                           const int64_t* fcen, uint32_t* rb, int64_t* rf) {
+    __shared__ int sl[RCH];
+    __shared__ double sv[RCH];
+    __shared__ int cnt[65];
+    const int64_t i = blockIdx.x;
+    const int64_t nch = (w + RCH - 1) / RCH;
+    const int64_t ei = ecen[i];
+    int n = 0;
+    for (int64_t pass = 0; pass * 256 < N; pass++) {
+        const int64_t j = pass * 256 + threadIdx.x;
+        const int64_t jj = j < N ? j : 0;
+        double s = 0.0;
+        Mag ent = mag_zero();
+        for (int64_t c0 = 0; c0 < w; c0 += RCH) {
+            if (nch > 1 || pass == 0) {
+                if (nch > 1) __syncthreads();
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int64_t l = c0 + 256 * u + threadIdx.x;
+                    v[u] = l < w ? da[i * w + l] : 0.0;
+                }
+                n = block_compact(v, c0, sl, sv, cnt);
+            }
+            for (int p0 = 0; p0 < n; p0 += 8) {
+                double b[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) b[u] = p0 + u < n ? db[(int64_t)sl[p0 + u] * N + jj] : 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; u++)
+                    if (p0 + u < n) s = __dadd_rn(s, __dmul_rn(sv[p0 + u], b[u]));
+            }
+            rad_fold(ent, s, ei, fcen[jj]);
+        }
+        if (j < N) mag_store(ent, &rb[i * N + j], &rf[i * N + j]);
+    }
+}
+
 __global__ void count_nonzero_kernel(const double* p, int64_t n, unsigned long long* cnt) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool nz = t < n && p[t] != 0.0;
@@ -1216,7 +1692,7 @@ Scratch& scratch() {
 }
 enum {
     S_RTOP, S_RBOT, S_CTOP, S_CBOT, S_SUM, S_APACK, S_BPACK, S_TW, S_TC, S_UNITS, S_ESC, S_FSC,
-    S_WA, S_WB, S_GREEDY, S_DA, S_DB, S_CEN_E, S_CEN_F, S_R1B, S_R1F, S_R2B, S_R2F, S_MISC, S_CTOP2, S_CBOT2, S_LCNT, S_LIDX, S_LVAL, S_DA2, S_DB2, S_CEN_E2, S_CEN_F2, S_RW1, S_RW2, S_LCNT2, S_LIDX2, S_LVAL2, S_RW1T, S_RW1B, S_RW2T, S_RW2B, S_CW1T, S_CW1B, S_CW2T, S_CW2B
+    S_WA, S_WB, S_GREEDY, S_DA, S_DB, S_CEN_E, S_CEN_F, S_R1B, S_R1F, S_R2B, S_R2F, S_MISC, S_CTOP2, S_CBOT2, S_LCNT, S_LIDX, S_LVAL, S_DA2, S_DB2, S_CEN_E2, S_CEN_F2, S_RW1, S_RW2, S_LCNT2, S_LIDX2, S_LVAL2, S_RW1T, S_RW1B, S_RW2T, S_RW2B, S_CW1T, S_CW1B, S_CW2T, S_CW2B, S_PARTA, S_PARTB
 };
 template <class T>
 T* sbuf(int k, size_t count, cudaStream_t st) {
@@ -1224,6 +1700,31 @@ T* sbuf(int k, size_t count, cudaStream_t st) {
 }
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// host-side trace of the launch sequence (APB_HOST_TRACE=1 prints per call)
+struct HostTrace {
+    bool on = std::getenv("APB_HOST_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t0;
+    char buf[1024];
+    int n = 0;
+    void start() {
+        if (!on) return;
+        t0 = std::chrono::steady_clock::now();
+        n = 0;
+    }
+    void mark(const char* what) {
+        if (!on || n > 900) return;
+        const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+        n += std::snprintf(buf + n, sizeof buf - n, " %s=%.1f", what, us);
+    }
+    void flush() {
+        if (on) std::fprintf(stderr, "host trace (us):%s\n", buf);
+    }
+};
+HostTrace& htrace() {
+    static HostTrace h;
+    return h;
+}
 
 void scan_cols(const BallsView& b, int64_t K, int64_t N, int64_t lo, int64_t hi, int64_t* ctop,
                int64_t* cbot, ScanSummary* sum, cudaStream_t st) {
@@ -1411,7 +1912,7 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
                  bool first, int64_t maxw_a, int64_t maxw_b, const int64_t* rtop_in,
                  const int64_t* rbot_in, const int64_t* ctop_in, const int64_t* cbot_in,
                  int64_t* int_out, int int_limbs, int64_t* esc_out, int64_t* fsc_out,
-                 cudaStream_t st) {
+                 cudaStream_t st, const std::function<int()>* after_gemm = nullptr) {
     const int64_t M = A->rows, K = A->cols, N = B->cols, w = hi - lo;
     BallsView a = view_of(&A->b), b = view_of(&B->b);
     const int64_t* rtop = rtop_in;
@@ -1462,13 +1963,25 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         return APB_ERR_CUDA;
     }
     int tok = prof_begin("pack", st);
-    pack_kernel<false><<<blocks_for((int64_t)Mp * Kp / 4, 256), 256, 0, st>>>(a, M, K, lo, hi, rtop, rbot, SA, Mp, Kp, Ap, esc);
     {
+        // byte-parallel recoding for up to 64 digits, byte-serial streams beyond
+        static const bool v1 = std::getenv("APB_PACK_V1") != nullptr;  // test hook
+        const unsigned ga = blocks_for((int64_t)Mp * Kp, 256);
+        const int ca = v1 ? 0 : (SA + 7) / 8;
+        if (ca >= 1 && ca <= 2) pack_a_v2_kernel<2><<<ga, 256, 0, st>>>(a, M, K, lo, hi, rtop, rbot, SA, Mp, Kp, Ap, esc);
+        else if (ca >= 3 && ca <= 5) pack_a_v2_kernel<5><<<ga, 256, 0, st>>>(a, M, K, lo, hi, rtop, rbot, SA, Mp, Kp, Ap, esc);
+        else if (ca >= 6 && ca <= 8) pack_a_v2_kernel<8><<<ga, 256, 0, st>>>(a, M, K, lo, hi, rtop, rbot, SA, Mp, Kp, Ap, esc);
+        else pack_kernel<false><<<blocks_for((int64_t)Mp * Kp / 4, 256), 256, 0, st>>>(a, M, K, lo, hi, rtop, rbot, SA, Mp, Kp, Ap, esc);
         dim3 gb((unsigned)(Np / 32), (unsigned)(Kp / 32));
-        pack_b_tiled_kernel<<<gb, 256, 0, st>>>(b, N, lo, hi, ctop, cbot, SB, Np, Kp, Bp, fsc);
+        const int cb = v1 ? 0 : (SB + 7) / 8;
+        if (cb >= 1 && cb <= 2) pack_b_v2_kernel<2><<<gb, 256, 0, st>>>(b, N, lo, hi, ctop, cbot, SB, Np, Kp, Bp, fsc);
+        else if (cb >= 3 && cb <= 5) pack_b_v2_kernel<5><<<gb, 256, 0, st>>>(b, N, lo, hi, ctop, cbot, SB, Np, Kp, Bp, fsc);
+        else if (cb >= 6 && cb <= 8) pack_b_v2_kernel<8><<<gb, 256, 0, st>>>(b, N, lo, hi, ctop, cbot, SB, Np, Kp, Bp, fsc);
+        else pack_b_tiled_kernel<<<gb, 256, 0, st>>>(b, N, lo, hi, ctop, cbot, SB, Np, Kp, Bp, fsc);
     }
     prof_end(tok, st);
     count_launch(2);
+    htrace().mark("pack_launched");
     const int tiles = (Mp / kSliceTile) * (Np / bn);
     const int ND = SA + SB - 1;
     // band kernel when every diagonal fits an int32 accumulator: pairs * w * 2^14 < 2^31
@@ -1577,7 +2090,29 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         P.cta_begin = (const int*)(dunits + off_begin);
         P.Tw = Tw;
         P.Tc = Tc;
+        static const int dbg = std::getenv("APB_GEMM_DEBUG") ? std::atoi(std::getenv("APB_GEMM_DEBUG")) : 0;
+        P.debug = dbg;  // timing experiments only (results are wrong when set)
+        if (dbg & 4) {  // clock64 trace of the band kernel, dumped to stderr after the call
+            static long long* ts = nullptr;
+            if (!ts) cudaMalloc(&ts, 148 * 32 * sizeof(long long));
+            cudaMemsetAsync(ts, 0, 148 * 32 * sizeof(long long), st);
+            P.dbg_ts = ts;
+        }
         rc = band_gemm_launch(Ap, Bp, P, (int)n_ctas, st);
+        if (P.dbg_ts) {
+            long long h[148 * 32];
+            cudaMemcpy(h, P.dbg_ts, sizeof h, cudaMemcpyDeviceToHost);
+            for (size_t c = 0; c < n_ctas; c++) {
+                std::fprintf(stderr, "cta %zu:", c);
+                const long long t0 = h[c * 32 + 31];
+                for (int k = 0; k < 4; k++)
+                    if (h[c * 32 + 8 * k])
+                        std::fprintf(stderr, " [w%lld i%lld c%lld e%lld..%lld]", h[c * 32 + 8 * k] - t0,
+                                     h[c * 32 + 8 * k + 1] - t0, h[c * 32 + 8 * k + 2] - t0, h[c * 32 + 8 * k + 3] - t0,
+                                     h[c * 32 + 8 * k + 4] - t0);
+                std::fprintf(stderr, "\n");
+            }
+        }
     } else {
         SliceGemmParams P;
         P.S_A = SA;
@@ -1594,6 +2129,9 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         rc = slice_gemm_launch(Ap, Bp, P, G, st);
     }
     if (rc) return rc;
+    htrace().mark("gemm_launched");
+    if (after_gemm && (rc = (*after_gemm)())) return rc;
+    htrace().mark("hook_done");
     RecombineArgs R;
     R.Tw = Tw;
     R.Tc = Tc;
@@ -1616,18 +2154,20 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     R.int_out = int_out;
     R.int_limbs = int_limbs;
     R.status = workspace().status_dev;
+    R.quad = band ? 1 : 0;
     tok = prof_begin("recombine", st);
     {
         const int NT = (NW + 1) / 2 + 2;
         const unsigned gb = blocks_for(M * N, 128);
+        const unsigned gbq = blocks_for(M * ((N + 3) / 4) * 4, 128);
         static const bool slow = std::getenv("APB_SLOW_RECOMBINE") != nullptr;  // test hook
         const bool fast = band && first && !int_out && R.C.mant && !slow;
-        if (fast && band_w == 4 && NW <= 20) recombine_fast_kernel<20, 32><<<gb, 128, 0, st>>>(R);
-        else if (fast && band_w == 4 && NW <= 40) recombine_fast_kernel<40, 32><<<gb, 128, 0, st>>>(R);
-        else if (fast && band_w == 4 && NW <= 72) recombine_fast_kernel<72, 32><<<gb, 128, 0, st>>>(R);
-        else if (fast && band_w == 2 && NW <= 40) recombine_fast_kernel<40, 16><<<gb, 128, 0, st>>>(R);
-        else if (fast && band_w == 2 && NW <= 80) recombine_fast_kernel<80, 16><<<gb, 128, 0, st>>>(R);
-        else if (fast && band_w == 2 && NW <= 144) recombine_fast_kernel<144, 16><<<gb, 128, 0, st>>>(R);
+        if (fast && band_w == 4 && NW <= 20) recombine_fast_kernel<20, 32><<<gbq, 128, 0, st>>>(R);
+        else if (fast && band_w == 4 && NW <= 40) recombine_fast_kernel<40, 32><<<gbq, 128, 0, st>>>(R);
+        else if (fast && band_w == 4 && NW <= 72) recombine_fast_kernel<72, 32><<<gbq, 128, 0, st>>>(R);
+        else if (fast && band_w == 2 && NW <= 40) recombine_fast_kernel<40, 16><<<gbq, 128, 0, st>>>(R);
+        else if (fast && band_w == 2 && NW <= 80) recombine_fast_kernel<80, 16><<<gbq, 128, 0, st>>>(R);
+        else if (fast && band_w == 2 && NW <= 144) recombine_fast_kernel<144, 16><<<gbq, 128, 0, st>>>(R);
         else if (NT <= 8) recombine_kernel<8><<<gb, 128, 0, st>>>(R);
         else if (NT <= 16) recombine_kernel<16><<<gb, 128, 0, st>>>(R);
         else if (NT <= 40) recombine_kernel<40><<<gb, 128, 0, st>>>(R);
@@ -1699,7 +2239,12 @@ int radius_compute(const apb_mat* A, const apb_mat* B, int wa, int wb, int slot,
         int* lidx = sbuf<int>(R.lidx, (size_t)K * std::max(M, N), st);
         double* lval = sbuf<double>(R.lval, (size_t)K * std::max(M, N), st);
         const int tk = prof_begin("rad_gemm", st);
-        if (a_trans && dens_b <= 0.25 && dens_b <= dens_a && lcnt && lidx && lval) {
+        static const bool v1 = std::getenv("APB_RAD_V1") != nullptr;  // test hook: list kernels
+        if (!v1 && a_trans && dens_b <= 0.25 && dens_b <= dens_a) {
+            rad_spcol_v2_kernel<<<(unsigned)N, 256, 0, st>>>(da, db, M, N, K, ecen, fcen, rb, rf);
+        } else if (!v1 && !a_trans && dens_a <= 0.25) {
+            rad_sprow_v2_kernel<<<(unsigned)M, 256, 0, st>>>(da, db, M, N, K, ecen, fcen, rb, rf);
+        } else if (a_trans && dens_b <= 0.25 && dens_b <= dens_a && lcnt && lidx && lval) {
             col_lists_kernel<<<blocks_for(N, 8), 256, 0, st>>>(db, K, N, lcnt, lidx, lval);
             dim3 grid(blocks_for(M, 32), blocks_for(N, 8));
             rad_spcol_kernel<<<grid, 256, 0, st>>>(da, M, N, K, lcnt, lidx, lval, ecen, fcen, rb, rf);
@@ -1781,6 +2326,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     // radius products' windows), centring, exact double planes and nonzero counts
     const int64_t M = A->rows, K = A->cols, N = B->cols;
     BallsView av = view_of(&A->b), bv = view_of(&B->b);
+    htrace().start();
     ScanSummary* sum = sbuf<ScanSummary>(S_SUM, 1, st);
     LineWins RW, CW;
     const int rslot[6] = {S_RTOP, S_RBOT, S_RW1T, S_RW1B, S_RW2T, S_RW2B};
@@ -1802,20 +2348,17 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     double* da2 = sbuf<double>(kRad[1].da, (size_t)M * K, st);
     double* db2 = sbuf<double>(kRad[1].db, (size_t)K * N, st);
     if (!sum || !mw1 || !mw2 || !ec1 || !ec2 || !fc1 || !fc2 || !da1 || !db1 || !da2 || !db2) return APB_ERR_CUDA;
-    cudaMemsetAsync(sum, 0, sizeof(ScanSummary), st);
-    cudaMemsetAsync(mw1, 0, 4 * sizeof(long long), st);
-    cudaMemsetAsync(mw2, 0, 4 * sizeof(long long), st);
     const int tk_scan = prof_begin("scan", st);
-    init_wins_kernel<<<blocks_for(M, 256), 256, 0, st>>>(RW, M);
-    init_wins_kernel<<<blocks_for(N, 256), 256, 0, st>>>(CW, N);
     {
-        dim3 gr(blocks_for(M, 8), blocks_for(K, 32 * ROW_CH));
-        fused_rows_kernel<<<gr, 256, 0, st>>>(av, M, K, RW, sum, mw1 + 2, mw2 + 2);
-        dim3 gc(blocks_for(N, 128), blocks_for(K, FCOL_CHUNK));
-        fused_cols_kernel<<<gc, 128, 0, st>>>(bv, K, N, CW, sum, mw1 + 3, mw2 + 3);
-        fused_finish_kernel<<<blocks_for(std::max(M, N), 256), 256, 0, st>>>(RW, CW, M, N, ec1, ec2, fc1, fc2, sum,
-                                                                            mw1, mw2);
-        count_launch(5);
+        const int cA = (int)((K + SCAN_A_COLS - 1) / SCAN_A_COLS), cB = (int)((K + SCAN_B_ROWS - 1) / SCAN_B_ROWS);
+        int64_t* pa = sbuf<int64_t>(S_PARTA, (size_t)SCAN_FIELDS * cA * M, st);
+        int64_t* pb = sbuf<int64_t>(S_PARTB, (size_t)SCAN_FIELDS * cB * N, st);
+        if (!pa || !pb) return APB_ERR_CUDA;
+        const int64_t nblk = M * cA + ((N + 31) / 32) * cB;
+        scan_v2_kernel<<<(unsigned)nblk, 256, 0, st>>>(av, bv, M, K, N, cA, cB, pa, pb, sum, mw1, mw2);
+        scan_v2_finish_kernel<<<blocks_for(32 * (M + N), 256), 256, 0, st>>>(
+            pa, pb, M, N, cA, cB, RW.top[0], RW.bot[0], CW.top[0], CW.bot[0], ec1, ec2, fc1, fc2, sum, mw1, mw2);
+        count_launch(2);
     }
     prof_end(tk_scan, st);
     ScanSummary* hs = pinned_summary();
@@ -1824,7 +2367,9 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     cudaMemcpyAsync(hw, mw1, 4 * sizeof(long long), cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(hw + 4, mw2, 4 * sizeof(long long), cudaMemcpyDeviceToHost, st);
     int rc;
+    htrace().mark("scan_launched");
     if ((rc = cuda_check(cudaStreamSynchronize(st), "matmul plan"))) return rc;
+    htrace().mark("synced");
     const ScanSummary hsum = *hs;
     long long hw1[4], hw2[4];
     for (int q = 0; q < 4; q++) {
@@ -1833,6 +2378,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     }
     Plan P;
     if ((rc = plan_finish(A, B, prec, hsum, P, st))) return rc;
+    htrace().mark("planned");
     if (P.special) return classical(A, B, prec, C, st);  // src/matmul.cpp:455-458
     stats().block_calls++;
     stats().last_block_count = P.steps.size() / 3;
@@ -1844,22 +2390,35 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     int64_t* r2f = sbuf<int64_t>(S_R2F, (size_t)M * N, st);
     if (!r1b || !r1f || !r2b || !r2f) return APB_ERR_CUDA;
     const bool rad_multi = hw1[0] > 900 || hw1[1] > 900 || hw2[0] > 900 || hw2[1] > 900;
-    cudaStream_t rs = rad_multi ? st : side_stream();  // the multi-block radius path syncs its stream
-    const int tk_rad = prof_begin("radius", rs);
-    if (!rad_multi) {  // exact double planes of both radius products, off the critical path
-        fused_planes_kernel<<<blocks_for(M * K, 256), 256, 0, rs>>>(av, M, K, 1, ec1, ec2, da1, da2, nullptr, nullptr);
-        fused_planes_kernel<<<blocks_for(K * N, 256), 256, 0, rs>>>(bv, K, N, 0, fc1, fc2, db1, db2, nullptr, nullptr);
-        count_launch(2);
-    }
+    // where the radius products run: 0 side stream from the start, 1 main stream
+    // after the midpoint product, 2 side stream issued right after the GEMM launch
+    static const int rad_order = std::getenv("APB_RAD_ORDER") ? std::atoi(std::getenv("APB_RAD_ORDER")) : 2;
+    const int order = rad_multi ? 1 : rad_order;
+    cudaStream_t rs = order == 1 ? st : side_stream();  // the multi-block radius path syncs its stream
     static cudaEvent_t ev_join = [] {
         cudaEvent_t e;
         cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
         return e;
     }();
-    if ((rc = radius_compute(A, B, 0, 2, 0, hw1, r1b, r1f, rs, 1))) return rc;  // |A| plane transposed
-    if ((rc = radius_compute(A, B, 1, 3, 1, hw2, r2b, r2f, rs))) return rc;
-    prof_end(tk_rad, rs);
-    if (rs != st) cudaEventRecord(ev_join, rs);
+    bool rad_done = false;
+    std::function<int()> launch_radius = [&]() -> int {
+        if (rad_done) return APB_OK;
+        rad_done = true;
+        int rc2;
+        const int tk_rad = prof_begin("radius", rs);
+        if (!rad_multi) {  // exact double planes of both radius products
+            fused_planes_kernel<<<blocks_for(M * K, 256), 256, 0, rs>>>(av, M, K, 1, ec1, ec2, da1, da2, nullptr, nullptr);
+            fused_planes_kernel<<<blocks_for(K * N, 256), 256, 0, rs>>>(bv, K, N, 0, fc1, fc2, db1, db2, nullptr, nullptr);
+            count_launch(2);
+        }
+        if ((rc2 = radius_compute(A, B, 0, 2, 0, hw1, r1b, r1f, rs, 1))) return rc2;  // |A| plane transposed
+        if ((rc2 = radius_compute(A, B, 1, 3, 1, hw2, r2b, r2f, rs))) return rc2;
+        prof_end(tk_rad, rs);
+        if (rs != st) cudaEventRecord(ev_join, rs);
+        return APB_OK;
+    };
+    if (order == 0 && (rc = launch_radius())) return rc;
+    const std::function<int()>* hook = order == 2 ? &launch_radius : nullptr;
     bool first = true;
     const bool single = P.steps.size() == 3 && P.steps[0] == 0 && P.steps[1] == A->cols;
     for (size_t s = 0; s < P.steps.size(); s += 3) {
@@ -1878,7 +2437,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
                 rc = scaled_block(A, B, lo, hi, prec, C, first, P.maxw_a, P.maxw_b,
                                   sbuf<int64_t>(S_RTOP, M, st), sbuf<int64_t>(S_RBOT, M, st),
                                   sbuf<int64_t>(S_CTOP, N, st), sbuf<int64_t>(S_CBOT, N, st), nullptr, 0,
-                                  nullptr, nullptr, st);
+                                  nullptr, nullptr, st, hook);
             } else {
                 rc = scaled_block(A, B, lo, hi, prec, C, first, 0, 0, nullptr, nullptr, nullptr, nullptr,
                                   nullptr, 0, nullptr, nullptr, st);
@@ -1887,11 +2446,14 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         }
         first = false;
     }
+    if ((rc = launch_radius())) return rc;  // order 1 (or no GEMM ran)
     if (rs != st) cudaStreamWaitEvent(st, ev_join, 0);
     const int tk_comb = prof_begin("combine", st);
     rad_combine_kernel<<<blocks_for(M * N, 256), 256, 0, st>>>(out_of(&C->b), M * N, r1b, r1f, r2b, r2f);
     prof_end(tk_comb, st);
     count_launch();
+    htrace().mark("done");
+    htrace().flush();
     return cuda_check(cudaGetLastError(), "block matmul");
 }
 

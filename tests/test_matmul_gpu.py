@@ -77,12 +77,18 @@ def test_full_config_vs_reference(cfg):
     assert ok.all(), f"{(~ok).sum()} entries differ"
 
 
-def test_unit_gemm_path_golden():
-    """the one-diagonal-per-pass kernel (used when a diagonal could overflow int32)
-    forced on the golden cases in a subprocess"""
+@pytest.mark.parametrize("hook", ["APB_FORCE_UNIT_GEMM=1", "APB_PACK_V1=1", "APB_RAD_V1=1", "APB_RAD_ORDER=1",
+                                  "APB_RAD_ORDER=0", "APB_BAND_BN=128", "APB_BAND_V2=1"])
+def test_kernel_variants_golden(hook):
+    """alternative kernels / schedules selected by the library's tuning hooks
+    (unit GEMM used when a diagonal could overflow int32, byte-serial pack,
+    list-based sparse radius, radius stream placement, 128-wide band tiles),
+    on the golden cases and configs 2 and 3 in a subprocess"""
     import subprocess
     import sys
-    env = dict(os.environ, APB_FORCE_UNIT_GEMM="1")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-k", "test_matmul_golden_gpu",
-                        os.path.abspath(__file__)], env=env, capture_output=True, text=True, timeout=600)
+    k, v = hook.split("=")
+    env = dict(os.environ, **{k: v})
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-k",
+                        "test_matmul_golden_gpu or test_full_config_vs_reference", os.path.abspath(__file__)],
+                       env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:]
