@@ -650,6 +650,7 @@ __global__ void __launch_bounds__(128) recombine_fast_kernel(RecombineArgs R) {
             w[u] = (b < NBC && b < NB) ? __ldcs(R.Tw + (size_t)b * plane + off) : 0u;
             c[u] = (b < NBC && b < NB) ? __ldcs(R.Tc + (size_t)b * plane + off) : 0;
         }
+        asm volatile("" ::: "memory");  // all 2 RB loads of the batch in flight
 #pragma unroll
         for (int u = 0; u < RB; u++) {
             const int k = kb + u;
@@ -1311,12 +1312,25 @@ __global__ void rad_planes_kernel(BallsView X, int64_t rows, int64_t cols, int64
 // rounded-to-nearest sums in the reference's order, 1024-term chunks, then
 // Mag::from_double_upper * (1 + 2^-29) and mag_add_up into r (src/matmul.cpp:423-435).
 // 64x64 output tile per 256 threads, 4x4 per thread, sequential in l per entry.
+// which radius-product kernel a (speculatively launched) set of candidates
+// runs, decided on the device from the scan's nonzero counts mw[2] (A side)
+// and mw[3] (B side) with the host's rule (radius_compute): 0 sparse columns
+// of Q, 1 sparse rows of P, 2 dense.  Bit-identical results either way.
+APB_DEV int rad_variant(const long long* mw, int64_t M, int64_t K, int64_t N, int a_trans) {
+    const double dens_a = M * K ? (double)mw[2] / (double)(M * K) : 1.0;
+    const double dens_b = K * N ? (double)mw[3] / (double)(K * N) : 1.0;
+    if (a_trans && dens_b <= 0.25 && dens_b <= dens_a) return 0;
+    if (!a_trans && dens_a <= 0.25) return 1;
+    return 2;
+}
+
 constexpr int RT = 32, RK = 32, RTHREADS = 64;
 __global__ void __launch_bounds__(64) rad_gemm_kernel(const double* __restrict__ da,
                                                        const double* __restrict__ db, int64_t M,
                                                        int64_t N, int64_t w, const int64_t* ecen,
                                                        const int64_t* fcen, uint32_t* rb, int64_t* rf,
-                                                       int accumulate, int a_trans) {
+                                                       int accumulate, int a_trans, const long long* sel = nullptr) {
+    if (sel && rad_variant(sel, M, w, N, a_trans) != 2) return;
     __shared__ double sA[RK][RT + 1];
     __shared__ double sB[RK][RT];
     const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
@@ -1605,6 +1619,157 @@ __global__ void __launch_bounds__(256) rad_sprow_v2_kernel(const double* __restr
             rad_fold(ent, s, ei, fcen[jj]);
         }
         if (j < N) mag_store(ent, &rb[i * N + j], &rf[i * N + j]);
+    }
+}
+
+APB_DEV void cp_async8(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
+                 "l"(gsrc)
+                 : "memory");
+}
+APB_DEV void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+// ---- v3: as v2, with R lines per thread (independent RN sums interleaved for
+// ILP, one list read serving R loads); the 8R gathered operands of a batch are
+// fetched with cp.async into a per-thread shared-memory column so they are all
+// in flight together (the compiler otherwise interleaves each load with its use)
+template <int R>
+__global__ void __launch_bounds__(256) rad_spcol_v3_kernel(const double* __restrict__ daT, const double* __restrict__ db,
+                                                           int64_t M, int64_t N, int64_t w, const int64_t* ecen,
+                                                           const int64_t* fcen, uint32_t* rb, int64_t* rf,
+                                                           const long long* sel = nullptr) {
+    if (sel && rad_variant(sel, M, w, N, 1) != 0) return;
+    __shared__ int sl[RCH];
+    __shared__ double sv[RCH];
+    __shared__ int cnt[65];
+    __shared__ double gbuf[8 * R][256];
+    const int64_t j = blockIdx.x;
+    const int64_t nch = (w + RCH - 1) / RCH;
+    const int64_t fj = fcen[j];
+    int n = 0;
+    for (int64_t pass = 0; pass * 256 * R < M; pass++) {
+        int64_t ii[R];
+        double s[R];
+        Mag ent[R];
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int64_t i = pass * 256 * R + 256 * r + threadIdx.x;
+            ii[r] = i < M ? i : 0;
+            s[r] = 0.0;
+            ent[r] = mag_zero();
+        }
+        for (int64_t c0 = 0; c0 < w; c0 += RCH) {
+            if (nch > 1 || pass == 0) {
+                if (nch > 1) __syncthreads();
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int64_t l = c0 + 256 * u + threadIdx.x;
+                    v[u] = l < w ? db[l * N + j] : 0.0;
+                }
+                n = block_compact(v, c0, sl, sv, cnt);
+            }
+            int p0 = 0;
+            for (; p0 + 8 <= n; p0 += 8) {
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const double* row = daT + (int64_t)sl[p0 + u] * M;
+#pragma unroll
+                    for (int r = 0; r < R; r++) cp_async8(&gbuf[u * R + r][threadIdx.x], row + ii[r]);
+                }
+                cp_async_wait_all();
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const double bv = sv[p0 + u];
+#pragma unroll
+                    for (int r = 0; r < R; r++) s[r] = __dadd_rn(s[r], __dmul_rn(gbuf[u * R + r][threadIdx.x], bv));
+                }
+            }
+            for (; p0 < n; p0++) {
+                const double* row = daT + (int64_t)sl[p0] * M;
+                const double bv = sv[p0];
+#pragma unroll
+                for (int r = 0; r < R; r++) s[r] = __dadd_rn(s[r], __dmul_rn(row[ii[r]], bv));
+            }
+#pragma unroll
+            for (int r = 0; r < R; r++) rad_fold(ent[r], s[r], ecen[ii[r]], fj);
+        }
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int64_t i = pass * 256 * R + 256 * r + threadIdx.x;
+            if (i < M) mag_store(ent[r], &rb[i * N + j], &rf[i * N + j]);
+        }
+    }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) rad_sprow_v3_kernel(const double* __restrict__ da, const double* __restrict__ db,
+                                                           int64_t M, int64_t N, int64_t w, const int64_t* ecen,
+                                                           const int64_t* fcen, uint32_t* rb, int64_t* rf,
+                                                           const long long* sel = nullptr) {
+    if (sel && rad_variant(sel, M, w, N, 0) != 1) return;
+    __shared__ int sl[RCH];
+    __shared__ double sv[RCH];
+    __shared__ int cnt[65];
+    __shared__ double gbuf[8 * R][256];
+    const int64_t i = blockIdx.x;
+    const int64_t nch = (w + RCH - 1) / RCH;
+    const int64_t ei = ecen[i];
+    int n = 0;
+    for (int64_t pass = 0; pass * 256 * R < N; pass++) {
+        int64_t jj[R];
+        double s[R];
+        Mag ent[R];
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int64_t j = pass * 256 * R + 256 * r + threadIdx.x;
+            jj[r] = j < N ? j : 0;
+            s[r] = 0.0;
+            ent[r] = mag_zero();
+        }
+        for (int64_t c0 = 0; c0 < w; c0 += RCH) {
+            if (nch > 1 || pass == 0) {
+                if (nch > 1) __syncthreads();
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int64_t l = c0 + 256 * u + threadIdx.x;
+                    v[u] = l < w ? da[i * w + l] : 0.0;
+                }
+                n = block_compact(v, c0, sl, sv, cnt);
+            }
+            int p0 = 0;
+            for (; p0 + 8 <= n; p0 += 8) {
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const double* row = db + (int64_t)sl[p0 + u] * N;
+#pragma unroll
+                    for (int r = 0; r < R; r++) cp_async8(&gbuf[u * R + r][threadIdx.x], row + jj[r]);
+                }
+                cp_async_wait_all();
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const double av = sv[p0 + u];
+#pragma unroll
+                    for (int r = 0; r < R; r++) s[r] = __dadd_rn(s[r], __dmul_rn(av, gbuf[u * R + r][threadIdx.x]));
+                }
+            }
+            for (; p0 < n; p0++) {
+                const double* row = db + (int64_t)sl[p0] * N;
+                const double av = sv[p0];
+#pragma unroll
+                for (int r = 0; r < R; r++) s[r] = __dadd_rn(s[r], __dmul_rn(av, row[jj[r]]));
+            }
+#pragma unroll
+            for (int r = 0; r < R; r++) rad_fold(ent[r], s[r], ei, fcen[jj[r]]);
+        }
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int64_t j = pass * 256 * R + 256 * r + threadIdx.x;
+            if (j < N) mag_store(ent[r], &rb[i * N + j], &rf[i * N + j]);
+        }
     }
 }
 
@@ -2240,10 +2405,13 @@ int radius_compute(const apb_mat* A, const apb_mat* B, int wa, int wb, int slot,
         double* lval = sbuf<double>(R.lval, (size_t)K * std::max(M, N), st);
         const int tk = prof_begin("rad_gemm", st);
         static const bool v1 = std::getenv("APB_RAD_V1") != nullptr;  // test hook: list kernels
+        static const bool v2 = std::getenv("APB_RAD_V2") != nullptr;  // test hook: one line per thread
         if (!v1 && a_trans && dens_b <= 0.25 && dens_b <= dens_a) {
-            rad_spcol_v2_kernel<<<(unsigned)N, 256, 0, st>>>(da, db, M, N, K, ecen, fcen, rb, rf);
+            if (v2 || M <= 256) rad_spcol_v2_kernel<<<(unsigned)N, 256, 0, st>>>(da, db, M, N, K, ecen, fcen, rb, rf);
+            else rad_spcol_v3_kernel<2><<<(unsigned)N, 256, 0, st>>>(da, db, M, N, K, ecen, fcen, rb, rf);
         } else if (!v1 && !a_trans && dens_a <= 0.25) {
-            rad_sprow_v2_kernel<<<(unsigned)M, 256, 0, st>>>(da, db, M, N, K, ecen, fcen, rb, rf);
+            if (v2 || N <= 256) rad_sprow_v2_kernel<<<(unsigned)M, 256, 0, st>>>(da, db, M, N, K, ecen, fcen, rb, rf);
+            else rad_sprow_v3_kernel<2><<<(unsigned)M, 256, 0, st>>>(da, db, M, N, K, ecen, fcen, rb, rf);
         } else if (a_trans && dens_b <= 0.25 && dens_b <= dens_a && lcnt && lidx && lval) {
             col_lists_kernel<<<blocks_for(N, 8), 256, 0, st>>>(db, K, N, lcnt, lidx, lval);
             dim3 grid(blocks_for(M, 32), blocks_for(N, 8));
@@ -2361,6 +2529,50 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         count_launch(2);
     }
     prof_end(tk_scan, st);
+    // where the radius products run: 0 side stream after planning, 1 main stream
+    // after the midpoint product, 2 side stream issued right after the GEMM
+    // launch, 3 main stream before the midpoint product, 4 (default) side stream
+    // right after the scan, before the host round trip -- speculatively assuming
+    // a single radius block, with the sparse/dense kernel chosen on the device;
+    // the multi-block case is redone on the main stream after the plan is known
+    static const int rad_order = std::getenv("APB_RAD_ORDER") ? std::atoi(std::getenv("APB_RAD_ORDER")) : 4;
+    static cudaEvent_t ev_join = [] {
+        cudaEvent_t e;
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        return e;
+    }();
+    static cudaEvent_t ev_scan = [] {
+        cudaEvent_t e;
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        return e;
+    }();
+    uint32_t* r1b = sbuf<uint32_t>(S_R1B, (size_t)M * N, st);
+    int64_t* r1f = sbuf<int64_t>(S_R1F, (size_t)M * N, st);
+    uint32_t* r2b = sbuf<uint32_t>(S_R2B, (size_t)M * N, st);
+    int64_t* r2f = sbuf<int64_t>(S_R2F, (size_t)M * N, st);
+    if (!r1b || !r1f || !r2b || !r2f) return APB_ERR_CUDA;
+    const bool spec = rad_order == 4;
+    if (spec) {
+        cudaStream_t ss = side_stream();
+        cudaEventRecord(ev_scan, st);
+        cudaStreamWaitEvent(ss, ev_scan, 0);
+        const int tk = prof_begin("radius", ss);
+        fused_planes_kernel<<<blocks_for(M * K, 256), 256, 0, ss>>>(av, M, K, 1, ec1, ec2, da1, da2, nullptr, nullptr);
+        fused_planes_kernel<<<blocks_for(K * N, 256), 256, 0, ss>>>(bv, K, N, 0, fc1, fc2, db1, db2, nullptr, nullptr);
+        const int tk1 = prof_begin("rad_gemm", ss);
+        rad_spcol_v3_kernel<2><<<(unsigned)N, 256, 0, ss>>>(da1, db1, M, N, K, ec1, fc1, r1b, r1f, mw1);
+        rad_gemm_kernel<<<dim3(blocks_for(N, RT), blocks_for(M, RT)), RTHREADS, 0, ss>>>(da1, db1, M, N, K, ec1, fc1,
+                                                                                       r1b, r1f, 0, 1, mw1);
+        prof_end(tk1, ss);
+        const int tk2 = prof_begin("rad_gemm", ss);
+        rad_sprow_v3_kernel<2><<<(unsigned)M, 256, 0, ss>>>(da2, db2, M, N, K, ec2, fc2, r2b, r2f, mw2);
+        rad_gemm_kernel<<<dim3(blocks_for(N, RT), blocks_for(M, RT)), RTHREADS, 0, ss>>>(da2, db2, M, N, K, ec2, fc2,
+                                                                                       r2b, r2f, 0, 0, mw2);
+        prof_end(tk2, ss);
+        prof_end(tk, ss);
+        cudaEventRecord(ev_join, ss);
+        count_launch(6);
+    }
     ScanSummary* hs = pinned_summary();
     long long* hw = (long long*)(hs + 1);
     cudaMemcpyAsync(hs, sum, sizeof(ScanSummary), cudaMemcpyDeviceToHost, st);
@@ -2379,28 +2591,18 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     Plan P;
     if ((rc = plan_finish(A, B, prec, hsum, P, st))) return rc;
     htrace().mark("planned");
-    if (P.special) return classical(A, B, prec, C, st);  // src/matmul.cpp:455-458
+    if (P.special) {  // src/matmul.cpp:455-458
+        if (spec) cudaStreamWaitEvent(st, ev_join, 0);  // the speculative radius still reads scratch
+        return classical(A, B, prec, C, st);
+    }
     stats().block_calls++;
     stats().last_block_count = P.steps.size() / 3;
-    // R_C += |A| R_B + R_A (|B| + R_B): FP64 work on a side stream, overlapping the
-    // tensor-core midpoint product (independent inputs)
-    uint32_t* r1b = sbuf<uint32_t>(S_R1B, (size_t)M * N, st);
-    int64_t* r1f = sbuf<int64_t>(S_R1F, (size_t)M * N, st);
-    uint32_t* r2b = sbuf<uint32_t>(S_R2B, (size_t)M * N, st);
-    int64_t* r2f = sbuf<int64_t>(S_R2F, (size_t)M * N, st);
-    if (!r1b || !r1f || !r2b || !r2f) return APB_ERR_CUDA;
+    // R_C += |A| R_B + R_A (|B| + R_B): FP64 work (independent of the midpoint product)
     const bool rad_multi = hw1[0] > 900 || hw1[1] > 900 || hw2[0] > 900 || hw2[1] > 900;
-    // where the radius products run: 0 side stream from the start, 1 main stream
-    // after the midpoint product, 2 side stream issued right after the GEMM launch
-    static const int rad_order = std::getenv("APB_RAD_ORDER") ? std::atoi(std::getenv("APB_RAD_ORDER")) : 2;
+    if (spec && rad_multi) cudaStreamWaitEvent(st, ev_join, 0);  // speculation void: redo below
     const int order = rad_multi ? 1 : rad_order;
-    cudaStream_t rs = order == 1 ? st : side_stream();  // the multi-block radius path syncs its stream
-    static cudaEvent_t ev_join = [] {
-        cudaEvent_t e;
-        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-        return e;
-    }();
-    bool rad_done = false;
+    cudaStream_t rs = (order == 1 || order == 3) ? st : side_stream();  // multi-block radius syncs its stream
+    bool rad_done = spec && !rad_multi;
     std::function<int()> launch_radius = [&]() -> int {
         if (rad_done) return APB_OK;
         rad_done = true;
@@ -2417,7 +2619,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         if (rs != st) cudaEventRecord(ev_join, rs);
         return APB_OK;
     };
-    if (order == 0 && (rc = launch_radius())) return rc;
+    if ((order == 0 || order == 3) && (rc = launch_radius())) return rc;
     const std::function<int()>* hook = order == 2 ? &launch_radius : nullptr;
     bool first = true;
     const bool single = P.steps.size() == 3 && P.steps[0] == 0 && P.steps[1] == A->cols;
