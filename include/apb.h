@@ -228,6 +228,11 @@ int apb_profile_read(const char* kernel, double* ms, uint64_t* launches);
  * relative to the first region's begin (regions on all streams); returns the
  * full text length (buf may be NULL to query it) */
 int apb_profile_dump(char* buf, size_t cap);
+/* device-side span timer of the exact-integer band GEMM (first CTA start to
+ * last CTA end, ns), accumulated over launches -- also inside the library's
+ * captured CUDA graphs, where per-call event regions are not recorded */
+int apb_gemm_timer_read(uint64_t* total_ns, uint64_t* launches);
+int apb_gemm_timer_reset(void);
 
 apb_matmul_stats* apb_matmul_stats_get(void);
 void apb_matmul_stats_reset(void);

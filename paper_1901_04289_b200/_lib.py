@@ -82,6 +82,10 @@ def lib():
     L.apb_profile_read.restype = I
     L.apb_profile_dump.argtypes = [C.c_char_p, C.c_size_t]
     L.apb_profile_dump.restype = I
+    L.apb_gemm_timer_read.argtypes = [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+    L.apb_gemm_timer_read.restype = I
+    L.apb_gemm_timer_reset.argtypes = []
+    L.apb_gemm_timer_reset.restype = I
     _lib = L
     return L
 

@@ -19,6 +19,7 @@ static thread_local std::string g_error;
 static apb_matmul_stats g_stats;
 
 void count_launch(uint64_t k) { g_launches += k; }
+void launch_count_adjust(int64_t d) { g_launches += (uint64_t)d; }
 void set_error(const char* msg) { g_error = msg ? msg : ""; }
 
 int cuda_check(cudaError_t e, const char* where) {
@@ -39,6 +40,8 @@ struct ProfRec {
 static std::mutex g_prof_mu;
 static bool g_prof_on = false;
 static std::vector<ProfRec> g_prof;
+
+bool prof_enabled() { return g_prof_on; }
 
 int prof_begin(const char* name, cudaStream_t st) {
     if (!g_prof_on) return -1;

@@ -23,10 +23,12 @@ struct Workspace {
 Workspace& workspace();
 
 void count_launch(uint64_t k = 1);
+void launch_count_adjust(int64_t d);  // graph replays: kernels counted at capture, added per launch
 
 // event-bracketed kernel timing (apb_profile_*); prof_begin returns a token
 // (-1 when profiling is off) to pass to prof_end after the launch(es)
 int prof_begin(const char* name, cudaStream_t st);
+bool prof_enabled();
 void prof_end(int token, cudaStream_t st);
 void set_error(const char* msg);
 int cuda_check(cudaError_t e, const char* where);

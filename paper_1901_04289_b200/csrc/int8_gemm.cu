@@ -550,6 +550,34 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// span timer: every CTA folds its entry time into a min and its exit time into
+// a max; the last CTA to leave adds the span to the running sum and resets
+__device__ __forceinline__ void span_timer_enter(unsigned long long* T) {
+    if (T && threadIdx.x == 0) atomicMin(&T[2], globaltimer());
+}
+__device__ __forceinline__ void span_timer_exit(unsigned long long* T) {
+    if (T && threadIdx.x == 0) {
+        atomicMax(&T[4], globaltimer());
+        __threadfence();
+        if (atomicAdd(&T[3], 1ull) == gridDim.x - 1) {
+            __threadfence();
+            const unsigned long long t0 = atomicAdd(&T[2], 0ull), t1 = atomicAdd(&T[4], 0ull);
+            T[0] += t1 - t0;
+            T[1] += 1;
+            T[2] = ~0ull;
+            T[3] = 0;
+            T[4] = 0;
+            __threadfence();
+        }
+    }
+}
+
 // ====================================================================
 // Band kernel v3: same work decomposition and output as band_gemm_kernel, with
 // a leaner MMA issue path (the v2 profile showed the single MMA thread, not the
@@ -582,6 +610,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int it_begin = P.cta_begin[blockIdx.x], it_end = P.cta_begin[blockIdx.x + 1];
     if (P.dbg_ts && threadIdx.x == 0) P.dbg_ts[blockIdx.x * 32 + 31] = clock64();
+    span_timer_enter(P.timer);
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < RA; i++) {
@@ -772,6 +801,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512)
                      : "memory");
     }
+    span_timer_exit(P.timer);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -853,8 +883,21 @@ static int band_launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const Ban
     return APB_OK;
 }
 
-int band_gemm_launch(const int8_t* Apack, const int8_t* Bpack, const BandGemmParams& P, int n_ctas,
+unsigned long long* gemm_timer() {
+    static unsigned long long* t = [] {
+        unsigned long long* p = nullptr;
+        cudaMalloc(&p, 8 * sizeof(unsigned long long));
+        const unsigned long long init[8] = {0, 0, ~0ull, 0, 0, 0, 0, 0};
+        cudaMemcpy(p, init, sizeof init, cudaMemcpyHostToDevice);
+        return p;
+    }();
+    return t;
+}
+
+int band_gemm_launch(const int8_t* Apack, const int8_t* Bpack, const BandGemmParams& Pin, int n_ctas,
                      cudaStream_t st) {
+    BandGemmParams P = Pin;
+    if (!P.timer) P.timer = gemm_timer();
     CUtensorMap ma, mb;
     int rc = make_map(&ma, Apack, (uint64_t)P.Kp, (uint64_t)P.S_A * P.Mp, BM);
     if (rc) return rc;
@@ -869,3 +912,23 @@ int band_gemm_launch(const int8_t* Apack, const int8_t* Bpack, const BandGemmPar
 }
 
 }  // namespace apb
+
+extern "C" {
+
+// span timer of the band GEMM: total device time (ns, %globaltimer, first CTA
+// start to last CTA end) and launch count since the last reset; graph-safe
+int apb_gemm_timer_read(uint64_t* total_ns, uint64_t* launches) {
+    unsigned long long h[2] = {0, 0};
+    if (cudaMemcpy(h, apb::gemm_timer(), sizeof h, cudaMemcpyDeviceToHost) != cudaSuccess) return APB_ERR_CUDA;
+    if (total_ns) *total_ns = h[0];
+    if (launches) *launches = h[1];
+    return APB_OK;
+}
+
+int apb_gemm_timer_reset(void) {
+    const unsigned long long init[5] = {0, 0, ~0ull, 0, 0};
+    return cudaMemcpy(apb::gemm_timer(), init, sizeof init, cudaMemcpyHostToDevice) == cudaSuccess ? APB_OK
+                                                                                                  : APB_ERR_CUDA;
+}
+
+}  // extern "C"

@@ -30,7 +30,12 @@ struct BandGemmParams {
     int32_t* Tc;              // [n_bands][Mp][Np] carry out of band b
     int debug = 0;            // timing experiments only: 1 skip TMA refills, 2 skip epilogue stores
     long long* dbg_ts = nullptr;  // optional per-CTA clock64 trace (timing experiments)
+    unsigned long long* timer = nullptr;  // device span timer (gemm_timer_*): [sum ns, launches, start, done, end]
 };
+
+// device-side span timer of the band GEMM (first CTA start to last CTA end,
+// %globaltimer ns), accumulated per launch -- works inside captured graphs
+unsigned long long* gemm_timer();
 
 int band_gemm_launch(const int8_t* Apack, const int8_t* Bpack, const BandGemmParams& P, int n_ctas,
                      cudaStream_t st);

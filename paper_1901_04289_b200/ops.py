@@ -142,13 +142,21 @@ class BallMatrix:
         return isinstance(self.balls, DeviceBallArray)
 
 
-def _matmul(a: BallMatrix, b: BallMatrix, prec: int, algo: int, stream=None, check=True) -> BallMatrix:
+def _matmul(a: BallMatrix, b: BallMatrix, prec: int, algo: int, stream=None, check=True,
+            out: BallMatrix | None = None) -> BallMatrix:
+    """`out` (device, a.rows x b.cols, limbs_for(prec) limbs) is reused when given:
+    repeated calls on the same buffers replay the library's captured CUDA graphs"""
     lib = _lib.lib()
     if a.cols != b.rows:
         raise _lib.InvalidArgument(1, "matmul: dimension mismatch")
     L = limbs_for(prec)
     if a.on_device:
-        c = BallMatrix(DeviceBallArray.empty(a.rows * b.cols, L), a.rows, b.cols)
+        if out is not None:
+            if (out.rows, out.cols) != (a.rows, b.cols) or out.balls.L != L:
+                raise _lib.InvalidArgument(1, "matmul: output shape / limb count mismatch")
+            c = out
+        else:
+            c = BallMatrix(DeviceBallArray.empty(a.rows * b.cols, L), a.rows, b.cols)
         am, bm, cm = a.c(), b.c(), c.c()
         st = _stream_ptr(stream)
         _lib.check(lib.apb_matmul(C.byref(am), C.byref(bm), prec, algo, C.byref(cm), st), "apb_matmul")

@@ -16,6 +16,7 @@ from paper_1901_04289_b200 import gen, ops  # noqa: E402
 def main():
     which = sys.argv[1] if len(sys.argv) > 1 else "c3"
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+    prof = os.environ.get("TIMELINE_NOPROF") is None  # host-trace-only mode keeps launches lean
     if which == "c3":
         a, b = gen.config3_matrices()
         n, p = 512, 256
@@ -32,7 +33,7 @@ def main():
         flush.fill_(1)
         torch.cuda.synchronize()
         lib.apb_profile_reset()
-        lib.apb_profile_enable(1)
+        lib.apb_profile_enable(1 if prof else 0)
         st = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)

@@ -78,7 +78,8 @@ def test_full_config_vs_reference(cfg):
 
 
 @pytest.mark.parametrize("hook", ["APB_FORCE_UNIT_GEMM=1", "APB_PACK_V1=1", "APB_RAD_V1=1", "APB_RAD_V2=1", "APB_RAD_ORDER=1",
-                                  "APB_RAD_ORDER=0", "APB_RAD_ORDER=2", "APB_RAD_ORDER=3", "APB_BAND_BN=128", "APB_BAND_V2=1"])
+                                  "APB_RAD_ORDER=0", "APB_RAD_ORDER=2", "APB_RAD_ORDER=3", "APB_BAND_BN=128", "APB_BAND_V2=1",
+                                  "APB_NO_SPEC_PACK=1", "APB_NO_GRAPHS=1"])
 def test_kernel_variants_golden(hook):
     """alternative kernels / schedules selected by the library's tuning hooks
     (unit GEMM used when a diagonal could overflow int32, byte-serial pack,
@@ -89,6 +90,50 @@ def test_kernel_variants_golden(hook):
     k, v = hook.split("=")
     env = dict(os.environ, **{k: v})
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-k",
-                        "test_matmul_golden_gpu or test_full_config_vs_reference", os.path.abspath(__file__)],
+                        "test_matmul_golden_gpu or test_full_config_vs_reference or test_repeated_calls", os.path.abspath(__file__)],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:]
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+def test_repeated_calls_replay_graphs(cfg):
+    """the same operands and output buffer three times: the first call runs
+    eagerly and captures the launch sequence, later calls replay the CUDA
+    graphs; every result bit-identical to the reference, counters consistent"""
+    from paper_1901_04289_b200 import ops
+    if cfg == "c2":
+        a, b = gen.config2_matrices()
+        n, p = 256, 128
+    else:
+        a, b = gen.config3_matrices()
+        n, p = 512, 256
+    A, B = _mat(a, n, n), _mat(b, n, n)
+    ref, _ = po.matmul(a, b, n, n, n, p, which="ref", algo=1, threads=os.cpu_count() or 8)
+    out = ops.block_matmul_ball(A, B, p)
+    launches = []
+    for rep in range(3):
+        ops.matmul_stats_reset() if hasattr(ops, "matmul_stats_reset") else None
+        l0 = ops.launch_count()
+        got = ops.block_matmul_ball(A, B, p, out=out)
+        launches.append(ops.launch_count() - l0)
+        assert got.balls.to_host().identical(ref).all(), f"rep {rep}"
+    assert launches[1] == launches[2] and launches[1] > 0, launches
+
+
+def test_graph_replay_tracks_new_inputs():
+    """same buffers, new contents: the replayed graphs read the current data"""
+    from paper_1901_04289_b200 import ops
+    n, p = 256, 128
+    a1, b1 = gen.config2_matrices(seed_salt=0)
+    a2, b2 = gen.config2_matrices(seed_salt=7)
+    A, B = _mat(a1, n, n), _mat(b1, n, n)
+    out = ops.block_matmul_ball(A, B, p)
+    ops.block_matmul_ball(A, B, p, out=out)
+    # overwrite the device operands in place with the second pair
+    for dst, src in ((A, a2), (B, b2)):
+        d = src.to_device()
+        for f in ("mant", "exp", "kind", "rad_man", "rad_exp"):
+            getattr(dst.balls, f).copy_(getattr(d, f))
+    got = ops.block_matmul_ball(A, B, p, out=out).balls.to_host()
+    ref, _ = po.matmul(a2, b2, n, n, n, p, which="ref", algo=1, threads=os.cpu_count() or 8)
+    assert got.identical(ref).all()
