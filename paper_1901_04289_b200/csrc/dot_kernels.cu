@@ -132,10 +132,10 @@ APB_DEV void write_state(apb_dot_state* st, const Plan& pl, uint64_t err, uint64
     st->srad = srad;
 }
 
-// srad_add (src/dot.cpp:288-295)
+// srad_add (src/dot.cpp:288-295); both factors are < 2^31 (one 32x32 multiply)
 APB_DEV uint64_t srad_term(uint64_t ab, int64_t af, uint64_t bb, int64_t bf, int64_t e_rad) {
     int64_t d = e_rad - (af + bf);
-    return d < 30 ? ((ab * bb) >> (30 + d)) + 1 : 1;
+    return d < 30 ? (((uint64_t)(uint32_t)ab * (uint32_t)bb) >> (30 + d)) + 1 : 1;
 }
 
 // dot_finalize (src/dot.cpp:306-321) given the reduced accumulator
@@ -187,6 +187,40 @@ APB_DEV void load_mant(uint64_t (&m)[L], const BallsView& a, int64_t e) {
     const uint64_t* src = a.mant + e * (int64_t)a.L;
 #pragma unroll
     for (int j = 0; j < L; j++) m[j] = (j >= off) ? __ldg(src + (j - off)) : 0ull;
+}
+
+// term i of dot b from precomputed element indices (ex, ey): the metadata always,
+// the mantissas only when `mant` (pass 1 needs them only for e_min)
+template <int L>
+APB_DEV void load_term_at(Term<L>& t, const DotArgs& A, int64_t b, int64_t i, int64_t ex, int64_t ey, bool mant) {
+    if (i < A.n) {
+        t.kx = __ldg(A.x.kind + ex);
+        t.ky = __ldg(A.y.kind + ey);
+        t.ex = __ldg(A.x.exp + ex);
+        t.ey = __ldg(A.y.exp + ey);
+        t.rx = __ldg(A.x.rad_man + ex);
+        t.ry = __ldg(A.y.rad_man + ey);
+        t.fx = __ldg(A.x.rad_exp + ex);
+        t.fy = __ldg(A.y.rad_exp + ey);
+        if (mant) {
+            load_mant<L>(t.xm, A.x, ex);
+            load_mant<L>(t.ym, A.y, ey);
+        }
+        t.neg = A.subtract != 0;
+    } else {  // the initial value as term N with y = 1 (src/dot.cpp:29-43)
+        t.kx = __ldg(A.init.kind + b);
+        t.ex = __ldg(A.init.exp + b);
+        t.rx = __ldg(A.init.rad_man + b);
+        t.fx = __ldg(A.init.rad_exp + b);
+        load_mant<L>(t.xm, A.init, b);
+        t.ky = APB_FINITE;
+        t.ey = 1;
+        t.ry = 0;
+        t.fy = 0;
+#pragma unroll
+        for (int j = 0; j < L; j++) t.ym[j] = (j == L - 1) ? (1ull << 63) : 0ull;
+        t.neg = false;
+    }
 }
 
 template <int L>
@@ -292,19 +326,20 @@ struct Acc {
 template <int L, int NS>
 APB_DEV void acc_term(Acc<L, NS>& a, const Term<L>& t, const Plan& pl) {
     const bool negate = t.neg ^ ((t.kx & APB_SIGN) != 0) ^ ((t.ky & APB_SIGN) != 0);
-    const int64_t shift = pl.e_s - (t.ex + t.ey);
-    if (shift >= 64 * (int64_t)pl.n_s) {
+    const int64_t shift64 = pl.e_s - (t.ex + t.ey);
+    if (shift64 >= 64 * (int64_t)pl.n_s) {
         a.err++;
         return;
     }
+    const int shift = (int)shift64;  // 0 <= shift < 64 n_s (e_s >= every term's exponent)
     // operand truncation to ncap limbs (src/dot.cpp:248-253)
-    const int64_t p_t = 64 * (int64_t)pl.n_s - shift;
-    const int64_t ncap = (p_t + 63) / 64 + 1;
+    const int p_t = 64 * pl.n_s - shift;
+    const int ncap = (p_t + 63) / 64 + 1;
     uint64_t xa[L], yb[L];
     bool trunc = false;
 #pragma unroll
     for (int j = 0; j < L; j++) {
-        const bool keep = (int64_t)(L - j) <= ncap;  // slot j is within the top ncap slots
+        const bool keep = (L - j) <= ncap;  // slot j is within the top ncap slots
         xa[j] = keep ? t.xm[j] : 0ull;
         yb[j] = keep ? t.ym[j] : 0ull;
         trunc |= (!keep) && (t.xm[j] | t.ym[j]);
@@ -330,28 +365,72 @@ APB_DEV void acc_term(Acc<L, NS>& a, const Term<L>& t, const Plan& pl) {
         }
         P[i + L] = cy;
     }
-    // contribution floor(P / 2^r), r = shift + 128L - 64 n_s
-    const int64_t r = shift + 128 * (int64_t)L - 64 * (int64_t)pl.n_s;
-    const int64_t rl = r >= 0 ? r / 64 : -((-r + 63) / 64);
-    const unsigned rb = (unsigned)(r - 64 * rl);
-    bool inexact = false;
-    if (r > 0) {
+    // contribution floor(P / 2^r), r = shift + 128 L - 64 n_s (>= 0 here: n_s <= 2L + 1
+    // whenever the term is not dropped); word shift by a barrel of static selects
+    const int r = shift + 128 * L - 64 * pl.n_s;
+    if (r < 0) {  // window wider than the product: exact, shifted left
+        const int rl = (-r) >> 6, rb = (-r) & 63;
+        uint64_t Cl[NS];
 #pragma unroll
-        for (int k = 0; k < 2 * L; k++) {
-            if (k < rl) inexact |= P[k] != 0;
-            else if (k == rl && rb) inexact |= (P[k] & ((1ull << rb) - 1)) != 0;
+        for (int j = 0; j < NS; j++) {
+            uint64_t lo = 0, hi = 0;  // Cl[j] = bits of P << (-r) at word j
+#pragma unroll
+            for (int k = 0; k < 2 * L; k++) {
+                if (k == j - rl) hi = P[k];
+                if (k == j - rl - 1) lo = P[k];
+            }
+            Cl[j] = rb ? (hi << rb) | (lo >> (64 - rb)) : hi;
+        }
+        if (!negate) {
+            uint64_t c = 0;
+#pragma unroll
+            for (int j = 0; j < NS; j++) {
+                const uint64_t s1 = a.s[j] + Cl[j];
+                const uint64_t c1 = s1 < Cl[j];
+                const uint64_t s2 = s1 + c;
+                c = c1 | (s2 < c);
+                a.s[j] = s2;
+            }
+        } else {
+            uint64_t bw = 0;
+#pragma unroll
+            for (int j = 0; j < NS; j++) {
+                const uint64_t x = a.s[j], y = Cl[j];
+                a.s[j] = x - y - bw;
+                bw = (x < y) || (x == y && bw);
+            }
+        }
+        return;
+    }
+    const int rl = r >> 6;
+    const unsigned rb = (unsigned)(r & 63);
+    // barrel: Q = P >> (64 rl) with sticky = OR of the dropped words
+    constexpr int W = 2 * L;
+    uint64_t Q[W];
+    uint64_t sticky = 0;
+#pragma unroll
+    for (int k = 0; k < W; k++) Q[k] = P[k];
+#pragma unroll
+    for (int bit = 1; bit <= W - 1; bit <<= 1) {  // rl <= W - 1
+        const bool on = (rl & bit) != 0;
+        uint64_t drop = 0;
+#pragma unroll
+        for (int k = 0; k < W; k++)
+            if (k < bit) drop |= Q[k];
+        if (on) sticky |= drop;
+#pragma unroll
+        for (int k = 0; k < W; k++) {
+            const uint64_t nv = (k + bit < W) ? Q[k + bit] : 0ull;
+            Q[k] = on ? nv : Q[k];
         }
     }
+    const bool inexact = sticky != 0 || (rb && (Q[0] & ((1ull << rb) - 1)) != 0);
     if (inexact) a.err++;
     uint64_t Cl[NS];
 #pragma unroll
     for (int j = 0; j < NS; j++) {
-        uint64_t lo = 0, hi = 0;
-#pragma unroll
-        for (int k = 0; k < 2 * L; k++) {
-            if (k == j + rl) lo = P[k];
-            if (k == j + rl + 1) hi = P[k];
-        }
+        const uint64_t lo = j < W ? Q[j] : 0ull;
+        const uint64_t hi = j + 1 < W ? Q[j + 1] : 0ull;
         Cl[j] = funnel_r(lo, hi, rb);
     }
     // two's complement add / subtract mod 2^(64 NS) (add_signed_range)
@@ -359,21 +438,19 @@ APB_DEV void acc_term(Acc<L, NS>& a, const Term<L>& t, const Plan& pl) {
         uint64_t c = 0;
 #pragma unroll
         for (int j = 0; j < NS; j++) {
-            uint64_t s1 = a.s[j] + Cl[j];
-            uint64_t c1 = s1 < Cl[j];
-            uint64_t s2 = s1 + c;
-            uint64_t c2 = s2 < c;
+            const uint64_t s1 = a.s[j] + Cl[j];
+            const uint64_t c1 = s1 < Cl[j];
+            const uint64_t s2 = s1 + c;
+            c = c1 | (s2 < c);
             a.s[j] = s2;
-            c = c1 | c2;
         }
     } else {
         uint64_t bw = 0;
 #pragma unroll
         for (int j = 0; j < NS; j++) {
-            uint64_t x = a.s[j], y = Cl[j];
-            uint64_t d = x - y - bw;
+            const uint64_t x = a.s[j], y = Cl[j];
+            a.s[j] = x - y - bw;
             bw = (x < y) || (x == y && bw);
-            a.s[j] = d;
         }
     }
 }
@@ -429,8 +506,14 @@ __global__ void __launch_bounds__(128, (TPL > 0 ? 3 : 4)) dot_small_kernel(DotAr
     uint64_t my_err = 0, my_srad = 0;
     my_pl.status = 2;
 
+    const int64_t xstep32 = 32 * A.idx.xstep, ystep32 = 32 * A.idx.ystep;
     for (int g = 0; g < nd; g++) {
         const int64_t b = b0 + g;
+        // element indices of this lane's first term (index math once per dot)
+        const int64_t bq = A.idx.bdiv == 1 ? b : b / A.idx.bdiv;
+        const int64_t br = A.idx.bdiv == 1 ? 0 : b - bq * A.idx.bdiv;
+        const int64_t ex0 = A.idx.x_off + bq * A.idx.xs1 + br * A.idx.xs2 + lane * A.idx.xstep;
+        const int64_t ey0 = A.idx.y_off + bq * A.idx.ys1 + br * A.idx.ys2 + lane * A.idx.ystep;
         // ---- pass 1: setup scan
         ScanAcc sc{INT64_MIN, INT64_MAX, INT64_MIN, 0, false};
         Term<L> keep[TPL > 0 ? TPL : 1];
@@ -439,14 +522,15 @@ __global__ void __launch_bounds__(128, (TPL > 0 ? 3 : 4)) dot_small_kernel(DotAr
             for (int q = 0; q < (TPL > 0 ? TPL : 1); q++) {
                 int64_t i = lane + 32 * (int64_t)q;
                 if (i < total) {
-                    load_term<L>(keep[q], A, b, i);
+                    load_term_at<L>(keep[q], A, b, i, ex0 + q * xstep32, ey0 + q * ystep32, true);
                     scan_term<L>(sc, keep[q], track_min, with_radius);
                 }
             }
         } else {
-            for (int64_t i = lane; i < total; i += 32) {
+            int64_t ex = ex0, ey = ey0;
+            for (int64_t i = lane; i < total; i += 32, ex += xstep32, ey += ystep32) {
                 Term<L> t;
-                load_term<L>(t, A, b, i);
+                load_term_at<L>(t, A, b, i, ex, ey, track_min);
                 scan_term<L>(sc, t, track_min, with_radius);
             }
         }
@@ -477,9 +561,10 @@ __global__ void __launch_bounds__(128, (TPL > 0 ? 3 : 4)) dot_small_kernel(DotAr
                 if (i < total) do_term(keep[q]);
             }
         } else {
-            for (int64_t i = lane; i < total; i += 32) {
+            int64_t ex = ex0, ey = ey0;
+            for (int64_t i = lane; i < total; i += 32, ex += xstep32, ey += ystep32) {
                 Term<L> t;
-                load_term<L>(t, A, b, i);
+                load_term_at<L>(t, A, b, i, ex, ey, true);
                 do_term(t);
             }
         }

@@ -768,6 +768,146 @@ __global__ void __launch_bounds__(128) recombine_fast_kernel(RecombineArgs R) {
     if (st) *R.status = st;
 }
 
+// Recombine for 16-bit band digits (2 diagonals per band, the default
+// 128x256 tile): the digit recurrence d = run + word_k + carry_{k-1} stays in
+// int32 (|carry| < 2^24, word < 2^16), the magnitude words are parked in
+// shared memory (one padded row per thread) so the p-bit output window and
+// the truncation error are read with dynamic word indices instead of select
+// chains.  Same results as recombine_fast_kernel<*, 16>.
+template <int NBC>
+__global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
+    constexpr int ND = NBC + 2;        // base-2^16 digits (band b: word digit b, carry digit b+1)
+    constexpr int NW = (ND + 1) / 2;   // 32-bit magnitude words
+    constexpr int STR = NW + 3;        // smem row stride (odd for bank spread), 2 guard words
+    __shared__ uint32_t sm[128 * STR];
+    uint32_t* row = sm + threadIdx.x * STR;
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t jr = u & 3, i = (u >> 2) % R.M, jq = (u >> 2) / R.M;
+    const int64_t j = 4 * jq + jr;
+    if (jq * 4 >= R.N || j >= R.N) return;
+    const int64_t t = i * R.N + j;
+    const size_t plane = (size_t)R.Mp * R.Np;
+    const size_t off = rc_off(R, i, j);
+    const int NB = R.nwords;
+    constexpr int RB = 8;
+    uint32_t Wd[NW];
+#pragma unroll
+    for (int q = 0; q < NW; q++) Wd[q] = 0;
+    int32_t run = 0, prev_c = 0;
+    bool neg = false;
+#pragma unroll
+    for (int kb = 0; kb < ND; kb += RB) {
+        uint32_t w[RB];
+        int32_t c[RB];
+#pragma unroll
+        for (int v = 0; v < RB; v++) {
+            const int b = kb + v;
+            w[v] = (b < NBC && b < NB) ? __ldcs(R.Tw + (size_t)b * plane + off) : 0u;
+            c[v] = (b < NBC && b < NB) ? __ldcs(R.Tc + (size_t)b * plane + off) : 0;
+        }
+#pragma unroll
+        for (int v = 0; v < RB; v++) {
+            const int k = kb + v;
+            if (k < ND) {
+                const int32_t d = run + (int32_t)w[v] + prev_c;
+                prev_c = c[v];
+                if (k == ND - 1) neg = d < 0;  // the arithmetic top digit carries the sign
+                else run = d >> 16;
+                Wd[k >> 1] |= ((uint32_t)d & 0xFFFFu) << (16 * (k & 1));
+            }
+        }
+    }
+    if (neg) {  // sign-fill above the top digit, then the magnitude
+        if (ND & 1) Wd[NW - 1] |= 0xFFFF0000u;
+        uint32_t cc = 1;
+#pragma unroll
+        for (int q = 0; q < NW; q++) {
+            const uint32_t v = ~Wd[q] + cc;
+            cc = (cc && v == 0) ? 1u : 0u;
+            Wd[q] = v;
+        }
+    }
+    // bit length of the magnitude and its words in shared memory (guards at [-1], [NW])
+    int top_w = -1;
+#pragma unroll
+    for (int q = 0; q < NW; q++) {
+        row[q + 1] = Wd[q];
+        if (Wd[q]) top_w = q;
+    }
+    row[0] = 0;
+    row[NW + 1] = 0;
+    BallsOut& O = R.C;
+    uint64_t* dst = O.mant + t * (int64_t)O.L;
+    if (top_w < 0) {  // exact zero: C stays Ball::zero()
+        for (int q = 0; q < O.L; q++) dst[q] = 0;
+        O.exp[t] = 0;
+        O.kind[t] = APB_ZERO;
+        O.rad_man[t] = 0;
+        O.rad_exp[t] = 0;
+        return;
+    }
+    const int64_t B = 32 * (int64_t)top_w + (int64_t)(32 - __clz(row[top_w + 1]));
+    // 32 bits of the magnitude starting at bit pos (zeros outside)
+    auto bits32 = [&](int64_t pos) -> uint32_t {
+        if (pos <= -32 || pos >= 32 * (int64_t)NW) return 0u;
+        const int64_t wi = pos >= 0 ? pos >> 5 : -1;
+        const int bo = (int)(pos - 32 * wi);
+        const uint32_t lo = row[wi + 1], hi = row[wi + 2];
+        return bo ? (lo >> bo) | (hi << (32 - bo)) : lo;
+    };
+    const int64_t exp2 = -R.escale[i] - R.fscale[j];
+    int st = 0;
+    const int64_t e = checked_add(exp2, B, &st);  // apfloat_from_bigint_scaled exponent
+    const int64_t p = R.prec;
+    const int64_t cut = B > p ? B - p : 0;  // bits [0, cut) are truncated
+    for (int r = 0; r < O.L; r++) {
+        const int64_t lo_bit = B - 64 * (int64_t)(r + 1);
+        uint64_t v = (uint64_t)bits32(lo_bit) | ((uint64_t)bits32(lo_bit + 32) << 32);
+        if (lo_bit < cut) {
+            const int64_t k = cut - lo_bit;
+            v = k >= 64 ? 0 : (v & ~((1ull << k) - 1));
+        }
+        dst[O.L - 1 - r] = v;
+    }
+    O.exp[t] = e;
+    O.kind[t] = (uint8_t)(APB_FINITE | (neg ? APB_SIGN : 0));
+    // truncation error: Mag upper bound of the discarded bits [0, cut)
+    Mag err = mag_zero();
+    if (cut > 0) {
+        int64_t top = -1;  // highest set bit below the cut
+        int64_t q = (cut - 1) >> 5;
+        uint32_t m = row[q + 1] & (((cut - 32 * q) >= 32) ? 0xFFFFFFFFu : ((1u << (cut - 32 * q)) - 1u));
+        while (true) {
+            if (m) {
+                top = 32 * q + 31 - __clz(m);
+                break;
+            }
+            if (q == 0) break;
+            q--;
+            m = row[q + 1];
+        }
+        if (top >= 0) {
+            const int64_t wpos = top - 63;  // 64-bit window with its MSB at `top`
+            const uint64_t window = (uint64_t)bits32(wpos) | ((uint64_t)bits32(wpos + 32) << 32);
+            bool low = (window & ((1ull << 34) - 1)) != 0;
+            if (!low && wpos > 0) {  // any set bit in [0, wpos)
+                int64_t qq = (wpos - 1) >> 5;
+                uint32_t mm = row[qq + 1] & (((wpos - 32 * qq) >= 32) ? 0xFFFFFFFFu : ((1u << (wpos - 32 * qq)) - 1u));
+                while (!mm && qq > 0) {
+                    qq--;
+                    mm = row[qq + 1];
+                }
+                low = mm != 0;
+            }
+            uint64_t bm = window >> 34;
+            if (low) bm++;
+            err = mag_parts(bm, checked_add(exp2, top + 1, &st));
+        }
+    }
+    mag_store(err, &O.rad_man[t], &O.rad_exp[t]);
+    if (st) *R.status = st;
+}
+
 // ------------------------------------------------------------ K7 radius
 // Mag planes of the four radius operands (src/matmul.cpp:498-509)
 APB_DEV Mag mid_upper(const BallsView& a, int64_t e) {
@@ -2353,10 +2493,13 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         const unsigned gb = blocks_for(M * N, 128);
         const unsigned gbq = blocks_for(M * ((N + 3) / 4) * 4, 128);
         static const bool slow = std::getenv("APB_SLOW_RECOMBINE") != nullptr;  // test hook
+        static const bool r64 = std::getenv("APB_RECOMBINE64") != nullptr;      // test hook
         const bool fast = band && first && !int_out && R.C.mant && !slow;
         if (fast && band_w == 4 && NW <= 20) recombine_fast_kernel<20, 32><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 4 && NW <= 40) recombine_fast_kernel<40, 32><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 4 && NW <= 72) recombine_fast_kernel<72, 32><<<gbq, 128, 0, st>>>(R);
+        else if (fast && band_w == 2 && NW <= 40 && !r64) recombine16_kernel<40><<<gbq, 128, 0, st>>>(R);
+        else if (fast && band_w == 2 && NW <= 80 && !r64) recombine16_kernel<80><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 2 && NW <= 40) recombine_fast_kernel<40, 16><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 2 && NW <= 80) recombine_fast_kernel<80, 16><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 2 && NW <= 144) recombine_fast_kernel<144, 16><<<gbq, 128, 0, st>>>(R);
