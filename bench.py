@@ -429,9 +429,16 @@ def main():
     if args.impl == "reference":
         return reference_arm(args, world, rank)
     import torch
-    torch.cuda.set_device(local)
+    dev = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev)
     if world > 1:
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL over NVLink on a real multi-GPU box; BENCH_DIST_BACKEND=gloo only for
+        # functional checks of the multi-rank path when fewer GPUs than ranks exist
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            torch.distributed.init_process_group(backend)
     from paper_1901_04289_b200 import build
     if not os.path.exists(build.LIB):
         raise SystemExit("libapb_b200.so missing: run __graft_entry__.build() first")
