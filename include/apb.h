@@ -201,6 +201,19 @@ int apb_matmul_plan_info(const apb_mat* A, const apb_mat* B, int64_t prec, apb_p
 /* End-to-end variants taking HOST ball arrays: host->device copy, kernels,
  * device->host copy inside one call (the drop-in path for callers holding
  * host data). */
+/* poly_mullow_classical (include/apball/poly.hpp:23-24, src/poly.cpp:11-26):
+ * out[k] = sum_i a_i b_{k-i} for k < len as one batch of variable-length fused
+ * ball dots (negative step on b); out needs len slots of >= ceil(prec/64) limbs. */
+int apb_poly_mullow(const apb_balls* a, int64_t alen, const apb_balls* b, int64_t blen, int64_t len,
+                    int64_t prec, apb_balls* out, void* stream);
+/* series_exp_basecase (include/apball/poly.hpp:27-29, src/poly.cpp:28-46):
+ * b_0 = 1, b_k = (sum_{j=1}^{k} (j a_j) b_{k-j}) / k; APB_ERR_INVALID (the
+ * reference's std::domain_error) unless a_0 is an exact zero.  Sequential in k. */
+int apb_series_exp(const apb_balls* a, int64_t alen, int64_t len, int64_t prec, apb_balls* out, void* stream);
+int apb_poly_mullow_host(const apb_balls* a, int64_t alen, const apb_balls* b, int64_t blen, int64_t len,
+                         int64_t prec, apb_balls* out);
+int apb_series_exp_host(const apb_balls* a, int64_t alen, int64_t len, int64_t prec, apb_balls* out);
+
 int apb_dot_batch_host(const apb_balls* x, const apb_balls* y, const apb_balls* initial,
                        int subtract, const apb_dot_index* idx, int64_t n, int64_t batch,
                        int64_t prec, int mode, apb_balls* out);

@@ -17,6 +17,8 @@
 //   matmul_auto         include/apball/matmul.hpp:91
 //   classical_matmul_ball include/apball/matmul.hpp:89
 //   complex_matmul_ball include/apball/matmul.hpp:92-93
+//   poly_mullow_classical include/apball/poly.hpp:23-24  (src/poly.cpp:11-26)
+//   series_exp_basecase include/apball/poly.hpp:27-29    (src/poly.cpp:28-46)
 #pragma once
 
 #include <cstdint>
@@ -29,6 +31,7 @@
 #include "apball/ball.hpp"
 #include "apball/dot.hpp"
 #include "apball/matmul.hpp"
+#include "apball/poly.hpp"
 
 namespace apball::b200 {
 
@@ -106,9 +109,10 @@ inline Ball get(const SoA& s, size_t e) {
     return b;
 }
 
-inline void check(int rc) {
+inline void check(int rc, bool domain = false) {
     if (rc == APB_OK) return;
     std::string msg = apb_last_error();
+    if (domain && rc == APB_ERR_INVALID) throw std::domain_error(msg);
     if (rc == APB_ERR_INVALID) throw std::invalid_argument(msg);
     if (rc == APB_ERR_OVERFLOW) throw std::overflow_error(msg);
     throw std::runtime_error("apb: " + msg);
@@ -207,6 +211,39 @@ inline ComplexBallMatrix complex_matmul_ball(const ComplexBallMatrix& a, const C
     detail::check(apb_matmul_complex_host(&m[0], &m[1], &m[2], &m[3], p, APB_MM_AUTO, &m[4], &m[5]));
     return ComplexBallMatrix::from_parts(detail::unpack_matrix(s[4], a.rows, b.cols),
                                          detail::unpack_matrix(s[5], a.rows, b.cols));
+}
+
+// poly_mullow_classical: one batched launch of variable-length negative-stride dots
+inline BallPoly poly_mullow_classical(const BallPoly& a, const BallPoly& b, std::size_t len, std::int64_t p) {
+    detail::SoA sa, sb, so;
+    std::vector<const Ball*> pa(a.c.size()), pb(b.c.size());
+    for (size_t i = 0; i < a.c.size(); i++) pa[i] = &a.c[i];
+    for (size_t i = 0; i < b.c.size(); i++) pb[i] = &b.c[i];
+    sa.resize(a.c.size() ? a.c.size() : 1, detail::limbs_needed(pa.data(), pa.size()));
+    sb.resize(b.c.size() ? b.c.size() : 1, detail::limbs_needed(pb.data(), pb.size()));
+    for (size_t i = 0; i < a.c.size(); i++) detail::put(sa, i, a.c[i]);
+    for (size_t i = 0; i < b.c.size(); i++) detail::put(sb, i, b.c[i]);
+    so.resize(len ? len : 1, (int32_t)((std::max<std::int64_t>(p, 2) + 63) / 64));
+    apb_balls va = sa.view(), vb = sb.view(), vo = so.view();
+    detail::check(apb_poly_mullow_host(&va, (int64_t)a.c.size(), &vb, (int64_t)b.c.size(), (int64_t)len, p, &vo));
+    BallPoly out = BallPoly::zero(len);
+    for (size_t k = 0; k < len; k++) out.c[k] = detail::get(so, k);
+    return out;
+}
+
+// series_exp_basecase: std::domain_error unless a.c[0] is an exact zero
+inline BallPoly series_exp_basecase(const BallPoly& a, std::size_t len, std::int64_t p) {
+    detail::SoA sa, so;
+    std::vector<const Ball*> pa(a.c.size());
+    for (size_t i = 0; i < a.c.size(); i++) pa[i] = &a.c[i];
+    sa.resize(a.c.size() ? a.c.size() : 1, detail::limbs_needed(pa.data(), pa.size()));
+    for (size_t i = 0; i < a.c.size(); i++) detail::put(sa, i, a.c[i]);
+    so.resize(len ? len : 1, (int32_t)((std::max<std::int64_t>(p, 2) + 63) / 64));
+    apb_balls va = sa.view(), vo = so.view();
+    detail::check(apb_series_exp_host(&va, (int64_t)a.c.size(), (int64_t)len, p, &vo), true);
+    BallPoly out = BallPoly::zero(len);
+    for (size_t k = 0; k < len; k++) out.c[k] = detail::get(so, k);
+    return out;
 }
 
 }  // namespace apball::b200

@@ -1612,3 +1612,147 @@ int orc_matmul_complex(const apb_mat* Are, const apb_mat* Aim, const apb_mat* Br
     for (int q = 0; q < 4; q++) free(p4[q]);
     return g_status;
 }
+
+/* ------------------------------------------------------------ poly */
+/* poly_mullow_classical (src/poly.cpp:11-26): coefficient k is one fused dot
+ * over (a_i, b_{k-i}), i in [max(0, k+1-|b|), min(k, |a|-1)] */
+int orc_poly_mullow(const apb_balls* a, int64_t alen, const apb_balls* b, int64_t blen, int64_t len,
+                    int64_t prec, apb_balls* out) {
+    g_status = APB_OK;
+    init_one();
+    int64_t nmax = alen < blen ? alen : blen;
+    if (nmax < 1) nmax = 1;
+    ball_t* xs = (ball_t*)malloc(sizeof(ball_t) * (size_t)nmax);
+    ball_t* ys = (ball_t*)malloc(sizeof(ball_t) * (size_t)nmax);
+    term_t* terms = (term_t*)malloc(sizeof(term_t) * (size_t)nmax);
+    static of_t mid;
+    for (int64_t k = 0; k < len; k++) {
+        of_t z;
+        ozero(&z);
+        if (alen == 0 || blen == 0) {
+            store_ball(out, k, &z, mzero());
+            continue;
+        }
+        const int64_t i0 = k + 1 > blen ? k + 1 - blen : 0;
+        const int64_t i1 = k < alen - 1 ? k : alen - 1;
+        if (i0 >= alen || i1 < i0) {
+            store_ball(out, k, &z, mzero());
+            continue;
+        }
+        const int64_t n = i1 - i0 + 1;
+        for (int64_t i = 0; i < n; i++) {
+            load_ball(&xs[i], a, i0 + i);
+            load_ball(&ys[i], b, k - i0 - i);
+            terms[i].x = &xs[i];
+            terms[i].y = &ys[i];
+            terms[i].neg = 0;
+        }
+        mag_t rad;
+        dot_core(terms, n, prec, 0, &mid, &rad, NULL, NULL, 0);
+        store_ball(out, k, &mid, rad);
+    }
+    free(xs);
+    free(ys);
+    free(terms);
+    return g_status;
+}
+
+/* apfloat_mul_u64_exact (src/apfloat.cpp:178-186) */
+static void omul_u64_exact(of_t* out, const of_t* x, uint64_t k) {
+    if (x->kind != APB_FINITE) {
+        *out = *x;
+        if (k == 0 && (x->kind == APB_PINF || x->kind == APB_NINF)) out->kind = APB_NAN;
+        return;
+    }
+    if (k == 0) {
+        ozero(out);
+        return;
+    }
+    uint64_t prod[OL];
+    uint64_t cy = 0;
+    for (int i = 0; i < x->n; i++) {
+        const u128 t = (u128)x->d[i] * k + cy;
+        prod[i] = (uint64_t)t;
+        cy = (uint64_t)(t >> 64);
+    }
+    prod[x->n] = cy;
+    onormalize(out, x->neg, checked_exp((i128)x->e + 64), prod, x->n + 1);
+}
+
+/* mag_inv_u64_upper (src/mag.cpp:155-164) */
+static mag_t minv_u64(uint64_t k) {
+    const unsigned len = bitw(k);
+    if ((k & (k - 1)) == 0) return mparts(MAG_ONE >> 1, 2 - (int64_t)len);
+    const u128 num = (u128)1 << (30 - 1 + len);
+    uint64_t q = (uint64_t)(num / k);
+    if (num % k) q++;
+    return mparts(q, 1 - (int64_t)len);
+}
+
+/* ball_div_u64 (src/ball.cpp:38-43) over apfloat_div_u64 (src/apfloat.cpp:308-331) */
+static void ball_div_u64(ball_t* r, const ball_t* x, uint64_t k, int64_t p) {
+    if (x->m.kind == APB_NAN) {
+        set_indeterminate(r);
+        return;
+    }
+    if (p < 2) p = 2;
+    mag_t err = mzero();
+    if (x->m.kind != APB_FINITE) {
+        r->m = x->m;
+    } else {
+        const int n = x->m.n;
+        const int64_t wl = (int64_t)n > p / 64 + 1 ? (int64_t)n : p / 64 + 1;
+        const int w = (int)wl + 1;
+        uint64_t q[OL] = {0};
+        uint64_t rem = 0;
+        for (int i = w - 1; i >= 0; i--) {
+            const uint64_t num = i + n >= w ? x->m.d[i + n - w] : 0;
+            const u128 cur = ((u128)rem << 64) | num;
+            q[i] = (uint64_t)(cur / k);
+            rem = (uint64_t)(cur % k);
+        }
+        onormalize(&r->m, x->m.neg, x->m.e, q, w);
+        err = oround(&r->m, p);
+        if (rem) err = madd(err, mfrom_u64(1, checked_exp((i128)x->m.e - 64 * (i128)w)));
+    }
+    r->r = madd(err, mmul(x->r, minv_u64(k)));
+}
+
+/* series_exp_basecase (src/poly.cpp:28-46); APB_ERR_INVALID for the reference's
+ * std::domain_error on a constant term that is not an exact zero */
+int orc_series_exp(const apb_balls* a, int64_t alen, int64_t len, int64_t prec, apb_balls* out) {
+    g_status = APB_OK;
+    init_one();
+    if (alen > 0 && ((a->kind[0] & APB_KIND_MASK) != APB_ZERO || a->rad_man[0] != 0)) return APB_ERR_INVALID;
+    if (len == 0) return APB_OK;
+    ball_t* b = (ball_t*)malloc(sizeof(ball_t) * (size_t)len);
+    ball_t* ja = (ball_t*)malloc(sizeof(ball_t) * (size_t)len);
+    term_t* terms = (term_t*)malloc(sizeof(term_t) * (size_t)len);
+    for (int64_t j = 0; j < len; j++) {
+        ozero(&ja[j].m);
+        ja[j].r = mzero();
+        if (j >= 1 && j < alen) {
+            static ball_t aj;
+            load_ball(&aj, a, j);
+            omul_u64_exact(&ja[j].m, &aj.m, (uint64_t)j);
+            ja[j].r = mmul(aj.r, mfrom_u64((uint64_t)j, 0));
+        }
+    }
+    b[0] = g_one;
+    for (int64_t k = 1; k < len; k++) {
+        for (int64_t i = 0; i < k; i++) {
+            terms[i].x = &ja[1 + i];
+            terms[i].y = &b[k - 1 - i];
+            terms[i].neg = 0;
+        }
+        static ball_t s;
+        dot_core(terms, k, prec, 0, &s.m, &s.r, NULL, NULL, 0);
+        ball_div_u64(&b[k], &s, (uint64_t)k, prec);
+    }
+    for (int64_t k = 0; k < len; k++) store_ball(out, k, &b[k].m, b[k].r);
+    free(b);
+    free(ja);
+    free(terms);
+    return g_status;
+}
+

@@ -33,6 +33,9 @@ int orc_dot_complex_batch(const apb_balls* xre, const apb_balls* xim, const apb_
                           int64_t batch, int64_t prec, int mode, apb_balls* ore, apb_balls* oim);
 
 /* matmul_auto / block / classical (src/matmul.cpp:442-531) */
+int orc_poly_mullow(const apb_balls* a, int64_t alen, const apb_balls* b, int64_t blen, int64_t len,
+                    int64_t prec, apb_balls* out);
+int orc_series_exp(const apb_balls* a, int64_t alen, int64_t len, int64_t prec, apb_balls* out);
 int orc_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, apb_mat* C,
                int64_t* block_count);
 int orc_matmul_complex(const apb_mat* Are, const apb_mat* Aim, const apb_mat* Bre,

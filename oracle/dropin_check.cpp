@@ -29,6 +29,25 @@ int main() {
     ComplexBallMatrix cc = complex_matmul_ball(ca, cb, 150), cg = b200::complex_matmul_ball(ca, cb, 150);
     for (size_t i = 0; i < cc.a.size(); i++)
         if (!complex_ball_identical(cc.a[i], cg.a[i])) bad++;
+    for (int t = 0; t < 10; t++) {
+        BallPoly pa, pb;
+        for (int i = 0; i < 20 + t; i++) pa.c.push_back(bench::random_ball(rng, 2, -20, 20, 30));
+        for (int i = 0; i < 15; i++) pb.c.push_back(bench::random_ball(rng, 2, -20, 20, 30));
+        BallPoly r = poly_mullow_classical(pa, pb, 40, 128), g = b200::poly_mullow_classical(pa, pb, 40, 128);
+        for (size_t k = 0; k < r.c.size(); k++)
+            if (!ball_identical(r.c[k], g.c[k])) bad++;
+        pa.c[0] = Ball::zero();
+        BallPoly e = series_exp_basecase(pa, 12, 100), eg = b200::series_exp_basecase(pa, 12, 100);
+        for (size_t k = 0; k < e.c.size(); k++)
+            if (!ball_identical(e.c[k], eg.c[k])) bad++;
+    }
+    try {
+        BallPoly one;
+        one.c = {Ball::exact(ApFloat::from_i64(1))};
+        b200::series_exp_basecase(one, 4, 64);
+        bad++;
+    } catch (const std::domain_error&) {
+    }
     std::printf("dropin mismatches: %d\n", bad);
     return bad != 0;
 }

@@ -99,6 +99,41 @@ def matmul_case(name, a, b, M, K, N, prec, algo=1):
     np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
 
 
+def poly_cases():
+    """poly_mullow_classical / series_exp_basecase fixtures from the reference:
+    restated KATs (tests/test_poly.cpp:15-61) and random cases with edge values"""
+    one = ball_from_i64([1, 1])
+    d = {"kind": np.array("poly"), "len": 3, "prec": 64, **pack("a", one), **pack("b", one),
+         **pack("out", po.poly_mullow(one, one, 3, 64))}
+    np.savez_compressed(os.path.join(OUT, "poly_kat_square.npz"), **d)   # :15-25 -> 1, 2, 1
+    x = ball_from_i64([0, 1, 0, 0, 0])
+    d = {"kind": np.array("series"), "len": 5, "prec": 128, **pack("a", x),
+         **pack("out", po.series_exp(x, 5, 128))}
+    np.savez_compressed(os.path.join(OUT, "series_kat_x.npz"), **d)       # :33-48 -> 1/k!
+    z = ball_from_i64([0, 0, 0, 0])
+    d = {"kind": np.array("series"), "len": 4, "prec": 64, **pack("a", z),
+         **pack("out", po.series_exp(z, 4, 64))}
+    np.savez_compressed(os.path.join(OUT, "series_kat_zero.npz"), **d)    # :50-56 -> 1, 0, 0, 0
+    rng = np.random.Generator(np.random.PCG64(20261020))
+    for q, (la, lb, ln, p) in enumerate([(5, 7, 12, 64), (16, 16, 32, 128), (33, 20, 40, 256), (9, 3, 20, 700),
+                                         (40, 40, 80, 128), (1, 1, 3, 30)]):
+        a, _ = gen.edge_dots(rng, 1, la, specials=(q == 2))
+        b, _ = gen.edge_dots(rng, 1, lb, specials=False)
+        d = {"kind": np.array("poly"), "len": ln, "prec": p, **pack("a", a), **pack("b", b),
+             **pack("out", po.poly_mullow(a, b, ln, p))}
+        np.savez_compressed(os.path.join(OUT, f"poly_rand{q}.npz"), **d)
+    for q, (la, ln, p) in enumerate([(6, 10, 64), (12, 12, 128), (20, 30, 256), (4, 16, 1000)]):
+        a, _ = gen.edge_dots(rng, 1, la, specials=False)
+        a.kind[0] = 0
+        a.mant[0] = 0
+        a.exp[0] = 0
+        a.rad_man[0] = 0
+        a.rad_exp[0] = 0
+        d = {"kind": np.array("series"), "len": ln, "prec": p, **pack("a", a),
+             **pack("out", po.series_exp(a, ln, p))}
+        np.savez_compressed(os.path.join(OUT, f"series_rand{q}.npz"), **d)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     # ---- c1 shape (65,536 x N=100 at p=128) at a small batch
@@ -204,4 +239,10 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    import sys
+    os.makedirs(OUT, exist_ok=True)
+    if "--poly" in sys.argv:  # only the poly fixtures (the others stay byte-identical)
+        poly_cases()
+    else:
+        main()
+        poly_cases()

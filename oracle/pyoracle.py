@@ -45,7 +45,7 @@ def ref_lib():
         for name in ("ref_dot_batch", "ref_dot_state", "ref_dot_complex_batch", "ref_matmul",
                      "ref_matmul_complex", "ref_plan_blocks", "ref_block_int_product",
                      "ref_radius_matmul_upper", "ref_dot_contains", "ref_abs_dot_upper",
-                     "ref_run_verify_suite", "ref_ball_addsub"):
+                     "ref_run_verify_suite", "ref_ball_addsub", "ref_poly_mullow", "ref_series_exp"):
             getattr(_ref, name).restype = I
     return _ref
 
@@ -55,7 +55,8 @@ def port_lib():
     if _port is None:
         _port = _load(PORT_SO)
         for name in ("orc_dot_batch", "orc_dot_complex_batch", "orc_matmul", "orc_matmul_complex",
-                     "orc_plan_blocks", "orc_block_int_product", "orc_radius_matmul_upper"):
+                     "orc_plan_blocks", "orc_block_int_product", "orc_radius_matmul_upper",
+                     "orc_poly_mullow", "orc_series_exp"):
             getattr(_port, name).restype = I
     return _port
 
@@ -286,3 +287,40 @@ def matmul_complex_rows(are, aim, bre, bim, rows, K, N, prec, threads=1):
     ad, _ = matmul(sub(are), bim, rows, K, N, prec, which="ref", algo=1, threads=threads)
     bc, _ = matmul(sub(aim), bre, rows, K, N, prec, which="ref", algo=1, threads=threads)
     return ball_addsub(ac, bd, prec, subtract=True), ball_addsub(ad, bc, prec)
+
+
+# ------------------------------------------------------------------- poly
+
+def poly_mullow(a: BallArray, b: BallArray, length: int, prec: int, *, which="ref") -> BallArray:
+    """poly_mullow_classical (src/poly.cpp:11-26) via the reference or the C restatement"""
+    from paper_1901_04289_b200.balls import limbs_for
+    out = BallArray.zeros(max(length, 1), max(limbs_for(prec), 1))
+    ac, bc, oc = a.c(), b.c(), out.c()
+    if which == "ref":
+        lib = ref_lib()
+        rc = lib.ref_poly_mullow(_p(ac), I64(a.count), _p(bc), I64(b.count), I64(length), I64(prec), _p(oc))
+        _check(rc, lib, "ref_poly_mullow")
+    else:
+        rc = port_lib().orc_poly_mullow(_p(ac), I64(a.count), _p(bc), I64(b.count), I64(length), I64(prec),
+                                        _p(oc))
+        _check(rc, None, "orc_poly_mullow")
+    return out.take(range(length)) if length < out.count else out
+
+
+def series_exp(a: BallArray, length: int, prec: int, *, which="ref") -> BallArray:
+    """series_exp_basecase (src/poly.cpp:28-46); raises ValueError (the reference's
+    std::domain_error) when a_0 is not an exact zero"""
+    from paper_1901_04289_b200.balls import limbs_for
+    out = BallArray.zeros(max(length, 1), max(limbs_for(prec), 1))
+    ac, oc = a.c(), out.c()
+    if which == "ref":
+        lib = ref_lib()
+        rc = lib.ref_series_exp(_p(ac), I64(a.count), I64(length), I64(prec), _p(oc))
+    else:
+        lib = port_lib()
+        rc = lib.orc_series_exp(_p(ac), I64(a.count), I64(length), I64(prec), _p(oc))
+    if rc == 1:
+        raise ValueError("series_exp_basecase: constant term must be exactly zero")
+    _check(rc, lib if which == "ref" else None, "series_exp")
+    return out.take(range(length)) if length < out.count else out
+

@@ -26,6 +26,7 @@
 #include "apball/dot.hpp"
 #include "apball/matmul.hpp"
 #include "apball/oracle.hpp"
+#include "apball/poly.hpp"
 #include "apb.h"
 
 using namespace apball;
@@ -114,6 +115,9 @@ int guarded(F&& f) {
     } catch (const std::overflow_error& e) {
         g_err = e.what();
         return APB_ERR_OVERFLOW;
+    } catch (const std::domain_error& e) {  // series_exp_basecase's constant-term check
+        g_err = e.what();
+        return APB_ERR_INVALID;
     } catch (const std::exception& e) {
         g_err = e.what();
         return APB_ERR_UNSUPPORTED;
@@ -489,6 +493,27 @@ int ref_ball_addsub(const apb_balls* x, const apb_balls* y, int subtract, int64_
 }
 
 // the reference's own verify suites (src/bench.cpp:486-731), for pinning
+// poly_mullow_classical / series_exp_basecase (include/apball/poly.hpp:23-29)
+int ref_poly_mullow(const apb_balls* a, int64_t alen, const apb_balls* b, int64_t blen, int64_t len,
+                    int64_t prec, apb_balls* out) {
+    return guarded([&] {
+        BallPoly pa, pb;
+        for (int64_t i = 0; i < alen; i++) pa.c.push_back(load_ball(a, i));
+        for (int64_t i = 0; i < blen; i++) pb.c.push_back(load_ball(b, i));
+        BallPoly r = poly_mullow_classical(pa, pb, size_t(len), prec);
+        for (int64_t k = 0; k < len; k++) store_ball(out, k, r.c[size_t(k)]);
+    });
+}
+
+int ref_series_exp(const apb_balls* a, int64_t alen, int64_t len, int64_t prec, apb_balls* out) {
+    return guarded([&] {
+        BallPoly pa;
+        for (int64_t i = 0; i < alen; i++) pa.c.push_back(load_ball(a, i));
+        BallPoly r = series_exp_basecase(pa, size_t(len), prec);
+        for (int64_t k = 0; k < len; k++) store_ball(out, k, r.c[size_t(k)]);
+    });
+}
+
 int ref_run_verify_suite(const char* name, uint64_t trials, uint64_t seed, uint64_t* failures) {
     return guarded([&] {
         std::string s(name);

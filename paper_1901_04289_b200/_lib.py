@@ -66,6 +66,14 @@ def lib():
     L.apb_dot_batch_host.restype = I
     L.apb_matmul_host.argtypes = [mp, mp, I64, I, mp]
     L.apb_matmul_host.restype = I
+    L.apb_poly_mullow.argtypes = [bp, I64, bp, I64, I64, I64, bp, P]
+    L.apb_poly_mullow.restype = I
+    L.apb_series_exp.argtypes = [bp, I64, I64, I64, bp, P]
+    L.apb_series_exp.restype = I
+    L.apb_poly_mullow_host.argtypes = [bp, I64, bp, I64, I64, I64, bp]
+    L.apb_poly_mullow_host.restype = I
+    L.apb_series_exp_host.argtypes = [bp, I64, I64, I64, bp]
+    L.apb_series_exp_host.restype = I
     L.apb_device_status.argtypes = [P]
     L.apb_device_status.restype = I
     L.apb_matmul_stats_get.restype = C.POINTER(apb_matmul_stats)

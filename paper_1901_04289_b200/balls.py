@@ -133,8 +133,23 @@ class BallArray:
         m[:, L - self.L:] = self.mant
         return BallArray(m, self.exp.copy(), self.kind.copy(), self.rad_man.copy(), self.rad_exp.copy())
 
+    @staticmethod
+    def from_i64(vals) -> "BallArray":
+        """exact balls of small integers (Ball::from_i64, include/apball/ball.hpp:22)"""
+        vals = list(vals)
+        a = BallArray.zeros(len(vals), 1)
+        for k, v in enumerate(vals):
+            if v == 0:
+                continue
+            m = abs(int(v))
+            bl = m.bit_length()
+            a.mant[k, 0] = np.uint64(m << (64 - bl))
+            a.exp[k] = bl
+            a.kind[k] = APB_FINITE | (APB_SIGN if v < 0 else 0)
+        return a
+
     def take(self, idx) -> "BallArray":
-        idx = np.asarray(idx)
+        idx = np.asarray(idx, dtype=np.int64)
         return BallArray(self.mant[idx], self.exp[idx], self.kind[idx], self.rad_man[idx], self.rad_exp[idx])
 
     def concat(self, other: "BallArray") -> "BallArray":

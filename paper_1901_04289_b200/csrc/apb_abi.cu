@@ -211,6 +211,53 @@ int apb_dot_batch(const apb_balls* x, const apb_balls* y, const apb_balls* initi
     return cuda_check(cudaGetLastError(), "apb_dot_batch launch");
 }
 
+int apb_poly_mullow(const apb_balls* a, int64_t alen, const apb_balls* b, int64_t blen, int64_t len,
+                    int64_t prec, apb_balls* out, void* stream) {
+    if (alen < 0 || blen < 0 || len < 0 || !out || !balls_ok(out) || (alen > 0 && (!balls_ok(a) || a->count < alen)) ||
+        (blen > 0 && (!balls_ok(b) || b->count < blen))) {
+        set_error("apb_poly_mullow: invalid arguments");
+        return APB_ERR_INVALID;
+    }
+    if (prec < 2) prec = 2;
+    if (out->L < limbs_for(prec) || out->count < len) {
+        set_error("apb_poly_mullow: output slots too small for prec");
+        return APB_ERR_INVALID;
+    }
+    const apb_balls* aa = alen > 0 ? a : out;
+    const apb_balls* bb = blen > 0 ? b : out;
+    int rc = poly_mullow_launch(aa, alen, bb, blen, len, prec, out, (cudaStream_t)stream);
+    if (rc) return rc;
+    return cuda_check(cudaGetLastError(), "apb_poly_mullow launch");
+}
+
+int apb_series_exp(const apb_balls* a, int64_t alen, int64_t len, int64_t prec, apb_balls* out, void* stream) {
+    if (alen < 0 || len < 0 || !out || !balls_ok(out) || (alen > 0 && (!balls_ok(a) || a->count < alen))) {
+        set_error("apb_series_exp: invalid arguments");
+        return APB_ERR_INVALID;
+    }
+    if (prec < 2) prec = 2;
+    if (out->L < limbs_for(prec) || out->count < len) {
+        set_error("apb_series_exp: output slots too small for prec");
+        return APB_ERR_INVALID;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (alen > 0) {  // the constant term must be an exact zero (src/poly.cpp:29-30: std::domain_error)
+        uint8_t k0 = 0;
+        uint32_t r0 = 0;
+        if (cudaMemcpyAsync(&k0, a->kind, 1, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaMemcpyAsync(&r0, a->rad_man, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return cuda_check(cudaGetLastError(), "apb_series_exp");
+        if ((k0 & APB_KIND_MASK) != APB_ZERO || r0 != 0) {
+            set_error("series_exp_basecase: constant term must be exactly zero");
+            return APB_ERR_INVALID;
+        }
+    }
+    int rc = series_exp_launch(alen > 0 ? a : out, alen, len, prec, out, st);
+    if (rc) return rc;
+    return cuda_check(cudaGetLastError(), "apb_series_exp launch");
+}
+
 int apb_dot_complex_batch(const apb_balls* xre, const apb_balls* xim, const apb_balls* yre,
                           const apb_balls* yim, const apb_dot_index* idx, int64_t n, int64_t batch,
                           int64_t prec, int mode, const apb_dot_tuning* tuning, apb_balls* out_re,
@@ -348,6 +395,31 @@ int apb_matmul_host(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, 
     tk = prof_begin("d2h", st);
     if ((rc = to_host(&dC.b, &C->b, st))) return rc;
     prof_end(tk, st);
+    return apb_device_status(st);
+}
+
+int apb_poly_mullow_host(const apb_balls* a, int64_t alen, const apb_balls* b, int64_t blen, int64_t len,
+                         int64_t prec, apb_balls* out) {
+    cudaStream_t st = host_stream();
+    apb_balls da{}, db{}, dout{};
+    int rc;
+    if (alen > 0 && (rc = to_device(a, &da, 5, st, true))) return rc;
+    if (blen > 0 && (rc = to_device(b, &db, 10, st, true))) return rc;
+    if ((rc = to_device(out, &dout, 0, st, false))) return rc;
+    if ((rc = apb_poly_mullow(alen > 0 ? &da : nullptr, alen, blen > 0 ? &db : nullptr, blen, len, prec, &dout, st)))
+        return rc;
+    if ((rc = to_host(&dout, out, st))) return rc;
+    return apb_device_status(st);
+}
+
+int apb_series_exp_host(const apb_balls* a, int64_t alen, int64_t len, int64_t prec, apb_balls* out) {
+    cudaStream_t st = host_stream();
+    apb_balls da{}, dout{};
+    int rc;
+    if (alen > 0 && (rc = to_device(a, &da, 5, st, true))) return rc;
+    if ((rc = to_device(out, &dout, 0, st, false))) return rc;
+    if ((rc = apb_series_exp(alen > 0 ? &da : nullptr, alen, len, prec, &dout, st))) return rc;
+    if ((rc = to_host(&dout, out, st))) return rc;
     return apb_device_status(st);
 }
 

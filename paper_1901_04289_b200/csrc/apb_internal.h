@@ -38,6 +38,10 @@ int dot_batch_launch(const apb_balls* x, const apb_balls* y, const apb_balls* in
                      int subtract, const apb_dot_index* idx, int64_t n, int64_t batch, int64_t prec,
                      int mode, const apb_dot_tuning* tuning, apb_balls* out, apb_dot_state* state,
                      uint64_t* acc, int64_t acc_stride, cudaStream_t st);
+int poly_mullow_launch(const apb_balls* a, int64_t alen, const apb_balls* b, int64_t blen, int64_t len,
+                       int64_t prec, apb_balls* out, cudaStream_t st);
+int series_exp_launch(const apb_balls* a, int64_t alen, int64_t len, int64_t prec, apb_balls* out,
+                      cudaStream_t st);
 int dot_complex_launch(const apb_balls* xre, const apb_balls* xim, const apb_balls* yre,
                        const apb_balls* yim, const apb_dot_index* idx, int64_t n, int64_t batch,
                        int64_t prec, int mode, apb_balls* ore, apb_balls* oim, cudaStream_t st);

@@ -31,7 +31,9 @@
 //   dot_complex_generic  complex dots (src/dot.cpp:470-568): two accumulators
 //       (re, im) over the 2N-term part views, thread per dot.
 
+#include <algorithm>
 #include <cstdint>
+#include <cstring>
 #include <cstdlib>
 #include <cuda_runtime.h>
 
@@ -58,7 +60,33 @@ struct DotArgs {
     int64_t acc_stride;
     uint8_t* fb_flag;  // per dot: 1 = needs the fallback path
     int* status;
+    // poly_mullow_classical mode (palen > 0): dot k runs over a[i0..i1] and
+    // b[k-i0] downwards (src/poly.cpp:11-26), its length varies with k
+    int64_t palen = 0, pblen = 0;
+    int dpw = 32;  // dots per warp in dot_small_kernel (fewer for small batches)
 };
+
+// element index of term 0, the steps, and the term count of dot b
+APB_DEV void dot_extent(const DotArgs& A, int64_t b, int64_t& ex0, int64_t& xs, int64_t& ey0, int64_t& ys,
+                        int64_t& n) {
+    if (A.palen > 0) {
+        const int64_t i0 = b + 1 > A.pblen ? b + 1 - A.pblen : 0;
+        const int64_t i1 = b < A.palen - 1 ? b : A.palen - 1;
+        n = (i0 >= A.palen || i1 < i0) ? 0 : i1 - i0 + 1;
+        ex0 = i0;
+        xs = 1;
+        ey0 = b - i0;
+        ys = -1;
+        return;
+    }
+    const int64_t bq = A.idx.bdiv == 1 ? b : b / A.idx.bdiv;
+    const int64_t br = A.idx.bdiv == 1 ? 0 : b - bq * A.idx.bdiv;
+    ex0 = A.idx.x_off + bq * A.idx.xs1 + br * A.idx.xs2;
+    ey0 = A.idx.y_off + bq * A.idx.ys1 + br * A.idx.ys2;
+    xs = A.idx.xstep;
+    ys = A.idx.ystep;
+    n = A.n;
+}
 
 APB_DEV int64_t x_elem(const apb_dot_index& ix, int64_t b, int64_t i) {
     return ix.x_off + (b / ix.bdiv) * ix.xs1 + (b % ix.bdiv) * ix.xs2 + i * ix.xstep;
@@ -192,8 +220,9 @@ APB_DEV void load_mant(uint64_t (&m)[L], const BallsView& a, int64_t e) {
 // term i of dot b from precomputed element indices (ex, ey): the metadata always,
 // the mantissas only when `mant` (pass 1 needs them only for e_min)
 template <int L>
-APB_DEV void load_term_at(Term<L>& t, const DotArgs& A, int64_t b, int64_t i, int64_t ex, int64_t ey, bool mant) {
-    if (i < A.n) {
+APB_DEV void load_term_at(Term<L>& t, const DotArgs& A, int64_t b, int64_t i, int64_t ex, int64_t ey, bool mant,
+                          int64_t n) {
+    if (i < n) {
         t.kx = __ldg(A.x.kind + ex);
         t.ky = __ldg(A.y.kind + ey);
         t.ex = __ldg(A.x.exp + ex);
@@ -493,10 +522,9 @@ template <int L, int NS, int TPL>
 __global__ void __launch_bounds__(128, (TPL > 0 ? 3 : 4)) dot_small_kernel(DotArgs A) {
     const int lane = threadIdx.x & 31;
     const int64_t warp_id = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int64_t b0 = warp_id * 32;
+    const int64_t b0 = warp_id * A.dpw;
     if (b0 >= A.batch) return;
-    const int nd = (int)(A.batch - b0 < 32 ? A.batch - b0 : 32);
-    const int64_t total = A.n + (A.has_init ? 1 : 0);
+    const int nd = (int)(A.batch - b0 < A.dpw ? A.batch - b0 : A.dpw);
     const bool with_radius = A.mode == APB_DOT_BALL;
     const bool track_min = A.prec > 128;
 
@@ -506,14 +534,15 @@ __global__ void __launch_bounds__(128, (TPL > 0 ? 3 : 4)) dot_small_kernel(DotAr
     uint64_t my_err = 0, my_srad = 0;
     my_pl.status = 2;
 
-    const int64_t xstep32 = 32 * A.idx.xstep, ystep32 = 32 * A.idx.ystep;
     for (int g = 0; g < nd; g++) {
         const int64_t b = b0 + g;
         // element indices of this lane's first term (index math once per dot)
-        const int64_t bq = A.idx.bdiv == 1 ? b : b / A.idx.bdiv;
-        const int64_t br = A.idx.bdiv == 1 ? 0 : b - bq * A.idx.bdiv;
-        const int64_t ex0 = A.idx.x_off + bq * A.idx.xs1 + br * A.idx.xs2 + lane * A.idx.xstep;
-        const int64_t ey0 = A.idx.y_off + bq * A.idx.ys1 + br * A.idx.ys2 + lane * A.idx.ystep;
+        int64_t ex0, xst, ey0, yst, nb;
+        dot_extent(A, b, ex0, xst, ey0, yst, nb);
+        const int64_t total = nb + (A.has_init ? 1 : 0);
+        ex0 += lane * xst;
+        ey0 += lane * yst;
+        const int64_t xstep32 = 32 * xst, ystep32 = 32 * yst;
         // ---- pass 1: setup scan
         ScanAcc sc{INT64_MIN, INT64_MAX, INT64_MIN, 0, false};
         Term<L> keep[TPL > 0 ? TPL : 1];
@@ -522,7 +551,7 @@ __global__ void __launch_bounds__(128, (TPL > 0 ? 3 : 4)) dot_small_kernel(DotAr
             for (int q = 0; q < (TPL > 0 ? TPL : 1); q++) {
                 int64_t i = lane + 32 * (int64_t)q;
                 if (i < total) {
-                    load_term_at<L>(keep[q], A, b, i, ex0 + q * xstep32, ey0 + q * ystep32, true);
+                    load_term_at<L>(keep[q], A, b, i, ex0 + q * xstep32, ey0 + q * ystep32, true, nb);
                     scan_term<L>(sc, keep[q], track_min, with_radius);
                 }
             }
@@ -530,7 +559,7 @@ __global__ void __launch_bounds__(128, (TPL > 0 ? 3 : 4)) dot_small_kernel(DotAr
             int64_t ex = ex0, ey = ey0;
             for (int64_t i = lane; i < total; i += 32, ex += xstep32, ey += ystep32) {
                 Term<L> t;
-                load_term_at<L>(t, A, b, i, ex, ey, track_min);
+                load_term_at<L>(t, A, b, i, ex, ey, track_min, nb);
                 scan_term<L>(sc, t, track_min, with_radius);
             }
         }
@@ -564,7 +593,7 @@ __global__ void __launch_bounds__(128, (TPL > 0 ? 3 : 4)) dot_small_kernel(DotAr
             int64_t ex = ex0, ey = ey0;
             for (int64_t i = lane; i < total; i += 32, ex += xstep32, ey += ystep32) {
                 Term<L> t;
-                load_term_at<L>(t, A, b, i, ex, ey, true);
+                load_term_at<L>(t, A, b, i, ex, ey, true, nb);
                 do_term(t);
             }
         }
@@ -1165,11 +1194,13 @@ __global__ void __launch_bounds__(128) dot_generic_kernel(DotArgs A, int fallbac
     const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= A.batch) return;
     if (fallback_only && !A.fb_flag[b]) return;
-    const int64_t total = A.n + (A.has_init ? 1 : 0);
+    int64_t ex0, xst, ey0, yst, nb;
+    dot_extent(A, b, ex0, xst, ey0, yst, nb);
+    const int64_t total = nb + (A.has_init ? 1 : 0);
     auto get = [&](int64_t i, GBall& xs, GBall& ys, bool& neg) {
-        if (i < A.n) {
-            gb_load(xs, A.x, x_elem(A.idx, b, i));
-            gb_load(ys, A.y, y_elem(A.idx, b, i));
+        if (i < nb) {
+            gb_load(xs, A.x, ex0 + i * xst);
+            gb_load(ys, A.y, ey0 + i * yst);
             neg = A.subtract != 0;
         } else {
             gb_load(xs, A.init, b);
@@ -1259,8 +1290,8 @@ __global__ void __launch_bounds__(128) dot_complex_generic_kernel(CDotArgs A) {
 
 template <int L, int NS, int TPL>
 static void launch_small(const DotArgs& A, cudaStream_t st) {
-    const int warps = 4;  // each warp: 32 consecutive dots
-    const int64_t nwarps = (A.batch + 31) / 32;
+    const int warps = 4;  // each warp: A.dpw consecutive dots
+    const int64_t nwarps = (A.batch + A.dpw - 1) / A.dpw;
     dim3 grid((unsigned)((nwarps + warps - 1) / warps));
     dot_small_kernel<L, NS, TPL><<<grid, 32 * warps, 0, st>>>(A);
     count_launch();
@@ -1281,6 +1312,7 @@ static int ns_bound(int64_t prec, int64_t total) {
 }
 
 static bool staged_ok(const DotArgs& A) {
+    if (A.palen > 0) return false;  // fixed-length affine indexing only
     auto al = [](const void* p, size_t a) { return ((uintptr_t)p % a) == 0; };
     bool ok = al(A.x.mant, 8) && al(A.x.exp, 8) && al(A.x.rad_exp, 8) && al(A.x.rad_man, 4) &&
               al(A.y.mant, 8) && al(A.y.exp, 8) && al(A.y.rad_exp, 8) && al(A.y.rad_man, 4);
@@ -1322,6 +1354,8 @@ static bool try_small_tpl(const DotArgs& A, int64_t total, cudaStream_t st) {
     return true;
 }
 
+int dot_dispatch(DotArgs& A, int Lin, int64_t total, cudaStream_t st);
+
 int dot_batch_launch(const apb_balls* x, const apb_balls* y, const apb_balls* initial,
                      int subtract, const apb_dot_index* idx, int64_t n, int64_t batch, int64_t prec,
                      int mode, const apb_dot_tuning* tuning, apb_balls* out, apb_dot_state* state,
@@ -1343,13 +1377,26 @@ int dot_batch_launch(const apb_balls* x, const apb_balls* y, const apb_balls* in
     A.state = state;
     A.acc = acc;
     A.acc_stride = acc_stride;
-    Workspace& ws = workspace();
-    A.status = ws.status_dev;
-    A.fb_flag = (uint8_t*)ws.scratch(st, (size_t)batch, 20);
-    cudaMemsetAsync(A.fb_flag, 0, (size_t)batch, st);
     const int64_t total = n + (initial ? 1 : 0);
     int Lin = x->L > y->L ? x->L : y->L;
     if (initial && initial->L > Lin) Lin = initial->L;
+    return dot_dispatch(A, Lin, total, st);
+}
+
+// template dispatch + fallback pass for a prepared DotArgs (total = max terms per dot)
+int dot_dispatch(DotArgs& A, int Lin, int64_t total, cudaStream_t st) {
+    const int64_t batch = A.batch, prec = A.prec;
+    Workspace& ws = workspace();
+    A.status = ws.status_dev;
+    A.fb_flag = (uint8_t*)ws.scratch(st, (size_t)batch, 20);
+    if (!A.fb_flag) {
+        set_error("out of device memory (dot flags)");
+        return APB_ERR_CUDA;
+    }
+    cudaMemsetAsync(A.fb_flag, 0, (size_t)batch, st);
+    // 32 dots per warp once the batch fills >= 8 warps per SM that way; fewer
+    // (down to one) for small batches so every SM gets warps
+    A.dpw = batch >= (int64_t)32 * 148 * 8 ? 32 : (int)std::max<int64_t>(1, batch / (148 * 8));
     const int nsb = ns_bound(prec, total);
     const int tok = prof_begin("dot", st);
     bool small = true;
@@ -1366,6 +1413,183 @@ int dot_batch_launch(const apb_balls* x, const apb_balls* y, const apb_balls* in
     prof_end(tok, st);
     count_launch();
     return APB_OK;
+}
+
+// ------------------------------------------------------------ poly (§8(f) row 2)
+
+// poly_mullow_classical (src/poly.cpp:11-26): output k is one dot over
+// (a_i, b_{k-i}), i in [max(0, k+1-|b|), min(k, |a|-1)], with a negative step on
+// b; all len outputs are one batch of variable-length dots.
+int poly_mullow_launch(const apb_balls* a, int64_t alen, const apb_balls* b, int64_t blen, int64_t len,
+                       int64_t prec, apb_balls* out, cudaStream_t st) {
+    if (len == 0) return APB_OK;
+    DotArgs A;
+    A.x = view_of(a);
+    A.y = view_of(b);
+    A.has_init = false;
+    A.init = view_of(a);
+    A.out = out_of(out);
+    std::memset(&A.idx, 0, sizeof A.idx);
+    A.idx.bdiv = 1;
+    A.palen = alen;
+    A.pblen = blen;
+    const int64_t nmax = alen < blen ? alen : blen;
+    A.n = nmax;
+    A.batch = len;
+    A.prec = prec;
+    A.mode = APB_DOT_BALL;
+    A.subtract = 0;
+    A.disable_reduction = 0;
+    A.state = nullptr;
+    A.acc = nullptr;
+    A.acc_stride = 0;
+    if (alen == 0 || blen == 0) A.palen = -1;  // every output is the exact zero
+    if (A.palen < 0) {
+        A.palen = 1;
+        A.pblen = 0;  // n = 0 for every k
+    }
+    return dot_dispatch(A, a->L > b->L ? a->L : b->L, nmax > 0 ? nmax : 1, st);
+}
+
+// apfloat_mul_u64_exact (src/apfloat.cpp:178-186)
+__device__ void gf_mul_u64_exact(GF& out, const GF& x, uint64_t k, int* status) {
+    if (x.kind != APB_FINITE) {
+        out = x;
+        if (k == 0 && (x.kind == APB_PINF || x.kind == APB_NINF)) out.kind = APB_NAN;
+        return;
+    }
+    if (k == 0) {
+        out.kind = APB_ZERO;
+        out.neg = 0;
+        out.e = 0;
+        out.n = 0;
+        return;
+    }
+    uint64_t prod[GCAP];
+    uint64_t cy = 0;
+    for (int i = 0; i < x.n; i++) {
+        const unsigned __int128 t = (unsigned __int128)x.d[i] * k + cy;
+        prod[i] = (uint64_t)t;
+        cy = (uint64_t)(t >> 64);
+    }
+    prod[x.n] = cy;
+    gf_normalize(out, x.neg, checked_add(x.e, 64, status), prod, x.n + 1, status);
+}
+
+// mag_inv_u64_upper (src/mag.cpp:155-164)
+APB_DEV Mag mag_inv_u64(uint64_t k) {
+    const unsigned len = bitw64(k);
+    if ((k & (k - 1)) == 0) return mag_parts(kMagOne >> 1, 2 - (int64_t)len);
+    const unsigned __int128 num = (unsigned __int128)1 << (30 - 1 + len);
+    uint64_t q = (uint64_t)(num / k);
+    if (num % k) q++;
+    return mag_parts(q, 1 - (int64_t)len);
+}
+
+// ball_div_u64 (src/ball.cpp:38-43) with apfloat_div_u64 (src/apfloat.cpp:308-331)
+__device__ void gb_div_u64(GBall& out, const GBall& x, uint64_t k, int64_t p, int* status) {
+    if (x.m.kind == APB_NAN) {
+        out.m.kind = APB_NAN;
+        out.m.neg = 0;
+        out.m.e = 0;
+        out.m.n = 0;
+        out.r = mag_inf();
+        return;
+    }
+    p = p < 2 ? 2 : p;
+    Mag err = mag_zero();
+    if (x.m.kind != APB_FINITE) {
+        out.m = x.m;
+    } else {
+        const int n = x.m.n;
+        const int64_t wl = (int64_t)n > p / 64 + 1 ? n : p / 64 + 1;
+        const int w = (int)wl + 1;
+        uint64_t q[GCAP];
+        uint64_t rem = 0;
+        for (int i = w - 1; i >= 0; i--) {
+            const uint64_t num = i + n >= w ? x.m.d[i + n - w] : 0ull;
+            const unsigned __int128 cur = ((unsigned __int128)rem << 64) | num;
+            q[i] = (uint64_t)(cur / k);
+            rem = (uint64_t)(cur % k);
+        }
+        gf_normalize(out.m, x.m.neg, x.m.e, q, w, status);
+        err = gf_round(out.m, p, status);
+        if (rem) err = mag_add(err, mag_from_u64(1, checked_add(x.m.e, -64 * (int64_t)w, status)));
+    }
+    out.r = mag_add(err, mag_mul(x.r, mag_inv_u64(k)));
+}
+
+// series_exp_basecase (src/poly.cpp:28-46): b_0 = 1, b_k = (sum_j (j a_j) b_{k-j}) / k.
+// The recurrence is sequential; one thread walks it with the generic fused dot
+// (the same Algorithm 1 restatement as dot_generic_kernel), reading b from the
+// output as it is produced.  ja (j a_j, exact) is staged in `ja` (L_a + 1 limbs).
+__global__ void series_exp_kernel(BallsView a, int64_t alen, int64_t len, int64_t prec, BallsOut out,
+                                  BallsOut ja, BallsOut sdot, int* status) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    GBall x, y, t;
+    // ja[j] = (j a_j exact, mag_mul_up(rad, Mag::from_u64_upper(j))), zero beyond |a|
+    for (int64_t j = 0; j < len; j++) {
+        if (j >= 1 && j < alen) {
+            gb_load(x, a, j);
+            gf_mul_u64_exact(t.m, x.m, (uint64_t)j, status);
+            t.r = mag_mul(x.r, mag_from_u64((uint64_t)j, 0));
+        } else {
+            t.m.kind = APB_ZERO;
+            t.m.neg = 0;
+            t.m.e = 0;
+            t.m.n = 0;
+            t.r = mag_zero();
+        }
+        gf_store(ja, j, t.m, t.r, status);
+    }
+    // b_0 = Ball::from_i64(1)
+    {
+        GFloat<1> one;
+        one.kind = APB_FINITE;
+        one.neg = 0;
+        one.e = 1;
+        one.n = 1;
+        one.d[0] = 1ull << 63;
+        gf_store(out, 0, one, mag_zero(), status);
+    }
+    const BallsView jav{ja.mant, ja.exp, ja.kind, ja.rad_man, ja.rad_exp, ja.L};
+    const BallsView bv{out.mant, out.exp, out.kind, out.rad_man, out.rad_exp, out.L};
+    const BallsView sv{sdot.mant, sdot.exp, sdot.kind, sdot.rad_man, sdot.rad_exp, sdot.L};
+    for (int64_t k = 1; k < len; k++) {
+        auto get = [&](int64_t i, GBall& xs, GBall& ys, bool& neg) {
+            gb_load(xs, jav, 1 + i);
+            gb_load(ys, bv, k - 1 - i);
+            neg = false;
+        };
+        g_dot(get, k, prec, false, false, sdot, 0, nullptr, nullptr, 0, status);
+        gb_load(x, sv, 0);
+        gb_div_u64(t, x, (uint64_t)k, prec, status);
+        gf_store(out, k, t.m, t.r, status);
+    }
+}
+
+int series_exp_launch(const apb_balls* a, int64_t alen, int64_t len, int64_t prec, apb_balls* out,
+                      cudaStream_t st) {
+    if (len == 0) return APB_OK;
+    Workspace& ws = workspace();
+    const int La = a->L + 1, Ls = out->L;
+    const size_t cnt = (size_t)len;
+    // ja (La limbs) and the dot scratch (one ball) in workspace slots 21-29
+    apb_balls ja{(uint64_t*)ws.scratch(st, cnt * La * 8, 21), (int64_t*)ws.scratch(st, cnt * 8, 22),
+                 (uint8_t*)ws.scratch(st, cnt, 23), (uint32_t*)ws.scratch(st, cnt * 4, 24),
+                 (int64_t*)ws.scratch(st, cnt * 8, 25), (int64_t)len, La};
+    apb_balls sd{(uint64_t*)ws.scratch(st, (size_t)Ls * 8, 26), (int64_t*)ws.scratch(st, 8, 27),
+                 (uint8_t*)ws.scratch(st, 1, 28), (uint32_t*)ws.scratch(st, 4, 29),
+                 (int64_t*)ws.scratch(st, 8, 30), 1, Ls};
+    if (!ja.mant || !ja.exp || !ja.kind || !ja.rad_man || !ja.rad_exp || !sd.mant || !sd.exp || !sd.kind ||
+        !sd.rad_man || !sd.rad_exp) {
+        set_error("out of device memory (series scratch)");
+        return APB_ERR_CUDA;
+    }
+    series_exp_kernel<<<1, 32, 0, st>>>(view_of(a), alen, len, prec, out_of(out), out_of(&ja), out_of(&sd),
+                                        ws.status_dev);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "series_exp");
 }
 
 int dot_complex_launch(const apb_balls* xre, const apb_balls* xim, const apb_balls* yre,

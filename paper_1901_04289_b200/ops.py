@@ -103,6 +103,51 @@ def dot_batch_host(x: BallArray, y: BallArray, n: int, batch: int, prec: int, *,
     return out
 
 
+# ------------------------------------------------------ poly consumers (§8(f))
+
+def poly_mullow_classical(a, b, length: int, prec: int, *, stream=None, check=True):
+    """poly_mullow_classical (include/apball/poly.hpp:23-24): coefficients k < length
+    of a*b, each the fused ball dot over (a_i, b_{k-i}) -- one batched launch.
+    Device arrays in, device array out; host BallArrays go through the host entry."""
+    lib = _lib.lib()
+    L = limbs_for(prec)
+    na, nb = a.count, b.count
+    if isinstance(a, BallArray) or isinstance(b, BallArray):
+        out = BallArray.zeros(max(length, 1), L)
+        ac, bc, oc = a.c(), b.c(), out.c()
+        _lib.check(lib.apb_poly_mullow_host(C.byref(ac), na, C.byref(bc), nb, length, prec, C.byref(oc)),
+                   "apb_poly_mullow_host")
+        return out.take(range(length))
+    out = DeviceBallArray.empty(max(length, 1), L)
+    ac, bc, oc = a.c(), b.c(), out.c()
+    st = _stream_ptr(stream)
+    _lib.check(lib.apb_poly_mullow(C.byref(ac), na, C.byref(bc), nb, length, prec, C.byref(oc), st),
+               "apb_poly_mullow")
+    if check:
+        _lib.check(lib.apb_device_status(st), "apb_poly_mullow")
+    return out
+
+
+def series_exp_basecase(a, length: int, prec: int, *, stream=None, check=True):
+    """series_exp_basecase (include/apball/poly.hpp:27-29): b_0 = 1,
+    b_k = (sum_{j=1}^{k} (j a_j) b_{k-j}) / k; raises InvalidArgument (the
+    reference's std::domain_error) unless a_0 is an exact zero."""
+    lib = _lib.lib()
+    L = limbs_for(prec)
+    if isinstance(a, BallArray):
+        out = BallArray.zeros(max(length, 1), L)
+        ac, oc = a.c(), out.c()
+        _lib.check(lib.apb_series_exp_host(C.byref(ac), a.count, length, prec, C.byref(oc)), "apb_series_exp_host")
+        return out.take(range(length))
+    out = DeviceBallArray.empty(max(length, 1), L)
+    ac, oc = a.c(), out.c()
+    st = _stream_ptr(stream)
+    _lib.check(lib.apb_series_exp(C.byref(ac), a.count, length, prec, C.byref(oc), st), "apb_series_exp")
+    if check:
+        _lib.check(lib.apb_device_status(st), "apb_series_exp")
+    return out
+
+
 # ------------------------------------------------- reference-shaped dots
 
 def dot_ball(initial: BallArray | None, subtract: bool, x: BallArray | None, xstep: int,

@@ -97,3 +97,47 @@ def test_kat_reduction():
 def test_reference_verify_suites(suite, trials):
     """the reference's own verify suites pass on the build used as oracle"""
     assert po.run_verify_suite(suite, trials, 7) == 0
+
+
+POLY = files("poly_")
+SERIES = files("series_")
+
+
+@pytest.mark.parametrize("path", POLY, ids=[name(p) for p in POLY])
+@pytest.mark.parametrize("which", ["port", "ref"])
+def test_poly_mullow_golden(path, which):
+    """poly_mullow_classical (src/poly.cpp:11-26) fixtures, incl. the restated
+    tests/test_poly.cpp:15-25 KAT (1+x)^2 = 1 + 2x + x^2"""
+    d = np.load(path)
+    a, b, out = balls(d, "a"), balls(d, "b"), balls(d, "out")
+    got = po.poly_mullow(a, b, int(d["len"]), int(d["prec"]), which=which)
+    assert got.identical(out).all()
+
+
+@pytest.mark.parametrize("path", SERIES, ids=[name(p) for p in SERIES])
+@pytest.mark.parametrize("which", ["port", "ref"])
+def test_series_exp_golden(path, which):
+    """series_exp_basecase (src/poly.cpp:28-46) fixtures, incl. the restated
+    tests/test_poly.cpp:33-56 KATs (exp(x) -> 1/k!, exp(0) -> 1)"""
+    d = np.load(path)
+    a, out = balls(d, "a"), balls(d, "out")
+    got = po.series_exp(a, int(d["len"]), int(d["prec"]), which=which)
+    assert got.identical(out).all()
+
+
+def test_poly_kat_values():
+    """(1+x)^2 = 1 + 2x + x^2 exactly; exp(x) has an exact 1/2 at k=2 (tests/test_poly.cpp:15-48)"""
+    d = np.load(files("poly_kat_square")[0])
+    out = balls(d, "out")
+    assert list(out.exp) == [1, 2, 1] and all(out.rad_man == 0)
+    assert all(out.mant[:, -1] == np.uint64(1 << 63))
+    e = balls(np.load(files("series_kat_x")[0]), "out")
+    assert e.rad_man[2] == 0 and e.exp[2] == 0 and e.mant[2, -1] == np.uint64(1 << 63)  # 1/2
+
+
+@pytest.mark.parametrize("which", ["port", "ref"])
+def test_series_exp_rejects_nonzero_constant(which):
+    """tests/test_poly.cpp:58-62: std::domain_error for a_0 != 0"""
+    from paper_1901_04289_b200.balls import BallArray
+    with pytest.raises(ValueError):
+        po.series_exp(BallArray.from_i64([1]), 4, 64, which=which)
