@@ -214,6 +214,17 @@ int apb_poly_mullow_host(const apb_balls* a, int64_t alen, const apb_balls* b, i
                          int64_t prec, apb_balls* out);
 int apb_series_exp_host(const apb_balls* a, int64_t alen, int64_t len, int64_t prec, apb_balls* out);
 
+/* Text wire format of the reference on HOST ball arrays (src/apfloat.cpp:333-390,
+ * src/mag.cpp:174-197, src/ball.cpp:45-56, src/matmul.cpp:552-570): one
+ * "mid +- rad" line per ball, e.g. "(+,3,8000000000000000) +- (20000000,-60)".
+ * The format calls return the text length (excluding the NUL) and write it when
+ * cap exceeds it; parse returns the number of balls read or -1 (apb_last_error
+ * names the malformed line).  Mantissas must fit the output's L slots. */
+int64_t apb_balls_format(const apb_balls* a, int64_t first, int64_t count, char* buf, int64_t cap);
+int64_t apb_balls_parse(const char* text, int64_t len, apb_balls* out, int64_t count);
+int64_t apb_mat_format(const apb_mat* m, char* buf, int64_t cap);
+int apb_mat_parse(const char* text, int64_t len, apb_mat* out);
+
 int apb_dot_batch_host(const apb_balls* x, const apb_balls* y, const apb_balls* initial,
                        int subtract, const apb_dot_index* idx, int64_t n, int64_t batch,
                        int64_t prec, int mode, apb_balls* out);

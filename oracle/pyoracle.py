@@ -324,3 +324,26 @@ def series_exp(a: BallArray, length: int, prec: int, *, which="ref") -> BallArra
     _check(rc, lib if which == "ref" else None, "series_exp")
     return out.take(range(length)) if length < out.count else out
 
+
+# ------------------------------------------------------------- wire format
+
+def balls_format(a: BallArray) -> str:
+    """Ball::to_string per line, from the reference itself"""
+    lib = ref_lib()
+    lib.ref_balls_format.restype = C.c_int64
+    ac = a.c()
+    n = lib.ref_balls_format(_p(ac), I64(0), I64(a.count), None, I64(0))
+    buf = C.create_string_buffer(n + 1)
+    lib.ref_balls_format(_p(ac), I64(0), I64(a.count), buf, I64(n + 1))
+    return buf.value.decode()
+
+
+def balls_parse(text: str, count: int, L: int) -> BallArray | None:
+    lib = ref_lib()
+    lib.ref_balls_parse.restype = C.c_int64
+    out = BallArray.zeros(count, L)
+    oc = out.c()
+    raw = text.encode()
+    got = lib.ref_balls_parse(raw, I64(len(raw)), _p(oc), I64(count))
+    return out if got == count else None
+

@@ -18,6 +18,7 @@
 #include <exception>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <thread>
 #include <vector>
 
@@ -512,6 +513,31 @@ int ref_series_exp(const apb_balls* a, int64_t alen, int64_t len, int64_t prec, 
         BallPoly r = series_exp_basecase(pa, size_t(len), prec);
         for (int64_t k = 0; k < len; k++) store_ball(out, k, r.c[size_t(k)]);
     });
+}
+
+// Ball::to_string / Ball::parse (src/ball.cpp:45-56): the reference's text form
+int64_t ref_balls_format(const apb_balls* a, int64_t first, int64_t count, char* buf, int64_t cap) {
+    std::string s;
+    for (int64_t i = first; i < first + count; i++) s += load_ball(a, i).to_string() + "\n";
+    const int64_t n = (int64_t)s.size();
+    if (buf && cap > n) {
+        std::memcpy(buf, s.data(), size_t(n));
+        buf[n] = 0;
+    }
+    return n;
+}
+
+int64_t ref_balls_parse(const char* text, int64_t len, apb_balls* out, int64_t count) {
+    std::string_view v(text, size_t(len));
+    int64_t i = 0;
+    while (i < count && !v.empty()) {
+        auto nl = v.find('\n');
+        auto b = Ball::parse(v.substr(0, nl));
+        if (!b) return -1;
+        store_ball(out, i++, *b);
+        v = nl == std::string_view::npos ? std::string_view() : v.substr(nl + 1);
+    }
+    return i;
 }
 
 int ref_run_verify_suite(const char* name, uint64_t trials, uint64_t seed, uint64_t* failures) {

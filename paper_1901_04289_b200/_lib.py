@@ -74,6 +74,14 @@ def lib():
     L.apb_poly_mullow_host.restype = I
     L.apb_series_exp_host.argtypes = [bp, I64, I64, I64, bp]
     L.apb_series_exp_host.restype = I
+    L.apb_balls_format.argtypes = [bp, I64, I64, C.c_char_p, I64]
+    L.apb_balls_format.restype = I64
+    L.apb_balls_parse.argtypes = [C.c_char_p, I64, bp, I64]
+    L.apb_balls_parse.restype = I64
+    L.apb_mat_format.argtypes = [mp, C.c_char_p, I64]
+    L.apb_mat_format.restype = I64
+    L.apb_mat_parse.argtypes = [C.c_char_p, I64, mp]
+    L.apb_mat_parse.restype = I
     L.apb_device_status.argtypes = [P]
     L.apb_device_status.restype = I
     L.apb_matmul_stats_get.restype = C.POINTER(apb_matmul_stats)
@@ -107,3 +115,7 @@ def check(rc: int, what: str = ""):
     if rc == 2:
         raise OverflowErrorApb(rc, f"{what}: {msg}")
     raise ApbError(rc, f"{what}: {msg}")
+
+
+def last_error() -> str:
+    return lib().apb_last_error().decode(errors="replace")

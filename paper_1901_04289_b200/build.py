@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libapb_b200.so")
-SOURCES = ["apb_abi.cu", "dot_kernels.cu", "matmul.cu", "int8_gemm.cu"]
+SOURCES = ["apb_abi.cu", "dot_kernels.cu", "matmul.cu", "int8_gemm.cu", "wire.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -43,7 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     procs = []
     for src in sources():
-        obj = os.path.join(CSRC, os.path.basename(src).replace(".cu", ".o"))
+        obj = os.path.join(CSRC, os.path.splitext(os.path.basename(src))[0] + ".o")
         cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-dc" if False else "-c", src, "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

@@ -148,6 +148,58 @@ def series_exp_basecase(a, length: int, prec: int, *, stream=None, check=True):
     return out
 
 
+# --------------------------------------------------- wire format (§8(f) row 3)
+
+def balls_to_text(a) -> str:
+    """the reference's text form, one "mid +- rad" line per ball (Ball::to_string,
+    src/ball.cpp:45-47); device arrays are copied to the host first"""
+    lib = _lib.lib()
+    h = a.to_host() if isinstance(a, DeviceBallArray) else a
+    hc = h.c()
+    n = lib.apb_balls_format(C.byref(hc), 0, h.count, None, 0)
+    if n < 0:
+        raise _lib.InvalidArgument(1, _lib.last_error())
+    buf = C.create_string_buffer(n + 1)
+    lib.apb_balls_format(C.byref(hc), 0, h.count, buf, n + 1)
+    return buf.value.decode()
+
+
+def balls_from_text(text: str, count: int, L: int) -> BallArray:
+    """inverse of balls_to_text (Ball::parse, src/ball.cpp:49-56); raises
+    InvalidArgument on a malformed line or a mantissa wider than L limbs"""
+    lib = _lib.lib()
+    out = BallArray.zeros(count, L)
+    oc = out.c()
+    raw = text.encode()
+    got = lib.apb_balls_parse(raw, len(raw), C.byref(oc), count)
+    if got != count:
+        raise _lib.InvalidArgument(1, _lib.last_error() if got < 0 else f"only {got} of {count} balls")
+    return out
+
+
+def matrix_to_text(m: BallMatrix) -> str:
+    """write_ball_matrix (src/matmul.cpp:554-557): "rows cols" then the balls"""
+    lib = _lib.lib()
+    h = BallMatrix(m.balls.to_host() if m.on_device else m.balls, m.rows, m.cols)
+    hc = h.c()
+    n = lib.apb_mat_format(C.byref(hc), None, 0)
+    buf = C.create_string_buffer(n + 1)
+    lib.apb_mat_format(C.byref(hc), buf, n + 1)
+    return buf.value.decode()
+
+
+def matrix_from_text(text: str, L: int) -> BallMatrix:
+    """read_ball_matrix (src/matmul.cpp:559-570)"""
+    lib = _lib.lib()
+    head = text.split("\n", 1)[0].split()
+    r, c = int(head[0]), int(head[1])
+    m = BallMatrix(BallArray.zeros(r * c, L), r, c)
+    mc = m.c()
+    raw = text.encode()
+    _lib.check(lib.apb_mat_parse(raw, len(raw), C.byref(mc)), "apb_mat_parse")
+    return m
+
+
 # ------------------------------------------------- reference-shaped dots
 
 def dot_ball(initial: BallArray | None, subtract: bool, x: BallArray | None, xstep: int,
