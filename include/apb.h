@@ -201,6 +201,12 @@ int apb_matmul_plan_info(const apb_mat* A, const apb_mat* B, int64_t prec, apb_p
 /* End-to-end variants taking HOST ball arrays: host->device copy, kernels,
  * device->host copy inside one call (the drop-in path for callers holding
  * host data). */
+/* host-buffer form of apb_dot_complex_batch (H2D, launch, D2H); threeprod_hits
+ * (nullable) is a HOST counter that receives the gate's hit count */
+int apb_dot_complex_batch_host(const apb_balls* xre, const apb_balls* xim, const apb_balls* yre,
+                               const apb_balls* yim, const apb_dot_index* idx, int64_t n, int64_t batch,
+                               int64_t prec, int mode, const apb_dot_tuning* tuning, apb_balls* out_re,
+                               apb_balls* out_im, uint64_t* threeprod_hits);
 /* poly_mullow_classical (include/apball/poly.hpp:23-24, src/poly.cpp:11-26):
  * out[k] = sum_i a_i b_{k-i} for k < len as one batch of variable-length fused
  * ball dots (negative step on b); out needs len slots of >= ceil(prec/64) limbs. */

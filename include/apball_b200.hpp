@@ -12,7 +12,7 @@
 // Replaced interfaces (reference file:line):
 //   dot_ball            include/apball/dot.hpp:73-74   (src/dot.cpp:402-405)
 //   dot_approx          include/apball/dot.hpp:77-78
-//   dot_complex_ball    include/apball/dot.hpp:86-87
+//   dot_complex_ball / dot_complex_approx  include/apball/dot.hpp:86-89
 //   block_matmul_ball   include/apball/matmul.hpp:90   (src/matmul.cpp:453-515)
 //   matmul_auto         include/apball/matmul.hpp:91
 //   classical_matmul_ball include/apball/matmul.hpp:89
@@ -168,6 +168,51 @@ inline Ball dot_ball(const Ball* initial, bool subtract, const Ball* x, std::ptr
 inline ApFloat dot_approx(const Ball* initial, bool subtract, const Ball* x, std::ptrdiff_t xstep,
                           const Ball* y, std::ptrdiff_t ystep, std::size_t n, std::int64_t p) {
     return detail::dot_impl(initial, subtract, x, xstep, y, ystep, n, p, APB_DOT_APPROX).mid;
+}
+
+// dot_complex_ball / dot_complex_approx (dot.hpp:86-89): the reference's
+// dot_tuning() knobs are honoured and dot_threeprod_hits() is advanced by the
+// number of terms passing the three-multiplication gate (src/dot.cpp:494-501)
+inline ComplexBall complex_dot_impl(const ComplexBall* x, std::ptrdiff_t xstep, const ComplexBall* y,
+                                    std::ptrdiff_t ystep, std::size_t n, std::int64_t p, int mode) {
+    std::vector<const Ball*> pxr(n), pxi(n), pyr(n), pyi(n);
+    for (size_t i = 0; i < n; i++) {
+        pxr[i] = &x[(std::ptrdiff_t)i * xstep].re;
+        pxi[i] = &x[(std::ptrdiff_t)i * xstep].im;
+        pyr[i] = &y[(std::ptrdiff_t)i * ystep].re;
+        pyi[i] = &y[(std::ptrdiff_t)i * ystep].im;
+    }
+    const std::vector<const Ball*>* pp[4] = {&pxr, &pxi, &pyr, &pyi};
+    detail::SoA s[4], ore, oim;
+    for (int q = 0; q < 4; q++) {
+        s[q].resize(n ? n : 1, detail::limbs_needed(pp[q]->data(), n));
+        for (size_t i = 0; i < n; i++) detail::put(s[q], i, *(*pp[q])[i]);
+    }
+    const int32_t L = (int32_t)((std::max<std::int64_t>(p, 2) + 63) / 64);
+    ore.resize(1, L);
+    oim.resize(1, L);
+    apb_balls v[4] = {s[0].view(), s[1].view(), s[2].view(), s[3].view()};
+    apb_balls vr = ore.view(), vi = oim.view();
+    apb_dot_index idx{1, 0, (int64_t)n, 0, 1, 0, (int64_t)n, 0, 1};
+    const DotTuning& t = dot_tuning();
+    apb_dot_tuning tun{t.disable_precision_reduction ? 1 : 0, t.force_threeprod ? 1 : 0,
+                       (int64_t)std::min<std::size_t>(t.threeprod_cutoff_limbs, (std::size_t)INT64_MAX)};
+    uint64_t hits = 0;
+    detail::check(apb_dot_complex_batch_host(&v[0], &v[1], &v[2], &v[3], &idx, (int64_t)n, 1, p, mode, &tun, &vr,
+                                             &vi, &hits));
+    dot_threeprod_hits() += hits;
+    return ComplexBall{detail::get(ore, 0), detail::get(oim, 0)};
+}
+
+inline ComplexBall dot_complex_ball(const ComplexBall* x, std::ptrdiff_t xstep, const ComplexBall* y,
+                                    std::ptrdiff_t ystep, std::size_t n, std::int64_t p) {
+    return complex_dot_impl(x, xstep, y, ystep, n, p, APB_DOT_BALL);
+}
+
+inline ApComplex dot_complex_approx(const ComplexBall* x, std::ptrdiff_t xstep, const ComplexBall* y,
+                                    std::ptrdiff_t ystep, std::size_t n, std::int64_t p) {
+    ComplexBall r = complex_dot_impl(x, xstep, y, ystep, n, p, APB_DOT_APPROX);
+    return ApComplex{r.re.mid, r.im.mid};
 }
 
 inline BallMatrix matmul_with(const BallMatrix& a, const BallMatrix& b, std::int64_t p, int algo) {

@@ -41,6 +41,29 @@ int main() {
         for (size_t k = 0; k < e.c.size(); k++)
             if (!ball_identical(e.c[k], eg.c[k])) bad++;
     }
+    {  // complex dots with the rewrite forced: identical results, hits counted
+        DotTuning& tun = dot_tuning();
+        tun.force_threeprod = true;
+        const std::uint64_t h0 = dot_threeprod_hits();
+        std::uint64_t ref_hits = 0, gpu_hits = 0;
+        for (int t = 0; t < 20; t++) {
+            std::vector<ComplexBall> x(9), y(9);
+            for (auto& c : x) c = {Ball::exact(bench::random_apfloat(rng, 3, -80, 80)), Ball::exact(bench::random_apfloat(rng, 3, -80, 80))};
+            for (auto& c : y) c = {Ball::exact(bench::random_apfloat(rng, 3, -80, 80)), Ball::exact(bench::random_apfloat(rng, 3, -80, 80))};
+            const std::uint64_t a0 = dot_threeprod_hits();
+            ComplexBall r = dot_complex_ball(x.data(), 1, y.data(), 1, 9, 1024);
+            const std::uint64_t a1 = dot_threeprod_hits();
+            ComplexBall g = b200::dot_complex_ball(x.data(), 1, y.data(), 1, 9, 1024);
+            const std::uint64_t a2 = dot_threeprod_hits();
+            ref_hits += a1 - a0;
+            gpu_hits += a2 - a1;
+            if (!complex_ball_identical(r, g)) bad++;
+        }
+        tun.force_threeprod = false;
+        if (ref_hits != gpu_hits || ref_hits == 0) bad++;
+        std::printf("threeprod hits ref %llu gpu %llu (start %llu)\n", (unsigned long long)ref_hits,
+                    (unsigned long long)gpu_hits, (unsigned long long)h0);
+    }
     try {
         BallPoly one;
         one.c = {Ball::exact(ApFloat::from_i64(1))};

@@ -125,7 +125,7 @@ def dot_state(x, y, n, batch, prec, *, which="ref", initial=None, subtract=False
 
 
 def dot_complex_batch(xre, xim, yre, yim, n, batch, prec, *, which="ref", mode=0, idx=None,
-                      threads=1, force_threeprod=False):
+                      threads=1, force_threeprod=False, want_hits=False):
     from paper_1901_04289_b200.balls import flat_index, limbs_for
     idx = idx or flat_index(n)
     ore, oim = BallArray.zeros(batch, limbs_for(prec)), BallArray.zeros(batch, limbs_for(prec))
@@ -137,6 +137,8 @@ def dot_complex_batch(xre, xim, yre, yim, n, batch, prec, *, which="ref", mode=0
                                        I64(prec), I(mode), I(force_threeprod), _p(a[4]), _p(a[5]),
                                        _p(hits), I(threads))
         _check(rc, lib, "ref_dot_complex_batch")
+        if want_hits:
+            return ore, oim, int(hits.value)
     else:
         lib = port_lib()
         rc = lib.orc_dot_complex_batch(*[_p(v) for v in a[:4]], _p(idx), I64(n), I64(batch),

@@ -263,6 +263,7 @@ int ref_dot_complex_batch(const apb_balls* xre, const apb_balls* xim, const apb_
                           const apb_balls* yim, const apb_dot_index* ix, int64_t n, int64_t batch,
                           int64_t prec, int mode, int force_threeprod, apb_balls* ore,
                           apb_balls* oim, uint64_t* hits, int threads) {
+    dot_threeprod_hits() = 0;  // thread-local counter of the calling thread (threads == 1 for counts)
     return guarded([&] {
         parallel_for(batch, threads, [&](int64_t lo, int64_t hi) {
             dot_tuning().force_threeprod = force_threeprod != 0;

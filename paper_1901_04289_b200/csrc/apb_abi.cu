@@ -262,8 +262,6 @@ int apb_dot_complex_batch(const apb_balls* xre, const apb_balls* xim, const apb_
                           const apb_balls* yim, const apb_dot_index* idx, int64_t n, int64_t batch,
                           int64_t prec, int mode, const apb_dot_tuning* tuning, apb_balls* out_re,
                           apb_balls* out_im, uint64_t* threeprod_hits, void* stream) {
-    (void)tuning;
-    (void)threeprod_hits;
     if (batch < 0 || n < 0 || !idx || !balls_ok(out_re) || !balls_ok(out_im) || idx->bdiv < 1) {
         set_error("apb_dot_complex_batch: invalid arguments");
         return APB_ERR_INVALID;
@@ -282,7 +280,7 @@ int apb_dot_complex_batch(const apb_balls* xre, const apb_balls* xim, const apb_
     const apb_balls* c = n > 0 ? yre : out_re;
     const apb_balls* d = n > 0 ? yim : out_re;
     int rc = dot_complex_launch(a, b, c, d, idx, n, batch, prec, mode, out_re, out_im,
-                                (cudaStream_t)stream);
+                                (cudaStream_t)stream, tuning, threeprod_hits);
     if (rc) return rc;
     return cuda_check(cudaGetLastError(), "apb_dot_complex_batch launch");
 }
@@ -395,6 +393,37 @@ int apb_matmul_host(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, 
     tk = prof_begin("d2h", st);
     if ((rc = to_host(&dC.b, &C->b, st))) return rc;
     prof_end(tk, st);
+    return apb_device_status(st);
+}
+
+int apb_dot_complex_batch_host(const apb_balls* xre, const apb_balls* xim, const apb_balls* yre,
+                               const apb_balls* yim, const apb_dot_index* idx, int64_t n, int64_t batch,
+                               int64_t prec, int mode, const apb_dot_tuning* tuning, apb_balls* out_re,
+                               apb_balls* out_im, uint64_t* threeprod_hits) {
+    cudaStream_t st = host_stream();
+    apb_balls d[6] = {};
+    const apb_balls* h[4] = {xre, xim, yre, yim};
+    int rc;
+    if (n > 0)
+        for (int q = 0; q < 4; q++)  // workspace slots 32..51
+            if ((rc = to_device(h[q], &d[q], 32 + 5 * q, st, true))) return rc;
+    apb_balls hre = *out_re, him = *out_im;
+    hre.count = him.count = batch;
+    if ((rc = to_device(&hre, &d[4], 0, st, false))) return rc;
+    if ((rc = to_device(&him, &d[5], 52, st, false))) return rc;
+    uint64_t* dh = nullptr;
+    if (threeprod_hits) {
+        dh = (uint64_t*)workspace().scratch(st, 8, 57);
+        if (!dh) return APB_ERR_CUDA;
+        cudaMemsetAsync(dh, 0, 8, st);
+    }
+    if ((rc = apb_dot_complex_batch(n > 0 ? &d[0] : nullptr, n > 0 ? &d[1] : nullptr, n > 0 ? &d[2] : nullptr,
+                                    n > 0 ? &d[3] : nullptr, idx, n, batch, prec, mode, tuning, &d[4], &d[5], dh,
+                                    st)))
+        return rc;
+    if ((rc = to_host(&d[4], &hre, st))) return rc;
+    if ((rc = to_host(&d[5], &him, st))) return rc;
+    if (dh) cudaMemcpyAsync(threeprod_hits, dh, 8, cudaMemcpyDeviceToHost, st);
     return apb_device_status(st);
 }
 

@@ -44,7 +44,8 @@ int series_exp_launch(const apb_balls* a, int64_t alen, int64_t len, int64_t pre
                       cudaStream_t st);
 int dot_complex_launch(const apb_balls* xre, const apb_balls* xim, const apb_balls* yre,
                        const apb_balls* yim, const apb_dot_index* idx, int64_t n, int64_t batch,
-                       int64_t prec, int mode, apb_balls* ore, apb_balls* oim, cudaStream_t st);
+                       int64_t prec, int mode, apb_balls* ore, apb_balls* oim, cudaStream_t st,
+                       const apb_dot_tuning* tuning = nullptr, uint64_t* hits = nullptr);
 
 // matmul launchers (matmul.cu)
 int matmul_launch(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, apb_mat* C,

@@ -1222,7 +1222,115 @@ struct CDotArgs {
     int64_t n, batch, prec;
     int mode;
     int* status;
+    unsigned long long* hits;  // dot_threeprod_hits (nullable)
+    int force_threeprod;
+    int64_t threeprod_cutoff;
 };
+
+// ---- exactness gate of the three-multiplication rewrite (src/dot.cpp:427-458).
+// The rewrite is result-neutral by construction (both routes exact), so the
+// device always evaluates the four-product form; the gate is evaluated only to
+// count its hits like dot_threeprod_hits() (include/apball/dot.hpp:54).
+APB_DEV int64_t gf_bottom(const GF& x) { return x.e - (64 * (int64_t)x.n - (int64_t)ctz64(x.d[0])); }
+
+APB_DEV bool window_fits(const Plan& pl, int64_t top, int64_t bottom) {
+    return top <= pl.e_s && bottom >= pl.e_s - 64 * (int64_t)pl.n_s;
+}
+
+// apfloat_add_exact (src/apfloat.cpp:272-306); false when the exact sum needs
+// more than max_limbs limbs (or more than GCAP here)
+__device__ bool gf_add_exact(GF& out, const GF& a, const GF& b, int max_limbs, int* status) {
+    if (a.kind != APB_FINITE && a.kind != APB_ZERO) return false;
+    if (b.kind != APB_FINITE && b.kind != APB_ZERO) return false;
+    if (a.kind == APB_ZERO) return out = b, true;
+    if (b.kind == APB_ZERO) return out = a, true;
+    const int64_t e_top = (a.e > b.e ? a.e : b.e) + 1;
+    const __int128 bot_a = (__int128)a.e - 64 * (int64_t)a.n, bot_b = (__int128)b.e - 64 * (int64_t)b.n;
+    const __int128 span = (__int128)e_top - (bot_a < bot_b ? bot_a : bot_b);
+    const __int128 k128 = (span + 63) / 64;
+    if (k128 > max_limbs || k128 + 1 > GCAP) return false;
+    const int k = (int)k128;
+    const int64_t win_bot = checked_add(e_top, -64 * (int64_t)k, status);
+    uint64_t A[GCAP], Bv[GCAP], S[GCAP];
+    for (int i = 0; i <= k; i++) A[i] = Bv[i] = 0;
+    // place |x| * 2^-win_bot (exact here: every bit lies inside the window)
+    auto place = [&](uint64_t* dst, const GF& x) {
+        const int64_t sh = x.e - 64 * (int64_t)x.n - win_bot;  // >= 0
+        const int64_t wq = sh >> 6;
+        const int bo = (int)(sh & 63);
+        for (int i = 0; i < x.n; i++) {
+            const int64_t w = wq + i;
+            dst[w] |= x.d[i] << bo;
+            if (bo && w + 1 <= k) dst[w + 1] |= x.d[i] >> (64 - bo);
+        }
+    };
+    place(A, a);
+    place(Bv, b);
+    bool sign;
+    auto sub = [&](const uint64_t* X, const uint64_t* Y) {
+        uint64_t bw = 0;
+        for (int i = 0; i <= k; i++) {
+            const uint64_t x = X[i], y = Y[i];
+            S[i] = x - y - bw;
+            bw = (x < y) || (x == y && bw);
+        }
+    };
+    if (a.neg == b.neg) {
+        uint64_t c = 0;
+        for (int i = 0; i <= k; i++) {
+            const uint64_t s1 = A[i] + Bv[i];
+            const uint64_t c1 = s1 < A[i];
+            const uint64_t s2 = s1 + c;
+            c = c1 | (s2 < s1);
+            S[i] = s2;
+        }
+        sign = a.neg;
+    } else {
+        int cmp = 0;
+        for (int i = k; i >= 0 && !cmp; i--) cmp = A[i] > Bv[i] ? 1 : (A[i] < Bv[i] ? -1 : 0);
+        if (cmp >= 0) {
+            sub(A, Bv);
+            sign = a.neg;
+        } else {
+            sub(Bv, A);
+            sign = b.neg;
+        }
+    }
+    gf_normalize(out, sign ? 1 : 0, checked_add(win_bot, 64 * (int64_t)(k + 1), status), S, k + 1, status);
+    return true;
+}
+
+__device__ bool threeprod_gate(const Plan& pre, const Plan& pim, const GF& a, const GF& b, const GF& c,
+                               const GF& d, bool force, int64_t cutoff, int* status) {
+    if (a.kind == APB_ZERO || b.kind == APB_ZERO || c.kind == APB_ZERO || d.kind == APB_ZERO) return false;
+    if (!force) {
+        if ((a.n < b.n ? a.n : b.n) < cutoff) return false;
+        if ((c.n < d.n ? c.n : d.n) < cutoff) return false;
+    }
+    const int64_t ba = gf_bottom(a), bb = gf_bottom(b), bc = gf_bottom(c), bd = gf_bottom(d);
+    // four-route products stay inside their windows; rewrite terms likewise
+    if (!window_fits(pre, a.e + c.e, ba + bc)) return false;
+    if (!window_fits(pre, b.e + d.e, bb + bd)) return false;
+    if (!window_fits(pim, a.e + d.e, ba + bd)) return false;
+    if (!window_fits(pim, b.e + c.e, bb + bc)) return false;
+    if (!window_fits(pim, a.e + c.e, ba + bc)) return false;
+    if (!window_fits(pim, b.e + d.e, bb + bd)) return false;
+    const int cap = a.n + b.n + c.n + d.n + 8;
+    GF sab, scd;
+    if (!gf_add_exact(sab, a, b, cap, status)) return false;
+    if (!gf_add_exact(scd, c, d, cap, status)) return false;
+    if (sab.kind == APB_ZERO || scd.kind == APB_ZERO) return true;  // e = 0 fits trivially
+    // e = (a+b)(c+d): bottom = sum of bottoms exactly; top is e_ab + e_cd or one less
+    const int64_t ebot = gf_bottom(sab) + gf_bottom(scd);
+    if (sab.n + scd.n <= GCAP) {
+        GF e;
+        gf_mul_exact(e, sab, scd, status);
+        return window_fits(pim, e.e, gf_bottom(e));
+    }
+    const int64_t etop_hi = sab.e + scd.e;
+    if (window_fits(pim, etop_hi, ebot)) return true;
+    return false;  // (only the exact top could still fit: conservatively counted as a miss)
+}
 
 __global__ void __launch_bounds__(128) dot_complex_generic_kernel(CDotArgs A) {
     const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1281,6 +1389,21 @@ __global__ void __launch_bounds__(128) dot_complex_generic_kernel(CDotArgs A) {
         gf_store(A.ore, b, are.m, approx ? mag_zero() : are.r, A.status);
         gf_store(A.oim, b, aim.m, approx ? mag_zero() : aim.r, A.status);
         return;
+    }
+    if (A.hits && pre.status == 0 && pim.status == 0) {  // complex_core's try_rewrite (src/dot.cpp:489-501)
+        unsigned long long h = 0;
+        GBall ga, gbb, gc, gd;
+        for (int64_t j = 0; j < A.n; j++) {
+            const int64_t ex = x_elem(A.idx, b, j), ey = y_elem(A.idx, b, j);
+            gb_load(ga, A.xre, ex);
+            gb_load(gbb, A.xim, ex);
+            gb_load(gc, A.yre, ey);
+            gb_load(gd, A.yim, ey);
+            if (threeprod_gate(pre, pim, ga.m, gbb.m, gc.m, gd.m, A.force_threeprod != 0, A.threeprod_cutoff,
+                               A.status))
+                h++;
+        }
+        if (h) atomicAdd(A.hits, h);
     }
     g_dot(get_re, 2 * A.n, A.prec, approx, false, A.ore, b, nullptr, nullptr, 0, A.status);
     g_dot(get_im, 2 * A.n, A.prec, approx, false, A.oim, b, nullptr, nullptr, 0, A.status);
@@ -1594,7 +1717,8 @@ int series_exp_launch(const apb_balls* a, int64_t alen, int64_t len, int64_t pre
 
 int dot_complex_launch(const apb_balls* xre, const apb_balls* xim, const apb_balls* yre,
                        const apb_balls* yim, const apb_dot_index* idx, int64_t n, int64_t batch,
-                       int64_t prec, int mode, apb_balls* ore, apb_balls* oim, cudaStream_t st) {
+                       int64_t prec, int mode, apb_balls* ore, apb_balls* oim, cudaStream_t st,
+                       const apb_dot_tuning* tuning, uint64_t* hits) {
     if (batch == 0) return APB_OK;
     CDotArgs A;
     A.xre = view_of(xre);
@@ -1609,6 +1733,9 @@ int dot_complex_launch(const apb_balls* xre, const apb_balls* xim, const apb_bal
     A.prec = prec;
     A.mode = mode;
     A.status = workspace().status_dev;
+    A.hits = (unsigned long long*)hits;
+    A.force_threeprod = tuning ? tuning->force_threeprod : 0;
+    A.threeprod_cutoff = tuning && tuning->threeprod_cutoff_limbs > 0 ? tuning->threeprod_cutoff_limbs : 128;
     const unsigned t = 128;
     dot_complex_generic_kernel<<<(unsigned)((batch + t - 1) / t), t, 0, st>>>(A);
     count_launch();

@@ -72,18 +72,27 @@ def dot_batch(x: DeviceBallArray, y: DeviceBallArray, n: int, batch: int, prec: 
 
 
 def dot_complex_batch(xre, xim, yre, yim, n: int, batch: int, prec: int, *, mode="ball",
-                      index=None, stream=None, check=True):
+                      index=None, stream=None, check=True, force_threeprod=False, threeprod_cutoff=128,
+                      want_hits=False):
+    """dot_complex_ball / dot_complex_approx over a batch (include/apball/dot.hpp:86-89).
+    want_hits also returns the number of terms passing the three-multiplication
+    gate (dot_threeprod_hits, dot.hpp:54; the rewrite itself is result-neutral)."""
+    import torch
     lib = _lib.lib()
     index = index or flat_index(n)
     ore, oim = DeviceBallArray.empty(batch, limbs_for(prec)), DeviceBallArray.empty(batch, limbs_for(prec))
     cs = [v.c() for v in (xre, xim, yre, yim, ore, oim)]
     st = _stream_ptr(stream)
+    tun = apb_dot_tuning(0, int(bool(force_threeprod)), int(threeprod_cutoff))
+    hits = torch.zeros(1, dtype=torch.int64, device="cuda") if want_hits else None
     rc = lib.apb_dot_complex_batch(*[C.byref(v) for v in cs[:4]], C.byref(index), n, batch, prec,
-                                   APB_DOT_APPROX if mode == "approx" else APB_DOT_BALL, None,
-                                   C.byref(cs[4]), C.byref(cs[5]), None, st)
+                                   APB_DOT_APPROX if mode == "approx" else APB_DOT_BALL, C.byref(tun),
+                                   C.byref(cs[4]), C.byref(cs[5]), hits.data_ptr() if want_hits else None, st)
     _lib.check(rc, "apb_dot_complex_batch")
-    if check:
+    if check or want_hits:
         _lib.check(lib.apb_device_status(st), "apb_dot_complex_batch")
+    if want_hits:
+        return ore, oim, int(hits.item())
     return ore, oim
 
 

@@ -130,3 +130,23 @@ def test_dot_kernel_variants(hook):
                         "test_dot_golden_gpu or test_edge_random or test_host_entry",
                         os.path.abspath(__file__)], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:]
+
+
+@pytest.mark.parametrize("force,bits,p", [(True, 192, 1024), (True, 128, 2048), (True, 64, 256),
+                                          (False, 192, 1024), (True, 192, 64)])
+def test_complex_threeprod_hits_vs_reference(force, bits, p):
+    """dot_threeprod_hits (include/apball/dot.hpp:54) counted like the reference's
+    gate (src/dot.cpp:427-458), on the inputs of its verify suite (exact values,
+    <= 3 limbs, exponents in [-80, 80], src/bench.cpp:587-625); the outputs equal
+    the reference's (rewritten) results -- the rewrite is unobservable"""
+    from paper_1901_04289_b200 import ops
+    rng = np.random.Generator(np.random.PCG64(100 + bits + p))
+    n, batch = 12, 64
+    parts = [gen.random_balls(rng, n * batch, bits, e_lo=-80, e_hi=80) for _ in range(4)]
+    ore, oim, hits = ops.dot_complex_batch(*[q.to_device() for q in parts], n, batch, p,
+                                           force_threeprod=force, want_hits=True)
+    rre, rim, rhits = po.dot_complex_batch(*parts, n, batch, p, force_threeprod=force, want_hits=True)
+    assert ore.to_host().identical(rre).all() and oim.to_host().identical(rim).all()
+    assert hits == rhits
+    if force and p >= 1024:
+        assert hits > 0
