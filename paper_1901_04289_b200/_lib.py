@@ -12,7 +12,7 @@ from .balls import (apb_balls, apb_dot_index, apb_dot_state, apb_dot_tuning, apb
                     apb_matmul_stats, apb_plan_info)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libapb_b200.so")
+LIB_PATH = os.environ.get("APB_LIB_PATH") or os.path.join(HERE, "libapb_b200.so")  # override: tuning variants
 
 _lib = None
 

@@ -64,6 +64,7 @@ struct DotArgs {
     // b[k-i0] downwards (src/poly.cpp:11-26), its length varies with k
     int64_t palen = 0, pblen = 0;
     int dpw = 32;  // dots per warp in dot_small_kernel (fewer for small batches)
+    bool mant16 = false;  // x and y both 2-limb with 16-byte aligned mantissa arrays
 };
 
 // element index of term 0, the steps, and the term count of dot b
@@ -647,6 +648,221 @@ __global__ void __launch_bounds__(128, (TPL > 0 ? 3 : 4)) dot_small_kernel(DotAr
     }
 }
 
+// ------------------------------------------------- lane-group kernel
+// TPD lanes per dot (TPD < 32): a warp runs 32/TPD dots side by side, each
+// group of TPD lanes striding over its dot's terms (lane `sub` takes terms
+// sub, sub+TPD, ...), so a length-100 dot keeps every lane busy and the carry
+// reduction needs log2(TPD) shuffle rounds instead of five.  A warp owns A.dpw
+// dots (a multiple of 32/TPD, <= 32) processed in rounds; after each round the
+// reduced state of dot g is parked in lane g, and the finalizes run on all
+// lanes at the end.  Pass 2 prefetches the next term of the lane while the
+// current one is accumulated.  Same arithmetic as dot_small_kernel.
+// x.y term at element indices (ex, ey) of the operand arrays (no initial-value case)
+template <int L>
+APB_DEV void load_xy(Term<L>& t, const DotArgs& A, int64_t ex, int64_t ey, bool mant, bool neg) {
+    t.kx = __ldg(A.x.kind + ex);
+    t.ky = __ldg(A.y.kind + ey);
+    t.ex = __ldg(A.x.exp + ex);
+    t.ey = __ldg(A.y.exp + ey);
+    t.rx = __ldg(A.x.rad_man + ex);
+    t.ry = __ldg(A.y.rad_man + ey);
+    t.fx = __ldg(A.x.rad_exp + ex);
+    t.fy = __ldg(A.y.rad_exp + ey);
+    if (mant) {
+        if (L == 2 && A.mant16) {  // both operands 2-limb and 16-byte aligned: one vector load each
+            const ulonglong2 vx = __ldg(reinterpret_cast<const ulonglong2*>(A.x.mant) + ex);
+            const ulonglong2 vy = __ldg(reinterpret_cast<const ulonglong2*>(A.y.mant) + ey);
+            t.xm[0] = vx.x;
+            t.xm[L - 1] = vx.y;
+            t.ym[0] = vy.x;
+            t.ym[L - 1] = vy.y;
+        } else {
+            load_mant<L>(t.xm, A.x, ex);
+            load_mant<L>(t.ym, A.y, ey);
+        }
+    }
+    t.neg = neg;
+}
+
+template <int L, int NS>
+APB_DEV void grp_term(Acc<L, NS>& acc, const Term<L>& t, const Plan& pl, bool with_radius) {
+    const bool xz = (t.kx & APB_KIND_MASK) == APB_ZERO, yz = (t.ky & APB_KIND_MASK) == APB_ZERO;
+    if (!xz && !yz) acc_term<L, NS>(acc, t, pl);
+    if (with_radius) rad_term<L, NS>(acc, t, pl);
+}
+
+template <int L, int NS, int TPD>
+#ifndef APB_GRP_MINB
+#define APB_GRP_MINB 3  // measured on config 1: 3 blocks + one-term prefetch beat 4 and 6 without
+#endif
+__global__ void __launch_bounds__(128, APB_GRP_MINB) dot_grp_kernel(DotArgs A) {
+    constexpr int DPR = 32 / TPD;
+    constexpr int PK = NS + 7;  // parked words per dot: s[NS], err, srad, e_max, e_min, e_rad, nnz, fb
+    __shared__ uint64_t park[4][32][PK];
+    const int lane = threadIdx.x & 31, sub = lane % TPD, grp = lane / TPD, wl = threadIdx.x >> 5;
+    const int64_t warp_id = (int64_t)blockIdx.x * (blockDim.x >> 5) + wl;
+    const int64_t b0 = warp_id * A.dpw;
+    if (b0 >= A.batch) return;
+    const int nd = (int)(A.batch - b0 < A.dpw ? A.batch - b0 : A.dpw);
+    const int rounds = (nd + DPR - 1) / DPR;
+    const bool with_radius = A.mode == APB_DOT_BALL;
+    const bool track_min = A.prec > 128;
+    const bool neg = A.subtract != 0;
+
+    for (int r = 0; r < rounds; r++) {
+        const int gi = r * DPR + grp;
+        const bool live = gi < nd;
+        const int64_t b = b0 + gi;
+        int64_t ex0 = 0, xst = 0, ey0 = 0, yst = 0, nb = 0;
+        if (live) dot_extent(A, b, ex0, xst, ey0, yst, nb);
+        const int64_t total = live ? nb + (A.has_init ? 1 : 0) : 0;
+        const bool init_lane = live && A.has_init && sub == 0;
+        ex0 += sub * xst;
+        ey0 += sub * yst;
+        const int64_t xstp = TPD * xst, ystp = TPD * yst;
+        // ---- pass 1: setup scan (metadata only unless e_min is tracked)
+        ScanAcc sc{INT64_MIN, INT64_MAX, INT64_MIN, 0, false};
+        {
+            constexpr int SB = 2;  // terms per lane with loads in flight together
+            int64_t ex = ex0, ey = ey0;
+            for (int64_t i0 = sub; i0 < nb; i0 += SB * TPD, ex += SB * xstp, ey += SB * ystp) {
+                Term<L> t[SB];
+#pragma unroll
+                for (int q = 0; q < SB; q++)
+                    if (i0 + q * TPD < nb) load_xy<L>(t[q], A, ex + q * xstp, ey + q * ystp, track_min, neg);
+#pragma unroll
+                for (int q = 0; q < SB; q++)
+                    if (i0 + q * TPD < nb) scan_term<L>(sc, t[q], track_min, with_radius);
+            }
+            if (init_lane) {
+                Term<L> t;
+                load_term_at<L>(t, A, b, nb, 0, 0, true, nb);
+                scan_term<L>(sc, t, track_min, with_radius);
+            }
+        }
+#pragma unroll
+        for (int o = TPD / 2; o; o >>= 1) {
+            int64_t v = __shfl_xor_sync(0xffffffffu, sc.e_max, o);
+            sc.e_max = v > sc.e_max ? v : sc.e_max;
+            v = __shfl_xor_sync(0xffffffffu, sc.e_min, o);
+            sc.e_min = v < sc.e_min ? v : sc.e_min;
+            v = __shfl_xor_sync(0xffffffffu, sc.e_rad, o);
+            sc.e_rad = v > sc.e_rad ? v : sc.e_rad;
+            sc.nnz += __shfl_xor_sync(0xffffffffu, sc.nnz, o);
+            sc.fb |= __shfl_xor_sync(0xffffffffu, (int)sc.fb, o) != 0;
+        }
+        const Plan pl = finish_plan(sc.e_max, sc.e_min, sc.e_rad, sc.nnz, sc.fb, total, A.prec, A.disable_reduction);
+
+        // ---- pass 2: accumulate (the group's plan is uniform across its lanes)
+        Acc<L, NS> acc;
+#pragma unroll
+        for (int j = 0; j < NS; j++) acc.s[j] = 0;
+        acc.err = 0;
+        acc.srad = 0;
+        if (live && pl.status == 0) {
+            int64_t ex = ex0, ey = ey0;
+            Term<L> cur;
+#ifndef APB_GRP_PREFETCH
+#define APB_GRP_PREFETCH 1
+#endif
+#if APB_GRP_PREFETCH == 2
+            Term<L> cur1;
+            if (sub < nb) load_xy<L>(cur, A, ex, ey, true, neg);
+            if (sub + TPD < nb) load_xy<L>(cur1, A, ex + xstp, ey + ystp, true, neg);
+            ex += 2 * xstp;
+            ey += 2 * ystp;
+            for (int64_t i = sub; i < nb; i += TPD, ex += xstp, ey += ystp) {
+                Term<L> nxt;
+                if (i + 2 * TPD < nb) load_xy<L>(nxt, A, ex, ey, true, neg);
+                grp_term<L, NS>(acc, cur, pl, with_radius);
+                cur = cur1;
+                cur1 = nxt;
+            }
+#elif APB_GRP_PREFETCH
+            if (sub < nb) load_xy<L>(cur, A, ex, ey, true, neg);
+            for (int64_t i = sub; i < nb; i += TPD) {
+                ex += xstp;
+                ey += ystp;
+                Term<L> nxt;
+                if (i + TPD < nb) load_xy<L>(nxt, A, ex, ey, true, neg);
+                grp_term<L, NS>(acc, cur, pl, with_radius);
+                cur = nxt;
+            }
+#else
+            for (int64_t i = sub; i < nb; i += TPD, ex += xstp, ey += ystp) {
+                load_xy<L>(cur, A, ex, ey, true, neg);
+                grp_term<L, NS>(acc, cur, pl, with_radius);
+            }
+#endif
+            if (init_lane) {
+                load_term_at<L>(cur, A, b, nb, 0, 0, true, nb);
+                grp_term<L, NS>(acc, cur, pl, with_radius);
+            }
+        }
+        // ---- group reduction of (s, err, srad) mod 2^(64 NS)
+#pragma unroll
+        for (int o = TPD / 2; o; o >>= 1) {
+            uint64_t c = 0;
+#pragma unroll
+            for (int j = 0; j < NS; j++) {
+                const uint64_t v = __shfl_xor_sync(0xffffffffu, acc.s[j], o);
+                const uint64_t s1 = acc.s[j] + v;
+                const uint64_t c1 = s1 < v;
+                const uint64_t s2 = s1 + c;
+                acc.s[j] = s2;
+                c = c1 | (s2 < c);
+            }
+            acc.err += __shfl_xor_sync(0xffffffffu, acc.err, o);
+            acc.srad += __shfl_xor_sync(0xffffffffu, acc.srad, o);
+        }
+        // ---- park dot gi's state (group leader) for the parallel finalize
+        if (live && sub == 0) {
+            uint64_t* pk = park[wl][gi];
+#pragma unroll
+            for (int j = 0; j < NS; j++) pk[j] = acc.s[j];
+            pk[NS] = acc.err;
+            pk[NS + 1] = acc.srad;
+            pk[NS + 2] = (uint64_t)sc.e_max;
+            pk[NS + 3] = (uint64_t)sc.e_min;
+            pk[NS + 4] = (uint64_t)sc.e_rad;
+            pk[NS + 5] = sc.nnz;
+            pk[NS + 6] = sc.fb ? 1 : 0;
+        }
+    }
+    __syncwarp();
+
+    // ---- parallel finalize: lane g owns dot b0 + g
+    if (lane < nd) {
+        const int64_t b = b0 + lane;
+        const uint64_t* pk = park[wl][lane];
+        int64_t ex0, xst, ey0, yst, nb;
+        dot_extent(A, b, ex0, xst, ey0, yst, nb);
+        const int64_t total = nb + (A.has_init ? 1 : 0);
+        const Plan pl = finish_plan((int64_t)pk[NS + 2], (int64_t)pk[NS + 3], (int64_t)pk[NS + 4], pk[NS + 5],
+                                    pk[NS + 6] != 0, total, A.prec, A.disable_reduction);
+        if (pl.status != 0) {
+            if (A.state) write_state(A.state + b, pl, 0, 0);
+            if (pl.status == 1) {
+                A.fb_flag[b] = 1;
+            } else {
+                GFloat<1> z;
+                z.kind = APB_ZERO;
+                z.neg = 0;
+                z.e = 0;
+                z.n = 0;
+                gf_store(A.out, b, z, mag_zero(), A.status);
+            }
+        } else {
+            uint64_t s[NS];
+#pragma unroll
+            for (int j = 0; j < NS; j++) s[j] = pk[j];
+            if (A.state) write_state(A.state + b, pl, pk[NS], pk[NS + 1]);
+            if (A.acc)
+                for (int j = 0; j < pl.n_s && j < A.acc_stride; j++) A.acc[b * A.acc_stride + j] = s[j];
+            finalize_store<NS>(pl, s, pk[NS], pk[NS + 1], A.prec, with_radius, A.out, b, A.status);
+        }
+    }
+}
 
 // ------------------------------------------------- staged small kernel
 // For dots of <= 128 terms with <= 2-limb operands (config 1): the warp's 32
@@ -1459,8 +1675,44 @@ static void launch_staged(const DotArgs& A, cudaStream_t st) {
     count_launch();
 }
 
+// TPD lanes per dot: about 16-32 terms per lane (APB_DOT_TPD overrides; 32 = dot_small)
+static int pick_tpd(int64_t total) {
+    static const int env = std::getenv("APB_DOT_TPD") ? std::atoi(std::getenv("APB_DOT_TPD")) : 0;
+    if (env == 1 || env == 2 || env == 4 || env == 8 || env == 16 || env == 32) return env;
+    if (total <= 24) return 1;
+    if (total <= 48) return 2;
+    if (total <= 160) return 4;
+    if (total <= 320) return 8;
+    if (total <= 640) return 16;
+    return 32;
+}
+
+template <int L, int NS, int TPD>
+static void launch_grp(DotArgs A, cudaStream_t st) {
+    constexpr int DPR = 32 / TPD;
+    // rounds per warp: enough warps for >= 32 per SM, at most TPD rounds (32 dots)
+    int64_t rounds = A.batch / ((int64_t)DPR * 148 * 32);
+    rounds = rounds < 1 ? 1 : (rounds > TPD ? TPD : rounds);
+    A.dpw = (int)(DPR * rounds);
+    const int warps = 4;
+    const int64_t nwarps = (A.batch + A.dpw - 1) / A.dpw;
+    dim3 grid((unsigned)((nwarps + warps - 1) / warps));
+    dot_grp_kernel<L, NS, TPD><<<grid, 32 * warps, 0, st>>>(A);
+    count_launch();
+}
+
 template <int L, int NS>
 static bool try_small_tpl(const DotArgs& A, int64_t total, cudaStream_t st) {
+    const int tpd = pick_tpd(total);
+    if (tpd < 32 && !std::getenv("APB_DOT_KEEP") && !std::getenv("APB_DOT_STAGE")) {
+        switch (tpd) {
+            case 1: launch_grp<L, NS, 1>(A, st); return true;
+            case 2: launch_grp<L, NS, 2>(A, st); return true;
+            case 4: launch_grp<L, NS, 4>(A, st); return true;
+            case 8: launch_grp<L, NS, 8>(A, st); return true;
+            default: launch_grp<L, NS, 16>(A, st); return true;
+        }
+    }
     // Default: one warp per 32 dots, operands re-read from L1/L2 per term
     // (measured fastest on config 1: 0.38 ms vs 0.53 ms register-resident and
     // 0.60 ms cp.async-staged).  The other two variants stay reachable for
@@ -1521,6 +1773,7 @@ int dot_dispatch(DotArgs& A, int Lin, int64_t total, cudaStream_t st) {
     // (down to one) for small batches so every SM gets warps
     A.dpw = batch >= (int64_t)32 * 148 * 8 ? 32 : (int)std::max<int64_t>(1, batch / (148 * 8));
     const int nsb = ns_bound(prec, total);
+    A.mant16 = A.x.L == 2 && A.y.L == 2 && ((uintptr_t)A.x.mant % 16) == 0 && ((uintptr_t)A.y.mant % 16) == 0;
     const int tok = prof_begin("dot", st);
     bool small = true;
     if (Lin <= 1 && nsb <= 3) try_small_tpl<1, 3>(A, total, st);
