@@ -19,6 +19,12 @@ namespace apb {
 APB_DEV unsigned bitw64(uint64_t v) { return v ? 64u - (unsigned)__clzll((long long)v) : 0u; }
 APB_DEV unsigned ctz64(uint64_t v) { return (unsigned)__ffsll((long long)v) - 1u; }
 
+// programmatic dependent launch (launch_pdl in apb_internal.h): wait for the
+// stream predecessor's completion and memory flush / let dependents launch early.
+// Both are no-ops for kernels launched without the attribute.
+APB_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+APB_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // (lo >> rb) | (hi << (64-rb)), rb in [0,64)
 APB_DEV uint64_t funnel_r(uint64_t lo, uint64_t hi, unsigned rb) {
     return rb ? (lo >> rb) | (hi << (64 - rb)) : lo;

@@ -5,7 +5,9 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
+#include <utility>
 
 #include "apb.h"
 
@@ -32,6 +34,29 @@ bool prof_enabled();
 void prof_end(int token, cudaStream_t st);
 void set_error(const char* msg);
 int cuda_check(cudaError_t e, const char* where);
+
+// Programmatic dependent launch: the kernel may be scheduled while its stream
+// predecessor drains; it must call griddep_wait() (apb_common.cuh) before it
+// reads the predecessor's output.  APB_NO_PDL=1 falls back to plain launches.
+inline bool pdl_enabled() {
+    static const bool on = std::getenv("APB_NO_PDL") == nullptr;
+    return on;
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // dot launchers (dot_kernels.cu)
 int dot_batch_launch(const apb_balls* x, const apb_balls* y, const apb_balls* initial,

@@ -379,15 +379,14 @@ APB_DEV void digit_words(const BallsView& X, int64_t e, bool valid, int64_t scal
 // A side: thread per entry (row r, inner kk), plane[s][r][kk] byte stores --
 // a warp writes one 32-byte segment per plane
 template <int NCW>
-__global__ void __launch_bounds__(256) pack_a_v2_kernel(BallsView X, int64_t rows, int64_t ld, int64_t lo, int64_t hi,
-                                                        const int64_t* top, const int64_t* bot, int S, int Rp, int Kp,
-                                                        int8_t* out, int64_t* scale_out,
-                                                        const long long* maxw_dev = nullptr) {
+APB_DEV void pack_a_v2_body(const BallsView& X, int64_t rows, int64_t ld, int64_t lo, int64_t hi,
+                            const int64_t* top, const int64_t* bot, int S, int Rp, int Kp, int8_t* out,
+                            int64_t* scale_out, const long long* maxw_dev, int64_t blk) {
     if (maxw_dev) {  // speculative launch: slice count from the scan, before the host knows it
         S = (int)((*maxw_dev + 2 + 7) / 8);
         if (S > 8 * NCW) return;
     }
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t t = blk * blockDim.x + threadIdx.x;
     if (t >= (int64_t)Rp * Kp) return;
     const int64_t r = t / Kp, kk = t % Kp;
     int64_t sc = 0;
@@ -404,26 +403,33 @@ __global__ void __launch_bounds__(256) pack_a_v2_kernel(BallsView X, int64_t row
     }
 }
 
+template <int NCW>
+__global__ void __launch_bounds__(256) pack_a_v2_kernel(BallsView X, int64_t rows, int64_t ld, int64_t lo, int64_t hi,
+                                                        const int64_t* top, const int64_t* bot, int S, int Rp, int Kp,
+                                                        int8_t* out, int64_t* scale_out,
+                                                        const long long* maxw_dev = nullptr) {
+    pack_a_v2_body<NCW>(X, rows, ld, lo, hi, top, bot, S, Rp, Kp, out, scale_out, maxw_dev, blockIdx.x);
+}
+
 // B side: 32 columns x 32 inner indices per 256 threads (4 consecutive kk per
 // thread, reads coalesced over columns j); digit bytes of 4 entries are merged
 // with byte permutes and transposed through shared memory so plane rows (fixed
 // j, contiguous kk) leave as 32-byte segments.
 template <int NCW>
-__global__ void __launch_bounds__(256) pack_b_v2_kernel(BallsView X, int64_t N, int64_t lo, int64_t hi,
-                                                        const int64_t* top, const int64_t* bot, int S, int Np, int Kp,
-                                                        int8_t* out, int64_t* scale_out,
-                                                        const long long* maxw_dev = nullptr) {
+APB_DEV void pack_b_v2_body(const BallsView& X, int64_t N, int64_t lo, int64_t hi, const int64_t* top,
+                            const int64_t* bot, int S, int Np, int Kp, int8_t* out, int64_t* scale_out,
+                            const long long* maxw_dev, int64_t bx, int64_t by) {
     if (maxw_dev) {
         S = (int)((*maxw_dev + 2 + 7) / 8);
         if (S > 8 * NCW) return;
     }
     __shared__ uint32_t tile[8][32][9];  // [digit in chunk][j][kk word], padded
     const int jl = threadIdx.x & 31, kq = threadIdx.x >> 5;
-    const int64_t j = (int64_t)blockIdx.x * 32 + jl;
-    const int64_t kk0 = (int64_t)blockIdx.y * 32 + 4 * kq;
+    const int64_t j = bx * 32 + jl;
+    const int64_t kk0 = by * 32 + 4 * kq;
     int64_t sc = 0;
     if (j < N) sc = top[j] == INT64_MIN ? 0 : -bot[j];
-    if (j < N && blockIdx.y == 0 && kq == 0) scale_out[j] = sc;
+    if (j < N && by == 0 && kq == 0) scale_out[j] = sc;
     uint64_t d[4][NCW];
 #pragma unroll
     for (int q = 0; q < 4; q++) {
@@ -460,12 +466,45 @@ __global__ void __launch_bounds__(256) pack_b_v2_kernel(BallsView X, int64_t N, 
             const int idx = it * 256 + threadIdx.x;
             const int m = idx & 7, r = (idx >> 3) & 31, b = idx >> 8;
             const int sdig = 8 * c + b;
-            const int64_t jj = (int64_t)blockIdx.x * 32 + r;
+            const int64_t jj = bx * 32 + r;
             if (sdig < S && jj < Np)
-                *(uint32_t*)(out + (size_t)sdig * plane + (size_t)jj * Kp + (size_t)blockIdx.y * 32 + 4 * m) =
+                *(uint32_t*)(out + (size_t)sdig * plane + (size_t)jj * Kp + (size_t)by * 32 + 4 * m) =
                     tile[b][r][m];
         }
         __syncthreads();
+    }
+}
+
+template <int NCW>
+__global__ void __launch_bounds__(256) pack_b_v2_kernel(BallsView X, int64_t N, int64_t lo, int64_t hi,
+                                                        const int64_t* top, const int64_t* bot, int S, int Np, int Kp,
+                                                        int8_t* out, int64_t* scale_out,
+                                                        const long long* maxw_dev = nullptr) {
+    pack_b_v2_body<NCW>(X, N, lo, hi, top, bot, S, Np, Kp, out, scale_out, maxw_dev, blockIdx.x, blockIdx.y);
+}
+
+// speculative single-block pack of both operands in one launch: blocks [0, ga)
+// pack A (thread per entry), the rest pack B (32 x 32 tiles, gbx per row of tiles)
+struct PackAB {
+    BallsView a, b;
+    int64_t M, K, N;
+    const int64_t *rtop, *rbot, *ctop, *cbot;
+    int Mp, Np, Kp;
+    int8_t *Ap, *Bp;
+    int64_t *esc, *fsc;
+    const long long *mwa, *mwb;
+    int64_t ga, gbx;
+};
+
+template <int NCW>
+__global__ void __launch_bounds__(256) pack_ab_v2_kernel(PackAB P) {
+    griddep_wait();
+    if ((int64_t)blockIdx.x < P.ga) {
+        pack_a_v2_body<NCW>(P.a, P.M, P.K, 0, P.K, P.rtop, P.rbot, 0, P.Mp, P.Kp, P.Ap, P.esc, P.mwa, blockIdx.x);
+    } else {
+        const int64_t bb = (int64_t)blockIdx.x - P.ga;
+        pack_b_v2_body<NCW>(P.b, P.N, 0, P.K, P.ctop, P.cbot, 0, P.Np, P.Kp, P.Bp, P.fsc, P.mwb, bb % P.gbx,
+                            bb / P.gbx);
     }
 }
 
@@ -532,6 +571,12 @@ struct RecombineArgs {
     int int_limbs;
     int* status;
     int quad;  // band GEMM layout: plane[(j/4)][i][j%4] (coalesced epilogue stores), else [i][j]
+    // optional fused radius combine (recombine16 only): C.rad = err (+) (r1 (+) r2), the
+    // rad_combine_kernel step of src/matmul.cpp:512-513 folded into the store
+    const uint32_t* r1b = nullptr;
+    const int64_t* r1f = nullptr;
+    const uint32_t* r2b = nullptr;
+    const int64_t* r2f = nullptr;
 };
 
 APB_DEV size_t rc_off(const RecombineArgs& R, int64_t i, int64_t j) {
@@ -838,12 +883,13 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
     row[NW + 1] = 0;
     BallsOut& O = R.C;
     uint64_t* dst = O.mant + t * (int64_t)O.L;
-    if (top_w < 0) {  // exact zero: C stays Ball::zero()
+    Mag rsum = mag_zero();
+    if (R.r1b) rsum = mag_add(mag_load(R.r1b[t], R.r1f[t]), mag_load(R.r2b[t], R.r2f[t]));
+    if (top_w < 0) {  // exact zero: C stays Ball::zero() (plus the radius products)
         for (int q = 0; q < O.L; q++) dst[q] = 0;
         O.exp[t] = 0;
         O.kind[t] = APB_ZERO;
-        O.rad_man[t] = 0;
-        O.rad_exp[t] = 0;
+        mag_store(rsum, &O.rad_man[t], &O.rad_exp[t]);
         return;
     }
     const int64_t B = 32 * (int64_t)top_w + (int64_t)(32 - __clz(row[top_w + 1]));
@@ -904,6 +950,7 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
             err = mag_parts(bm, checked_add(exp2, top + 1, &st));
         }
     }
+    if (R.r1b) err = mag_add(err, rsum);
     mag_store(err, &O.rad_man[t], &O.rad_exp[t]);
     if (st) *R.status = st;
 }
@@ -1248,6 +1295,7 @@ __global__ void __launch_bounds__(256) scan_v2_kernel(BallsView A, BallsView B, 
                                                       int cA, int cB, int64_t* pa, int64_t* pb, ScanSummary* sum,
                                                       long long* mw1, long long* mw2) {
     __shared__ int64_t red[8][32][SCAN_FIELDS + 1];
+    griddep_launch();  // the finish kernel may be scheduled now (it waits for this grid)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // the finish kernel accumulates into these
         *sum = ScanSummary{};
@@ -1311,6 +1359,8 @@ __global__ void scan_v2_finish_kernel(const int64_t* pa, const int64_t* pb, int6
                                       int64_t* ecen1, int64_t* ecen2, int64_t* fcen1, int64_t* fcen2,
                                       ScanSummary* sum, long long* mw1, long long* mw2) {
     // warp per line (rows of A first, then columns of B), lanes over the chunk partials
+    griddep_launch();
+    griddep_wait();
     const int lane = threadIdx.x & 31;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (wid >= M + N) return;
@@ -2245,11 +2295,25 @@ BandGeom band_geom(int64_t M, int64_t N, int64_t w) {
 // digit-word template (2, 5 or 8 words) of the byte-parallel pack for S slices; 0 = byte-serial
 inline int pack_ncw(int S) { return S <= 16 ? 2 : S <= 40 ? 5 : S <= 64 ? 8 : 0; }
 
+// radius products to fold into the recombine (single block): the recombine waits
+// for `ready` (recorded by the radius stream) and stores C.rad = err (+) (r1 (+) r2)
+struct RadFuse {
+    const uint32_t* r1b;
+    const int64_t* r1f;
+    const uint32_t* r2b;
+    const int64_t* r2f;
+    cudaEvent_t ready;
+    bool capturing;
+    bool used;  // out: the recombine took the radius (no rad_combine_kernel needed)
+};
+void wait_event(cudaStream_t s, cudaEvent_t ev, bool capturing);
+
 int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int64_t prec, apb_mat* C,
                  bool first, int64_t maxw_a, int64_t maxw_b, const int64_t* rtop_in,
                  const int64_t* rbot_in, const int64_t* ctop_in, const int64_t* cbot_in,
                  int64_t* int_out, int int_limbs, int64_t* esc_out, int64_t* fsc_out,
-                 cudaStream_t st, const std::function<int()>* after_gemm = nullptr, bool prepacked = false) {
+                 cudaStream_t st, const std::function<int()>* after_gemm = nullptr, bool prepacked = false,
+                 RadFuse* fuse = nullptr) {
     const int64_t M = A->rows, K = A->cols, N = B->cols, w = hi - lo;
     BallsView a = view_of(&A->b), b = view_of(&B->b);
     const int64_t* rtop = rtop_in;
@@ -2495,6 +2559,16 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         static const bool slow = std::getenv("APB_SLOW_RECOMBINE") != nullptr;  // test hook
         static const bool r64 = std::getenv("APB_RECOMBINE64") != nullptr;      // test hook
         const bool fast = band && first && !int_out && R.C.mant && !slow;
+        if (fuse) {
+            fuse->used = fast && band_w == 2 && NW <= 80 && !r64;  // recombine16 below
+            if (fuse->used) {
+                wait_event(st, fuse->ready, fuse->capturing);
+                R.r1b = fuse->r1b;
+                R.r1f = fuse->r1f;
+                R.r2b = fuse->r2b;
+                R.r2f = fuse->r2f;
+            }
+        }
         if (fast && band_w == 4 && NW <= 20) recombine_fast_kernel<20, 32><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 4 && NW <= 40) recombine_fast_kernel<40, 32><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 4 && NW <= 72) recombine_fast_kernel<72, 32><<<gbq, 128, 0, st>>>(R);
@@ -2781,6 +2855,12 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     static const bool no_spec_pack = std::getenv("APB_NO_SPEC_PACK") != nullptr;  // test hook
     static const bool no_graphs = std::getenv("APB_NO_GRAPHS") != nullptr;        // test hook
     static cudaEvent_t ev_join = make_event(), ev_fin = make_event(), ev_plan = make_event();
+    static cudaEvent_t ev_fork = make_event(), ev_cjoin = make_event();
+    static cudaStream_t cps = [] {
+        cudaStream_t t;
+        cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking);
+        return t;
+    }();
     const bool spec = rad_order == 4;
     // speculative slice packing for the single-block plan of (almost) every
     // input, issued before the host round trip: the slice counts come from the
@@ -2807,34 +2887,50 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         const int tk_scan = prof_begin("scan", s);
         const int64_t nblk = M * cA + ((N + 31) / 32) * cB;
         scan_v2_kernel<<<(unsigned)nblk, 256, 0, s>>>(av, bv, M, K, N, cA, cB, pa, pb, sum, mw1, mw2);
-        scan_v2_finish_kernel<<<blocks_for(32 * (M + N), 256), 256, 0, s>>>(
-            pa, pb, M, N, cA, cB, RW.top[0], RW.bot[0], CW.top[0], CW.bot[0], ec1, ec2, fc1, fc2, sum, mw1, mw2);
+        launch_pdl(scan_v2_finish_kernel, dim3(blocks_for(32 * (M + N), 256)), dim3(256), 0, s, pa, pb, M, N, cA, cB,
+                   RW.top[0], RW.bot[0], CW.top[0], CW.bot[0], ec1, ec2, fc1, fc2, sum, mw1, mw2);
         count_launch(2);
         prof_end(tk_scan, s);
         rec_event(ev_fin, s, capturing);
-        cudaMemcpyAsync(hs, sum, sizeof(ScanSummary), cudaMemcpyDeviceToHost, s);
-        cudaMemcpyAsync(hw, mw1, 4 * sizeof(long long), cudaMemcpyDeviceToHost, s);
-        cudaMemcpyAsync(hw + 4, mw2, 4 * sizeof(long long), cudaMemcpyDeviceToHost, s);
-        rec_event(ev_plan, s, capturing);
+        // the planner summary leaves on a copy stream so the pack follows the scan directly
+        cudaEventRecord(ev_fork, s);
+        cudaStreamWaitEvent(cps, ev_fork, 0);
+        cudaMemcpyAsync(hs, sum, sizeof(ScanSummary), cudaMemcpyDeviceToHost, cps);
+        cudaMemcpyAsync(hw, mw1, 4 * sizeof(long long), cudaMemcpyDeviceToHost, cps);
+        cudaMemcpyAsync(hw + 4, mw2, 4 * sizeof(long long), cudaMemcpyDeviceToHost, cps);
+        rec_event(ev_plan, cps, capturing);
         if (sncw) {
             const int tk = prof_begin("pack", s);
-            const unsigned ga = blocks_for((int64_t)sgeo.Mp * sgeo.Kp, 256);
-            const dim3 gb((unsigned)(sgeo.Np / 32), (unsigned)(sgeo.Kp / 32));
-            const long long* mwa = &sum->maxw_a;
-            const long long* mwb = &sum->maxw_b;
-            if (sncw == 2) {
-                pack_a_v2_kernel<2><<<ga, 256, 0, s>>>(av, M, K, 0, K, RW.top[0], RW.bot[0], 0, sgeo.Mp, sgeo.Kp, sAp, esc, mwa);
-                pack_b_v2_kernel<2><<<gb, 256, 0, s>>>(bv, N, 0, K, CW.top[0], CW.bot[0], 0, sgeo.Np, sgeo.Kp, sBp, fsc, mwb);
-            } else if (sncw == 5) {
-                pack_a_v2_kernel<5><<<ga, 256, 0, s>>>(av, M, K, 0, K, RW.top[0], RW.bot[0], 0, sgeo.Mp, sgeo.Kp, sAp, esc, mwa);
-                pack_b_v2_kernel<5><<<gb, 256, 0, s>>>(bv, N, 0, K, CW.top[0], CW.bot[0], 0, sgeo.Np, sgeo.Kp, sBp, fsc, mwb);
-            } else {
-                pack_a_v2_kernel<8><<<ga, 256, 0, s>>>(av, M, K, 0, K, RW.top[0], RW.bot[0], 0, sgeo.Mp, sgeo.Kp, sAp, esc, mwa);
-                pack_b_v2_kernel<8><<<gb, 256, 0, s>>>(bv, N, 0, K, CW.top[0], CW.bot[0], 0, sgeo.Np, sgeo.Kp, sBp, fsc, mwb);
-            }
+            PackAB pk;
+            pk.a = av;
+            pk.b = bv;
+            pk.M = M;
+            pk.K = K;
+            pk.N = N;
+            pk.rtop = RW.top[0];
+            pk.rbot = RW.bot[0];
+            pk.ctop = CW.top[0];
+            pk.cbot = CW.bot[0];
+            pk.Mp = sgeo.Mp;
+            pk.Np = sgeo.Np;
+            pk.Kp = sgeo.Kp;
+            pk.Ap = sAp;
+            pk.Bp = sBp;
+            pk.esc = esc;
+            pk.fsc = fsc;
+            pk.mwa = &sum->maxw_a;
+            pk.mwb = &sum->maxw_b;
+            pk.ga = blocks_for((int64_t)sgeo.Mp * sgeo.Kp, 256);
+            pk.gbx = sgeo.Np / 32;
+            const dim3 g((unsigned)(pk.ga + pk.gbx * (sgeo.Kp / 32)));
+            if (sncw == 2) launch_pdl(pack_ab_v2_kernel<2>, g, dim3(256), 0, s, pk);
+            else if (sncw == 5) launch_pdl(pack_ab_v2_kernel<5>, g, dim3(256), 0, s, pk);
+            else launch_pdl(pack_ab_v2_kernel<8>, g, dim3(256), 0, s, pk);
             prof_end(tk, s);
-            count_launch(2);
+            count_launch(1);
         }
+        cudaEventRecord(ev_cjoin, cps);
+        cudaStreamWaitEvent(s, ev_cjoin, 0);
         return cuda_check(cudaGetLastError(), "matmul scan");
     };
     // speculative radius products (single radius block; sparse/dense chosen on the device)
@@ -2917,10 +3013,13 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     const bool single = P.steps.size() == 3 && P.steps[0] == 0 && P.steps[1] == A->cols && P.steps[2] == 0;
     const bool prepacked =
         single && sncw && slices_for(P.maxw_a) <= 8 * sncw && slices_for(P.maxw_b) <= 8 * sncw;
+    static const bool no_fuse = std::getenv("APB_NO_RAD_FUSE") != nullptr;  // test hook
     auto phase2 = [&](cudaStream_t s, bool capturing) -> int {
+        RadFuse fz{r1b, r1f, r2b, r2f, ev_join, capturing, false};
         int rc2 = scaled_block(A, B, 0, K, prec, C, true, P.maxw_a, P.maxw_b, RW.top[0], RW.bot[0], CW.top[0],
-                               CW.bot[0], nullptr, 0, nullptr, nullptr, s, nullptr, true);
+                               CW.bot[0], nullptr, 0, nullptr, nullptr, s, nullptr, true, no_fuse ? nullptr : &fz);
         if (rc2) return rc2;
+        if (fz.used) return cuda_check(cudaGetLastError(), "block matmul");
         wait_event(s, ev_join, capturing);
         const int tk_comb = prof_begin("combine", s);
         rad_combine_kernel<<<blocks_for(M * N, 256), 256, 0, s>>>(out_of(&C->b), M * N, r1b, r1f, r2b, r2f);
