@@ -321,7 +321,11 @@ struct BandCfg {
     static constexpr int A_STAGES = 4;
     static constexpr int TILE_A = 128 * BK;
     static constexpr int TILE_B = BNT * BK;
-    static constexpr int B_STAGES = BNT == 128 ? 8 : 5;
+#ifndef APB_BAND_BSTAGES
+#define APB_BAND_BSTAGES 4
+#endif
+    // 4 B stages at BNT=256 leave ~34 KB of shared memory for a co-resident radius block
+    static constexpr int B_STAGES = BNT == 128 ? 8 : APB_BAND_BSTAGES;
     static constexpr int SMEM = A_STAGES * TILE_A + B_STAGES * TILE_B + 1024 + 512;
     static constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BNT >> 3) << 17) |
                                       ((uint32_t)(BM >> 4) << 24);
@@ -607,6 +611,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* tempty = tfull + 1;
     uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
 
+    if (P.spec_maxw && ((int)((P.spec_maxw[0] + 9) / 8) != P.S_A || (int)((P.spec_maxw[1] + 9) / 8) != P.S_B))
+        return;  // speculation void: the host redoes the product
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int it_begin = P.cta_begin[blockIdx.x], it_end = P.cta_begin[blockIdx.x + 1];
     if (P.dbg_ts && threadIdx.x == 0) P.dbg_ts[blockIdx.x * 32 + 31] = clock64();
@@ -875,11 +881,33 @@ static int band_launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const Ban
     if (!attr) {
         cudaFuncSetAttribute(band_gemm_kernel<BNT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         cudaFuncSetAttribute(band3_gemm_kernel<BNT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        // full shared-memory carveout, so the SM keeps room for a co-resident radius block
+        cudaFuncSetAttribute(band3_gemm_kernel<BNT, W>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr = true;
     }
     static const bool v2 = std::getenv("APB_BAND_V2") != nullptr;  // previous issue loop (A/B timing)
-    if (v2) band_gemm_kernel<BNT, W><<<n_ctas, THREADS, Cfg::SMEM, st>>>(ma, mb, P);
-    else band3_gemm_kernel<BNT, W><<<n_ctas, THREADS, Cfg::SMEM, st>>>(ma, mb, P);
+    if (v2) {
+        band_gemm_kernel<BNT, W><<<n_ctas, THREADS, Cfg::SMEM, st>>>(ma, mb, P);
+        return APB_OK;
+    }
+    // highest launch priority: the persistent CTAs (one per SM) take SMs ahead of
+    // the radius products queued on the side stream
+    static const int prio = [] {
+        int least = 0, greatest = 0;
+        cudaDeviceGetStreamPriorityRange(&least, &greatest);
+        return std::getenv("APB_NO_PRIO") ? least : greatest;
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)n_ctas);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributePriority;
+    at[0].val.priority = prio;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, band3_gemm_kernel<BNT, W>, ma, mb, P);
     return APB_OK;
 }
 

@@ -31,6 +31,10 @@ struct BandGemmParams {
     int debug = 0;            // timing experiments only: 1 skip TMA refills, 2 skip epilogue stores
     long long* dbg_ts = nullptr;  // optional per-CTA clock64 trace (timing experiments)
     unsigned long long* timer = nullptr;  // device span timer (gemm_timer_*): [sum ns, launches, start, done, end]
+    // speculative launch (before the host has planned): the planner's window
+    // heights (maxw_a, maxw_b) on the device; the kernel stands down unless they
+    // give exactly S_A and S_B slices
+    const long long* spec_maxw = nullptr;
 };
 
 // device-side span timer of the band GEMM (first CTA start to last CTA end,

@@ -43,6 +43,7 @@ struct ScanSummary {
     int special_a, special_b;
     long long prec_a, prec_b;   // entry_precision
     long long maxw_a, maxw_b;   // max row / column window width over the scanned range
+    long long mw[8];            // block_matmul: radius window widths / nonzero counts (mw1, mw2)
 };
 
 // bit width of a finite nonzero midpoint stored in L top-aligned slots
@@ -577,6 +578,9 @@ struct RecombineArgs {
     const int64_t* r1f = nullptr;
     const uint32_t* r2b = nullptr;
     const int64_t* r2f = nullptr;
+    // speculative launch: stand down unless the device window heights give (sa, sb) slices
+    const long long* spec_maxw = nullptr;
+    int spec_sa = 0, spec_sb = 0;
 };
 
 APB_DEV size_t rc_off(const RecombineArgs& R, int64_t i, int64_t j) {
@@ -825,6 +829,8 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
     constexpr int NW = (ND + 1) / 2;   // 32-bit magnitude words
     constexpr int STR = NW + 3;        // smem row stride (odd for bank spread), 2 guard words
     __shared__ uint32_t sm[128 * STR];
+    if (R.spec_maxw && ((int)((R.spec_maxw[0] + 9) / 8) != R.spec_sa || (int)((R.spec_maxw[1] + 9) / 8) != R.spec_sb))
+        return;  // speculation void (the GEMM stood down too)
     uint32_t* row = sm + threadIdx.x * STR;
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t jr = u & 3, i = (u >> 2) % R.M, jq = (u >> 2) / R.M;
@@ -1525,16 +1531,14 @@ APB_DEV int rad_variant(const long long* mw, int64_t M, int64_t K, int64_t N, in
 }
 
 constexpr int RT = 32, RK = 32, RTHREADS = 64;
-__global__ void __launch_bounds__(64) rad_gemm_kernel(const double* __restrict__ da,
-                                                       const double* __restrict__ db, int64_t M,
-                                                       int64_t N, int64_t w, const int64_t* ecen,
-                                                       const int64_t* fcen, uint32_t* rb, int64_t* rf,
-                                                       int accumulate, int a_trans, const long long* sel = nullptr) {
+APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restrict__ db, int64_t M, int64_t N,
+                           int64_t w, const int64_t* ecen, const int64_t* fcen, uint32_t* rb, int64_t* rf,
+                           int accumulate, int a_trans, const long long* sel, int64_t bx, int64_t by) {
     if (sel && rad_variant(sel, M, w, N, a_trans) != 2) return;
     __shared__ double sA[RK][RT + 1];
     __shared__ double sB[RK][RT];
     const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
-    const int64_t i0 = (int64_t)blockIdx.y * RT, j0 = (int64_t)blockIdx.x * RT;
+    const int64_t i0 = by * RT, j0 = bx * RT;
     double s[4][4];
     Mag ent[4][4];
 #pragma unroll
@@ -1595,6 +1599,14 @@ __global__ void __launch_bounds__(64) rad_gemm_kernel(const double* __restrict__
             }
             mag_store(m, &rb[o], &rf[o]);
         }
+}
+
+__global__ void __launch_bounds__(64) rad_gemm_kernel(const double* __restrict__ da,
+                                                       const double* __restrict__ db, int64_t M,
+                                                       int64_t N, int64_t w, const int64_t* ecen,
+                                                       const int64_t* fcen, uint32_t* rb, int64_t* rf,
+                                                       int accumulate, int a_trans, const long long* sel = nullptr) {
+    rad_gemm_body(da, db, M, N, w, ecen, fcen, rb, rf, accumulate, a_trans, sel, blockIdx.x, blockIdx.y);
 }
 
 
@@ -1706,7 +1718,52 @@ __global__ void __launch_bounds__(256) rad_sprow_kernel(const double* __restrict
 // chunk folds as rad_spcol/rad_sprow (bit-identical results).
 constexpr int RCH = 1024;
 
-// ordered compaction of v[u] (term l = c0 + 256 u + tid) into (sl, sv); returns count
+template <int R, int T>
+struct RadSmem {
+    int sl[RCH];
+    double sv[RCH];
+    int cnt[65];
+    double gbuf[8 * R][T];
+};
+
+// ordered compaction of v[u] (term l = c0 + T u + tid, T threads, U = RCH / T) into
+// (sl, sv); returns the count.  cnt holds the 32 (u, warp) counts in l order.
+template <int T>
+APB_DEV int block_compact_t(const double (&v)[RCH / T], int64_t c0, int* sl, double* sv, int* cnt) {
+    constexpr int U = RCH / T, NWP = T / 32;
+    static_assert(U * NWP == 32, "32 (u, warp) groups");
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned bal[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        bal[u] = __ballot_sync(0xffffffffu, v[u] != 0.0);
+        if (lane == 0) cnt[u * NWP + warp] = __popc(bal[u]);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const int c = cnt[lane];
+        int x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        cnt[32 + lane] = x - c;
+        if (lane == 31) cnt[64] = x;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        if (v[u] != 0.0) {
+            const int pos = cnt[32 + u * NWP + warp] + __popc(bal[u] & ((1u << lane) - 1u));
+            sl[pos] = (int)(c0 + T * u + tid);
+            sv[pos] = v[u];
+        }
+    }
+    __syncthreads();
+    return cnt[64];
+}
+
 APB_DEV int block_compact(const double (&v)[4], int64_t c0, int* sl, double* sv, int* cnt) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     unsigned bal[4];
@@ -1835,27 +1892,27 @@ APB_DEV void cp_async_wait_all() {
 // ILP, one list read serving R loads); the 8R gathered operands of a batch are
 // fetched with cp.async into a per-thread shared-memory column so they are all
 // in flight together (the compiler otherwise interleaves each load with its use)
-template <int R>
-__global__ void __launch_bounds__(256) rad_spcol_v3_kernel(const double* __restrict__ daT, const double* __restrict__ db,
+template <int R, int T>
+APB_DEV void rad_spcol_v3_body(RadSmem<R, T>& sm, int64_t blk, const double* __restrict__ daT, const double* __restrict__ db,
                                                            int64_t M, int64_t N, int64_t w, const int64_t* ecen,
                                                            const int64_t* fcen, uint32_t* rb, int64_t* rf,
                                                            const long long* sel = nullptr) {
     if (sel && rad_variant(sel, M, w, N, 1) != 0) return;
-    __shared__ int sl[RCH];
-    __shared__ double sv[RCH];
-    __shared__ int cnt[65];
-    __shared__ double gbuf[8 * R][256];
-    const int64_t j = blockIdx.x;
+    int* sl = sm.sl;
+    double* sv = sm.sv;
+    int* cnt = sm.cnt;
+    auto& gbuf = sm.gbuf;
+    const int64_t j = blk;
     const int64_t nch = (w + RCH - 1) / RCH;
     const int64_t fj = fcen[j];
     int n = 0;
-    for (int64_t pass = 0; pass * 256 * R < M; pass++) {
+    for (int64_t pass = 0; pass * T * R < M; pass++) {
         int64_t ii[R];
         double s[R];
         Mag ent[R];
 #pragma unroll
         for (int r = 0; r < R; r++) {
-            const int64_t i = pass * 256 * R + 256 * r + threadIdx.x;
+            const int64_t i = pass * T * R + T * r + threadIdx.x;
             ii[r] = i < M ? i : 0;
             s[r] = 0.0;
             ent[r] = mag_zero();
@@ -1863,13 +1920,13 @@ __global__ void __launch_bounds__(256) rad_spcol_v3_kernel(const double* __restr
         for (int64_t c0 = 0; c0 < w; c0 += RCH) {
             if (nch > 1 || pass == 0) {
                 if (nch > 1) __syncthreads();
-                double v[4];
+                double v[RCH / T];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int64_t l = c0 + 256 * u + threadIdx.x;
+                for (int u = 0; u < RCH / T; u++) {
+                    const int64_t l = c0 + T * u + threadIdx.x;
                     v[u] = l < w ? db[l * N + j] : 0.0;
                 }
-                n = block_compact(v, c0, sl, sv, cnt);
+                n = block_compact_t<T>(v, c0, sl, sv, cnt);
             }
             int p0 = 0;
             for (; p0 + 8 <= n; p0 += 8) {
@@ -1898,33 +1955,42 @@ __global__ void __launch_bounds__(256) rad_spcol_v3_kernel(const double* __restr
         }
 #pragma unroll
         for (int r = 0; r < R; r++) {
-            const int64_t i = pass * 256 * R + 256 * r + threadIdx.x;
+            const int64_t i = pass * T * R + T * r + threadIdx.x;
             if (i < M) mag_store(ent[r], &rb[i * N + j], &rf[i * N + j]);
         }
     }
 }
 
-template <int R>
-__global__ void __launch_bounds__(256) rad_sprow_v3_kernel(const double* __restrict__ da, const double* __restrict__ db,
+template <int R, int T = 256>
+__global__ void __launch_bounds__(T) rad_spcol_v3_kernel(const double* __restrict__ daT, const double* __restrict__ db,
+                                                           int64_t M, int64_t N, int64_t w, const int64_t* ecen,
+                                                           const int64_t* fcen, uint32_t* rb, int64_t* rf,
+                                                           const long long* sel = nullptr) {
+    __shared__ RadSmem<R, T> sm;
+    rad_spcol_v3_body<R, T>(sm, blockIdx.x, daT, db, M, N, w, ecen, fcen, rb, rf, sel);
+}
+
+template <int R, int T>
+APB_DEV void rad_sprow_v3_body(RadSmem<R, T>& sm, int64_t blk, const double* __restrict__ da, const double* __restrict__ db,
                                                            int64_t M, int64_t N, int64_t w, const int64_t* ecen,
                                                            const int64_t* fcen, uint32_t* rb, int64_t* rf,
                                                            const long long* sel = nullptr) {
     if (sel && rad_variant(sel, M, w, N, 0) != 1) return;
-    __shared__ int sl[RCH];
-    __shared__ double sv[RCH];
-    __shared__ int cnt[65];
-    __shared__ double gbuf[8 * R][256];
-    const int64_t i = blockIdx.x;
+    int* sl = sm.sl;
+    double* sv = sm.sv;
+    int* cnt = sm.cnt;
+    auto& gbuf = sm.gbuf;
+    const int64_t i = blk;
     const int64_t nch = (w + RCH - 1) / RCH;
     const int64_t ei = ecen[i];
     int n = 0;
-    for (int64_t pass = 0; pass * 256 * R < N; pass++) {
+    for (int64_t pass = 0; pass * T * R < N; pass++) {
         int64_t jj[R];
         double s[R];
         Mag ent[R];
 #pragma unroll
         for (int r = 0; r < R; r++) {
-            const int64_t j = pass * 256 * R + 256 * r + threadIdx.x;
+            const int64_t j = pass * T * R + T * r + threadIdx.x;
             jj[r] = j < N ? j : 0;
             s[r] = 0.0;
             ent[r] = mag_zero();
@@ -1932,13 +1998,13 @@ __global__ void __launch_bounds__(256) rad_sprow_v3_kernel(const double* __restr
         for (int64_t c0 = 0; c0 < w; c0 += RCH) {
             if (nch > 1 || pass == 0) {
                 if (nch > 1) __syncthreads();
-                double v[4];
+                double v[RCH / T];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int64_t l = c0 + 256 * u + threadIdx.x;
+                for (int u = 0; u < RCH / T; u++) {
+                    const int64_t l = c0 + T * u + threadIdx.x;
                     v[u] = l < w ? da[i * w + l] : 0.0;
                 }
-                n = block_compact(v, c0, sl, sv, cnt);
+                n = block_compact_t<T>(v, c0, sl, sv, cnt);
             }
             int p0 = 0;
             for (; p0 + 8 <= n; p0 += 8) {
@@ -1967,8 +2033,72 @@ __global__ void __launch_bounds__(256) rad_sprow_v3_kernel(const double* __restr
         }
 #pragma unroll
         for (int r = 0; r < R; r++) {
-            const int64_t j = pass * 256 * R + 256 * r + threadIdx.x;
+            const int64_t j = pass * T * R + T * r + threadIdx.x;
             if (j < N) mag_store(ent[r], &rb[i * N + j], &rf[i * N + j]);
+        }
+    }
+}
+
+template <int R, int T = 256>
+__global__ void __launch_bounds__(T) rad_sprow_v3_kernel(const double* __restrict__ da, const double* __restrict__ db,
+                                                           int64_t M, int64_t N, int64_t w, const int64_t* ecen,
+                                                           const int64_t* fcen, uint32_t* rb, int64_t* rf,
+                                                           const long long* sel = nullptr) {
+    __shared__ RadSmem<R, T> sm;
+    rad_sprow_v3_body<R, T>(sm, blockIdx.x, da, db, M, N, w, ecen, fcen, rb, rf, sel);
+}
+
+// both radius products of a speculative single block in one launch each
+// (src/matmul.cpp:498-513): R1 = |A| R_B (plane 1, |A| transposed) and
+// R2 = R_A (|B| + R_B) (plane 2); the device picks sparse / dense (rad_variant)
+struct RadPair {
+    int64_t M, K, N;
+    double *da1, *db1, *da2, *db2;
+    const int64_t *ec1, *fc1, *ec2, *fc2;
+    uint32_t *r1b, *r2b;
+    int64_t *r1f, *r2f;
+    const long long *mw1, *mw2;
+};
+
+// blocks [0, N): column lists of R_B (product 1); [N, N + M): row lists of R_A (product 2)
+template <int R, int T>
+__global__ void __launch_bounds__(T) rad_sparse2_kernel(RadPair P) {
+    __shared__ RadSmem<R, T> sm;
+    if ((int64_t)blockIdx.x < P.N)
+        rad_spcol_v3_body<R, T>(sm, blockIdx.x, P.da1, P.db1, P.M, P.N, P.K, P.ec1, P.fc1, P.r1b, P.r1f, P.mw1);
+    else
+        rad_sprow_v3_body<R, T>(sm, (int64_t)blockIdx.x - P.N, P.da2, P.db2, P.M, P.N, P.K, P.ec2, P.fc2, P.r2b,
+                                P.r2f, P.mw2);
+}
+
+// dense variants (stand down unless picked): blockIdx.z = product
+__global__ void __launch_bounds__(64) rad_gemm2_kernel(RadPair P) {
+    if (blockIdx.z == 0)
+        rad_gemm_body(P.da1, P.db1, P.M, P.N, P.K, P.ec1, P.fc1, P.r1b, P.r1f, 0, 1, P.mw1, blockIdx.x, blockIdx.y);
+    else
+        rad_gemm_body(P.da2, P.db2, P.M, P.N, P.K, P.ec2, P.fc2, P.r2b, P.r2f, 0, 0, P.mw2, blockIdx.x, blockIdx.y);
+}
+
+// exact double planes of both sides in one launch: blocks [0, nA) A, the rest B
+__global__ void fused_planes2_kernel(BallsView A, BallsView B, RadPair P, int64_t nA) {
+    const bool a = (int64_t)blockIdx.x < nA;
+    const int64_t t = ((int64_t)blockIdx.x - (a ? 0 : nA)) * blockDim.x + threadIdx.x;
+    const int64_t rows = a ? P.M : P.K, cols = a ? P.K : P.N;
+    double v1 = 0.0, v2 = 0.0;
+    if (t < rows * cols) {
+        const BallsView& X = a ? A : B;
+        const int64_t line = a ? t / cols : t % cols;  // A: row i; B: column j
+        const Mag m1 = rad_operand(X, t, a ? 0 : 2);
+        const Mag m2 = rad_operand(X, t, a ? 1 : 3);
+        const int64_t c1 = a ? P.ec1[line] : P.fc1[line], c2 = a ? P.ec2[line] : P.fc2[line];
+        if (m1.kind == 1) v1 = ldexp((double)m1.b, (int)(m1.f - 30 + c1));
+        if (m2.kind == 1) v2 = ldexp((double)m2.b, (int)(m2.f - 30 + c2));
+        if (a) {  // |A| plane stored transposed ([l][i]) for coalesced column-list products
+            P.da1[(t % cols) * rows + t / cols] = v1;
+            P.da2[t] = v2;
+        } else {
+            P.db1[t] = v1;
+            P.db2[t] = v2;
         }
     }
 }
@@ -2313,7 +2443,7 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
                  const int64_t* rbot_in, const int64_t* ctop_in, const int64_t* cbot_in,
                  int64_t* int_out, int int_limbs, int64_t* esc_out, int64_t* fsc_out,
                  cudaStream_t st, const std::function<int()>* after_gemm = nullptr, bool prepacked = false,
-                 RadFuse* fuse = nullptr) {
+                 RadFuse* fuse = nullptr, const long long* spec_maxw = nullptr) {
     const int64_t M = A->rows, K = A->cols, N = B->cols, w = hi - lo;
     BallsView a = view_of(&A->b), b = view_of(&B->b);
     const int64_t* rtop = rtop_in;
@@ -2486,6 +2616,7 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         P.cta_begin = (const int*)(dunits + off_begin);
         P.Tw = Tw;
         P.Tc = Tc;
+        P.spec_maxw = spec_maxw;
         static const int dbg = std::getenv("APB_GEMM_DEBUG") ? std::atoi(std::getenv("APB_GEMM_DEBUG")) : 0;
         P.debug = dbg;  // timing experiments only (results are wrong when set)
         if (dbg & 4) {  // clock64 trace of the band kernel, dumped to stderr after the call
@@ -2551,6 +2682,9 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     R.int_limbs = int_limbs;
     R.status = workspace().status_dev;
     R.quad = band ? 1 : 0;
+    R.spec_maxw = spec_maxw;
+    R.spec_sa = SA;
+    R.spec_sb = SB;
     tok = prof_begin("recombine", st);
     {
         const int NT = (NW + 1) / 2 + 2;
@@ -2748,6 +2882,10 @@ cudaStream_t side_stream() {
 struct GraphSet {
     cudaGraphExec_t g1 = nullptr, gr = nullptr;
     int64_t n1 = 0, nr = 0;  // kernels per launch (launch counter)
+    // the whole single-block step as one graph (scan .. recombine, radius branch),
+    // the GEMM and recombine speculating on the slice counts k2s of the last call
+    std::map<std::vector<int64_t>, std::pair<cudaGraphExec_t, int64_t>> g1s;
+    std::vector<int64_t> k2s;  // slice counts of the last call's plan
     std::map<std::vector<int64_t>, std::pair<cudaGraphExec_t, int64_t>> g2;
 };
 
@@ -2762,6 +2900,7 @@ struct GraphCache {
         cudaDeviceSynchronize();
         for (auto& kv : sets) {
             if (kv.second.g1) cudaGraphExecDestroy(kv.second.g1);
+            for (auto& g : kv.second.g1s) cudaGraphExecDestroy(g.second.first);
             if (kv.second.gr) cudaGraphExecDestroy(kv.second.gr);
             for (auto& g : kv.second.g2) cudaGraphExecDestroy(g.second.first);
         }
@@ -2825,8 +2964,9 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         CW.top[q] = sbuf<int64_t>(cslot[2 * q], N, st);
         CW.bot[q] = sbuf<int64_t>(cslot[2 * q + 1], N, st);
     }
-    long long* mw1 = sbuf<long long>(kRad[0].mw, 4, st);
-    long long* mw2 = sbuf<long long>(kRad[1].mw, 4, st);
+    // the radius windows ride in the summary: one D2H for the planner
+    long long* mw1 = sum ? sum->mw : nullptr;
+    long long* mw2 = sum ? sum->mw + 4 : nullptr;
     int64_t* ec1 = sbuf<int64_t>(kRad[0].ce, M, st);
     int64_t* ec2 = sbuf<int64_t>(kRad[1].ce, M, st);
     int64_t* fc1 = sbuf<int64_t>(kRad[0].cf, N, st);
@@ -2881,7 +3021,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         if (!sAp || !sBp || !esc || !fsc) return APB_ERR_CUDA;
     }
     ScanSummary* hs = pinned_summary();
-    long long* hw = (long long*)(hs + 1);
+    long long* hw = hs->mw;
 
     auto phase1 = [&](cudaStream_t s, bool capturing) -> int {
         const int tk_scan = prof_begin("scan", s);
@@ -2896,8 +3036,6 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         cudaEventRecord(ev_fork, s);
         cudaStreamWaitEvent(cps, ev_fork, 0);
         cudaMemcpyAsync(hs, sum, sizeof(ScanSummary), cudaMemcpyDeviceToHost, cps);
-        cudaMemcpyAsync(hw, mw1, 4 * sizeof(long long), cudaMemcpyDeviceToHost, cps);
-        cudaMemcpyAsync(hw + 4, mw2, 4 * sizeof(long long), cudaMemcpyDeviceToHost, cps);
         rec_event(ev_plan, cps, capturing);
         if (sncw) {
             const int tk = prof_begin("pack", s);
@@ -2936,18 +3074,37 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     // speculative radius products (single radius block; sparse/dense chosen on the device)
     auto phaseR = [&](cudaStream_t ss, bool capturing) -> int {
         const int tk = prof_begin("radius", ss);
+        RadPair rp{M, K, N, da1, db1, da2, db2, ec1, fc1, ec2, fc2, r1b, r2b, r1f, r2f, mw1, mw2};
+        static const bool split = std::getenv("APB_RAD_SPLIT") != nullptr;  // previous 6-launch schedule
+        if (!split) {
+            const int64_t nA = blocks_for(M * K, 256);
+            fused_planes2_kernel<<<(unsigned)(nA + blocks_for(K * N, 256)), 256, 0, ss>>>(av, bv, rp, nA);
+            rad_sparse2_kernel<2, 128><<<(unsigned)(N + M), 128, 0, ss>>>(rp);
+            rad_gemm2_kernel<<<dim3(blocks_for(N, RT), blocks_for(M, RT), 2), RTHREADS, 0, ss>>>(rp);
+            prof_end(tk, ss);
+            rec_event(ev_join, ss, capturing);
+            count_launch(3);
+            return cuda_check(cudaGetLastError(), "radius");
+        }
         fused_planes_kernel<<<blocks_for(M * K, 256), 256, 0, ss>>>(av, M, K, 1, ec1, ec2, da1, da2, nullptr, nullptr);
         fused_planes_kernel<<<blocks_for(K * N, 256), 256, 0, ss>>>(bv, K, N, 0, fc1, fc2, db1, db2, nullptr, nullptr);
+        // sparse products first, as 128-thread blocks small enough (registers, ~29 KB
+        // smem) to share an SM with a band-GEMM CTA; the dense variants (which stand
+        // down unless the device picked them) last
+        static const bool carve = [] {
+            cudaFuncSetAttribute(rad_spcol_v3_kernel<2, 128>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            cudaFuncSetAttribute(rad_sprow_v3_kernel<2, 128>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            return true;
+        }();
+        (void)carve;
         const int tk1 = prof_begin("rad_gemm", ss);
-        rad_spcol_v3_kernel<2><<<(unsigned)N, 256, 0, ss>>>(da1, db1, M, N, K, ec1, fc1, r1b, r1f, mw1);
+        rad_spcol_v3_kernel<2, 128><<<(unsigned)N, 128, 0, ss>>>(da1, db1, M, N, K, ec1, fc1, r1b, r1f, mw1);
+        rad_sprow_v3_kernel<2, 128><<<(unsigned)M, 128, 0, ss>>>(da2, db2, M, N, K, ec2, fc2, r2b, r2f, mw2);
         rad_gemm_kernel<<<dim3(blocks_for(N, RT), blocks_for(M, RT)), RTHREADS, 0, ss>>>(da1, db1, M, N, K, ec1, fc1,
                                                                                        r1b, r1f, 0, 1, mw1);
-        prof_end(tk1, ss);
-        const int tk2 = prof_begin("rad_gemm", ss);
-        rad_sprow_v3_kernel<2><<<(unsigned)M, 256, 0, ss>>>(da2, db2, M, N, K, ec2, fc2, r2b, r2f, mw2);
         rad_gemm_kernel<<<dim3(blocks_for(N, RT), blocks_for(M, RT)), RTHREADS, 0, ss>>>(da2, db2, M, N, K, ec2, fc2,
                                                                                        r2b, r2f, 0, 0, mw2);
-        prof_end(tk2, ss);
+        prof_end(tk1, ss);
         prof_end(tk, ss);
         rec_event(ev_join, ss, capturing);
         count_launch(6);
@@ -2971,7 +3128,14 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     }
     int rc;
     cudaStream_t side = side_stream();
-    if (gs) {
+    static const bool no_spec_step = std::getenv("APB_NO_SPEC_STEP") != nullptr;  // test hook
+    const auto g1s_it = gs ? gs->g1s.find(gs->k2s) : std::map<std::vector<int64_t>, std::pair<cudaGraphExec_t, int64_t>>::iterator{};
+    const bool full_spec = gs && g1s_it != gs->g1s.end() && !no_spec_step;
+    const std::vector<int64_t> k2_spec = full_spec ? gs->k2s : std::vector<int64_t>{};
+    if (full_spec) {
+        if (cudaGraphLaunch(g1s_it->second.first, st) != cudaSuccess) return cuda_check(cudaGetLastError(), "graph G1S");
+        launch_count_adjust(g1s_it->second.second);
+    } else if (gs) {
         if (cudaGraphLaunch(gs->g1, st) != cudaSuccess) return cuda_check(cudaGetLastError(), "graph G1");
         cudaStreamWaitEvent(side, ev_fin, 0);
         if (cudaGraphLaunch(gs->gr, side) != cudaSuccess) return cuda_check(cudaGetLastError(), "graph GR");
@@ -3027,10 +3191,55 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         count_launch();
         return cuda_check(cudaGetLastError(), "block matmul");
     };
+    if (full_spec) {
+        const std::vector<int64_t> k2 = {slices_for(P.maxw_a), slices_for(P.maxw_b)};
+        gs->k2s = k2;
+        if (!rad_multi && prepacked && k2 == k2_spec) {  // the whole step already ran in G1S
+            stats().int_gemm_products++;
+            stats().last_height_a = (uint64_t)P.maxw_a;
+            stats().last_height_b = (uint64_t)P.maxw_b;
+            stats().last_slices_a = (uint64_t)k2[0];
+            stats().last_slices_b = (uint64_t)k2[1];
+            htrace().mark("done");
+            htrace().flush();
+            return APB_OK;
+        }
+        // the GEMM / recombine of G1S stood down (or the plan is not single-block):
+        // continue below exactly as after G1 + GR (whose work G1S contains)
+    }
     if (gs && spec && !rad_multi && prepacked) {  // the speculation held: G2
         const std::vector<int64_t> k2 = {slices_for(P.maxw_a), slices_for(P.maxw_b)};
         auto it = gs->g2.find(k2);
-        if (it != gs->g2.end()) {
+        gs->k2s = k2;
+        if (it != gs->g2.end() && !full_spec && !gs->g1s.count(k2) && !no_spec_step) {
+            // capture the fused single-graph step for the next call with these operands
+            static cudaEvent_t ev_rdone = make_event();
+            int64_t ns = 0;
+            const uint64_t gemm_products = stats().int_gemm_products;
+            cudaGraphExec_t g1 = capture(
+                [&](cudaStream_t cs) -> int {
+                    int r = phase1(cs, true);
+                    if (r) return r;
+                    cudaStreamWaitEvent(side, ev_fork, 0);  // radius branch after the scan
+                    if ((r = phaseR(side, true))) return r;
+                    cudaEventRecord(ev_rdone, side);
+                    // the GEMM takes every SM: let the (short) radius branch finish first
+                    // instead of having its blocks queue behind the GEMM (APB_RAD_AFTER=1: old order)
+                    static const bool rad_after = std::getenv("APB_RAD_AFTER") != nullptr;
+                    if (!rad_after) cudaStreamWaitEvent(cs, ev_rdone, 0);
+                    RadFuse fz{r1b, r1f, r2b, r2f, ev_rdone, false, false};
+                    r = scaled_block(A, B, 0, K, prec, C, true, P.maxw_a, P.maxw_b, RW.top[0], RW.bot[0],
+                                     CW.top[0], CW.bot[0], nullptr, 0, nullptr, nullptr, cs, nullptr, true, &fz,
+                                     &sum->maxw_a);
+                    if (!r && !fz.used) r = APB_ERR_UNSUPPORTED;  // needs the fused recombine
+                    cudaStreamWaitEvent(cs, ev_rdone, 0);           // rejoin the radius branch
+                    return r;
+                },
+                &ns);
+            stats().int_gemm_products = gemm_products;
+            if (g1) gs->g1s[k2] = {g1, ns};
+        }
+        if (it != gs->g2.end() && !full_spec) {
             // host-side effects of scaled_block that a replay skips
             stats().int_gemm_products++;
             stats().last_height_a = (uint64_t)P.maxw_a;
@@ -3044,11 +3253,13 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
             return APB_OK;
         }
         if ((rc = phase2(st, false))) return rc;
-        int64_t n2 = 0;
-        const uint64_t gemm_products = stats().int_gemm_products;
-        cudaGraphExec_t g2 = capture([&](cudaStream_t cs) { return phase2(cs, true); }, &n2);
-        stats().int_gemm_products = gemm_products;  // the capture pass ran no product
-        if (g2) gs->g2[k2] = {g2, n2};
+        if (it == gs->g2.end()) {
+            int64_t n2 = 0;
+            const uint64_t gemm_products = stats().int_gemm_products;
+            cudaGraphExec_t g2 = capture([&](cudaStream_t cs) { return phase2(cs, true); }, &n2);
+            stats().int_gemm_products = gemm_products;  // the capture pass ran no product
+            if (g2) gs->g2[k2] = {g2, n2};
+        }
         htrace().mark("done");
         htrace().flush();
         return APB_OK;

@@ -80,7 +80,8 @@ def test_full_config_vs_reference(cfg):
 @pytest.mark.parametrize("hook", ["APB_FORCE_UNIT_GEMM=1", "APB_PACK_V1=1", "APB_RAD_V1=1", "APB_RAD_V2=1", "APB_RAD_ORDER=1",
                                   "APB_RAD_ORDER=0", "APB_RAD_ORDER=2", "APB_RAD_ORDER=3", "APB_BAND_BN=128", "APB_BAND_V2=1",
                                   "APB_NO_SPEC_PACK=1", "APB_NO_GRAPHS=1",
-                                  "APB_RECOMBINE64=1", "APB_NO_RAD_FUSE=1", "APB_NO_PDL=1"])
+                                  "APB_RECOMBINE64=1", "APB_NO_RAD_FUSE=1", "APB_NO_PDL=1",
+                                  "APB_NO_SPEC_STEP=1", "APB_NO_PRIO=1", "APB_RAD_SPLIT=1", "APB_RAD_AFTER=1"])
 def test_kernel_variants_golden(hook):
     """alternative kernels / schedules selected by the library's tuning hooks
     (unit GEMM used when a diagonal could overflow int32, byte-serial pack,
