@@ -171,6 +171,16 @@ int apb_block_int_product(const apb_mat* A, const apb_mat* B, int64_t lo, int64_
                           int64_t* row_scale, int64_t* col_scale, uint64_t* out,
                           int64_t out_limbs, void* stream);
 
+/* Measurement baseline: the same exact block product as apb_block_int_product
+ * computed with 32-bit limbs on the CUDA cores (IMAD.WIDE.U32, one thread per
+ * output entry) instead of int8 slices on the tensor cores -- the alternative
+ * the int8 design is chosen against (BASELINE.json north_star).  Same outputs;
+ * *gemm_ms (nullable) receives the product kernel's time.  Heights above
+ * 19 x 32 bits return APB_ERR_UNSUPPORTED.  Synchronizes the stream. */
+int apb_block_int_product_imad(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi,
+                               int64_t* row_scale, int64_t* col_scale, uint64_t* out,
+                               int64_t out_limbs, float* gemm_ms, void* stream);
+
 /* Parity hook: greedy block plan (include/apball/matmul.hpp:73, src/matmul.cpp:132-161).
  * steps_out receives up to max_steps triples (lo, hi, basecase); *n_steps the count. */
 int apb_plan_blocks(const apb_mat* A, const apb_mat* B, int64_t prec, int64_t* steps_out,

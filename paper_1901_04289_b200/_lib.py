@@ -58,6 +58,8 @@ def lib():
     L.apb_matmul_complex.restype = I
     L.apb_block_int_product.argtypes = [mp, mp, I64, I64, P, P, P, I64, P]
     L.apb_block_int_product.restype = I
+    L.apb_block_int_product_imad.argtypes = [mp, mp, I64, I64, P, P, P, I64, P, P]
+    L.apb_block_int_product_imad.restype = I
     L.apb_plan_blocks.argtypes = [mp, mp, I64, P, I64, P, P]
     L.apb_plan_blocks.restype = I
     L.apb_radius_matmul_upper.argtypes = [P, P, P, P, I64, I64, I64, P, P, P]

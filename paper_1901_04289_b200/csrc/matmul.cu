@@ -572,6 +572,7 @@ struct RecombineArgs {
     int int_limbs;
     int* status;
     int quad;  // band GEMM layout: plane[(j/4)][i][j%4] (coalesced epilogue stores), else [i][j]
+    int digit_bits = 32;  // bits per Tw plane digit: 8 x diagonals per word
     // optional fused radius combine (recombine16 only): C.rad = err (+) (r1 (+) r2), the
     // rad_combine_kernel step of src/matmul.cpp:512-513 folded into the store
     const uint32_t* r1b = nullptr;
@@ -598,7 +599,13 @@ __global__ void __launch_bounds__(128) recombine_kernel(RecombineArgs R) {
     const int NT = (R.nwords + 1) / 2 + 2;
     uint64_t T[CAP];
     for (int q = 0; q < NT; q++) T[q] = 0;
-    for (int w = 0; w < R.nwords; w++) T[w >> 1] |= (uint64_t)R.Tw[(size_t)w * plane + off] << (32 * (w & 1));
+    // plane w holds digit w in base 2^(8 diagonals per word): 32-bit words (4 diagonals,
+    // unit / 128-wide band kernel) or 16-bit digits (2 diagonals, 256-wide band kernel)
+    const int db = R.digit_bits;
+    for (int w = 0; w < R.nwords; w++) {
+        const int64_t bit = (int64_t)db * w;
+        T[bit >> 6] |= (uint64_t)R.Tw[(size_t)w * plane + off] << (bit & 63);
+    }
     for (int g = 0; g < R.n_groups; g++) {
         const int64_t c = R.Tc[(size_t)g * plane + off];
         if (c == 0) continue;
@@ -959,6 +966,141 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
     if (R.r1b) err = mag_add(err, rsum);
     mag_store(err, &O.rad_man[t], &O.rad_exp[t]);
     if (st) *R.status = st;
+}
+
+
+// ------------------------------------------------ IMAD-limb baseline (K5')
+// The same exact block product on CUDA cores, the alternative the north star
+// weighs the int8 slices against: scaled integers as sign-magnitude 32-bit limb
+// planes, one thread per output entry, Q x Q IMAD.WIDE.U32 limb products per
+// term into 2Q signed 64-bit column sums (|sum| < K 2^32 Q), carried into two's
+// complement limbs at the end.  Used for measurement (apb_block_int_product_imad)
+// and checked against the tensor-core product bit for bit.
+
+// magnitude limbs of mid * 2^scale: A planes [q][r][kk] (rows x w), B planes [q][kk][j] (w x N)
+template <int Q>
+__global__ void __launch_bounds__(256) limb_pack_kernel(BallsView X, int64_t rows, int64_t cols, int64_t ld,
+                                                        int64_t lo, int a_side, const int64_t* top,
+                                                        const int64_t* bot, uint32_t* out, uint8_t* sgn,
+                                                        int64_t* scale_out) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= rows * cols) return;
+    const int64_t r = t / cols, c = t % cols;  // A: (row, kk); B: (kk, col)
+    const int64_t line = a_side ? r : c;
+    const int64_t sc = top[line] == INT64_MIN ? 0 : -bot[line];
+    if (scale_out && (a_side ? c == 0 : r == 0)) scale_out[line] = sc;
+    const int64_t e = a_side ? r * ld + lo + c : (lo + r) * ld + c;
+    const uint8_t kd = X.kind[e];
+    const bool live = (kd & APB_KIND_MASK) == APB_FINITE;
+    const int L = X.L;
+    const int64_t sh = live ? X.exp[e] - 64 * (int64_t)L + sc : 0;
+    const int64_t lq = (-sh) >> 6;
+    const int bo = (int)((-sh) & 63);
+    const uint64_t* m = X.mant + e * (int64_t)L;
+    const size_t plane = (size_t)rows * cols;
+#pragma unroll
+    for (int q2 = 0; q2 < (Q + 1) / 2; q2++) {
+        const int64_t li = q2 + lq;
+        const uint64_t g0 = (live && li >= 0 && li < L) ? m[li] : 0ull;
+        const uint64_t g1 = (live && li + 1 >= 0 && li + 1 < L) ? m[li + 1] : 0ull;
+        const uint64_t wv = bo ? (g0 >> bo) | (g1 << (64 - bo)) : g0;
+        out[(size_t)(2 * q2) * plane + t] = (uint32_t)wv;
+        if (2 * q2 + 1 < Q) out[(size_t)(2 * q2 + 1) * plane + t] = (uint32_t)(wv >> 32);
+    }
+    sgn[t] = live && (kd & APB_SIGN) ? 1 : 0;
+}
+
+template <int Q, int TM, int TN>
+__global__ void __launch_bounds__(256) imad_gemm_kernel(const uint32_t* __restrict__ Al, const uint8_t* __restrict__ As,
+                                                        const uint32_t* __restrict__ Bl, const uint8_t* __restrict__ Bs,
+                                                        int64_t M, int64_t N, int64_t w, uint64_t* out, int out_limbs) {
+    // 16 x 16 threads, each TM x TN outputs (rows ty + 16 r, cols tx + 16 c); K staged
+    // through shared memory KT terms at a time (limb planes [q][kk][row|col])
+    constexpr int KT = 8, BM_ = 16 * TM, BN_ = 16 * TN;
+    __shared__ uint32_t sa[Q][KT][BM_];
+    __shared__ uint32_t sb[Q][KT][BN_];
+    __shared__ uint8_t ssa[KT][BM_], ssb[KT][BN_];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t i0 = (int64_t)blockIdx.y * BM_, j0 = (int64_t)blockIdx.x * BN_;
+    const size_t pa = (size_t)M * w, pb = (size_t)w * N;
+    int64_t acc[TM][TN][2 * Q];
+#pragma unroll
+    for (int r = 0; r < TM; r++)
+#pragma unroll
+        for (int c = 0; c < TN; c++)
+#pragma unroll
+            for (int q = 0; q < 2 * Q; q++) acc[r][c][q] = 0;
+    for (int64_t k0 = 0; k0 < w; k0 += KT) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < KT * BM_; e += 256) {  // A: (row, kk), kk fastest (contiguous in k)
+            const int kk = e % KT, row = e / KT;
+            const int64_t i = i0 + row, k = k0 + kk;
+            const bool ok = i < M && k < w;
+#pragma unroll
+            for (int q = 0; q < Q; q++) sa[q][kk][row] = ok ? __ldg(Al + q * pa + i * w + k) : 0u;
+            ssa[kk][row] = ok ? __ldg(As + i * w + k) : 0;
+        }
+        for (int e = threadIdx.x; e < KT * BN_; e += 256) {  // B: (kk, col), col fastest
+            const int col = e % BN_, kk = e / BN_;
+            const int64_t j = j0 + col, k = k0 + kk;
+            const bool ok = j < N && k < w;
+#pragma unroll
+            for (int q = 0; q < Q; q++) sb[q][kk][col] = ok ? __ldg(Bl + q * pb + k * N + j) : 0u;
+            ssb[kk][col] = ok ? __ldg(Bs + k * N + j) : 0;
+        }
+        __syncthreads();
+#pragma unroll 2
+        for (int kk = 0; kk < KT; kk++) {
+            uint32_t a[TM][Q], bb[TN][Q];
+            int64_t sgn_a[TM], sgn_b[TN];
+#pragma unroll
+            for (int r = 0; r < TM; r++) {
+#pragma unroll
+                for (int q = 0; q < Q; q++) a[r][q] = sa[q][kk][ty + 16 * r];
+                sgn_a[r] = ssa[kk][ty + 16 * r];
+            }
+#pragma unroll
+            for (int c = 0; c < TN; c++) {
+#pragma unroll
+                for (int q = 0; q < Q; q++) bb[c][q] = sb[q][kk][tx + 16 * c];
+                sgn_b[c] = ssb[kk][tx + 16 * c];
+            }
+#pragma unroll
+            for (int r = 0; r < TM; r++)
+#pragma unroll
+                for (int c = 0; c < TN; c++) {
+                    const int64_t msk = -(sgn_a[r] ^ sgn_b[c]);
+#pragma unroll
+                    for (int qa = 0; qa < Q; qa++)
+#pragma unroll
+                        for (int qb = 0; qb < Q; qb++) {
+                            const uint64_t p = (uint64_t)a[r][qa] * bb[c][qb];
+                            acc[r][c][qa + qb] += (((int64_t)(p & 0xFFFFFFFFull)) ^ msk) - msk;
+                            acc[r][c][qa + qb + 1] += (((int64_t)(p >> 32)) ^ msk) - msk;
+                        }
+                }
+        }
+    }
+    // column sums -> two's complement 32-bit words -> 64-bit limbs (the carry out of
+    // the last column still holds magnitude bits: keep emitting it)
+#pragma unroll
+    for (int r = 0; r < TM; r++)
+#pragma unroll
+        for (int c = 0; c < TN; c++) {
+            const int64_t i = i0 + ty + 16 * r, j = j0 + tx + 16 * c;
+            if (i >= M || j >= N) continue;
+            uint64_t* dst = out + (size_t)(i * N + j) * out_limbs;
+            int64_t carry = 0;
+            uint64_t lw = 0;
+            int li = 0;
+            for (int q = 0; li < out_limbs; q++) {
+                const int64_t v = (q < 2 * Q ? acc[r][c][q] : 0) + carry;
+                const uint64_t wd = (uint64_t)v & 0xFFFFFFFFull;
+                carry = v >> 32;
+                if (q & 1) dst[li++] = lw | (wd << 32);
+                else lw = wd;
+            }
+        }
 }
 
 // ------------------------------------------------------------ K7 radius
@@ -2682,6 +2824,7 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     R.int_limbs = int_limbs;
     R.status = workspace().status_dev;
     R.quad = band ? 1 : 0;
+    R.digit_bits = band ? 8 * band_w : 32;
     R.spec_maxw = spec_maxw;
     R.spec_sa = SA;
     R.spec_sb = SB;
@@ -3398,6 +3541,78 @@ int apb_matmul_complex(const apb_mat* Are, const apb_mat* Aim, const apb_mat* Br
     return cuda_check(cudaGetLastError(), "complex matmul");
 }
 
+// IMAD-limb baseline of apb_block_int_product: same scan, 32-bit limb planes,
+// CUDA-core product (imad_gemm_kernel); the GEMM time goes to *gemm_ms if given
+int imad_block_product(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int64_t* row_scale,
+                       int64_t* col_scale, uint64_t* out, int64_t out_limbs, float* gemm_ms, cudaStream_t st) {
+    const int64_t M = A->rows, N = B->cols, w = hi - lo;
+    BallsView a = view_of(&A->b), b = view_of(&B->b);
+    int64_t* rt = sbuf<int64_t>(S_RTOP, M, st);
+    int64_t* rb = sbuf<int64_t>(S_RBOT, M, st);
+    int64_t* ct = sbuf<int64_t>(S_CTOP, N, st);
+    int64_t* cb = sbuf<int64_t>(S_CBOT, N, st);
+    ScanSummary* sum = sbuf<ScanSummary>(S_SUM, 1, st);
+    if (!rt || !rb || !ct || !cb || !sum) return APB_ERR_CUDA;
+    cudaMemsetAsync(sum, 0, sizeof(ScanSummary), st);
+    scan_rows_kernel<<<blocks_for(M, 8), 256, 0, st>>>(a, M, A->cols, lo, hi, rt, rb, sum);
+    scan_cols(b, A->cols, N, lo, hi, ct, cb, sum, st);
+    ScanSummary h;
+    cudaMemcpyAsync(&h, sum, sizeof h, cudaMemcpyDeviceToHost, st);
+    int rc = cuda_check(cudaStreamSynchronize(st), "imad scan");
+    if (rc) return rc;
+    const int Qn = (int)((std::max(h.maxw_a, h.maxw_b) + 31) / 32);
+    int Q = 0;
+    for (int c : {4, 6, 8, 11, 14, 19})
+        if (!Q && Qn <= c) Q = c;
+    if (!Q) {
+        set_error("imad baseline: entry height above 19 limbs");
+        return APB_ERR_UNSUPPORTED;
+    }
+    uint32_t* Al = sbuf<uint32_t>(S_APACK, (size_t)Q * M * w, st);
+    uint32_t* Bl = sbuf<uint32_t>(S_BPACK, (size_t)Q * w * N, st);
+    uint8_t* As = sbuf<uint8_t>(S_TW, (size_t)M * w, st);
+    uint8_t* Bs = sbuf<uint8_t>(S_TC, (size_t)w * N, st);
+    if (!Al || !Bl || !As || !Bs) return APB_ERR_CUDA;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const dim3 g((unsigned)((N + 15) / 16), (unsigned)((M + 15) / 16));
+    const dim3 g2((unsigned)((N + 31) / 32), (unsigned)((M + 31) / 32));
+    const dim3 g21((unsigned)((N + 15) / 16), (unsigned)((M + 31) / 32));
+#define APB_IMAD_Q(QQ)                                                                                       \
+    case QQ:                                                                                                 \
+        limb_pack_kernel<QQ><<<blocks_for(M * w, 256), 256, 0, st>>>(a, M, w, A->cols, lo, 1, rt, rb, Al, As,  \
+                                                                       row_scale);                            \
+        limb_pack_kernel<QQ><<<blocks_for(w * N, 256), 256, 0, st>>>(b, w, N, N, lo, 0, ct, cb, Bl, Bs,        \
+                                                                       col_scale);                            \
+        cudaEventRecord(e0, st);                                                                              \
+        if constexpr (QQ <= 6)                                                                                \
+            imad_gemm_kernel<QQ, 2, 2><<<g2, 256, 0, st>>>(Al, As, Bl, Bs, M, N, w, out, (int)out_limbs);        \
+        else if constexpr (QQ <= 8)                                                                           \
+            imad_gemm_kernel<QQ, 2, 1><<<g21, 256, 0, st>>>(Al, As, Bl, Bs, M, N, w, out, (int)out_limbs);       \
+        else                                                                                                  \
+            imad_gemm_kernel<QQ, 1, 1><<<g, 256, 0, st>>>(Al, As, Bl, Bs, M, N, w, out, (int)out_limbs);         \
+        cudaEventRecord(e1, st);                                                                              \
+        break;
+    switch (Q) {
+        APB_IMAD_Q(4)
+        APB_IMAD_Q(6)
+        APB_IMAD_Q(8)
+        APB_IMAD_Q(11)
+        APB_IMAD_Q(14)
+        APB_IMAD_Q(19)
+    }
+#undef APB_IMAD_Q
+    count_launch(3);
+    rc = cuda_check(cudaEventSynchronize(e1), "imad gemm");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (gemm_ms) *gemm_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return rc;
+}
+
 int apb_block_int_product(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int64_t* row_scale,
                           int64_t* col_scale, uint64_t* out, int64_t out_limbs, void* stream) {
     if (!A || !B || A->cols != B->rows || lo < 0 || hi > A->cols || hi <= lo) {
@@ -3406,6 +3621,15 @@ int apb_block_int_product(const apb_mat* A, const apb_mat* B, int64_t lo, int64_
     }
     return scaled_block(A, B, lo, hi, 0, nullptr, true, 0, 0, nullptr, nullptr, nullptr, nullptr,
                         (int64_t*)out, (int)out_limbs, row_scale, col_scale, (cudaStream_t)stream);
+}
+
+int apb_block_int_product_imad(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int64_t* row_scale,
+                               int64_t* col_scale, uint64_t* out, int64_t out_limbs, float* gemm_ms, void* stream) {
+    if (!A || !B || A->cols != B->rows || lo < 0 || hi > A->cols || hi <= lo) {
+        set_error("int_matmul: dimension mismatch");
+        return APB_ERR_INVALID;
+    }
+    return imad_block_product(A, B, lo, hi, row_scale, col_scale, out, out_limbs, gemm_ms, (cudaStream_t)stream);
 }
 
 int apb_plan_blocks(const apb_mat* A, const apb_mat* B, int64_t prec, int64_t* steps_out, int64_t max_steps,

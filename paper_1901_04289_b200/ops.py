@@ -359,6 +359,24 @@ def block_int_product(a: BallMatrix, b: BallMatrix, lo: int, hi: int, out_limbs:
             out.cpu().numpy().view(np.uint64).reshape(a.rows * b.cols, out_limbs))
 
 
+def block_int_product_imad(a: BallMatrix, b: BallMatrix, lo: int, hi: int, out_limbs: int, stream=None):
+    """block_int_product on the CUDA cores with 32-bit limbs (the IMAD baseline the
+    int8 tensor-core product is measured against); returns (row_scale, col_scale, T, gemm_ms)"""
+    import torch
+    lib = _lib.lib()
+    am, bm = a.c(), b.c()
+    rs = torch.zeros(a.rows, dtype=torch.int64, device="cuda")
+    cs = torch.zeros(b.cols, dtype=torch.int64, device="cuda")
+    out = torch.zeros(a.rows * b.cols * out_limbs, dtype=torch.int64, device="cuda")
+    ms = C.c_float(0.0)
+    st = _stream_ptr(stream)
+    _lib.check(lib.apb_block_int_product_imad(C.byref(am), C.byref(bm), lo, hi, rs.data_ptr(), cs.data_ptr(),
+                                              out.data_ptr(), out_limbs, C.byref(ms), st),
+               "apb_block_int_product_imad")
+    return (rs.cpu().numpy(), cs.cpu().numpy(),
+            out.cpu().numpy().view(np.uint64).reshape(a.rows * b.cols, out_limbs), ms.value)
+
+
 def radius_matmul_upper(pm, pe, qm, qe, m: int, n: int, k: int, stream=None):
     """radius_matmul_upper (include/apball/matmul.hpp:87) on Mag planes (mantissa, exponent)"""
     import torch

@@ -139,3 +139,68 @@ def test_graph_replay_tracks_new_inputs():
     got = ops.block_matmul_ball(A, B, p, out=out).balls.to_host()
     ref, _ = po.matmul(a2, b2, n, n, n, p, which="ref", algo=1, threads=os.cpu_count() or 8)
     assert got.identical(ref).all()
+
+
+@pytest.mark.parametrize("path", MM, ids=[name(p) for p in MM])
+def test_imad_baseline_golden(path):
+    """the CUDA-core IMAD-limb baseline of the exact block product equals the
+    reference's int_matmul on every golden block (heights up to 19 x 32 bits)"""
+    from paper_1901_04289_b200 import ops
+    d = np.load(path)
+    a, b = balls(d, "a"), balls(d, "b")
+    M, K, N = (int(d[k]) for k in ("M", "K", "N"))
+    A, B = _mat(a, M, K), _mat(b, K, N)
+    checked = 0
+    for bi in d["int_blocks"]:
+        lo, hi, _ = (int(v) for v in d["plan"][int(bi)])
+        T = d[f"int_{bi}_T"]
+        try:
+            rs, cs, got, ms = ops.block_int_product_imad(A, B, lo, hi, T.shape[1])
+        except RuntimeError as e:
+            assert "19 limbs" in str(e)
+            continue
+        np.testing.assert_array_equal(rs, d[f"int_{bi}_rows"])
+        np.testing.assert_array_equal(cs, d[f"int_{bi}_cols"])
+        bad = np.nonzero((got != T).any(axis=1))[0]
+        assert len(bad) == 0, f"{len(bad)} entries differ, first {bad[:5]}"
+        checked += 1
+    assert checked or not len(d["int_blocks"]) or int(d["prec"]) > 512
+
+
+def test_imad_baseline_matches_tensor_core_c3():
+    """config 3 at full size: IMAD-limb and int8 tensor-core exact products agree bit for bit"""
+    from paper_1901_04289_b200 import ops
+    a, b = gen.config3_matrices()
+    A, B = _mat(a, 512, 512), _mat(b, 512, 512)
+    rs, cs, t8 = ops.block_int_product(A, B, 0, 512, 10)
+    rs2, cs2, ti, ms = ops.block_int_product_imad(A, B, 0, 512, 10)
+    np.testing.assert_array_equal(rs, rs2)
+    np.testing.assert_array_equal(cs, cs2)
+    np.testing.assert_array_equal(t8, ti)
+    assert ms > 0
+
+
+def test_multiblock_wide_vs_reference():
+    """multi-block plan on a matrix wide enough for the 256-column band tiles
+    (16-bit band digits through the general recombine, blocks after the first
+    adding into C): bit-identical to block_matmul_ball, exact block products
+    identical between the tensor-core and IMAD-limb paths"""
+    from paper_1901_04289_b200 import ops
+    rng = np.random.default_rng(0xB200 + 300)
+    n = 300
+    k = np.arange(n)
+    ea = np.tile((k // 110) * 600, n) + np.repeat(np.arange(n) % 5, n)
+    eb = np.repeat(-(k // 110) * 600, n)
+    a = gen.random_balls(rng, n * n, 128, exps=ea, rad_k=110, rad_frac=0.2, zero_frac=0.05)
+    b = gen.random_balls(rng, n * n, 128, exps=eb, rad_k=110, rad_frac=0.2, zero_frac=0.05)
+    A, B = _mat(a, n, n), _mat(b, n, n)
+    plan = ops.plan_blocks(A, B, 128)
+    assert sum(1 for r in plan if not r[2]) >= 2, plan
+    got = ops.block_matmul_ball(A, B, 128).balls.to_host()
+    ref, nb = po.matmul(a, b, n, n, n, 128, which="ref", algo=1, threads=os.cpu_count() or 8)
+    ok = got.identical(ref)
+    assert ok.all(), f"{(~ok).sum()} entries differ"
+    lo, hi, _ = next(r for r in plan if not r[2])
+    _, _, t8 = ops.block_int_product(A, B, lo, hi, 8)
+    _, _, ti, _ = ops.block_int_product_imad(A, B, lo, hi, 8)
+    np.testing.assert_array_equal(t8, ti)
