@@ -1429,6 +1429,118 @@ __global__ void __launch_bounds__(128) dot_generic_kernel(DotArgs A, int fallbac
           A.status);
 }
 
+// ------------------------------------------------------------ wide dots
+// Runtime-size operands and accumulators (p > 512 or n_s > 9, e.g. config 5's
+// p = 1024 / 4096 sweep): one warp per dot, lanes striding over the terms, each
+// lane with a private n_s-limb accumulator (the generic g_acc_term incl.
+// mulhigh_approx, thread-local), then a warp-shuffle carry-propagating reduction
+// of the 32 accumulators (two's complement addition mod 2^(64 n_s) is
+// associative) and lane 0's dot_finalize.  Special-value dots are flagged for the
+// thread-per-dot fallback pass (dot_generic_kernel).
+__global__ void __launch_bounds__(128) dot_wide_kernel(DotArgs A) {
+    const int lane = threadIdx.x & 31;
+    const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (b >= A.batch) return;
+    int64_t ex0, xst, ey0, yst, nb;
+    dot_extent(A, b, ex0, xst, ey0, yst, nb);
+    const int64_t total = nb + (A.has_init ? 1 : 0);
+    const bool approx = A.mode == APB_DOT_APPROX;
+    auto get = [&](int64_t i, GBall& xs, GBall& ys, bool& neg) {
+        if (i < nb) {
+            gb_load(xs, A.x, ex0 + i * xst);
+            gb_load(ys, A.y, ey0 + i * yst);
+            neg = A.subtract != 0;
+        } else {
+            gb_load(xs, A.init, b);
+            gb_one(ys);
+            neg = false;
+        }
+    };
+    // ---- pass 1: setup_core over this lane's terms, warp-reduced
+    GBall xs, ys;
+    ScanAcc sc{INT64_MIN, INT64_MAX, INT64_MIN, 0, false};
+    const bool track_min = A.prec > 128;
+    for (int64_t i = lane; i < total && !sc.fb; i += 32) {
+        bool neg;
+        get(i, xs, ys, neg);
+        const GF& xm = xs.m;
+        const GF& ym = ys.m;
+        if (!(xm.kind == APB_ZERO || xm.kind == APB_FINITE) || !(ym.kind == APB_ZERO || ym.kind == APB_FINITE) ||
+            (xm.kind != APB_ZERO && exp_huge(xm.e)) || (ym.kind != APB_ZERO && exp_huge(ym.e))) {
+            sc.fb = true;
+            break;
+        }
+        if (xm.kind != APB_ZERO && ym.kind != APB_ZERO) {
+            sc.nnz++;
+            const int64_t ee = xm.e + ym.e;
+            if (ee > sc.e_max) sc.e_max = ee;
+            if (track_min) {
+                const int64_t lo = ee - 64 * (int64_t)(xm.n + ym.n);
+                if (lo < sc.e_min) sc.e_min = lo;
+            }
+        }
+        if (!approx) {
+            const Mag& xr = xs.r;
+            const Mag& yr = ys.r;
+            if (xr.kind == 2 || yr.kind == 2 || (xr.kind == 1 && exp_huge(xr.f)) || (yr.kind == 1 && exp_huge(yr.f))) {
+                sc.fb = true;
+                break;
+            }
+            if (yr.kind == 1 && xm.kind != APB_ZERO && xm.e + yr.f > sc.e_rad) sc.e_rad = xm.e + yr.f;
+            if (xr.kind == 1 && ym.kind != APB_ZERO && ym.e + xr.f > sc.e_rad) sc.e_rad = ym.e + xr.f;
+            if (xr.kind == 1 && yr.kind == 1 && xr.f + yr.f > sc.e_rad) sc.e_rad = xr.f + yr.f;
+        }
+    }
+    const bool fb = __any_sync(0xffffffffu, sc.fb);
+    const Plan pl = finish_plan(warp_max(sc.e_max), warp_min(sc.e_min), warp_max(sc.e_rad), warp_sum(sc.nnz), fb,
+                                total, A.prec, A.disable_reduction != 0);
+    if (pl.status != 0) {
+        if (lane == 0) {
+            if (A.state) write_state(A.state + b, pl, 0, 0);
+            if (pl.status == 1) {
+                A.fb_flag[b] = 1;
+            } else {
+                GFloat<1> z;
+                z.kind = APB_ZERO;
+                z.neg = 0;
+                z.e = 0;
+                z.n = 0;
+                gf_store(A.out, b, z, mag_zero(), A.status);
+            }
+        }
+        return;
+    }
+    // ---- pass 2: lane-private accumulators
+    uint64_t s[GCAP];
+    for (int j = 0; j < pl.n_s; j++) s[j] = 0;
+    uint64_t err = 0, srad = 0;
+    for (int64_t i = lane; i < total; i += 32) {
+        bool neg;
+        get(i, xs, ys, neg);
+        if (xs.m.kind != APB_ZERO && ys.m.kind != APB_ZERO) g_acc_term(pl, s, err, xs.m, ys.m, neg);
+        if (!approx) g_rad_term(srad, xs, ys, pl.e_rad);
+    }
+    // ---- warp reduction mod 2^(64 n_s)
+    for (int o = 16; o; o >>= 1) {
+        uint64_t c = 0;
+        for (int j = 0; j < pl.n_s; j++) {
+            const uint64_t v = __shfl_xor_sync(0xffffffffu, s[j], o);
+            const uint64_t s1 = s[j] + v;
+            const uint64_t c1 = s1 < v;
+            const uint64_t s2 = s1 + c;
+            s[j] = s2;
+            c = c1 | (s2 < c);
+        }
+        err += __shfl_xor_sync(0xffffffffu, err, o);
+        srad += __shfl_xor_sync(0xffffffffu, srad, o);
+    }
+    if (lane != 0) return;
+    if (A.state) write_state(A.state + b, pl, err, srad);
+    if (A.acc)
+        for (int j = 0; j < pl.n_s && j < A.acc_stride; j++) A.acc[b * A.acc_stride + j] = s[j];
+    finalize_store<GCAP>(pl, s, err, srad, A.prec, !approx, A.out, b, A.status);
+}
+
 // ------------------------------------------------------------ complex
 
 struct CDotArgs {
@@ -1783,9 +1895,17 @@ int dot_dispatch(DotArgs& A, int Lin, int64_t total, cudaStream_t st) {
     else if (Lin <= 4 && nsb <= 9) try_small_tpl<4, 9>(A, total, st);
     else if (Lin <= 8 && nsb <= 9) try_small_tpl<8, 9>(A, total, st);
     else small = false;
+    // wide precisions: warp per dot (APB_DOT_GENERIC=1: the thread-per-dot kernel alone)
+    static const bool generic_only = std::getenv("APB_DOT_GENERIC") != nullptr;
+    bool flagged = small;
+    if (!small && !generic_only) {
+        dot_wide_kernel<<<(unsigned)((batch * 32 + 127) / 128), 128, 0, st>>>(A);
+        count_launch();
+        flagged = true;
+    }
     const unsigned gthreads = 128;
     dim3 ggrid((unsigned)((batch + gthreads - 1) / gthreads));
-    dot_generic_kernel<<<ggrid, gthreads, 0, st>>>(A, small ? 1 : 0);
+    dot_generic_kernel<<<ggrid, gthreads, 0, st>>>(A, flagged ? 1 : 0);
     prof_end(tok, st);
     count_launch();
     return APB_OK;
