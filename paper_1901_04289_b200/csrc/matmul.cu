@@ -1677,29 +1677,50 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
                            int64_t w, const int64_t* ecen, const int64_t* fcen, uint32_t* rb, int64_t* rf,
                            int accumulate, int a_trans, const long long* sel, int64_t bx, int64_t by) {
     if (sel && rad_variant(sel, M, w, N, a_trans) != 2) return;
+    // 32 x 32 outputs per 64 threads (4 x 4 each), K tiles of 32 staged in shared
+    // memory with the next tile prefetched into registers; per-entry sequential RN
+    // sums (__dmul_rn / __dadd_rn, no contraction) folded into the Mag bound at
+    // every 1024-term chunk end (src/matmul.cpp:404-431); the folded Mags wait in
+    // shared memory (they are touched once per chunk)
     __shared__ double sA[RK][RT + 1];
     __shared__ double sB[RK][RT];
+    __shared__ uint32_t eb[16][RTHREADS];
+    __shared__ int64_t ef[16][RTHREADS];
+    constexpr int PER = RK * RT / RTHREADS;  // tile elements per thread per operand
     const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
     const int64_t i0 = by * RT, j0 = bx * RT;
     double s[4][4];
-    Mag ent[4][4];
 #pragma unroll
     for (int r = 0; r < 4; r++)
 #pragma unroll
         for (int c = 0; c < 4; c++) {
             s[r][c] = 0.0;
-            ent[r][c] = mag_zero();
+            eb[4 * r + c][threadIdx.x] = 0;
+            ef[4 * r + c][threadIdx.x] = 0;
         }
     const Mag infl = mag_parts((1ull << 29) + 1, 1);
-    for (int64_t l0 = 0; l0 < w; l0 += RK) {
-        for (int q = threadIdx.x; q < RK * RT; q += RTHREADS) {
+    double pa[PER], pb[PER];
+    auto fetch = [&](int64_t l0) {
+#pragma unroll
+        for (int u = 0; u < PER; u++) {
+            const int q = threadIdx.x + RTHREADS * u;
             const int kk = q / RT, rr = q % RT;
-            const int64_t gi = i0 + rr, gl = l0 + kk;
-            sA[kk][rr] = (gi < M && gl < w) ? (a_trans ? da[gl * M + gi] : da[gi * w + gl]) : 0.0;
-            const int64_t gj = j0 + rr;
-            sB[kk][rr] = (gj < N && gl < w) ? db[gl * N + gj] : 0.0;
+            const int64_t gi = i0 + rr, gl = l0 + kk, gj = j0 + rr;
+            pa[u] = (gi < M && gl < w) ? (a_trans ? da[gl * M + gi] : da[gi * w + gl]) : 0.0;
+            pb[u] = (gj < N && gl < w) ? db[gl * N + gj] : 0.0;
+        }
+    };
+    fetch(0);
+    for (int64_t l0 = 0; l0 < w; l0 += RK) {
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < PER; u++) {
+            const int q = threadIdx.x + RTHREADS * u;
+            sA[q / RT][q % RT] = pa[u];
+            sB[q / RT][q % RT] = pb[u];
         }
         __syncthreads();
+        if (l0 + RK < w) fetch(l0 + RK);
         const int kmax = (w - l0) < RK ? (int)(w - l0) : RK;
         for (int kk = 0; kk < kmax; kk++) {
             double a[4], b[4];
@@ -1711,21 +1732,22 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
             for (int r = 0; r < 4; r++)
 #pragma unroll
                 for (int c = 0; c < 4; c++) s[r][c] = __dadd_rn(s[r][c], __dmul_rn(a[r], b[c]));
-            const int64_t l = l0 + kk + 1;
-            if ((l % 1024) == 0 || l == w) {  // chunk boundary
-#pragma unroll
-                for (int r = 0; r < 4; r++)
-#pragma unroll
-                    for (int c = 0; c < 4; c++) {
-                        const int64_t gi = i0 + ty * 4 + r, gj = j0 + tx * 4 + c;
-                        if (s[r][c] != 0.0 && gi < M && gj < N)
-                            ent[r][c] = mag_add(ent[r][c],
-                                                mag_mul(mag_from_double(s[r][c], -ecen[gi] - fcen[gj]), infl));
-                        s[r][c] = 0.0;
-                    }
-            }
         }
-        __syncthreads();
+        const int64_t l = l0 + kmax;  // RK divides 1024: chunk ends fall on tile ends
+        if ((l & 1023) == 0 || l == w) {
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    const int64_t gi = i0 + ty * 4 + r, gj = j0 + tx * 4 + c;
+                    if (s[r][c] != 0.0 && gi < M && gj < N) {
+                        const Mag e = mag_add(mag_load(eb[4 * r + c][threadIdx.x], ef[4 * r + c][threadIdx.x]),
+                                              mag_mul(mag_from_double(s[r][c], -ecen[gi] - fcen[gj]), infl));
+                        mag_store(e, &eb[4 * r + c][threadIdx.x], &ef[4 * r + c][threadIdx.x]);
+                    }
+                    s[r][c] = 0.0;
+                }
+        }
     }
 #pragma unroll
     for (int r = 0; r < 4; r++)
@@ -1734,7 +1756,7 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
             const int64_t gi = i0 + ty * 4 + r, gj = j0 + tx * 4 + c;
             if (gi >= M || gj >= N) continue;
             const int64_t o = gi * N + gj;
-            Mag m = ent[r][c];
+            Mag m = mag_load(eb[4 * r + c][threadIdx.x], ef[4 * r + c][threadIdx.x]);
             if (accumulate) {
                 if (m.kind == 0) continue;
                 m = mag_add(mag_load(rb[o], rf[o]), m);

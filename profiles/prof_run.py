@@ -29,6 +29,22 @@ def main():
         A, B = ops.BallMatrix(a.to_device(), 256, 256), ops.BallMatrix(b.to_device(), 256, 256)
         for _ in range(reps):
             ops.block_matmul_ball(A, B, 128)
+    if which in ("c5d", "all"):  # wide-precision dots (warp per dot)
+        for p in (1024, 4096):
+            x, y = gen.config5_dots(batch=2048, p=p)
+            dx, dy = x.to_device(), y.to_device()
+            for _ in range(reps):
+                ops.dot_batch(dx, dy, 1000, 2048, p)
+    if which in ("c5m", "all"):  # slice GEMM (unit path) at p = 512, N = 1024
+        a, b = gen.config5_matrices(n=1024, p=512)
+        A, B = ops.BallMatrix(a.to_device(), 1024, 1024), ops.BallMatrix(b.to_device(), 1024, 1024)
+        for _ in range(reps):
+            ops.block_matmul_ball(A, B, 512)
+    if which in ("imad", "all"):  # IMAD-limb baseline product at N = 512, p = 128
+        a, b = gen.config5_matrices(n=512, p=128)
+        A, B = ops.BallMatrix(a.to_device(), 512, 512), ops.BallMatrix(b.to_device(), 512, 512)
+        for _ in range(reps):
+            ops.block_int_product_imad(A, B, 0, 512, 6)
     torch.cuda.synchronize()
     print("prof_run ok", which, reps)
 
