@@ -131,6 +131,17 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
           "=r"(v[31])                                                                            \
         : "r"(taddr))
 
+#define TMEM_ST32(taddr, v)                                                                      \
+    asm volatile(                                                                                \
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"          \
+        ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), \
+          "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]),        \
+          "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]),      \
+          "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),      \
+          "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])                                           \
+        : "memory")
+
 // instruction descriptor: s32 accumulate, s8 x s8, K-major both, M=128, N=128
 constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                             ((uint32_t)(BM >> 4) << 24);
@@ -594,6 +605,15 @@ __device__ __forceinline__ void span_timer_exit(unsigned long long* T) {
 //    producer, which waits on that step's empty barrier);
 //  * the MMA loop runs on one thread with smem descriptors advanced by adds;
 //  * the epilogue issues all of a column chunk's TMEM loads before one wait.
+// K blocks between normalisations for an item whose sweep has `pairs` A slices:
+// each diagonal gains at most pairs * 128 * 2^14 per K block (0 = never needed)
+__device__ __forceinline__ int item_kb_norm(const BandGemmParams& P, int pairs) {
+    if (!P.kb_norm) return 0;
+    const int lim = (int)((((int64_t)1 << 17) - 1) / ((int64_t)pairs * BK));
+    const int k = min(P.kb_norm, lim);
+    return k >= P.n_kb ? 0 : max(k, 1);
+}
+
 template <int BNT, int BAND_W>
 __global__ void __launch_bounds__(THREADS, 1)
     band3_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -703,6 +723,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 fence_after();
                 if (P.dbg_ts && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 1] = clock64();
                 uint32_t init_mask = 0;
+                const int kbn = item_kb_norm(P, s_hi - s_lo + 1);
                 for (int kb = 0; kb < P.n_kb; kb++) {
                     const int t_first = max(0, d0 - s_hi);
                     const uint32_t b_first = bi;
@@ -726,6 +747,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                         mma_commit(&empty[slot]);
                     }
                     bi = b_first + (uint32_t)(min(P.S_B - 1, d0 + BAND_W - 1 - s_lo) - t_first + 1);
+                    if (kbn && (kb + 1) % kbn == 0 && kb + 1 < P.n_kb) {
+                        // the epilogue folds the accumulators back to [0, 256) before more K
+                        mma_commit(tfull);
+                        tph ^= 1;
+                        mbar_wait(tempty, tph ^ 1);
+                        fence_after();
+                    }
                 }
                 mma_commit(tfull);
                 if (P.dbg_ts && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 2] = clock64();
@@ -742,6 +770,57 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int m0 = (W.x / P.n_tiles_n) * 128, n0 = (W.x % P.n_tiles_n) * BNT;
             const int d0 = BAND_W * W.y;
             const int row = m0 + 32 * q + lane;
+            const int kbn = item_kb_norm(P, min(P.S_A - 1, d0 + BAND_W - 1) - max(0, d0 - (P.S_B - 1)) + 1);
+            const int n_norm = kbn ? (P.n_kb - 1) / kbn : 0;
+            for (int ev = 0; ev < n_norm; ev++) {
+                // in-place normalisation: D_w = r_w + 256 q_w, r_w in [0, 256); q_w moves to
+                // D_{w+1} (weight 256), the top q to the band's carry (Tc, accumulated here)
+                mbar_wait(tfull, tph);
+                fence_after();
+#pragma unroll 1
+                for (int h = 0; h < BNT / 64; h++) {
+                    int32_t cq[32];
+#pragma unroll
+                    for (int c = 0; c < 32; c++) cq[c] = 0;
+#pragma unroll
+                    for (int w0 = 0; w0 < BAND_W; w0++) {
+                        // a diagonal past the last one is never accumulated by the MMAs: its
+                        // region starts at 0 here and keeps the residue passed through it
+                        uint32_t v[32];
+                        const uint32_t taddr =
+                            tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(w0 * BNT + col0 + 32 * h);
+                        if (d0 + w0 < P.ND || ev) {
+                            TMEM_LD32(taddr, v);
+                            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < 32; c++) v[c] = 0;
+                        }
+#pragma unroll
+                        for (int c = 0; c < 32; c++) {
+                            const int32_t val = (int32_t)v[c] + cq[c];
+                            v[c] = (uint32_t)(val & 255);
+                            cq[c] = val >> 8;
+                        }
+                        TMEM_ST32(taddr, v);
+                    }
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    const size_t q0 = (size_t)W.y * (P.Np >> 2) + ((size_t)(n0 + col0 + 32 * h) >> 2);
+#pragma unroll
+                    for (int c = 0; c < 32; c += 4) {
+                        const size_t off = (((q0 + (c >> 2)) * P.Mp + row) << 2);
+                        int4 t = ev ? *(int4*)(P.Tc + off) : make_int4(0, 0, 0, 0);
+                        t.x += cq[c];
+                        t.y += cq[c + 1];
+                        t.z += cq[c + 2];
+                        t.w += cq[c + 3];
+                        *(int4*)(P.Tc + off) = t;
+                    }
+                }
+                fence_before();
+                mbar_arrive(tempty);
+                tph ^= 1;
+            }
             mbar_wait(tfull, tph);
             fence_after();
             if (P.dbg_ts && warp == 2 && lane == 0 && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 3] = clock64();
@@ -762,7 +841,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int u = 0; u < WB; u++) {
                         // diagonals past the last one contribute D = 0, so every band's
                         // carry leaves at the band boundary (word aligned for the recombine)
-                        if (d0 + w0 + u < P.ND) {
+                        if (d0 + w0 + u < P.ND || n_norm) {
                             const uint32_t taddr =
                                 tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)((w0 + u) * BNT + col0 + 32 * h);
                             TMEM_LD32(taddr, v[u]);
@@ -789,7 +868,15 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int c = 0; c < 32; c += 4) {
                         const size_t off = (((q0 + (c >> 2)) * P.Mp + row) << 2);
                         *(uint4*)(P.Tw + off) = make_uint4(word[c], word[c + 1], word[c + 2], word[c + 3]);
-                        *(int4*)(P.Tc + off) = make_int4(carry[c], carry[c + 1], carry[c + 2], carry[c + 3]);
+                        int4 t = make_int4(carry[c], carry[c + 1], carry[c + 2], carry[c + 3]);
+                        if (n_norm) {  // plus the carries folded out by the normalisations
+                            const int4 o = *(int4*)(P.Tc + off);
+                            t.x += o.x;
+                            t.y += o.y;
+                            t.z += o.z;
+                            t.w += o.w;
+                        }
+                        *(int4*)(P.Tc + off) = t;
                     }
                 }
             }

@@ -23,6 +23,9 @@ struct SliceGemmParams {
 struct BandGemmParams {
     int S_A, S_B, Mp, Np, Kp, n_kb, ND;
     int bn, band_w;           // (128, 4) or (256, 2): output tile width / diagonals per item
+    // K blocks between in-place normalisations of the TMEM accumulators (0 = none):
+    // needed when pairs * K * 2^14 could reach 2^31 (high precision, long K)
+    int kb_norm = 0;
     int n_tiles_n;            // Np / 128
     const int2* items;        // (tile = mt * n_tiles_n + nt, band)
     const int* cta_begin;     // [n_ctas + 1] item ranges per CTA

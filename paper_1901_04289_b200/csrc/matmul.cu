@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(128) recombine_kernel(RecombineArgs R) {
     const size_t plane = (size_t)R.Mp * R.Np;
     const size_t off = rc_off(R, i, j);
     // T = (bytes as unsigned) + sum_g carry_g * 256^(d1_g), two's complement in NT limbs
-    const int NT = (R.nwords + 1) / 2 + 2;
+    const int NT = (int)(((int64_t)R.digit_bits * R.nwords + 63) / 64) + 2;
     uint64_t T[CAP];
     for (int q = 0; q < NT; q++) T[q] = 0;
     // plane w holds digit w in base 2^(8 diagonals per word): 32-bit words (4 diagonals,
@@ -2675,7 +2675,16 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     const int ND = SA + SB - 1;
     // band kernel when every diagonal fits an int32 accumulator: pairs * w * 2^14 < 2^31
     static const bool force_unit = std::getenv("APB_FORCE_UNIT_GEMM") != nullptr;  // test hook
-    const bool band = !force_unit && (int64_t)std::min(SA, SB) * w < (int64_t)1 << 17;
+    // (or, beyond that, with in-place normalisations of the accumulators every kb_norm
+    // K blocks: pairs * 128 kb_norm < 2^17)
+    const int64_t pairs = std::min(SA, SB);
+    static const bool no_norm = std::getenv("APB_NO_BAND_NORM") != nullptr;  // test hook: unit GEMM instead
+    const bool fits = pairs * w < (int64_t)1 << 17;
+    static const int kb_force = std::getenv("APB_BAND_KBNORM") ? std::atoi(std::getenv("APB_BAND_KBNORM")) : 0;
+    // per item on the device: min(kb_norm, (2^17 - 1) / (its pairs * 128)); 1 << 20 = "as needed"
+    int kb_norm = fits ? 0 : (((int64_t)1 << 17) - 1) / (pairs * kSliceBK) >= 1 ? 1 << 20 : 0;
+    if (kb_force > 0) kb_norm = kb_force;  // test hook: an event every kb_force K blocks
+    const bool band = !force_unit && (fits || (!no_norm && kb_norm > 0));
     // work tables depend only on (band, S_A, S_B, w, tile grid): built once on the
     // host (LPT item assignment / unit groups), cached as device copies
     struct Tables {
@@ -2776,6 +2785,7 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         P.n_tiles_n = Np / bn;
         P.bn = bn;
         P.band_w = band_w;
+        P.kb_norm = kb_norm;
         P.items = (const int2*)(dunits + off_items);
         P.cta_begin = (const int*)(dunits + off_begin);
         P.Tw = Tw;
@@ -2852,7 +2862,7 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     R.spec_sb = SB;
     tok = prof_begin("recombine", st);
     {
-        const int NT = (NW + 1) / 2 + 2;
+        const int NT = (int)(((int64_t)R.digit_bits * NW + 63) / 64) + 2;
         const unsigned gb = blocks_for(M * N, 128);
         const unsigned gbq = blocks_for(M * ((N + 3) / 4) * 4, 128);
         static const bool slow = std::getenv("APB_SLOW_RECOMBINE") != nullptr;  // test hook

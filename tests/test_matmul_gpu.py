@@ -81,7 +81,8 @@ def test_full_config_vs_reference(cfg):
                                   "APB_RAD_ORDER=0", "APB_RAD_ORDER=2", "APB_RAD_ORDER=3", "APB_BAND_BN=128", "APB_BAND_V2=1",
                                   "APB_NO_SPEC_PACK=1", "APB_NO_GRAPHS=1",
                                   "APB_RECOMBINE64=1", "APB_NO_RAD_FUSE=1", "APB_NO_PDL=1",
-                                  "APB_NO_SPEC_STEP=1", "APB_NO_PRIO=1", "APB_RAD_SPLIT=1", "APB_RAD_AFTER=1"])
+                                  "APB_NO_SPEC_STEP=1", "APB_NO_PRIO=1", "APB_RAD_SPLIT=1", "APB_RAD_AFTER=1",
+                                  "APB_BAND_KBNORM=1"])
 def test_kernel_variants_golden(hook):
     """alternative kernels / schedules selected by the library's tuning hooks
     (unit GEMM used when a diagonal could overflow int32, byte-serial pack,
@@ -204,3 +205,34 @@ def test_multiblock_wide_vs_reference():
     _, _, t8 = ops.block_int_product(A, B, lo, hi, 8)
     _, _, ti, _ = ops.block_int_product_imad(A, B, lo, hi, 8)
     np.testing.assert_array_equal(t8, ti)
+
+
+@pytest.mark.parametrize("n,p", [(2048, 512), (1024, 1024)])
+def test_band_normalised_high_precision(n, p):
+    """BASELINE config 5 shapes where a diagonal could overflow int32 over the full K
+    (pairs * K >= 2^17): the band GEMM with in-place accumulator normalisations equals
+    the one-diagonal-at-a-time unit GEMM on every entry, and sampled rows equal the
+    reference"""
+    import subprocess
+    import sys
+    from paper_1901_04289_b200 import ops
+    a, b = gen.config5_matrices(n=n, p=p)
+    A, B = _mat(a, n, n), _mat(b, n, n)
+    got = ops.block_matmul_ball(A, B, p).balls.to_host()
+    rows = 2
+    ref, _ = po.matmul(a.take(np.arange(rows * n)), b, rows, n, n, p, which="ref", algo=1,
+                       threads=os.cpu_count() or 8)
+    assert got.take(np.arange(rows * n)).identical(ref).all()
+    # unit path in a subprocess on the same inputs: full-matrix equality
+    code = ("import sys, numpy as np; sys.path[:0] = %r; from paper_1901_04289_b200 import gen, ops;"
+            "a, b = gen.config5_matrices(n=%d, p=%d);"
+            "A = ops.BallMatrix(a.to_device(), %d, %d); B = ops.BallMatrix(b.to_device(), %d, %d);"
+            "c = ops.block_matmul_ball(A, B, %d).balls.to_host(); np.save(sys.argv[1], c.mant)"
+            % (sys.path[:3], n, p, n, n, n, n, p))
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        f = os.path.join(d, "unit.npy")
+        env = dict(os.environ, APB_NO_BAND_NORM="1")
+        r = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        np.testing.assert_array_equal(np.load(f), got.mant)
