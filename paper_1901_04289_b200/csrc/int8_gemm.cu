@@ -614,8 +614,13 @@ __device__ __forceinline__ int item_kb_norm(const BandGemmParams& P, int pairs) 
     return k >= P.n_kb ? 0 : max(k, 1);
 }
 
+#ifndef APB_BAND_MAXNREG
+#define APB_BAND_MAXNREG 168
+#endif
+// register cap (168 = the most 10 warps fit: 3 warps per SM sub-partition); 144 leaves room on every SM sub-partition for a co-resident 4-warp
+// radius block (APB_RAD_BESIDE schedule), at the price of epilogue spills
 template <int BNT, int BAND_W>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __maxnreg__(BNT == 256 ? APB_BAND_MAXNREG : 168)
     band3_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       BandGemmParams P) {
     using Cfg = BandCfg<BNT, BAND_W>;

@@ -3247,13 +3247,15 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         return cuda_check(cudaGetLastError(), "matmul scan");
     };
     // speculative radius products (single radius block; sparse/dense chosen on the device)
-    auto phaseR = [&](cudaStream_t ss, bool capturing) -> int {
+    // `mid` (optional): a wait enqueued between the planes and the products
+    auto phaseR = [&](cudaStream_t ss, bool capturing, cudaEvent_t mid = nullptr) -> int {
         const int tk = prof_begin("radius", ss);
         RadPair rp{M, K, N, da1, db1, da2, db2, ec1, fc1, ec2, fc2, r1b, r2b, r1f, r2f, mw1, mw2};
         static const bool split = std::getenv("APB_RAD_SPLIT") != nullptr;  // previous 6-launch schedule
         if (!split) {
             const int64_t nA = blocks_for(M * K, 256);
             fused_planes2_kernel<<<(unsigned)(nA + blocks_for(K * N, 256)), 256, 0, ss>>>(av, bv, rp, nA);
+            if (mid) cudaStreamWaitEvent(ss, mid, 0);
             rad_sparse2_kernel<2, 128><<<(unsigned)(N + M), 128, 0, ss>>>(rp);
             rad_gemm2_kernel<<<dim3(blocks_for(N, RT), blocks_for(M, RT), 2), RTHREADS, 0, ss>>>(rp);
             prof_end(tk, ss);
@@ -3395,13 +3397,17 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
                 [&](cudaStream_t cs) -> int {
                     int r = phase1(cs, true);
                     if (r) return r;
-                    cudaStreamWaitEvent(side, ev_fork, 0);  // radius branch after the scan
-                    if ((r = phaseR(side, true))) return r;
+                    // radius branch: planes beside the pack, products before the GEMM, which
+                    // waits for them (measured fastest: squeezed beside a GEMM CTA, one block
+                    // per SM, the products outlast the GEMM).  APB_RAD_BESIDE=1: products
+                    // issued after the pack, next to the GEMM (with APB_BAND_MAXNREG=144 builds)
+                    static const bool rad_first = std::getenv("APB_RAD_BESIDE") == nullptr;
+                    static cudaEvent_t ev_packed = make_event();
+                    cudaStreamWaitEvent(side, ev_fork, 0);  // the planes beside the pack
+                    if (!rad_first) cudaEventRecord(ev_packed, cs);
+                    if ((r = phaseR(side, true, rad_first ? nullptr : ev_packed))) return r;
                     cudaEventRecord(ev_rdone, side);
-                    // the GEMM takes every SM: let the (short) radius branch finish first
-                    // instead of having its blocks queue behind the GEMM (APB_RAD_AFTER=1: old order)
-                    static const bool rad_after = std::getenv("APB_RAD_AFTER") != nullptr;
-                    if (!rad_after) cudaStreamWaitEvent(cs, ev_rdone, 0);
+                    if (rad_first) cudaStreamWaitEvent(cs, ev_rdone, 0);
                     RadFuse fz{r1b, r1f, r2b, r2f, ev_rdone, false, false};
                     r = scaled_block(A, B, 0, K, prec, C, true, P.maxw_a, P.maxw_b, RW.top[0], RW.bot[0],
                                      CW.top[0], CW.bot[0], nullptr, 0, nullptr, nullptr, cs, nullptr, true, &fz,

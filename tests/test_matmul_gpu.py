@@ -81,7 +81,7 @@ def test_full_config_vs_reference(cfg):
                                   "APB_RAD_ORDER=0", "APB_RAD_ORDER=2", "APB_RAD_ORDER=3", "APB_BAND_BN=128", "APB_BAND_V2=1",
                                   "APB_NO_SPEC_PACK=1", "APB_NO_GRAPHS=1",
                                   "APB_RECOMBINE64=1", "APB_NO_RAD_FUSE=1", "APB_NO_PDL=1",
-                                  "APB_NO_SPEC_STEP=1", "APB_NO_PRIO=1", "APB_RAD_SPLIT=1", "APB_RAD_AFTER=1",
+                                  "APB_NO_SPEC_STEP=1", "APB_NO_PRIO=1", "APB_RAD_SPLIT=1", "APB_RAD_BESIDE=1",
                                   "APB_BAND_KBNORM=1"])
 def test_kernel_variants_golden(hook):
     """alternative kernels / schedules selected by the library's tuning hooks
