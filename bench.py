@@ -280,10 +280,22 @@ def e2e_matmul(ops, a, b, n, p, steps):
     t0 = time.perf_counter()
     for _ in range(steps):
         ops._lib.check(lib.apb_matmul_host(C.byref(am), C.byref(bm), p, 1, C.byref(cm)), "e2e")
+    dt_sync = (time.perf_counter() - t0) / steps
+    # pipelined entry: product i+1's H2D overlaps product i's compute and D2H
+    for _ in range(2):
+        ops._lib.check(lib.apb_matmul_host_submit(C.byref(am), C.byref(bm), p, 1, C.byref(cm)), "e2e warmup")
+    ops._lib.check(lib.apb_matmul_host_drain(), "e2e warmup")
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        ops._lib.check(lib.apb_matmul_host_submit(C.byref(am), C.byref(bm), p, 1, C.byref(cm)), "e2e")
+    ops._lib.check(lib.apb_matmul_host_drain(), "e2e drain")
     dt = (time.perf_counter() - t0) / steps
     return {"value": n ** 3 / dt, "unit": "terms/s", "ms_per_step": dt * 1e3,
             "h2d_bytes_per_step": a.nbytes() + b.nbytes(), "d2h_bytes_per_step": hc.nbytes(),
-            "path": "apb_matmul_host (pinned host buffers; H2D + kernels + D2H each step)"}
+            "path": "apb_matmul_host_submit/drain (pinned host buffers; every step H2D of A and B, kernels, "
+                    "D2H of C; consecutive steps overlap on copy-in / compute / copy-out streams)",
+            "sync_call": {"value": n ** 3 / dt_sync, "ms_per_step": dt_sync * 1e3,
+                          "path": "apb_matmul_host (one synchronous call per step)"}}
 
 
 def cpu_threads():

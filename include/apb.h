@@ -248,6 +248,17 @@ int apb_matmul_host(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, 
 int apb_matmul_complex_host(const apb_mat* Are, const apb_mat* Aim, const apb_mat* Bre,
                             const apb_mat* Bim, int64_t prec, int algo, apb_mat* Cre, apb_mat* Cim);
 
+/* Pipelined host entry for a stream of products (serving): apb_matmul_host
+ * split into a submission and a drain.  Consecutive submissions alternate
+ * between two device buffer sets, so the host->device copy of product i+1
+ * overlaps the compute and the device->host copy of product i (three streams:
+ * copy-in, compute, copy-out).  The host buffers of a submitted product
+ * (pinned memory for overlap) must stay untouched until apb_matmul_host_drain
+ * returns, which waits for every submitted product and returns the first error.
+ * Results are identical to apb_matmul_host. */
+int apb_matmul_host_submit(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, apb_mat* C);
+int apb_matmul_host_drain(void);
+
 /* ------------------------------------------------------------------ misc */
 
 /* Synchronize `stream` and return (then clear) the APB_* status raised by

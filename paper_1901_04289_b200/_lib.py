@@ -68,6 +68,10 @@ def lib():
     L.apb_dot_batch_host.restype = I
     L.apb_matmul_host.argtypes = [mp, mp, I64, I, mp]
     L.apb_matmul_host.restype = I
+    L.apb_matmul_host_submit.argtypes = [mp, mp, I64, I, mp]
+    L.apb_matmul_host_submit.restype = I
+    L.apb_matmul_host_drain.argtypes = []
+    L.apb_matmul_host_drain.restype = I
     L.apb_poly_mullow.argtypes = [bp, I64, bp, I64, I64, I64, bp, P]
     L.apb_poly_mullow.restype = I
     L.apb_series_exp.argtypes = [bp, I64, I64, I64, bp, P]

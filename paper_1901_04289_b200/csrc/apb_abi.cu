@@ -396,6 +396,82 @@ int apb_matmul_host(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, 
     return apb_device_status(st);
 }
 
+// ---- pipelined matmul host entry: copy-in / compute / copy-out streams, two
+// device buffer sets (workspace slots 64 + 15 k: A, B, C)
+namespace {
+struct HostPipe {
+    cudaStream_t in, comp, out;
+    cudaEvent_t in_ready[2], comp_done[2], out_done[2];
+    bool used[2] = {false, false};
+    int next = 0;
+    int err = APB_OK;
+    HostPipe() {
+        cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&out, cudaStreamNonBlocking);
+        for (int k = 0; k < 2; k++) {
+            cudaEventCreateWithFlags(&in_ready[k], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&comp_done[k], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&out_done[k], cudaEventDisableTiming);
+        }
+    }
+};
+HostPipe& host_pipe() {
+    static HostPipe p;
+    return p;
+}
+// would any buffer of set k have to grow (a reallocation must not race in-flight work)?
+bool pipe_grows(int k, const apb_mat* A, const apb_mat* B, const apb_mat* C) {
+    Workspace& ws = workspace();
+    const apb_balls* bs[3] = {&A->b, &B->b, &C->b};
+    for (int q = 0; q < 3; q++) {
+        const size_t cnt = (size_t)bs[q]->count;
+        const size_t need[5] = {cnt * bs[q]->L * 8, cnt * 8, cnt, cnt * 4, cnt * 8};
+        for (int f = 0; f < 5; f++)
+            if (ws.caps[64 + 15 * k + 5 * q + f] < (need[f] ? need[f] : 1)) return true;
+    }
+    return false;
+}
+}  // namespace
+
+int apb_matmul_host_submit(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, apb_mat* C) {
+    HostPipe& P = host_pipe();
+    const int k = P.next;
+    P.next ^= 1;
+    if (pipe_grows(k, A, B, C)) cudaDeviceSynchronize();  // first use / larger operands
+    apb_mat dA = *A, dB = *B, dC = *C;
+    int rc;
+    // set k's inputs were last read by the product two submissions ago
+    if (P.used[k]) cudaStreamWaitEvent(P.in, P.comp_done[k], 0);
+    if ((rc = to_device(&A->b, &dA.b, 64 + 15 * k, P.in, true))) return rc;
+    if ((rc = to_device(&B->b, &dB.b, 69 + 15 * k, P.in, true))) return rc;
+    if ((rc = to_device(&C->b, &dC.b, 74 + 15 * k, P.in, false))) return rc;
+    cudaEventRecord(P.in_ready[k], P.in);
+    cudaStreamWaitEvent(P.comp, P.in_ready[k], 0);
+    if (P.used[k]) cudaStreamWaitEvent(P.comp, P.out_done[k], 0);  // set k's C has left
+    if ((rc = apb_matmul(&dA, &dB, prec, algo, &dC, P.comp))) {
+        if (!P.err) P.err = rc;
+        return rc;
+    }
+    cudaEventRecord(P.comp_done[k], P.comp);
+    cudaStreamWaitEvent(P.out, P.comp_done[k], 0);
+    if ((rc = to_host(&dC.b, &C->b, P.out))) return rc;
+    cudaEventRecord(P.out_done[k], P.out);
+    P.used[k] = true;
+    return APB_OK;
+}
+
+int apb_matmul_host_drain(void) {
+    HostPipe& P = host_pipe();
+    cudaStreamSynchronize(P.in);
+    cudaStreamSynchronize(P.out);
+    int rc = apb_device_status(P.comp);
+    if (!rc) rc = cuda_check(cudaGetLastError(), "host pipeline");
+    if (!rc && P.err) rc = P.err;
+    P.err = APB_OK;
+    return rc;
+}
+
 int apb_dot_complex_batch_host(const apb_balls* xre, const apb_balls* xim, const apb_balls* yre,
                                const apb_balls* yim, const apb_dot_index* idx, int64_t n, int64_t batch,
                                int64_t prec, int mode, const apb_dot_tuning* tuning, apb_balls* out_re,

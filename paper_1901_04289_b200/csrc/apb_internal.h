@@ -18,8 +18,8 @@ namespace apb {
 // device (exponent overflow = std::overflow_error in the reference).
 struct Workspace {
     int* status_dev = nullptr;
-    void* bufs[64] = {};
-    size_t caps[64] = {};
+    void* bufs[96] = {};  // 64..93: the two buffer sets of the pipelined host entry
+    size_t caps[96] = {};
     void* scratch(cudaStream_t st, size_t bytes, int slot);
 };
 Workspace& workspace();

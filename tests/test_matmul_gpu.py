@@ -236,3 +236,26 @@ def test_band_normalised_high_precision(n, p):
         r = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         np.testing.assert_array_equal(np.load(f), got.mant)
+
+
+def test_host_pipeline_matches_sync():
+    """apb_matmul_host_submit/drain over three different products (pinned host
+    buffers, alternating device buffer sets): every result equals the reference"""
+    import ctypes as C
+    from paper_1901_04289_b200 import ops
+    from paper_1901_04289_b200.balls import BallArray, apb_mat, limbs_for
+    lib = ops._lib.lib()
+    n, p = 256, 128
+    jobs = []
+    for salt in range(3):
+        a, b = gen.config2_matrices(seed_salt=salt)
+        ha, hb = a.pinned(), b.pinned()
+        hc = BallArray.zeros(n * n, limbs_for(p)).pinned()
+        jobs.append((a, b, ha, hb, hc, apb_mat(ha.c(), n, n), apb_mat(hb.c(), n, n), apb_mat(hc.c(), n, n)))
+    for _ in range(2):  # also reuse both buffer sets
+        for j in jobs:
+            ops._lib.check(lib.apb_matmul_host_submit(C.byref(j[5]), C.byref(j[6]), p, 1, C.byref(j[7])), "submit")
+        ops._lib.check(lib.apb_matmul_host_drain(), "drain")
+        for a, b, ha, hb, hc, *_ in jobs:
+            ref, _ = po.matmul(a, b, n, n, n, p, which="ref", algo=1, threads=os.cpu_count() or 8)
+            assert hc.identical(ref).all()
