@@ -9,7 +9,7 @@ ball matmul N=512, p=256, on which the north-star's "% of int8 tensor peak"
 target is stated.  One step = one block_matmul_ball (plan, scale/pack, tcgen05
 slice GEMM, recombine, radius) on device-resident inputs; the L2 is flushed
 (256 MiB write) before every step, outside the timed events.  The same JSON
-line carries configs 1 and 2 under "also".
+line carries configs 1, 2 and 4 under "also".
 
 --gpus N (launched by torchrun): weak scaling, one process per GPU; every rank
 multiplies its own row block A_r (512 x 512, seed salted by rank) by the
@@ -266,6 +266,59 @@ def run_matmul(torch, cfg, steps, warmup, world, rank, want_e2e=True, want_cpu=T
     return res
 
 
+def run_complex(torch, steps, warmup):
+    """BASELINE config 4: complex ball matmul N=1024, p=512 (4 real block products,
+    ball_sub / ball_add), device-resident operands, L2 flushed before every step"""
+    import ctypes as C
+    from paper_1901_04289_b200 import gen, ops
+    lib = ops._lib.lib()
+    n, p = 1024, 512
+    parts = gen.config4_matrices(n=n, p=p)
+    M = [ops.BallMatrix(x.to_device(), n, n) for x in parts]
+    flush = L2Flush(torch)
+    st = torch.cuda.current_stream()
+    for _ in range(warmup):
+        ops.complex_matmul_ball(*M, p)
+    torch.cuda.synchronize()
+    lib.apb_gemm_timer_reset()
+    ms_all = []
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for _ in range(steps):
+            flush()
+            s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(st)
+            ops.complex_matmul_ball(*M, p, check=False)
+            e0.record(st)
+            torch.cuda.synchronize()
+            ms_all.append(s0.elapsed_time(e0))
+    gns, gl = C.c_uint64(0), C.c_uint64(0)
+    lib.apb_gemm_timer_read(C.byref(gns), C.byref(gl))
+    ms = sum(ms_all) / steps
+    stats = ops.matmul_stats()
+    ha, hb = stats["last_height_a"], stats["last_height_b"]
+    credited = 2.0 * n ** 3 * ((ha + 7) // 8) * ((hb + 7) // 8)
+    per_launch_ms = gns.value / max(gl.value, 1) / 1e6
+    achieved = credited / (per_launch_ms * 1e-3) / 1e12
+    peak, _ = int8_peak()
+    # reference on a row sample (row-split is bit-identical for single-block plans)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    T = cpu_threads()
+    rows = max(2, T)
+    t0 = time.perf_counter()
+    po.matmul_complex_rows(*parts, rows, n, n, p, threads=T)
+    dt = time.perf_counter() - t0
+    return {"metric": "complex ball matmul terms/s (N^3 complex multiply-adds per second)",
+            "value": n ** 3 / (ms * 1e-3), "unit": "terms/s", "ms_per_step": ms,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
+                         "frac": achieved / peak, "kernel": "band3_gemm_kernel<256,2>",
+                         "kernel_ms": per_launch_ms, "kernel_launches_timed": gl.value,
+                         "work": f"4 real products x 2*N^3*ceil(h/8)^2 = 4 x {credited:.4g} int8 ops"},
+            "clocks": clk.summary(),
+            "cpu_baseline": {"value": rows * n * n / dt, "unit": "terms/s", "cores": T, "kind": "reference",
+                             "sample": f"complex_matmul_ball on {rows} of {n} rows of A (row-split over {T} threads)"}}
+
+
 def e2e_matmul(ops, a, b, n, p, steps):
     """host->device copy of A, B from pinned memory, compute, device->host read of C,
     every step, through the C ABI's host entry (apb_matmul_host)"""
@@ -460,10 +513,14 @@ def main():
         res = run_matmul(torch, args.config, args.steps, args.warmup, world, rank, p_override=args.prec)
     also = {}
     if not args.no_also and world == 1:
-        for cfg in ("c2", "c1") if args.config == "c3" else ():
+        for cfg in ("c2", "c1", "c4") if args.config == "c3" else ():
             try:
-                r = run_dots(torch, 5, 3, 1, 0, want_e2e=False, want_cpu=True) if cfg == "c1" else \
-                    run_matmul(torch, cfg, 5, 3, 1, 0, want_e2e=False, want_cpu=True)
+                if cfg == "c1":
+                    r = run_dots(torch, 5, 3, 1, 0, want_e2e=False, want_cpu=True)
+                elif cfg == "c4":
+                    r = run_complex(torch, 3, 3)
+                else:
+                    r = run_matmul(torch, cfg, 5, 3, 1, 0, want_e2e=False, want_cpu=True)
                 also[cfg] = {k: r[k] for k in ("metric", "value", "unit", "ms_per_step", "roofline",
                                                "cpu_baseline") if k in r}
             except Exception as e:  # noqa: BLE001
