@@ -44,6 +44,8 @@ struct ScanSummary {
     long long prec_a, prec_b;   // entry_precision
     long long maxw_a, maxw_b;   // max row / column window width over the scanned range
     long long mw[8];            // block_matmul: radius window widths / nonzero counts (mw1, mw2)
+    int rad_centred;            // 1: an operand exponent exceeds +-kRadUncentred (centred planes needed)
+    int _pad;
 };
 
 // bit width of a finite nonzero midpoint stored in L top-aligned slots
@@ -1398,7 +1400,8 @@ APB_DEV void sacc_set(ScanAcc& a, int f, int64_t v) {
 // one entry: midpoint window + entry precision, the two radius-operand Mag
 // windows of this side with nonzero counts, specials.  A side: |A|, R_A;
 // B side: R_B, |B| + R_B (the operands of src/matmul.cpp:498-509)
-APB_DEV void scan_entry(const BallsView& X, int64_t e, bool a_side, ScanAcc& acc) {
+APB_DEV void scan_entry(const BallsView& X, int64_t e, bool a_side, ScanAcc& acc, Mag* op1 = nullptr,
+                        Mag* op2 = nullptr) {
     const uint8_t kd = X.kind[e];
     const int64_t ex = X.exp[e];
     const uint32_t rb = X.rad_man[e];
@@ -1424,6 +1427,10 @@ APB_DEV void scan_entry(const BallsView& X, int64_t e, bool a_side, ScanAcc& acc
     const Mag r = (rb != 0 && rb != APB_RAD_INF) ? mag_parts(rb, rexp) : mag_zero();
     const Mag o1 = a_side ? mu : r;
     const Mag o2 = a_side ? r : mag_add(mu, r);
+    if (op1) {
+        *op1 = o1;
+        *op2 = o2;
+    }
     if (o1.kind == 1) {
         win_merge(acc.t[1], acc.b[1], o1.f, o1.f - 30);
         acc.cnt += 1;
@@ -1434,6 +1441,17 @@ APB_DEV void scan_entry(const BallsView& X, int64_t e, bool a_side, ScanAcc& acc
     }
 }
 
+// uncentred exact double of a radius operand (the planes the scan writes for the
+// speculative radius products; used only when every operand exponent is within
+// +-kRadUncentred, so products and sums of <= 2^17 terms stay normal and the
+// result equals the centred computation of src/matmul.cpp:404-431 scaled by a
+// power of two, which the Mag conversion undoes exactly)
+constexpr int64_t kRadUncentred = 480;
+APB_DEV double uncentred(const Mag& m) {
+    return (m.kind == 1 && m.f <= kRadUncentred + 64 && m.f >= -kRadUncentred - 64) ? ldexp((double)m.b, (int)(m.f - 30))
+                                                                                      : 0.0;
+}
+
 constexpr int SCAN_A_COLS = 256;  // entries of a row per A block (one per thread)
 constexpr int SCAN_B_ROWS = 32;   // rows per B block: 32 columns x 8 warps x 4 rows
 
@@ -1441,7 +1459,9 @@ constexpr int SCAN_B_ROWS = 32;   // rows per B block: 32 columns x 8 warps x 4 
 // pa[f][c][i] (A, cA chunks per row) and pb[f][c][j] (B, cB chunks per column).
 __global__ void __launch_bounds__(256) scan_v2_kernel(BallsView A, BallsView B, int64_t M, int64_t K, int64_t N,
                                                       int cA, int cB, int64_t* pa, int64_t* pb, ScanSummary* sum,
-                                                      long long* mw1, long long* mw2) {
+                                                      long long* mw1, long long* mw2, double* da1T = nullptr,
+                                                      double* da2 = nullptr, double* db1 = nullptr,
+                                                      double* db2 = nullptr) {
     __shared__ int64_t red[8][32][SCAN_FIELDS + 1];
     griddep_launch();  // the finish kernel may be scheduled now (it waits for this grid)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1456,7 +1476,14 @@ __global__ void __launch_bounds__(256) scan_v2_kernel(BallsView A, BallsView B, 
         const int64_t i = blockIdx.x / cA;
         const int c = (int)(blockIdx.x % cA);
         const int64_t k = (int64_t)c * SCAN_A_COLS + threadIdx.x;
-        if (k < K) scan_entry(A, i * K + k, true, acc);
+        if (k < K) {
+            Mag o1, o2;
+            scan_entry(A, i * K + k, true, acc, &o1, &o2);
+            if (da1T) {  // |A| transposed ([k][i]) and R_A, uncentred
+                da1T[k * M + i] = uncentred(o1);
+                da2[i * K + k] = uncentred(o2);
+            }
+        }
 #pragma unroll
         for (int o = 16; o; o >>= 1) sacc_shfl(acc, o);
         if (lane == 0)
@@ -1481,7 +1508,14 @@ __global__ void __launch_bounds__(256) scan_v2_kernel(BallsView A, BallsView B, 
 #pragma unroll
             for (int u = 0; u < SCAN_B_ROWS / 8; u++) {
                 const int64_t k = (int64_t)c * SCAN_B_ROWS + warp + 8 * u;
-                if (k < K) scan_entry(B, k * N + j, false, acc);
+                if (k < K) {
+                    Mag o1, o2;
+                    scan_entry(B, k * N + j, false, acc, &o1, &o2);
+                    if (db1) {  // R_B and |B| + R_B, uncentred
+                        db1[k * N + j] = uncentred(o1);
+                        db2[k * N + j] = uncentred(o2);
+                    }
+                }
             }
         }
         for (int f = 0; f < SCAN_FIELDS; f++) red[warp][lane][f] = sacc_get(acc, f);
@@ -1540,6 +1574,12 @@ __global__ void scan_v2_finish_kernel(const int64_t* pa, const int64_t* pb, int6
     const unsigned long long n2 = (unsigned long long)(acc.cnt >> 32);
     const int s = a_side ? 0 : 1;
     if (acc.special) atomicOr(a_side ? &sum->special_a : &sum->special_b, 1);
+    {  // operand Mag exponents: f in [b + 30, t] per operand window
+        bool far = false;
+        for (int q = 1; q < 3; q++)
+            if (acc.t[q] != INT64_MIN && (acc.t[q] > kRadUncentred || acc.b[q] + 30 < -kRadUncentred)) far = true;
+        if (far) atomicOr(&sum->rad_centred, 1);
+    }
     if (acc.prec) atomicMax(a_side ? &sum->prec_a : &sum->prec_b, (long long)acc.prec);
     if (w0) atomicMax(a_side ? &sum->maxw_a : &sum->maxw_b, w0);
     if (w1) atomicMax(&mw1[s], w1);
@@ -1675,8 +1715,10 @@ APB_DEV int rad_variant(const long long* mw, int64_t M, int64_t K, int64_t N, in
 constexpr int RT = 32, RK = 32, RTHREADS = 64;
 APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restrict__ db, int64_t M, int64_t N,
                            int64_t w, const int64_t* ecen, const int64_t* fcen, uint32_t* rb, int64_t* rf,
-                           int accumulate, int a_trans, const long long* sel, int64_t bx, int64_t by) {
+                           int accumulate, int a_trans, const long long* sel, int64_t bx, int64_t by,
+                           const int* cflag = nullptr) {
     if (sel && rad_variant(sel, M, w, N, a_trans) != 2) return;
+    const bool cen = !cflag || *cflag;  // uncentred planes (scan-written) unless flagged
     // 32 x 32 outputs per 64 threads (4 x 4 each), K tiles of 32 staged in shared
     // memory with the next tile prefetched into registers; per-entry sequential RN
     // sums (__dmul_rn / __dadd_rn, no contraction) folded into the Mag bound at
@@ -1742,7 +1784,7 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
                     const int64_t gi = i0 + ty * 4 + r, gj = j0 + tx * 4 + c;
                     if (s[r][c] != 0.0 && gi < M && gj < N) {
                         const Mag e = mag_add(mag_load(eb[4 * r + c][threadIdx.x], ef[4 * r + c][threadIdx.x]),
-                                              mag_mul(mag_from_double(s[r][c], -ecen[gi] - fcen[gj]), infl));
+                                              mag_mul(mag_from_double(s[r][c], cen ? -ecen[gi] - fcen[gj] : 0), infl));
                         mag_store(e, &eb[4 * r + c][threadIdx.x], &ef[4 * r + c][threadIdx.x]);
                     }
                     s[r][c] = 0.0;
@@ -2060,7 +2102,7 @@ template <int R, int T>
 APB_DEV void rad_spcol_v3_body(RadSmem<R, T>& sm, int64_t blk, const double* __restrict__ daT, const double* __restrict__ db,
                                                            int64_t M, int64_t N, int64_t w, const int64_t* ecen,
                                                            const int64_t* fcen, uint32_t* rb, int64_t* rf,
-                                                           const long long* sel = nullptr) {
+                                                           const long long* sel = nullptr, const int* cflag = nullptr) {
     if (sel && rad_variant(sel, M, w, N, 1) != 0) return;
     int* sl = sm.sl;
     double* sv = sm.sv;
@@ -2068,7 +2110,8 @@ APB_DEV void rad_spcol_v3_body(RadSmem<R, T>& sm, int64_t blk, const double* __r
     auto& gbuf = sm.gbuf;
     const int64_t j = blk;
     const int64_t nch = (w + RCH - 1) / RCH;
-    const int64_t fj = fcen[j];
+    const bool cen = !cflag || *cflag;  // uncentred planes (scan-written) unless flagged
+    const int64_t fj = cen ? fcen[j] : 0;
     int n = 0;
     for (int64_t pass = 0; pass * T * R < M; pass++) {
         int64_t ii[R];
@@ -2115,7 +2158,7 @@ APB_DEV void rad_spcol_v3_body(RadSmem<R, T>& sm, int64_t blk, const double* __r
                 for (int r = 0; r < R; r++) s[r] = __dadd_rn(s[r], __dmul_rn(row[ii[r]], bv));
             }
 #pragma unroll
-            for (int r = 0; r < R; r++) rad_fold(ent[r], s[r], ecen[ii[r]], fj);
+            for (int r = 0; r < R; r++) rad_fold(ent[r], s[r], cen ? ecen[ii[r]] : 0, fj);
         }
 #pragma unroll
         for (int r = 0; r < R; r++) {
@@ -2138,7 +2181,7 @@ template <int R, int T>
 APB_DEV void rad_sprow_v3_body(RadSmem<R, T>& sm, int64_t blk, const double* __restrict__ da, const double* __restrict__ db,
                                                            int64_t M, int64_t N, int64_t w, const int64_t* ecen,
                                                            const int64_t* fcen, uint32_t* rb, int64_t* rf,
-                                                           const long long* sel = nullptr) {
+                                                           const long long* sel = nullptr, const int* cflag = nullptr) {
     if (sel && rad_variant(sel, M, w, N, 0) != 1) return;
     int* sl = sm.sl;
     double* sv = sm.sv;
@@ -2146,7 +2189,8 @@ APB_DEV void rad_sprow_v3_body(RadSmem<R, T>& sm, int64_t blk, const double* __r
     auto& gbuf = sm.gbuf;
     const int64_t i = blk;
     const int64_t nch = (w + RCH - 1) / RCH;
-    const int64_t ei = ecen[i];
+    const bool cen = !cflag || *cflag;
+    const int64_t ei = cen ? ecen[i] : 0;
     int n = 0;
     for (int64_t pass = 0; pass * T * R < N; pass++) {
         int64_t jj[R];
@@ -2193,7 +2237,7 @@ APB_DEV void rad_sprow_v3_body(RadSmem<R, T>& sm, int64_t blk, const double* __r
                 for (int r = 0; r < R; r++) s[r] = __dadd_rn(s[r], __dmul_rn(av, row[jj[r]]));
             }
 #pragma unroll
-            for (int r = 0; r < R; r++) rad_fold(ent[r], s[r], ei, fcen[jj[r]]);
+            for (int r = 0; r < R; r++) rad_fold(ent[r], s[r], ei, cen ? fcen[jj[r]] : 0);
         }
 #pragma unroll
         for (int r = 0; r < R; r++) {
@@ -2222,6 +2266,7 @@ struct RadPair {
     uint32_t *r1b, *r2b;
     int64_t *r1f, *r2f;
     const long long *mw1, *mw2;
+    const int* cflag;  // nullable: 0 = the scan's uncentred planes are exact (no planes pass)
 };
 
 // blocks [0, N): column lists of R_B (product 1); [N, N + M): row lists of R_A (product 2)
@@ -2229,22 +2274,26 @@ template <int R, int T>
 __global__ void __launch_bounds__(T) rad_sparse2_kernel(RadPair P) {
     __shared__ RadSmem<R, T> sm;
     if ((int64_t)blockIdx.x < P.N)
-        rad_spcol_v3_body<R, T>(sm, blockIdx.x, P.da1, P.db1, P.M, P.N, P.K, P.ec1, P.fc1, P.r1b, P.r1f, P.mw1);
+        rad_spcol_v3_body<R, T>(sm, blockIdx.x, P.da1, P.db1, P.M, P.N, P.K, P.ec1, P.fc1, P.r1b, P.r1f, P.mw1,
+                                P.cflag);
     else
         rad_sprow_v3_body<R, T>(sm, (int64_t)blockIdx.x - P.N, P.da2, P.db2, P.M, P.N, P.K, P.ec2, P.fc2, P.r2b,
-                                P.r2f, P.mw2);
+                                P.r2f, P.mw2, P.cflag);
 }
 
 // dense variants (stand down unless picked): blockIdx.z = product
 __global__ void __launch_bounds__(64) rad_gemm2_kernel(RadPair P) {
     if (blockIdx.z == 0)
-        rad_gemm_body(P.da1, P.db1, P.M, P.N, P.K, P.ec1, P.fc1, P.r1b, P.r1f, 0, 1, P.mw1, blockIdx.x, blockIdx.y);
+        rad_gemm_body(P.da1, P.db1, P.M, P.N, P.K, P.ec1, P.fc1, P.r1b, P.r1f, 0, 1, P.mw1, blockIdx.x, blockIdx.y,
+                      P.cflag);
     else
-        rad_gemm_body(P.da2, P.db2, P.M, P.N, P.K, P.ec2, P.fc2, P.r2b, P.r2f, 0, 0, P.mw2, blockIdx.x, blockIdx.y);
+        rad_gemm_body(P.da2, P.db2, P.M, P.N, P.K, P.ec2, P.fc2, P.r2b, P.r2f, 0, 0, P.mw2, blockIdx.x, blockIdx.y,
+                      P.cflag);
 }
 
 // exact double planes of both sides in one launch: blocks [0, nA) A, the rest B
 __global__ void fused_planes2_kernel(BallsView A, BallsView B, RadPair P, int64_t nA) {
+    if (P.cflag && !*P.cflag) return;  // the scan's uncentred planes are exact
     const bool a = (int64_t)blockIdx.x < nA;
     const int64_t t = ((int64_t)blockIdx.x - (a ? 0 : nA)) * blockDim.x + threadIdx.x;
     const int64_t rows = a ? P.M : P.K, cols = a ? P.K : P.N;
@@ -3201,7 +3250,12 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     auto phase1 = [&](cudaStream_t s, bool capturing) -> int {
         const int tk_scan = prof_begin("scan", s);
         const int64_t nblk = M * cA + ((N + 31) / 32) * cB;
-        scan_v2_kernel<<<(unsigned)nblk, 256, 0, s>>>(av, bv, M, K, N, cA, cB, pa, pb, sum, mw1, mw2);
+        static const bool no_scan_planes = std::getenv("APB_NO_SCAN_PLANES") != nullptr;  // test hook
+        if (no_scan_planes)
+            scan_v2_kernel<<<(unsigned)nblk, 256, 0, s>>>(av, bv, M, K, N, cA, cB, pa, pb, sum, mw1, mw2);
+        else
+            scan_v2_kernel<<<(unsigned)nblk, 256, 0, s>>>(av, bv, M, K, N, cA, cB, pa, pb, sum, mw1, mw2, da1, da2,
+                                                          db1, db2);
         launch_pdl(scan_v2_finish_kernel, dim3(blocks_for(32 * (M + N), 256)), dim3(256), 0, s, pa, pb, M, N, cA, cB,
                    RW.top[0], RW.bot[0], CW.top[0], CW.bot[0], ec1, ec2, fc1, fc2, sum, mw1, mw2);
         count_launch(2);
@@ -3250,17 +3304,20 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     // `mid` (optional): a wait enqueued between the planes and the products
     auto phaseR = [&](cudaStream_t ss, bool capturing, cudaEvent_t mid = nullptr) -> int {
         const int tk = prof_begin("radius", ss);
-        RadPair rp{M, K, N, da1, db1, da2, db2, ec1, fc1, ec2, fc2, r1b, r2b, r1f, r2f, mw1, mw2};
+        static const bool no_scan_planes = std::getenv("APB_NO_SCAN_PLANES") != nullptr;
+        RadPair rp{M, K, N, da1, db1, da2, db2, ec1, fc1, ec2, fc2, r1b, r2b, r1f, r2f, mw1, mw2,
+                   no_scan_planes ? nullptr : &sum->rad_centred};
         static const bool split = std::getenv("APB_RAD_SPLIT") != nullptr;  // previous 6-launch schedule
         if (!split) {
             const int64_t nA = blocks_for(M * K, 256);
-            fused_planes2_kernel<<<(unsigned)(nA + blocks_for(K * N, 256)), 256, 0, ss>>>(av, bv, rp, nA);
+            if (no_scan_planes)  // else the scan wrote uncentred planes (host redoes if flagged)
+                fused_planes2_kernel<<<(unsigned)(nA + blocks_for(K * N, 256)), 256, 0, ss>>>(av, bv, rp, nA);
             if (mid) cudaStreamWaitEvent(ss, mid, 0);
-            rad_sparse2_kernel<2, 128><<<(unsigned)(N + M), 128, 0, ss>>>(rp);
+            rad_sparse2_kernel<2, 256><<<(unsigned)(N + M), 256, 0, ss>>>(rp);
             rad_gemm2_kernel<<<dim3(blocks_for(N, RT), blocks_for(M, RT), 2), RTHREADS, 0, ss>>>(rp);
             prof_end(tk, ss);
             rec_event(ev_join, ss, capturing);
-            count_launch(3);
+            count_launch(no_scan_planes ? 3 : 2);
             return cuda_check(cudaGetLastError(), "radius");
         }
         fused_planes_kernel<<<blocks_for(M * K, 256), 256, 0, ss>>>(av, M, K, 1, ec1, ec2, da1, da2, nullptr, nullptr);
@@ -3351,6 +3408,10 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     stats().last_block_count = P.steps.size() / 3;
     // R_C += |A| R_B + R_A (|B| + R_B): FP64 work (independent of the midpoint product)
     const bool rad_multi = hw1[0] > 900 || hw1[1] > 900 || hw2[0] > 900 || hw2[1] > 900;
+    // the speculative radius used the scan's uncentred planes: void if an operand
+    // exponent was too far out (redo with centred planes, like a multi-block radius)
+    static const bool no_scan_planes_h = std::getenv("APB_NO_SCAN_PLANES") != nullptr;
+    const bool rad_redo = rad_multi || (!no_scan_planes_h && hsum.rad_centred);
     const bool single = P.steps.size() == 3 && P.steps[0] == 0 && P.steps[1] == A->cols && P.steps[2] == 0;
     const bool prepacked =
         single && sncw && slices_for(P.maxw_a) <= 8 * sncw && slices_for(P.maxw_b) <= 8 * sncw;
@@ -3371,7 +3432,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     if (full_spec) {
         const std::vector<int64_t> k2 = {slices_for(P.maxw_a), slices_for(P.maxw_b)};
         gs->k2s = k2;
-        if (!rad_multi && prepacked && k2 == k2_spec) {  // the whole step already ran in G1S
+        if (!rad_redo && prepacked && k2 == k2_spec) {  // the whole step already ran in G1S
             stats().int_gemm_products++;
             stats().last_height_a = (uint64_t)P.maxw_a;
             stats().last_height_b = (uint64_t)P.maxw_b;
@@ -3384,7 +3445,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         // the GEMM / recombine of G1S stood down (or the plan is not single-block):
         // continue below exactly as after G1 + GR (whose work G1S contains)
     }
-    if (gs && spec && !rad_multi && prepacked) {  // the speculation held: G2
+    if (gs && spec && !rad_redo && prepacked) {  // the speculation held: G2
         const std::vector<int64_t> k2 = {slices_for(P.maxw_a), slices_for(P.maxw_b)};
         auto it = gs->g2.find(k2);
         gs->k2s = k2;
@@ -3445,10 +3506,10 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         htrace().flush();
         return APB_OK;
     }
-    if (spec && rad_multi) cudaStreamWaitEvent(st, ev_join, 0);  // speculation void: redo below
-    const int order = rad_multi ? 1 : rad_order;
+    if (spec && rad_redo) cudaStreamWaitEvent(st, ev_join, 0);  // speculation void: redo below
+    const int order = rad_redo ? 1 : rad_order;
     cudaStream_t rs = (order == 1 || order == 3) ? st : side;  // multi-block radius syncs its stream
-    bool rad_done = spec && !rad_multi;
+    bool rad_done = spec && !rad_redo;
     std::function<int()> launch_radius = [&]() -> int {
         if (rad_done) return APB_OK;
         rad_done = true;

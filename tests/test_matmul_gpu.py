@@ -82,7 +82,7 @@ def test_full_config_vs_reference(cfg):
                                   "APB_NO_SPEC_PACK=1", "APB_NO_GRAPHS=1",
                                   "APB_RECOMBINE64=1", "APB_NO_RAD_FUSE=1", "APB_NO_PDL=1",
                                   "APB_NO_SPEC_STEP=1", "APB_NO_PRIO=1", "APB_RAD_SPLIT=1", "APB_RAD_BESIDE=1",
-                                  "APB_BAND_KBNORM=1"])
+                                  "APB_BAND_KBNORM=1", "APB_NO_SCAN_PLANES=1"])
 def test_kernel_variants_golden(hook):
     """alternative kernels / schedules selected by the library's tuning hooks
     (unit GEMM used when a diagonal could overflow int32, byte-serial pack,
@@ -259,3 +259,25 @@ def test_host_pipeline_matches_sync():
         for a, b, ha, hb, hc, *_ in jobs:
             ref, _ = po.matmul(a, b, n, n, n, p, which="ref", algo=1, threads=os.cpu_count() or 8)
             assert hc.identical(ref).all()
+
+
+@pytest.mark.parametrize("shift", [700, -700, 0])
+def test_radius_planes_far_exponents(shift):
+    """single-block products whose operand exponents sit far from 1 (|e| ~ 700):
+    the scan's uncentred radius planes are flagged unsafe on the device and the
+    centred planes (src/matmul.cpp:386-403) take over; repeated calls (graph
+    replays) stay bit-identical to the reference"""
+    from paper_1901_04289_b200 import ops
+    rng = np.random.default_rng(0xB200 + 700 + shift)
+    n, p = 256, 128
+    ea = shift + rng.integers(-4, 5, size=n * n)
+    eb = -shift // 2 + rng.integers(-4, 5, size=n * n)
+    a = gen.random_balls(rng, n * n, p, exps=ea, rad_k=130, rad_frac=0.3)
+    b = gen.random_balls(rng, n * n, p, exps=eb, rad_k=130, rad_frac=0.3)
+    A, B = _mat(a, n, n), _mat(b, n, n)
+    ref, _ = po.matmul(a, b, n, n, n, p, which="ref", algo=1, threads=os.cpu_count() or 8)
+    out = ops.block_matmul_ball(A, B, p)
+    for rep in range(3):
+        got = ops.block_matmul_ball(A, B, p, out=out).balls.to_host()
+        ok = got.identical(ref)
+        assert ok.all(), f"rep {rep}: {(~ok).sum()} entries differ"
