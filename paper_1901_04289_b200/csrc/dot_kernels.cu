@@ -864,6 +864,275 @@ __global__ void __launch_bounds__(128, APB_GRP_MINB) dot_grp_kernel(DotArgs A) {
     }
 }
 
+// ------------------------------------------------- bulk-staged kernel
+// Contiguous batches (dot b = elements [b n, (b+1) n) of x and y, n even, 2-limb
+// operands, 16-byte aligned arrays -- config 1): a persistent CTA of 8 warps
+// streams chunks of 8 consecutive dots through a 3-stage shared-memory ring with
+// cp.async.bulk (10 bulk copies per chunk: the five SoA arrays of x and y, each
+// one contiguous range), so the memory system always has ~2 chunks per SM in
+// flight without holding registers.  Warp w takes dot w of the chunk: lanes over
+// its terms, both passes read shared memory; the reduced states are parked per
+// warp and finalized 32 at a time, one dot per lane.  Arithmetic = dot_small.
+#ifndef APB_BLK_DOTS
+#define APB_BLK_DOTS 16
+#endif
+#ifndef APB_BLK_STAGES
+#define APB_BLK_STAGES 1
+#endif
+constexpr int BLK_DOTS = APB_BLK_DOTS, BLK_STAGES = APB_BLK_STAGES;  // dots (= warps) per chunk, ring depth
+
+struct BlkLayout {  // byte offsets of one stage (16-byte aligned pieces)
+    int xm, ym, xe, ye, xf, yf, xr, yr, xk, yk, bytes;
+};
+__host__ __device__ inline int align16(int v) { return (v + 15) & ~15; }
+__host__ __device__ inline BlkLayout blk_layout(int n, int L) {
+    BlkLayout o;
+    const int E = BLK_DOTS * n;
+    int off = 0;
+    o.xm = off; off += align16(E * L * 8);
+    o.ym = off; off += align16(E * L * 8);
+    o.xe = off; off += align16(E * 8);
+    o.ye = off; off += align16(E * 8);
+    o.xf = off; off += align16(E * 8);
+    o.yf = off; off += align16(E * 8);
+    o.xr = off; off += align16(E * 4);
+    o.yr = off; off += align16(E * 4);
+    o.xk = off; off += align16(E);
+    o.yk = off; off += align16(E);
+    o.bytes = off;
+    return o;
+}
+
+APB_DEV uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+APB_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+APB_DEV void mbar_init1(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+}
+APB_DEV void mbar_expect(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+APB_DEV void mbar_wait_par(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "W_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra W_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+template <int L>
+APB_DEV void blk_issue(uint8_t* st, uint64_t* bar, const DotArgs& A, const BlkLayout& lay, int64_t chunk, int n) {
+    const int64_t d0 = chunk * BLK_DOTS;
+    const int nd = (int)(A.batch - d0 < BLK_DOTS ? A.batch - d0 : BLK_DOTS);
+    const int64_t ex = A.idx.x_off + d0 * n, ey = A.idx.y_off + d0 * n;
+    const uint32_t E = (uint32_t)(nd * n);
+    mbar_expect(bar, E * (2 * (L * 8 + 8 + 8 + 4 + 1)));
+    bulk_g2s(st + lay.xm, A.x.mant + ex * L, E * L * 8, bar);
+    bulk_g2s(st + lay.ym, A.y.mant + ey * L, E * L * 8, bar);
+    bulk_g2s(st + lay.xe, A.x.exp + ex, E * 8, bar);
+    bulk_g2s(st + lay.ye, A.y.exp + ey, E * 8, bar);
+    bulk_g2s(st + lay.xf, A.x.rad_exp + ex, E * 8, bar);
+    bulk_g2s(st + lay.yf, A.y.rad_exp + ey, E * 8, bar);
+    bulk_g2s(st + lay.xr, A.x.rad_man + ex, E * 4, bar);
+    bulk_g2s(st + lay.yr, A.y.rad_man + ey, E * 4, bar);
+    bulk_g2s(st + lay.xk, A.x.kind + ex, E, bar);
+    bulk_g2s(st + lay.yk, A.y.kind + ey, E, bar);
+}
+
+template <int L>
+APB_DEV void blk_term(Term<L>& t, const uint8_t* st, const BlkLayout& lay, int e, bool neg, bool mant) {
+    t.kx = st[lay.xk + e];
+    t.ky = st[lay.yk + e];
+    t.ex = ((const int64_t*)(st + lay.xe))[e];
+    t.ey = ((const int64_t*)(st + lay.ye))[e];
+    t.fx = ((const int64_t*)(st + lay.xf))[e];
+    t.fy = ((const int64_t*)(st + lay.yf))[e];
+    t.rx = ((const uint32_t*)(st + lay.xr))[e];
+    t.ry = ((const uint32_t*)(st + lay.yr))[e];
+    if (mant) {
+#pragma unroll
+        for (int j = 0; j < L; j++) {
+            t.xm[j] = ((const uint64_t*)(st + lay.xm))[e * L + j];
+            t.ym[j] = ((const uint64_t*)(st + lay.ym))[e * L + j];
+        }
+    }
+    t.neg = neg;
+}
+
+template <int L, int NS>
+__global__ void __launch_bounds__(32 * BLK_DOTS, 1) dot_blk_kernel(DotArgs A, int64_t nchunks) {
+    extern __shared__ __align__(128) uint8_t blk_smem[];
+    constexpr int PK = NS + 8;  // s[NS], err, srad, e_max, e_min, e_rad, nnz, fb, dot index
+    const int n = (int)A.n;
+    const BlkLayout lay = blk_layout(n, L);
+    uint8_t* stages = blk_smem;
+    uint64_t* bars = (uint64_t*)(blk_smem + BLK_STAGES * lay.bytes);
+    uint64_t* park = bars + BLK_STAGES;  // [warps][32][PK]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint64_t* mypark = park + (size_t)w * 32 * PK;
+    const bool with_radius = A.mode == APB_DOT_BALL;
+    const bool track_min = A.prec > 128;
+    const bool neg = A.subtract != 0;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < BLK_STAGES; q++) mbar_init1(&bars[q]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // this CTA's chunks: blockIdx.x + k * gridDim.x
+    const int64_t my_n = nchunks > blockIdx.x ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (threadIdx.x == 0)
+        for (int64_t k = 0; k < BLK_STAGES - 1 && k < my_n; k++)
+            blk_issue<L>(stages + k * lay.bytes, &bars[k], A, lay, blockIdx.x + k * gridDim.x, n);
+    int parked = 0;
+    for (int64_t k = 0; k < my_n; k++) {
+        __syncthreads();  // every warp is done with chunk k-1: its stage is free
+        if (threadIdx.x == 0 && k + BLK_STAGES - 1 < my_n) {
+            const int64_t kk = k + BLK_STAGES - 1;
+            blk_issue<L>(stages + (kk % BLK_STAGES) * lay.bytes, &bars[kk % BLK_STAGES], A, lay,
+                         blockIdx.x + kk * gridDim.x, n);
+        }
+        const int sidx = (int)(k % BLK_STAGES);
+        mbar_wait_par(&bars[sidx], (uint32_t)((k / BLK_STAGES) & 1));
+        const uint8_t* st = stages + sidx * lay.bytes;
+        const int64_t chunk = blockIdx.x + k * gridDim.x;
+        const int64_t b = chunk * BLK_DOTS + w;
+        if (b < A.batch) {
+            const int e0 = w * n;
+            ScanAcc sc{INT64_MIN, INT64_MAX, INT64_MIN, 0, false};
+            for (int i = lane; i < n; i += 32) {
+                Term<L> t;
+                blk_term<L>(t, st, lay, e0 + i, neg, track_min);
+                scan_term<L>(sc, t, track_min, with_radius);
+            }
+            const bool fb = __any_sync(0xffffffffu, sc.fb);
+            sc.e_max = warp_max(sc.e_max);
+            sc.e_min = warp_min(sc.e_min);
+            sc.e_rad = warp_max(sc.e_rad);
+            sc.nnz = warp_sum(sc.nnz);
+            const Plan pl = finish_plan(sc.e_max, sc.e_min, sc.e_rad, sc.nnz, fb, n, A.prec, A.disable_reduction);
+            Acc<L, NS> acc;
+#pragma unroll
+            for (int j = 0; j < NS; j++) acc.s[j] = 0;
+            acc.err = 0;
+            acc.srad = 0;
+            if (pl.status == 0) {
+                for (int i = lane; i < n; i += 32) {
+                    Term<L> t;
+                    blk_term<L>(t, st, lay, e0 + i, neg, true);
+                    const bool xz = (t.kx & APB_KIND_MASK) == APB_ZERO, yz = (t.ky & APB_KIND_MASK) == APB_ZERO;
+                    if (!xz && !yz) acc_term<L, NS>(acc, t, pl);
+                    if (with_radius) rad_term<L, NS>(acc, t, pl);
+                }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                uint64_t c = 0;
+#pragma unroll
+                for (int j = 0; j < NS; j++) {
+                    const uint64_t v = __shfl_xor_sync(0xffffffffu, acc.s[j], o);
+                    const uint64_t s1 = acc.s[j] + v;
+                    const uint64_t c1 = s1 < v;
+                    const uint64_t s2 = s1 + c;
+                    acc.s[j] = s2;
+                    c = c1 | (s2 < c);
+                }
+                acc.err += __shfl_xor_sync(0xffffffffu, acc.err, o);
+                acc.srad += __shfl_xor_sync(0xffffffffu, acc.srad, o);
+            }
+            if (lane == 0) {
+                uint64_t* pk = mypark + (size_t)parked * PK;
+#pragma unroll
+                for (int j = 0; j < NS; j++) pk[j] = acc.s[j];
+                pk[NS] = acc.err;
+                pk[NS + 1] = acc.srad;
+                pk[NS + 2] = (uint64_t)sc.e_max;
+                pk[NS + 3] = (uint64_t)sc.e_min;
+                pk[NS + 4] = (uint64_t)sc.e_rad;
+                pk[NS + 5] = sc.nnz;
+                pk[NS + 6] = fb ? 1 : 0;
+                pk[NS + 7] = (uint64_t)b;
+            }
+            parked++;
+        }
+        // finalize 32 parked dots (or the rest at the end), one per lane
+        if (parked == 32 || (k + 1 == my_n && parked > 0)) {
+            __syncwarp();
+            if (lane < parked) {
+                const uint64_t* pk = mypark + (size_t)lane * PK;
+                const int64_t bb = (int64_t)pk[NS + 7];
+                const Plan pl = finish_plan((int64_t)pk[NS + 2], (int64_t)pk[NS + 3], (int64_t)pk[NS + 4], pk[NS + 5],
+                                            pk[NS + 6] != 0, n, A.prec, A.disable_reduction);
+                if (pl.status != 0) {
+                    if (A.state) write_state(A.state + bb, pl, 0, 0);
+                    if (pl.status == 1) {
+                        A.fb_flag[bb] = 1;
+                    } else {
+                        GFloat<1> z;
+                        z.kind = APB_ZERO;
+                        z.neg = 0;
+                        z.e = 0;
+                        z.n = 0;
+                        gf_store(A.out, bb, z, mag_zero(), A.status);
+                    }
+                } else {
+                    uint64_t sv[NS];
+#pragma unroll
+                    for (int j = 0; j < NS; j++) sv[j] = pk[j];
+                    if (A.state) write_state(A.state + bb, pl, pk[NS], pk[NS + 1]);
+                    if (A.acc)
+                        for (int j = 0; j < pl.n_s && j < A.acc_stride; j++) A.acc[bb * A.acc_stride + j] = sv[j];
+                    finalize_store<NS>(pl, sv, pk[NS], pk[NS + 1], A.prec, with_radius, A.out, bb, A.status);
+                }
+            }
+            __syncwarp();
+            parked = 0;
+        }
+    }
+}
+
+// eligibility: contiguous dots of even length n, equal 2-limb x / y, 16-byte
+// aligned arrays and offsets, no initial value, stage fits shared memory
+static bool blk_ok(const DotArgs& A, int L) {
+    // opt-in (APB_DOT_BULK=1): measured compute-bound at 0.24-0.30 ms on config 1
+    // against 0.234 ms for dot_grp_kernel, whose lane groups need fewer instructions
+    static const bool on = std::getenv("APB_DOT_BULK") != nullptr;
+    if (!on || A.palen > 0 || A.has_init || A.n <= 0 || ((BLK_DOTS * A.n) & 15) || A.x.L != L || A.y.L != L)
+        return false;  // (chunk offsets of the 1-byte kind arrays stay 16-byte aligned)
+    if (A.idx.xstep != 1 || A.idx.ystep != 1 || A.idx.xs1 != A.n || A.idx.ys1 != A.n) return false;
+    if (A.idx.bdiv != 1 && (A.idx.xs2 != 0 || A.idx.ys2 != 0)) return false;
+    if ((A.idx.x_off & 15) || (A.idx.y_off & 15)) return false;
+    auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+    if (!al(A.x.mant) || !al(A.x.exp) || !al(A.x.kind) || !al(A.x.rad_man) || !al(A.x.rad_exp)) return false;
+    if (!al(A.y.mant) || !al(A.y.exp) || !al(A.y.kind) || !al(A.y.rad_man) || !al(A.y.rad_exp)) return false;
+    const BlkLayout lay = blk_layout((int)A.n, L);
+    return (size_t)BLK_STAGES * lay.bytes + 64 + (size_t)BLK_DOTS * 32 * 16 * 8 <= 225 * 1024;
+}
+
+template <int L, int NS>
+static void launch_blk(const DotArgs& A, cudaStream_t st) {
+    constexpr int PK = NS + 8;
+    const BlkLayout lay = blk_layout((int)A.n, L);
+    const size_t shm = (size_t)BLK_STAGES * lay.bytes + BLK_STAGES * 8 + (size_t)BLK_DOTS * 32 * PK * 8;
+    static size_t attr = 0;
+    if (shm > attr) {
+        cudaFuncSetAttribute(dot_blk_kernel<L, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        attr = shm;
+    }
+    const int64_t nchunks = (A.batch + BLK_DOTS - 1) / BLK_DOTS;
+    const unsigned grid = (unsigned)std::min<int64_t>(nchunks, 148);
+    dot_blk_kernel<L, NS><<<grid, 32 * BLK_DOTS, shm, st>>>(A, nchunks);
+    count_launch();
+}
+
 // ------------------------------------------------- staged small kernel
 // For dots of <= 128 terms with <= 2-limb operands (config 1): the warp's 32
 // dots are software-pipelined through shared memory -- while dot g is
@@ -1815,6 +2084,10 @@ static void launch_grp(DotArgs A, cudaStream_t st) {
 
 template <int L, int NS>
 static bool try_small_tpl(const DotArgs& A, int64_t total, cudaStream_t st) {
+    if (L == 2 && A.batch >= 148 * BLK_DOTS * 4 && blk_ok(A, L)) {  // contiguous batch: bulk-staged
+        launch_blk<L, NS>(A, st);
+        return true;
+    }
     const int tpd = pick_tpd(total);
     if (tpd < 32 && !std::getenv("APB_DOT_KEEP") && !std::getenv("APB_DOT_STAGE")) {
         switch (tpd) {

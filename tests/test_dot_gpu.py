@@ -118,7 +118,7 @@ def test_reference_shaped_dot_ball():
     assert got.identical(ref).all()
 
 
-@pytest.mark.parametrize("hook", ["APB_DOT_KEEP", "APB_DOT_STAGE", "APB_DOT_GENERIC", "APB_DOT_TPD"])
+@pytest.mark.parametrize("hook", ["APB_DOT_KEEP", "APB_DOT_STAGE", "APB_DOT_GENERIC", "APB_DOT_TPD", "APB_DOT_BULK"])
 def test_dot_kernel_variants(hook):
     """the register-resident (KEEP) and cp.async-staged (STAGE) dot kernels,
     selected by their tuning hooks in a subprocess, on the golden and edge cases"""
@@ -127,7 +127,7 @@ def test_dot_kernel_variants(hook):
     import sys
     env = dict(os.environ, **{hook: "32" if hook == "APB_DOT_TPD" else "1"})  # TPD 32: one warp per dot
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-k",
-                        "test_dot_golden_gpu or test_edge_random or test_host_entry",
+                        "test_dot_golden_gpu or test_edge_random or test_host_entry or test_c1_full",
                         os.path.abspath(__file__)], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:]
 
