@@ -608,23 +608,22 @@ __global__ void __launch_bounds__(128) recombine_kernel(RecombineArgs R) {
         const int64_t bit = (int64_t)db * w;
         T[bit >> 6] |= (uint64_t)R.Tw[(size_t)w * plane + off] << (bit & 63);
     }
+    // carries: c_g << (8 d1_g) collected per 64-bit limb in signed 128-bit sums (each
+    // term < 2^95 in magnitude, a few per limb), then one signed carry pass over T
+    __int128 cs[CAP];
+    for (int q = 0; q < NT; q++) cs[q] = 0;
     for (int g = 0; g < R.n_groups; g++) {
         const int64_t c = R.Tc[(size_t)g * plane + off];
         if (c == 0) continue;
         const int64_t bit = 8 * (int64_t)R.group_d1[g];
-        const int li = (int)(bit >> 6), bo = (int)(bit & 63);
-        // add c << bit, sign-extended
-        const uint64_t ext = c < 0 ? ~0ull : 0ull;
-        uint64_t lo = (uint64_t)c << bo;
-        uint64_t hi = bo ? (((uint64_t)c >> (64 - bo)) | (ext << bo)) : ext;
-        uint64_t cy = 0;
-        for (int q = li; q < NT; q++) {
-            uint64_t add = q == li ? lo : (q == li + 1 ? hi : ext);
-            uint64_t s1 = T[q] + add;
-            uint64_t c1 = s1 < add;
-            uint64_t s2 = s1 + cy;
-            cy = c1 | (s2 < cy);
-            T[q] = s2;
+        cs[bit >> 6] += (__int128)c << (bit & 63);
+    }
+    {
+        __int128 cy = 0;
+        for (int q = 0; q < NT; q++) {
+            const __int128 v = (__int128)T[q] + cs[q] + cy;
+            T[q] = (uint64_t)v;
+            cy = v >> 64;  // arithmetic: the sign travels up (two's complement mod 2^(64 NT))
         }
     }
     if (R.int_out)
