@@ -1723,8 +1723,8 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
     // sums (__dmul_rn / __dadd_rn, no contraction) folded into the Mag bound at
     // every 1024-term chunk end (src/matmul.cpp:404-431); the folded Mags wait in
     // shared memory (they are touched once per chunk)
-    __shared__ double sA[RK][RT + 1];
-    __shared__ double sB[RK][RT];
+    __shared__ __align__(16) double sA[RK][RT + 2];  // rows 16-byte aligned: 128-bit operand loads
+    __shared__ __align__(16) double sB[RK][RT];
     __shared__ uint32_t eb[16][RTHREADS];
     __shared__ int64_t ef[16][RTHREADS];
     constexpr int PER = RK * RT / RTHREADS;  // tile elements per thread per operand
@@ -1741,7 +1741,21 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
         }
     const Mag infl = mag_parts((1ull << 29) + 1, 1);
     double pa[PER], pb[PER];
+    const bool rows_in = i0 + RT <= M && j0 + RT <= N;
     auto fetch = [&](int64_t l0) {
+        if (rows_in && l0 + RK <= w && a_trans) {  // interior tile: strided pointers, no bounds tests
+            // element u: kk = tid / 32 + 2 u (RTHREADS = 64), rr = tid % 32
+            const int kk0 = threadIdx.x / RT, rr = threadIdx.x % RT;
+            const double* pA = da + (l0 + kk0) * M + i0 + rr;
+            const double* pB = db + (l0 + kk0) * N + j0 + rr;
+            const int64_t sa = (int64_t)(RTHREADS / RT) * M, sb = (int64_t)(RTHREADS / RT) * N;
+#pragma unroll
+            for (int u = 0; u < PER; u++) {
+                pa[u] = __ldg(pA + u * sa);
+                pb[u] = __ldg(pB + u * sb);
+            }
+            return;
+        }
 #pragma unroll
         for (int u = 0; u < PER; u++) {
             const int q = threadIdx.x + RTHREADS * u;
@@ -1765,10 +1779,20 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
         const int kmax = (w - l0) < RK ? (int)(w - l0) : RK;
         for (int kk = 0; kk < kmax; kk++) {
             double a[4], b[4];
-#pragma unroll
-            for (int r = 0; r < 4; r++) a[r] = sA[kk][ty * 4 + r];
-#pragma unroll
-            for (int c = 0; c < 4; c++) b[c] = sB[kk][tx * 4 + c];
+            {
+                const double2 a01 = *reinterpret_cast<const double2*>(&sA[kk][ty * 4]);
+                const double2 a23 = *reinterpret_cast<const double2*>(&sA[kk][ty * 4 + 2]);
+                const double2 b01 = *reinterpret_cast<const double2*>(&sB[kk][tx * 4]);
+                const double2 b23 = *reinterpret_cast<const double2*>(&sB[kk][tx * 4 + 2]);
+                a[0] = a01.x;
+                a[1] = a01.y;
+                a[2] = a23.x;
+                a[3] = a23.y;
+                b[0] = b01.x;
+                b[1] = b01.y;
+                b[2] = b23.x;
+                b[3] = b23.y;
+            }
 #pragma unroll
             for (int r = 0; r < 4; r++)
 #pragma unroll

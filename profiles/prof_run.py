@@ -45,6 +45,16 @@ def main():
         A, B = ops.BallMatrix(a.to_device(), 512, 512), ops.BallMatrix(b.to_device(), 512, 512)
         for _ in range(reps):
             ops.block_int_product_imad(A, B, 0, 512, 6)
+    if which in ("c5m64", "all"):  # dense radius products + band GEMM at N = 2048, p = 64
+        a, b = gen.config5_matrices(n=2048, p=64)
+        A, B = ops.BallMatrix(a.to_device(), 2048, 2048), ops.BallMatrix(b.to_device(), 2048, 2048)
+        for _ in range(reps):
+            ops.block_matmul_ball(A, B, 64)
+    if which in ("c5ds", "all"):  # dot_small_kernel: 8192 dots of N = 1000 at p = 256
+        x, y = gen.config5_dots(p=256)
+        dx, dy = x.to_device(), y.to_device()
+        for _ in range(reps):
+            ops.dot_batch(dx, dy, 1000, 8192, 256)
     torch.cuda.synchronize()
     print("prof_run ok", which, reps)
 
