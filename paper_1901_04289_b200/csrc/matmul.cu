@@ -1148,180 +1148,9 @@ struct LineWins {
     int64_t* bot[3];
 };
 
-__global__ void init_wins_kernel(LineWins W, int64_t n) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-#pragma unroll
-    for (int q = 0; q < 3; q++) {
-        W.top[q][t] = INT64_MIN;
-        W.bot[q][t] = INT64_MAX;
-    }
-}
-
 APB_DEV void win_merge(int64_t& top, int64_t& bot, int64_t t, int64_t b) {
     top = t > top ? t : top;
     bot = b < bot ? b : bot;
-}
-
-APB_DEV void win_atomic(int64_t* top, int64_t* bot, int64_t t, int64_t b) {
-    if (t == INT64_MIN) return;
-    atomicMax((long long*)top, (long long)t);
-    atomicMin((long long*)bot, (long long)b);
-}
-
-// rows of A: warp per (row, 32*CH chunk of k), lanes over k (coalesced)
-constexpr int ROW_CH = 4;
-__global__ void __launch_bounds__(256) fused_rows_kernel(BallsView A, int64_t M, int64_t K, LineWins W,
-                                                         ScanSummary* sum, long long* nz1, long long* nz2) {
-    const int lane = threadIdx.x & 31;
-    const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (i >= M) return;
-    const int64_t k0 = (int64_t)blockIdx.y * 32 * ROW_CH;
-    int64_t t0 = INT64_MIN, b0 = INT64_MAX, t1 = INT64_MIN, b1 = INT64_MAX, t2 = INT64_MIN, b2 = INT64_MAX;
-    int64_t prec = 0;
-    int special = 0;
-    int c1 = 0, c2 = 0;  // nonzero |A| and R_A entries (radius sparsity)
-#pragma unroll
-    for (int c = 0; c < ROW_CH; c++) {
-        const int64_t k = k0 + 32 * c + lane;
-        if (k >= K) break;
-        const int64_t e = i * K + k;
-        special |= ball_special(A, e);
-        int64_t t, b;
-        if (mid_window(A, e, t, b)) {
-            win_merge(t0, b0, t, b);
-            prec = (t - b) > prec ? (t - b) : prec;
-        }
-        const Mag m1 = mid_upper(A, e);
-        if (m1.kind == 1) {
-            win_merge(t1, b1, m1.f, m1.f - 30);
-            c1++;
-        }
-        const uint32_t rb = A.rad_man[e];
-        if (rb != 0 && rb != APB_RAD_INF) {
-            const Mag m2 = mag_parts(rb, A.rad_exp[e]);
-            win_merge(t2, b2, m2.f, m2.f - 30);
-            c2++;
-        }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        int64_t x;
-        x = __shfl_xor_sync(0xffffffffu, t0, o); t0 = x > t0 ? x : t0;
-        x = __shfl_xor_sync(0xffffffffu, b0, o); b0 = x < b0 ? x : b0;
-        x = __shfl_xor_sync(0xffffffffu, t1, o); t1 = x > t1 ? x : t1;
-        x = __shfl_xor_sync(0xffffffffu, b1, o); b1 = x < b1 ? x : b1;
-        x = __shfl_xor_sync(0xffffffffu, t2, o); t2 = x > t2 ? x : t2;
-        x = __shfl_xor_sync(0xffffffffu, b2, o); b2 = x < b2 ? x : b2;
-        x = __shfl_xor_sync(0xffffffffu, prec, o); prec = x > prec ? x : prec;
-        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
-        c2 += __shfl_xor_sync(0xffffffffu, c2, o);
-    }
-    special = __any_sync(0xffffffffu, special);
-    if (lane == 0) {
-        if (c1) atomicAdd((unsigned long long*)nz1, (unsigned long long)c1);
-        if (c2) atomicAdd((unsigned long long*)nz2, (unsigned long long)c2);
-        win_atomic(&W.top[0][i], &W.bot[0][i], t0, b0);
-        win_atomic(&W.top[1][i], &W.bot[1][i], t1, b1);
-        win_atomic(&W.top[2][i], &W.bot[2][i], t2, b2);
-        if (special) atomicOr(&sum->special_a, 1);
-        if (prec) atomicMax(&sum->prec_a, (long long)prec);
-    }
-}
-
-constexpr int FCOL_CHUNK = 4;
-// columns of B: thread per (column, FCOL_CHUNK rows), coalesced across threads
-__global__ void __launch_bounds__(128) fused_cols_kernel(BallsView B, int64_t K, int64_t N, LineWins W,
-                                                         ScanSummary* sum, long long* nz1, long long* nz2) {
-    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t k0 = (int64_t)blockIdx.y * FCOL_CHUNK;
-    const int64_t k1 = k0 + FCOL_CHUNK < K ? k0 + FCOL_CHUNK : K;
-    int64_t t0 = INT64_MIN, b0 = INT64_MAX, t1 = INT64_MIN, b1 = INT64_MAX, t2 = INT64_MIN, b2 = INT64_MAX;
-    int64_t prec = 0;
-    int special = 0;
-    int c1 = 0, c2 = 0;  // nonzero R_B and |B| + R_B entries
-    if (j < N) {
-        for (int64_t k = k0; k < k1; k++) {
-            const int64_t e = k * N + j;
-            special |= ball_special(B, e);
-            int64_t t, b;
-            if (mid_window(B, e, t, b)) {
-                win_merge(t0, b0, t, b);
-                prec = (t - b) > prec ? (t - b) : prec;
-            }
-            const uint32_t rb = B.rad_man[e];
-            const Mag r = (rb != 0 && rb != APB_RAD_INF) ? mag_parts(rb, B.rad_exp[e]) : mag_zero();
-            if (r.kind == 1) {
-                win_merge(t1, b1, r.f, r.f - 30);
-                c1++;
-            }
-            const Mag s = mag_add(mid_upper(B, e), r);
-            if (s.kind == 1) {
-                win_merge(t2, b2, s.f, s.f - 30);
-                c2++;
-            }
-        }
-        win_atomic(&W.top[0][j], &W.bot[0][j], t0, b0);
-        win_atomic(&W.top[1][j], &W.bot[1][j], t1, b1);
-        win_atomic(&W.top[2][j], &W.bot[2][j], t2, b2);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        int64_t x = __shfl_xor_sync(0xffffffffu, prec, o);
-        prec = x > prec ? x : prec;
-        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
-        c2 += __shfl_xor_sync(0xffffffffu, c2, o);
-    }
-    special = __any_sync(0xffffffffu, special);
-    if ((threadIdx.x & 31) == 0) {
-        if (special) atomicOr(&sum->special_b, 1);
-        if (prec) atomicMax(&sum->prec_b, (long long)prec);
-        if (c1) atomicAdd((unsigned long long*)nz1, (unsigned long long)c1);
-        if (c2) atomicAdd((unsigned long long*)nz2, (unsigned long long)c2);
-    }
-}
-
-// widths, centring exponents: rows -> maxw_a, ecen1/ecen2 and radius widths
-// (mw1[0], mw2[0]); columns -> maxw_b, fcen1/fcen2 (mw1[1], mw2[1])
-__global__ void fused_finish_kernel(LineWins R, LineWins C, int64_t M, int64_t N, int64_t* ecen1,
-                                    int64_t* ecen2, int64_t* fcen1, int64_t* fcen2, ScanSummary* sum,
-                                    long long* mw1, long long* mw2) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    long long wa = 0, wb = 0, r1 = 0, r2 = 0, c1 = 0, c2 = 0;
-    if (t < M) {
-        if (R.top[0][t] != INT64_MIN) wa = R.top[0][t] - R.bot[0][t];
-        const int64_t t1 = R.top[1][t], b1 = R.bot[1][t], t2 = R.top[2][t], b2 = R.bot[2][t];
-        ecen1[t] = t1 == INT64_MIN ? 0 : -((t1 + b1) / 2);
-        ecen2[t] = t2 == INT64_MIN ? 0 : -((t2 + b2) / 2);
-        if (t1 != INT64_MIN) r1 = t1 - b1;
-        if (t2 != INT64_MIN) r2 = t2 - b2;
-    }
-    if (t < N) {
-        if (C.top[0][t] != INT64_MIN) wb = C.top[0][t] - C.bot[0][t];
-        const int64_t t1 = C.top[1][t], b1 = C.bot[1][t], t2 = C.top[2][t], b2 = C.bot[2][t];
-        fcen1[t] = t1 == INT64_MIN ? 0 : -((t1 + b1) / 2);
-        fcen2[t] = t2 == INT64_MIN ? 0 : -((t2 + b2) / 2);
-        if (t1 != INT64_MIN) c1 = t1 - b1;
-        if (t2 != INT64_MIN) c2 = t2 - b2;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        long long x;
-        x = __shfl_xor_sync(0xffffffffu, wa, o); wa = x > wa ? x : wa;
-        x = __shfl_xor_sync(0xffffffffu, wb, o); wb = x > wb ? x : wb;
-        x = __shfl_xor_sync(0xffffffffu, r1, o); r1 = x > r1 ? x : r1;
-        x = __shfl_xor_sync(0xffffffffu, r2, o); r2 = x > r2 ? x : r2;
-        x = __shfl_xor_sync(0xffffffffu, c1, o); c1 = x > c1 ? x : c1;
-        x = __shfl_xor_sync(0xffffffffu, c2, o); c2 = x > c2 ? x : c2;
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (wa) atomicMax(&sum->maxw_a, wa);
-        if (wb) atomicMax(&sum->maxw_b, wb);
-        if (r1) atomicMax(&mw1[0], r1);
-        if (r2) atomicMax(&mw2[0], r2);
-        if (c1) atomicMax(&mw1[1], c1);
-        if (c2) atomicMax(&mw2[1], c2);
-    }
 }
 
 // ---- one-pass plan scan, v2: thread per entry, every field loaded up front,
@@ -2305,7 +2134,10 @@ __global__ void __launch_bounds__(T) rad_sparse2_kernel(RadPair P) {
 }
 
 // dense variants (stand down unless picked): blockIdx.z = product
-__global__ void __launch_bounds__(64) rad_gemm2_kernel(RadPair P) {
+#ifndef APB_RADG_MINB
+#define APB_RADG_MINB 8  // 128 registers, no spills: 16 warps per SM
+#endif
+__global__ void __launch_bounds__(64, APB_RADG_MINB) rad_gemm2_kernel(RadPair P) {
     if (blockIdx.z == 0)
         rad_gemm_body(P.da1, P.db1, P.M, P.N, P.K, P.ec1, P.fc1, P.r1b, P.r1f, 0, 1, P.mw1, blockIdx.x, blockIdx.y,
                       P.cflag);
@@ -2354,17 +2186,6 @@ __global__ void rad_combine_kernel(BallsOut C, int64_t cnt, const uint32_t* r1b,
     Mag r = mag_add(mag_load(r1b[t], r1f[t]), mag_load(r2b[t], r2f[t]));
     Mag c = mag_load(C.rad_man[t], C.rad_exp[t]);
     mag_store(mag_add(c, r), &C.rad_man[t], &C.rad_exp[t]);
-}
-
-// Mag-arithmetic path when an operand plane holds inf (src/matmul.cpp:372-385)
-__global__ void rad_mag_path_kernel(BallsView A, BallsView B, int64_t M, int64_t K, int64_t N,
-                                    int wa, int wb, uint32_t* rb, int64_t* rf) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= M * N) return;
-    const int64_t i = t / N, j = t % N;
-    Mag acc = mag_zero();
-    for (int64_t l = 0; l < K; l++) acc = mag_add(acc, mag_mul(rad_operand(A, i * K + l, wa), rad_operand(B, l * N + j, wb)));
-    mag_store(acc, &rb[t], &rf[t]);
 }
 
 // ------------------------------------------------------------ K8 complex
