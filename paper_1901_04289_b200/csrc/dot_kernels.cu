@@ -1414,35 +1414,41 @@ __device__ void gb_addmul(GBall& acc, const GBall& x, const GBall& y, int64_t p,
     acc.r = mag_add(rad, mag_add(perr, aerr));
 }
 
+// Column-wise ("comba") exact sum of the partial products a_i b_j with i + j >= base,
+// each placed at limb i + j - base of a wlen-limb result: every output limb is
+// written once (three-word running column sum), no read-modify-write of a
+// local-memory product array.  With base = 0 this is the full product; with the
+// base of mulhigh_approx it is exactly the window that routine accumulates (the
+// same pairs, full 128-bit products, exact carries), so both agree bit for bit.
+__device__ void g_comba(const uint64_t* a, int na, const uint64_t* b, int nb, int base, uint64_t* out, int wlen) {
+    uint64_t c0 = 0, c1 = 0, c2 = 0;
+    for (int c = 0; c < wlen; c++) {
+        const int col = c + base;  // i + j
+        const int ilo = col - (nb - 1) > 0 ? col - (nb - 1) : 0;
+        const int ihi = col < na - 1 ? col : na - 1;
+        for (int i = ilo; i <= ihi; i++) {
+            uint64_t lo, hi;
+            mul64(a[i], b[col - i], lo, hi);
+            c0 += lo;
+            const uint64_t k0 = c0 < lo;
+            const uint64_t h = hi + k0;  // hi <= 2^64 - 2: no wrap
+            c1 += h;
+            c2 += c1 < h;
+        }
+        out[c] = c0;
+        c0 = c1;
+        c1 = c2;
+        c2 = 0;
+    }
+}
+
 // mulhigh_approx (include/apball/limb.hpp:194-228)
 __device__ void g_mulhigh(const uint64_t* a, int na, const uint64_t* b, int nb, int k, uint64_t* out) {
     const int total = na + nb;
     const int base = total - k >= 2 ? total - k - 2 : 0;
     const int wlen = total - base;
     uint64_t w[2 * GCAP];
-    for (int i = 0; i < wlen; i++) w[i] = 0;
-    for (int j = 0; j < nb; j++) {
-        int i0 = base > j ? base - j : 0;
-        if (i0 >= na) continue;
-        int len = na - i0;
-        int off = i0 + j - base;
-        uint64_t cy = 0;
-        for (int i = 0; i < len; i++) {
-            uint64_t lo, hi;
-            mul64(a[i0 + i], b[j], lo, hi);
-            uint64_t s1 = w[off + i] + lo;
-            uint64_t c1 = s1 < lo;
-            uint64_t s2 = s1 + cy;
-            uint64_t c2 = s2 < cy;
-            w[off + i] = s2;
-            cy = hi + c1 + c2;
-        }
-        for (int q = off + len; q < wlen && cy; q++) {
-            uint64_t s = w[q] + cy;
-            cy = s < cy;
-            w[q] = s;
-        }
-    }
+    g_comba(a, na, b, nb, base, w, wlen);
     for (int i = 0; i < k; i++) out[i] = w[wlen - k + i];
 }
 
@@ -1544,23 +1550,7 @@ __device__ void g_acc_term(const Plan& pl, uint64_t* s, uint64_t& err, const GF&
             short_prod = true;
         }
     }
-    if (!short_prod) {
-        for (int q = 0; q < nt; q++) t[q] = 0;
-        for (int j = 0; j < nb; j++) {
-            uint64_t cy = 0;
-            for (int i = 0; i < na; i++) {
-                uint64_t lo, hi;
-                mul64(a[i], bb[j], lo, hi);
-                uint64_t s1 = t[i + j] + lo;
-                uint64_t c1 = s1 < lo;
-                uint64_t s2 = s1 + cy;
-                uint64_t c2 = s2 < cy;
-                t[i + j] = s2;
-                cy = hi + c1 + c2;
-            }
-            t[na + j] = cy;
-        }
-    }
+    if (!short_prod) g_comba(a, na, bb, nb, 0, t, nt);  // full product, column-wise
     g_acc_aligned(pl, s, err, t, lead, e_term, negate);
 }
 
