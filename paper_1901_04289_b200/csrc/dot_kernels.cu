@@ -2063,6 +2063,8 @@ static void launch_grp(DotArgs A, cudaStream_t st) {
     constexpr int DPR = 32 / TPD;
     // rounds per warp: enough warps for >= 32 per SM, at most TPD rounds (32 dots)
     int64_t rounds = A.batch / ((int64_t)DPR * 148 * 32);
+    static const int env_rounds = std::getenv("APB_DOT_ROUNDS") ? std::atoi(std::getenv("APB_DOT_ROUNDS")) : 0;
+    if (env_rounds > 0) rounds = env_rounds;  // tuning hook
     rounds = rounds < 1 ? 1 : (rounds > TPD ? TPD : rounds);
     A.dpw = (int)(DPR * rounds);
     const int warps = 4;

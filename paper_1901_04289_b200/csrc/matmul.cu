@@ -502,12 +502,16 @@ struct PackAB {
 template <int NCW>
 __global__ void __launch_bounds__(256) pack_ab_v2_kernel(PackAB P) {
     griddep_wait();
-    if ((int64_t)blockIdx.x < P.ga) {
-        pack_a_v2_body<NCW>(P.a, P.M, P.K, 0, P.K, P.rtop, P.rbot, 0, P.Mp, P.Kp, P.Ap, P.esc, P.mwa, blockIdx.x);
-    } else {
-        const int64_t bb = (int64_t)blockIdx.x - P.ga;
+    // the B blocks (4 entries per thread + a shared-memory transpose) are the long
+    // ones: they take the low block indices so they are dispatched first
+    const int64_t nb = P.gbx * (P.Kp / 32);
+    if ((int64_t)blockIdx.x < nb) {
+        const int64_t bb = blockIdx.x;
         pack_b_v2_body<NCW>(P.b, P.N, 0, P.K, P.ctop, P.cbot, 0, P.Np, P.Kp, P.Bp, P.fsc, P.mwb, bb % P.gbx,
                             bb / P.gbx);
+    } else {
+        pack_a_v2_body<NCW>(P.a, P.M, P.K, 0, P.K, P.rtop, P.rbot, 0, P.Mp, P.Kp, P.Ap, P.esc, P.mwa,
+                            (int64_t)blockIdx.x - nb);
     }
 }
 
@@ -3134,9 +3138,16 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
             pk.ga = blocks_for((int64_t)sgeo.Mp * sgeo.Kp, 256);
             pk.gbx = sgeo.Np / 32;
             const dim3 g((unsigned)(pk.ga + pk.gbx * (sgeo.Kp / 32)));
-            if (sncw == 2) launch_pdl(pack_ab_v2_kernel<2>, g, dim3(256), 0, s, pk);
-            else if (sncw == 5) launch_pdl(pack_ab_v2_kernel<5>, g, dim3(256), 0, s, pk);
-            else launch_pdl(pack_ab_v2_kernel<8>, g, dim3(256), 0, s, pk);
+            // plain launch (not PDL): early-resident pack blocks waiting on the scan
+            // would hold the SMs the radius products need right after it
+            static const bool pack_pdl = std::getenv("APB_PACK_PDL") != nullptr;
+            auto lp = [&](auto kern) {
+                if (pack_pdl) launch_pdl(kern, g, dim3(256), 0, s, pk);
+                else kern<<<g, 256, 0, s>>>(pk);
+            };
+            if (sncw == 2) lp(pack_ab_v2_kernel<2>);
+            else if (sncw == 5) lp(pack_ab_v2_kernel<5>);
+            else lp(pack_ab_v2_kernel<8>);
             prof_end(tk, s);
             count_launch(1);
         }
@@ -3157,7 +3168,23 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
             if (no_scan_planes)  // else the scan wrote uncentred planes (host redoes if flagged)
                 fused_planes2_kernel<<<(unsigned)(nA + blocks_for(K * N, 256)), 256, 0, ss>>>(av, bv, rp, nA);
             if (mid) cudaStreamWaitEvent(ss, mid, 0);
-            rad_sparse2_kernel<2, 256><<<(unsigned)(N + M), 256, 0, ss>>>(rp);
+            {  // highest priority: its blocks are dispatched ahead of the pack's
+                static const int prio = [] {
+                    int least = 0, greatest = 0;
+                    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+                    return std::getenv("APB_NO_PRIO") ? least : greatest;
+                }();
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3((unsigned)(N + M));
+                cfg.blockDim = dim3(256);
+                cfg.stream = ss;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributePriority;
+                at[0].val.priority = prio;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                cudaLaunchKernelEx(&cfg, rad_sparse2_kernel<2, 256>, rp);
+            }
             rad_gemm2_kernel<<<dim3(blocks_for(N, RT), blocks_for(M, RT), 2), RTHREADS, 0, ss>>>(rp);
             prof_end(tk, ss);
             rec_event(ev_join, ss, capturing);
