@@ -411,7 +411,7 @@ def run_dots(torch, steps, warmup, world, rank, want_e2e=True, want_cpu=True):
                       "batch": batch, "n": n, "prec": p},
            "roofline": {"bound": "hbm", "achieved": alg_bytes / (kms * 1e-3) / 1e9, "peak": peak,
                         "unit": "GB/s", "frac": alg_bytes / (kms * 1e-3) / 1e9 / peak,
-                        "traffic": ncu_traffic("dot_small_kernel"), "kernel": "dot_small_kernel<2,3,0>",
+                        "traffic": ncu_traffic("dot_grp_kernel"), "kernel": "dot_grp_kernel<2,3,4>",
                         "kernel_ms": kms, "work": f"{alg_bytes} algorithmic bytes per launch",
                         "peak_source": src},
            "gpu_launches": launches, "clocks": clk.summary()}
