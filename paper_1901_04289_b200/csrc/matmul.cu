@@ -1234,13 +1234,15 @@ APB_DEV void sacc_set(ScanAcc& a, int f, int64_t v) {
 // B side: R_B, |B| + R_B (the operands of src/matmul.cpp:498-509)
 APB_DEV void scan_entry(const BallsView& X, int64_t e, bool a_side, ScanAcc& acc, Mag* op1 = nullptr,
                         Mag* op2 = nullptr) {
-    const uint8_t kd = X.kind[e];
-    const int64_t ex = X.exp[e];
-    const uint32_t rb = X.rad_man[e];
-    const int64_t rexp = X.rad_exp[e];
+    // read-only loads (__ldg): they may be hoisted above the plane stores of an
+    // earlier entry, so a thread's entries are all in flight together
+    const uint8_t kd = __ldg(X.kind + e);
+    const int64_t ex = __ldg(X.exp + e);
+    const uint32_t rb = __ldg(X.rad_man + e);
+    const int64_t rexp = __ldg(X.rad_exp + e);
     const uint64_t* m = X.mant + e * (int64_t)X.L;
-    const uint64_t mtop = m[X.L - 1];
-    const uint64_t m0 = m[0];
+    const uint64_t mtop = __ldg(m + X.L - 1);
+    const uint64_t m0 = __ldg(m);
     const int k = kd & APB_KIND_MASK;
     acc.special |= ((k != APB_ZERO && k != APB_FINITE) || rb == APB_RAD_INF) ? 1 : 0;
     Mag mu = mag_zero();
@@ -1284,7 +1286,7 @@ APB_DEV double uncentred(const Mag& m) {
                                                                                       : 0.0;
 }
 
-constexpr int SCAN_A_COLS = 256;  // entries of a row per A block (one per thread)
+constexpr int SCAN_A_COLS = 512;  // entries of a row per A block (two per thread)
 constexpr int SCAN_B_ROWS = 32;   // rows per B block: 32 columns x 8 warps x 4 rows
 
 // blocks [0, nbA): A rows; [nbA, nbA + nbB): B column tiles.  Partials land in
@@ -1307,13 +1309,16 @@ __global__ void __launch_bounds__(256) scan_v2_kernel(BallsView A, BallsView B, 
     if ((int64_t)blockIdx.x < nbA) {
         const int64_t i = blockIdx.x / cA;
         const int c = (int)(blockIdx.x % cA);
-        const int64_t k = (int64_t)c * SCAN_A_COLS + threadIdx.x;
-        if (k < K) {
-            Mag o1, o2;
-            scan_entry(A, i * K + k, true, acc, &o1, &o2);
-            if (da1T) {  // |A| transposed ([k][i]) and R_A, uncentred
-                da1T[k * M + i] = uncentred(o1);
-                da2[i * K + k] = uncentred(o2);
+#pragma unroll
+        for (int h = 0; h < SCAN_A_COLS / 256; h++) {
+            const int64_t k = (int64_t)c * SCAN_A_COLS + 256 * h + threadIdx.x;
+            if (k < K) {
+                Mag o1, o2;
+                scan_entry(A, i * K + k, true, acc, &o1, &o2);
+                if (da1T) {  // |A| transposed ([k][i]) and R_A, uncentred
+                    da1T[k * M + i] = uncentred(o1);
+                    da2[i * K + k] = uncentred(o2);
+                }
             }
         }
 #pragma unroll
@@ -1372,52 +1377,66 @@ __global__ void scan_v2_finish_kernel(const int64_t* pa, const int64_t* pb, int6
                                       int64_t* rtop, int64_t* rbot, int64_t* ctop, int64_t* cbot,
                                       int64_t* ecen1, int64_t* ecen2, int64_t* fcen1, int64_t* fcen2,
                                       ScanSummary* sum, long long* mw1, long long* mw2) {
-    // warp per line (rows of A first, then columns of B), lanes over the chunk partials
+    // warp per line (rows of A first, then columns of B), lanes over the chunk partials;
+    // the summary maxima / counts are reduced per block in shared memory first (one set
+    // of global atomics per block instead of per line)
+    __shared__ long long red[2][8];  // per side: special, far, prec, w0, w1, w2, n1, n2
     griddep_launch();
+    if (threadIdx.x < 16) red[threadIdx.x >> 3][threadIdx.x & 7] = 0;
+    __syncthreads();
     griddep_wait();
     const int lane = threadIdx.x & 31;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (wid >= M + N) return;
-    const bool a_side = wid < M;
-    const int64_t line = a_side ? wid : wid - M;
-    const int64_t n = a_side ? M : N;
-    const int nc = a_side ? cA : cB;
-    const int64_t* P = a_side ? pa : pb;
-    const int64_t stride = (int64_t)nc * n;
-    ScanAcc acc;
-    sacc_init(acc);
-    for (int c = lane; c < nc; c += 32) {
-        ScanAcc o;
+    if (wid < M + N) {
+        const bool a_side = wid < M;
+        const int64_t line = a_side ? wid : wid - M;
+        const int64_t n = a_side ? M : N;
+        const int nc = a_side ? cA : cB;
+        const int64_t* P = a_side ? pa : pb;
+        const int64_t stride = (int64_t)nc * n;
+        ScanAcc acc;
+        sacc_init(acc);
+        for (int c = lane; c < nc; c += 32) {
+            ScanAcc o;
 #pragma unroll
-        for (int f = 0; f < SCAN_FIELDS; f++) sacc_set(o, f, P[f * stride + (int64_t)c * n + line]);
-        sacc_merge(acc, o);
-    }
+            for (int f = 0; f < SCAN_FIELDS; f++) sacc_set(o, f, P[f * stride + (int64_t)c * n + line]);
+            sacc_merge(acc, o);
+        }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) sacc_shfl(acc, o);
-    if (lane != 0) return;
-    (a_side ? rtop : ctop)[line] = acc.t[0];
-    (a_side ? rbot : cbot)[line] = acc.b[0];
-    (a_side ? ecen1 : fcen1)[line] = acc.t[1] == INT64_MIN ? 0 : -((acc.t[1] + acc.b[1]) / 2);
-    (a_side ? ecen2 : fcen2)[line] = acc.t[2] == INT64_MIN ? 0 : -((acc.t[2] + acc.b[2]) / 2);
-    const long long w0 = acc.t[0] == INT64_MIN ? 0 : acc.t[0] - acc.b[0];
-    const long long w1 = acc.t[1] == INT64_MIN ? 0 : acc.t[1] - acc.b[1];
-    const long long w2 = acc.t[2] == INT64_MIN ? 0 : acc.t[2] - acc.b[2];
-    const unsigned long long n1 = (unsigned long long)(acc.cnt & 0xffffffffll);
-    const unsigned long long n2 = (unsigned long long)(acc.cnt >> 32);
-    const int s = a_side ? 0 : 1;
-    if (acc.special) atomicOr(a_side ? &sum->special_a : &sum->special_b, 1);
-    {  // operand Mag exponents: f in [b + 30, t] per operand window
-        bool far = false;
-        for (int q = 1; q < 3; q++)
-            if (acc.t[q] != INT64_MIN && (acc.t[q] > kRadUncentred || acc.b[q] + 30 < -kRadUncentred)) far = true;
-        if (far) atomicOr(&sum->rad_centred, 1);
+        for (int o = 16; o; o >>= 1) sacc_shfl(acc, o);
+        if (lane == 0) {
+            (a_side ? rtop : ctop)[line] = acc.t[0];
+            (a_side ? rbot : cbot)[line] = acc.b[0];
+            (a_side ? ecen1 : fcen1)[line] = acc.t[1] == INT64_MIN ? 0 : -((acc.t[1] + acc.b[1]) / 2);
+            (a_side ? ecen2 : fcen2)[line] = acc.t[2] == INT64_MIN ? 0 : -((acc.t[2] + acc.b[2]) / 2);
+            bool far = false;  // operand Mag exponents: f in [b + 30, t] per operand window
+            for (int q = 1; q < 3; q++)
+                if (acc.t[q] != INT64_MIN && (acc.t[q] > kRadUncentred || acc.b[q] + 30 < -kRadUncentred))
+                    far = true;
+            long long* r = red[a_side ? 0 : 1];
+            if (acc.special) atomicMax(&r[0], 1ll);
+            if (far) atomicMax(&r[1], 1ll);
+            if (acc.prec) atomicMax(&r[2], (long long)acc.prec);
+            if (acc.t[0] != INT64_MIN) atomicMax(&r[3], (long long)(acc.t[0] - acc.b[0]));
+            if (acc.t[1] != INT64_MIN) atomicMax(&r[4], (long long)(acc.t[1] - acc.b[1]));
+            if (acc.t[2] != INT64_MIN) atomicMax(&r[5], (long long)(acc.t[2] - acc.b[2]));
+            atomicAdd((unsigned long long*)&r[6], (unsigned long long)(acc.cnt & 0xffffffffll));
+            atomicAdd((unsigned long long*)&r[7], (unsigned long long)(acc.cnt >> 32));
+        }
     }
-    if (acc.prec) atomicMax(a_side ? &sum->prec_a : &sum->prec_b, (long long)acc.prec);
-    if (w0) atomicMax(a_side ? &sum->maxw_a : &sum->maxw_b, w0);
-    if (w1) atomicMax(&mw1[s], w1);
-    if (w2) atomicMax(&mw2[s], w2);
-    if (n1) atomicAdd((unsigned long long*)&mw1[2 + s], n1);
-    if (n2) atomicAdd((unsigned long long*)&mw2[2 + s], n2);
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        const int sd = threadIdx.x;  // 0: A rows, 1: B columns
+        const long long* r = red[sd];
+        if (r[0]) atomicOr(sd ? &sum->special_b : &sum->special_a, 1);
+        if (r[1]) atomicOr(&sum->rad_centred, 1);
+        if (r[2]) atomicMax(sd ? &sum->prec_b : &sum->prec_a, r[2]);
+        if (r[3]) atomicMax(sd ? &sum->maxw_b : &sum->maxw_a, r[3]);
+        if (r[4]) atomicMax(&mw1[sd], r[4]);
+        if (r[5]) atomicMax(&mw2[sd], r[5]);
+        if (r[6]) atomicAdd((unsigned long long*)&mw1[2 + sd], (unsigned long long)r[6]);
+        if (r[7]) atomicAdd((unsigned long long*)&mw2[2 + sd], (unsigned long long)r[7]);
+    }
 }
 
 // exact double planes of both radius products + nonzero counts, one pass per side
@@ -3095,7 +3114,8 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     ScanSummary* hs = pinned_summary();
     long long* hw = hs->mw;
 
-    auto phase1 = [&](cudaStream_t s, bool capturing) -> int {
+    // `mid` (optional): work enqueued on `s` between the scan and the pack
+    auto phase1 = [&](cudaStream_t s, bool capturing, const std::function<int(cudaStream_t)>* mid = nullptr) -> int {
         const int tk_scan = prof_begin("scan", s);
         const int64_t nblk = M * cA + ((N + 31) / 32) * cB;
         static const bool no_scan_planes = std::getenv("APB_NO_SCAN_PLANES") != nullptr;  // test hook
@@ -3114,6 +3134,10 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         cudaStreamWaitEvent(cps, ev_fork, 0);
         cudaMemcpyAsync(hs, sum, sizeof(ScanSummary), cudaMemcpyDeviceToHost, cps);
         rec_event(ev_plan, cps, capturing);
+        if (mid) {
+            const int r = (*mid)(s);
+            if (r) return r;
+        }
         if (sncw) {
             const int tk = prof_begin("pack", s);
             PackAB pk;
@@ -3327,6 +3351,29 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
             const uint64_t gemm_products = stats().int_gemm_products;
             cudaGraphExec_t g1 = capture(
                 [&](cudaStream_t cs) -> int {
+                    // APB_RAD_MAIN=1: radius products in stream order between the scan and the
+                    // pack (measured 1 us slower than the side branch below, which overlaps them
+                    // with the pack's tail)
+                    static const bool rad_main = std::getenv("APB_RAD_MAIN") != nullptr;
+                    if (rad_main && !std::getenv("APB_RAD_BESIDE")) {
+                        const std::function<int(cudaStream_t)> radmid = [&](cudaStream_t ms) {
+                            const int q = phaseR(ms, true);
+                            cudaEventRecord(ev_rdone, ms);
+                            return q;
+                        };
+                        int r = phase1(cs, true, &radmid);
+                        if (r) return r;
+                        RadFuse fz{r1b, r1f, r2b, r2f, ev_rdone, false, false};
+                        r = scaled_block(A, B, 0, K, prec, C, true, P.maxw_a, P.maxw_b, RW.top[0], RW.bot[0],
+                                         CW.top[0], CW.bot[0], nullptr, 0, nullptr, nullptr, cs, nullptr, true, &fz,
+                                         &sum->maxw_a);
+                        if (!r && !fz.used) {  // recombine16 did not fold the radius: combine here
+                            rad_combine_kernel<<<blocks_for(M * N, 256), 256, 0, cs>>>(out_of(&C->b), M * N, r1b,
+                                                                                        r1f, r2b, r2f);
+                            count_launch();
+                        }
+                        return r;
+                    }
                     int r = phase1(cs, true);
                     if (r) return r;
                     // radius branch: planes beside the pack, products before the GEMM, which
