@@ -174,8 +174,16 @@ def abs_dot_upper(x, y, n, batch, idx=None):
 
 # ----------------------------------------------------------------- matmul
 
+def row_split_threads(threads, M, algo=0):
+    """threads for a row-split reference product: with matmul_auto (algo 0, also inside
+    complex_matmul_ball) every row block must stay above the classical dispatch cutoff
+    (<= 60 rows, src/matmul.cpp:517-531), else the split product takes another path"""
+    return max(1, min(threads, M // 64)) if algo == 0 else max(1, threads)
+
+
 def matmul(a: BallArray, b: BallArray, M, K, N, prec, *, which="ref", algo=0, threads=1):
     from paper_1901_04289_b200.balls import limbs_for
+    threads = row_split_threads(threads, M, algo)
     c = BallArray.zeros(M * N, limbs_for(prec))
     A, B, Cm = apb_mat(a.c(), M, K), apb_mat(b.c(), K, N), apb_mat(c.c(), M, N)
     if which == "ref":
@@ -192,6 +200,7 @@ def matmul(a: BallArray, b: BallArray, M, K, N, prec, *, which="ref", algo=0, th
 
 def matmul_complex(are, aim, bre, bim, M, K, N, prec, *, which="ref", threads=1):
     from paper_1901_04289_b200.balls import limbs_for
+    threads = row_split_threads(threads, M, 0)
     cre, cim = BallArray.zeros(M * N, limbs_for(prec)), BallArray.zeros(M * N, limbs_for(prec))
     mats = [apb_mat(are.c(), M, K), apb_mat(aim.c(), M, K), apb_mat(bre.c(), K, N),
             apb_mat(bim.c(), K, N), apb_mat(cre.c(), M, N), apb_mat(cim.c(), M, N)]

@@ -281,3 +281,17 @@ def test_radius_planes_far_exponents(shift):
         got = ops.block_matmul_ball(A, B, p, out=out).balls.to_host()
         ok = got.identical(ref)
         assert ok.all(), f"rep {rep}: {(~ok).sum()} entries differ"
+
+
+def test_complex_c4_shape_vs_reference():
+    """config 4 distributions (independent 512-bit parts, exponents in [-16, 16], radii
+    2^-515|m|) at N=256: every entry of both parts bit-identical to complex_matmul_ball
+    (reference run multithreaded on the host)"""
+    from paper_1901_04289_b200 import ops
+    n, p = 256, 512
+    parts = gen.config4_matrices(n=n, p=p)
+    M4 = [_mat(x, n, n) for x in parts]
+    cre, cim = ops.complex_matmul_ball(*M4, p)
+    rre, rim = po.matmul_complex(*parts, n, n, n, p, which="ref", threads=os.cpu_count() or 8)
+    assert cre.balls.to_host().identical(rre).all()
+    assert cim.balls.to_host().identical(rim).all()
