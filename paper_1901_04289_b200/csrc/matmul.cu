@@ -705,7 +705,10 @@ __global__ void __launch_bounds__(128) recombine_fast_kernel(RecombineArgs R) {
     // one streaming pass over the digits, base 2^DB: digit k = word_k + carry_{k-1}
     // + the running carry; batches of RB bands are loaded before they are
     // consumed so RB * 2 loads are in flight per thread with few live registers
-    constexpr int RB = 8;
+#ifndef APB_RC16_RB
+#define APB_RC16_RB 8
+#endif
+    constexpr int RB = APB_RC16_RB;  // band loads in flight per thread
     uint64_t T[NL];
 #pragma unroll
     for (int q = 0; q < NL; q++) T[q] = 0;
@@ -852,7 +855,10 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
     const size_t plane = (size_t)R.Mp * R.Np;
     const size_t off = rc_off(R, i, j);
     const int NB = R.nwords;
-    constexpr int RB = 8;
+#ifndef APB_RC16_RB
+#define APB_RC16_RB 8
+#endif
+    constexpr int RB = APB_RC16_RB;  // band loads in flight per thread
     uint32_t Wd[NW];
 #pragma unroll
     for (int q = 0; q < NW; q++) Wd[q] = 0;
