@@ -864,6 +864,9 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
     for (int q = 0; q < NW; q++) Wd[q] = 0;
     int32_t run = 0, prev_c = 0;
     bool neg = false;
+    // band planes by pointer stepping (one 64-bit add per band, no per-band multiply)
+    const uint32_t* pw = R.Tw + off;
+    const int32_t* pc = R.Tc + off;
 #pragma unroll
     for (int kb = 0; kb < ND; kb += RB) {
         uint32_t w[RB];
@@ -871,8 +874,13 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
 #pragma unroll
         for (int v = 0; v < RB; v++) {
             const int b = kb + v;
-            w[v] = (b < NBC && b < NB) ? __ldcs(R.Tw + (size_t)b * plane + off) : 0u;
-            c[v] = (b < NBC && b < NB) ? __ldcs(R.Tc + (size_t)b * plane + off) : 0;
+            const bool live = b < NBC && b < NB;
+            w[v] = live ? __ldcs(pw) : 0u;
+            c[v] = live ? __ldcs(pc) : 0;
+            if (b < NBC) {
+                pw += plane;
+                pc += plane;
+            }
         }
 #pragma unroll
         for (int v = 0; v < RB; v++) {

@@ -29,7 +29,9 @@ int main() {
     cudaMalloc(&out, 8);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int blocks = sms * 8, threads = 256, iters = 4096;
+    const int threads = 256, iters = 4096;
+    for (int occ : {1, 2, 4, 8}) {  // resident warps per SM = 8 * occ
+    const int blocks = sms * occ;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -44,9 +46,10 @@ int main() {
             cudaEventElapsedTime(&ms, e0, e1);
             const double ops = (double)blocks * threads * iters * 16 * (mode == 0 ? 2 : 1);  // instructions
             if (rep)
-                printf("{\"mode\": \"%s\", \"ms\": %.3f, \"fp64_instr_per_s\": %.4g, \"per_sm_per_clk_at_1.965GHz\": %.2f}\n",
-                       mode == 0 ? "dmul+dadd" : "fma", ms, ops / (ms * 1e-3), ops / (ms * 1e-3) / sms / 1.965e9);
+                printf("{\"mode\": \"%s\", \"warps_per_sm\": %d, \"ms\": %.3f, \"fp64_instr_per_s\": %.4g, \"per_sm_per_clk_at_1.965GHz\": %.2f}\n",
+                       mode == 0 ? "dmul+dadd" : "fma", 8 * occ, ms, ops / (ms * 1e-3), ops / (ms * 1e-3) / sms / 1.965e9);
         }
+    }
     }
     return 0;
 }
