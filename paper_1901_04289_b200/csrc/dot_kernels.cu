@@ -2284,12 +2284,89 @@ __device__ void gb_div_u64(GBall& out, const GBall& x, uint64_t k, int64_t p, in
 // The recurrence is sequential; one thread walks it with the generic fused dot
 // (the same Algorithm 1 restatement as dot_generic_kernel), reading b from the
 // output as it is produced.  ja (j a_j, exact) is staged in `ja` (L_a + 1 limbs).
+// one dot (Algorithm 1 over a term callback) computed by a whole warp: lanes
+// stride over the terms with private runtime-size accumulators, shuffle carry
+// reduction, lane 0 finalizes into (out, ob); special values: lane 0 runs the
+// fallback (ball_fallback_addmul per term) exactly as g_dot does
+template <class GetTerm>
+__device__ void warp_g_dot(GetTerm&& get, int64_t total, int64_t p, const BallsOut& out, int64_t ob, int* status) {
+    const int lane = threadIdx.x & 31;
+    GBall xs, ys;
+    ScanAcc sc{INT64_MIN, INT64_MAX, INT64_MIN, 0, false};
+    const bool track_min = p > 128;
+    for (int64_t i = lane; i < total && !sc.fb; i += 32) {
+        bool neg;
+        get(i, xs, ys, neg);
+        const GF& xm = xs.m;
+        const GF& ym = ys.m;
+        if (!(xm.kind == APB_ZERO || xm.kind == APB_FINITE) || !(ym.kind == APB_ZERO || ym.kind == APB_FINITE) ||
+            (xm.kind != APB_ZERO && exp_huge(xm.e)) || (ym.kind != APB_ZERO && exp_huge(ym.e))) {
+            sc.fb = true;
+            break;
+        }
+        if (xm.kind != APB_ZERO && ym.kind != APB_ZERO) {
+            sc.nnz++;
+            const int64_t ee = xm.e + ym.e;
+            if (ee > sc.e_max) sc.e_max = ee;
+            if (track_min) {
+                const int64_t lo = ee - 64 * (int64_t)(xm.n + ym.n);
+                if (lo < sc.e_min) sc.e_min = lo;
+            }
+        }
+        const Mag& xr = xs.r;
+        const Mag& yr = ys.r;
+        if (xr.kind == 2 || yr.kind == 2 || (xr.kind == 1 && exp_huge(xr.f)) || (yr.kind == 1 && exp_huge(yr.f))) {
+            sc.fb = true;
+            break;
+        }
+        if (yr.kind == 1 && xm.kind != APB_ZERO && xm.e + yr.f > sc.e_rad) sc.e_rad = xm.e + yr.f;
+        if (xr.kind == 1 && ym.kind != APB_ZERO && ym.e + xr.f > sc.e_rad) sc.e_rad = ym.e + xr.f;
+        if (xr.kind == 1 && yr.kind == 1 && xr.f + yr.f > sc.e_rad) sc.e_rad = xr.f + yr.f;
+    }
+    const bool fb = __any_sync(0xffffffffu, sc.fb);
+    const Plan pl = finish_plan(warp_max(sc.e_max), warp_min(sc.e_min), warp_max(sc.e_rad), warp_sum(sc.nnz), fb,
+                                total, p, false);
+    if (pl.status != 0) {
+        if (lane == 0) g_dot(get, total, p, false, false, out, ob, nullptr, nullptr, 0, status);  // zero / fallback
+        return;
+    }
+    uint64_t s[GCAP];
+    for (int j = 0; j < pl.n_s; j++) s[j] = 0;
+    uint64_t err = 0, srad = 0;
+    for (int64_t i = lane; i < total; i += 32) {
+        bool neg;
+        get(i, xs, ys, neg);
+        if (xs.m.kind != APB_ZERO && ys.m.kind != APB_ZERO) g_acc_term(pl, s, err, xs.m, ys.m, neg);
+        g_rad_term(srad, xs, ys, pl.e_rad);
+    }
+    for (int o = 16; o; o >>= 1) {
+        uint64_t c = 0;
+        for (int j = 0; j < pl.n_s; j++) {
+            const uint64_t v = __shfl_xor_sync(0xffffffffu, s[j], o);
+            const uint64_t s1 = s[j] + v;
+            const uint64_t c1 = s1 < v;
+            const uint64_t s2 = s1 + c;
+            s[j] = s2;
+            c = c1 | (s2 < c);
+        }
+        err += __shfl_xor_sync(0xffffffffu, err, o);
+        srad += __shfl_xor_sync(0xffffffffu, srad, o);
+    }
+    if (lane == 0) finalize_store<GCAP>(pl, s, err, srad, p, true, out, ob, status);
+}
+
+// series_exp_basecase (src/poly.cpp:29-46) on one warp: b_0 = 1, then for
+// k = 1.. the dot sum_{i<k} (i+1) a_{i+1} b_{k-1-i} (one warp-wide dot, lanes
+// over the terms) and lane 0's b_k = dot / k (ball_div_u64); the recurrence
+// itself is sequential.  (APB_SERIES_SERIAL=1: the previous one-thread version.)
 __global__ void series_exp_kernel(BallsView a, int64_t alen, int64_t len, int64_t prec, BallsOut out,
-                                  BallsOut ja, BallsOut sdot, int* status) {
-    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+                                  BallsOut ja, BallsOut sdot, int* status, int serial) {
+    if (blockIdx.x != 0) return;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x >= 32) return;
     GBall x, y, t;
     // ja[j] = (j a_j exact, mag_mul_up(rad, Mag::from_u64_upper(j))), zero beyond |a|
-    for (int64_t j = 0; j < len; j++) {
+    for (int64_t j = lane; j < len; j += 32) {
         if (j >= 1 && j < alen) {
             gb_load(x, a, j);
             gf_mul_u64_exact(t.m, x.m, (uint64_t)j, status);
@@ -2303,8 +2380,7 @@ __global__ void series_exp_kernel(BallsView a, int64_t alen, int64_t len, int64_
         }
         gf_store(ja, j, t.m, t.r, status);
     }
-    // b_0 = Ball::from_i64(1)
-    {
+    if (lane == 0) {  // b_0 = Ball::from_i64(1)
         GFloat<1> one;
         one.kind = APB_FINITE;
         one.neg = 0;
@@ -2313,6 +2389,7 @@ __global__ void series_exp_kernel(BallsView a, int64_t alen, int64_t len, int64_
         one.d[0] = 1ull << 63;
         gf_store(out, 0, one, mag_zero(), status);
     }
+    __syncwarp();
     const BallsView jav{ja.mant, ja.exp, ja.kind, ja.rad_man, ja.rad_exp, ja.L};
     const BallsView bv{out.mant, out.exp, out.kind, out.rad_man, out.rad_exp, out.L};
     const BallsView sv{sdot.mant, sdot.exp, sdot.kind, sdot.rad_man, sdot.rad_exp, sdot.L};
@@ -2322,10 +2399,17 @@ __global__ void series_exp_kernel(BallsView a, int64_t alen, int64_t len, int64_
             gb_load(ys, bv, k - 1 - i);
             neg = false;
         };
-        g_dot(get, k, prec, false, false, sdot, 0, nullptr, nullptr, 0, status);
-        gb_load(x, sv, 0);
-        gb_div_u64(t, x, (uint64_t)k, prec, status);
-        gf_store(out, k, t.m, t.r, status);
+        if (serial) {
+            if (lane == 0) g_dot(get, k, prec, false, false, sdot, 0, nullptr, nullptr, 0, status);
+        } else {
+            warp_g_dot(get, k, prec, sdot, 0, status);
+        }
+        if (lane == 0) {
+            gb_load(x, sv, 0);
+            gb_div_u64(t, x, (uint64_t)k, prec, status);
+            gf_store(out, k, t.m, t.r, status);
+        }
+        __syncwarp();  // b_k (global, written by lane 0) is read by every lane next step
     }
 }
 
@@ -2347,8 +2431,9 @@ int series_exp_launch(const apb_balls* a, int64_t alen, int64_t len, int64_t pre
         set_error("out of device memory (series scratch)");
         return APB_ERR_CUDA;
     }
+    static const int serial = std::getenv("APB_SERIES_SERIAL") ? 1 : 0;  // test hook
     series_exp_kernel<<<1, 32, 0, st>>>(view_of(a), alen, len, prec, out_of(out), out_of(&ja), out_of(&sd),
-                                        ws.status_dev);
+                                        ws.status_dev, serial);
     count_launch();
     return cuda_check(cudaGetLastError(), "series_exp");
 }

@@ -79,3 +79,24 @@ def test_poly_mullow_large_vs_reference():
     ref = po.poly_mullow(a, b, 1024, 128)
     got = ops.poly_mullow_classical(a.to_device(), b.to_device(), 1024, 128).to_host()
     assert got.identical(ref).all()
+
+
+def test_series_exp_warp_matches_serial_and_reference():
+    """the warp-cooperative series_exp (lanes over each step's dot) equals the
+    one-thread version (APB_SERIES_SERIAL) and the reference at a length where
+    every step's dot spans several lane rounds"""
+    import os
+    import subprocess
+    import sys
+    from paper_1901_04289_b200 import ops
+    rng = np.random.Generator(np.random.PCG64(4242))
+    la, ln, p = 150, 160, 256
+    a, _ = gen.edge_dots(rng, 1, la, specials=False)
+    a.kind[0], a.mant[0], a.exp[0], a.rad_man[0], a.rad_exp[0] = 0, 0, 0, 0, 0
+    ref = po.series_exp(a, ln, p)
+    got = ops.series_exp_basecase(a, ln, p)
+    assert got.identical(ref).all()
+    env = dict(os.environ, APB_SERIES_SERIAL="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-k", "test_series_exp and not warp",
+                        os.path.abspath(__file__)], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:]
