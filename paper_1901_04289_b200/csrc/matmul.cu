@@ -1578,6 +1578,10 @@ APB_DEV int rad_variant(const long long* mw, int64_t M, int64_t K, int64_t N, in
 }
 
 constexpr int RT = 32, RK = 32, RTHREADS = 64;
+// PT x PT outputs per thread: PT = 4 (64 threads per 32 x 32 tile) for large
+// products, PT = 2 (256 threads) when the grid is too small to fill the SMs with
+// the 64-thread tiles (c2: 128 tiles, ~2 warps per SM, FP64 latency-bound)
+template <int PT>
 APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restrict__ db, int64_t M, int64_t N,
                            int64_t w, const int64_t* ecen, const int64_t* fcen, uint32_t* rb, int64_t* rf,
                            int accumulate, int a_trans, const long long* sel, int64_t bx, int64_t by,
@@ -1591,30 +1595,31 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
     // shared memory (they are touched once per chunk)
     __shared__ __align__(16) double sA[RK][RT + 2];  // rows 16-byte aligned: 128-bit operand loads
     __shared__ __align__(16) double sB[RK][RT];
-    __shared__ uint32_t eb[16][RTHREADS];
-    __shared__ int64_t ef[16][RTHREADS];
-    constexpr int PER = RK * RT / RTHREADS;  // tile elements per thread per operand
-    const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+    constexpr int NT = (RT / PT) * (RT / PT);  // threads per tile
+    __shared__ uint32_t eb[PT * PT][NT];
+    __shared__ int64_t ef[PT * PT][NT];
+    constexpr int PER = RK * RT / NT;  // tile elements per thread per operand
+    const int tx = threadIdx.x % (RT / PT), ty = threadIdx.x / (RT / PT);
     const int64_t i0 = by * RT, j0 = bx * RT;
-    double s[4][4];
+    double s[PT][PT];
 #pragma unroll
-    for (int r = 0; r < 4; r++)
+    for (int r = 0; r < PT; r++)
 #pragma unroll
-        for (int c = 0; c < 4; c++) {
+        for (int c = 0; c < PT; c++) {
             s[r][c] = 0.0;
-            eb[4 * r + c][threadIdx.x] = 0;
-            ef[4 * r + c][threadIdx.x] = 0;
+            eb[PT * r + c][threadIdx.x] = 0;
+            ef[PT * r + c][threadIdx.x] = 0;
         }
     const Mag infl = mag_parts((1ull << 29) + 1, 1);
     double pa[PER], pb[PER];
     const bool rows_in = i0 + RT <= M && j0 + RT <= N;
     auto fetch = [&](int64_t l0) {
         if (rows_in && l0 + RK <= w && a_trans) {  // interior tile: strided pointers, no bounds tests
-            // element u: kk = tid / 32 + 2 u (RTHREADS = 64), rr = tid % 32
+            // element u: kk = tid / 32 + (NT / 32) u, rr = tid % 32
             const int kk0 = threadIdx.x / RT, rr = threadIdx.x % RT;
             const double* pA = da + (l0 + kk0) * M + i0 + rr;
             const double* pB = db + (l0 + kk0) * N + j0 + rr;
-            const int64_t sa = (int64_t)(RTHREADS / RT) * M, sb = (int64_t)(RTHREADS / RT) * N;
+            const int64_t sa = (int64_t)(NT / RT) * M, sb = (int64_t)(NT / RT) * N;
 #pragma unroll
             for (int u = 0; u < PER; u++) {
                 pa[u] = __ldg(pA + u * sa);
@@ -1624,7 +1629,7 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
         }
 #pragma unroll
         for (int u = 0; u < PER; u++) {
-            const int q = threadIdx.x + RTHREADS * u;
+            const int q = threadIdx.x + NT * u;
             const int kk = q / RT, rr = q % RT;
             const int64_t gi = i0 + rr, gl = l0 + kk, gj = j0 + rr;
             pa[u] = (gi < M && gl < w) ? (a_trans ? da[gl * M + gi] : da[gi * w + gl]) : 0.0;
@@ -1636,7 +1641,7 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
         __syncthreads();
 #pragma unroll
         for (int u = 0; u < PER; u++) {
-            const int q = threadIdx.x + RTHREADS * u;
+            const int q = threadIdx.x + NT * u;
             sA[q / RT][q % RT] = pa[u];
             sB[q / RT][q % RT] = pb[u];
         }
@@ -1644,50 +1649,45 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
         if (l0 + RK < w) fetch(l0 + RK);
         const int kmax = (w - l0) < RK ? (int)(w - l0) : RK;
         for (int kk = 0; kk < kmax; kk++) {
-            double a[4], b[4];
-            {
-                const double2 a01 = *reinterpret_cast<const double2*>(&sA[kk][ty * 4]);
-                const double2 a23 = *reinterpret_cast<const double2*>(&sA[kk][ty * 4 + 2]);
-                const double2 b01 = *reinterpret_cast<const double2*>(&sB[kk][tx * 4]);
-                const double2 b23 = *reinterpret_cast<const double2*>(&sB[kk][tx * 4 + 2]);
-                a[0] = a01.x;
-                a[1] = a01.y;
-                a[2] = a23.x;
-                a[3] = a23.y;
-                b[0] = b01.x;
-                b[1] = b01.y;
-                b[2] = b23.x;
-                b[3] = b23.y;
+            double a[PT], b[PT];
+#pragma unroll
+            for (int h = 0; h < PT; h += 2) {
+                const double2 av = *reinterpret_cast<const double2*>(&sA[kk][ty * PT + h]);
+                const double2 bv = *reinterpret_cast<const double2*>(&sB[kk][tx * PT + h]);
+                a[h] = av.x;
+                a[h + 1] = av.y;
+                b[h] = bv.x;
+                b[h + 1] = bv.y;
             }
 #pragma unroll
-            for (int r = 0; r < 4; r++)
+            for (int r = 0; r < PT; r++)
 #pragma unroll
-                for (int c = 0; c < 4; c++) s[r][c] = __dadd_rn(s[r][c], __dmul_rn(a[r], b[c]));
+                for (int c = 0; c < PT; c++) s[r][c] = __dadd_rn(s[r][c], __dmul_rn(a[r], b[c]));
         }
         const int64_t l = l0 + kmax;  // RK divides 1024: chunk ends fall on tile ends
         if ((l & 1023) == 0 || l == w) {
 #pragma unroll
-            for (int r = 0; r < 4; r++)
+            for (int r = 0; r < PT; r++)
 #pragma unroll
-                for (int c = 0; c < 4; c++) {
-                    const int64_t gi = i0 + ty * 4 + r, gj = j0 + tx * 4 + c;
+                for (int c = 0; c < PT; c++) {
+                    const int64_t gi = i0 + ty * PT + r, gj = j0 + tx * PT + c;
                     if (s[r][c] != 0.0 && gi < M && gj < N) {
-                        const Mag e = mag_add(mag_load(eb[4 * r + c][threadIdx.x], ef[4 * r + c][threadIdx.x]),
+                        const Mag e = mag_add(mag_load(eb[PT * r + c][threadIdx.x], ef[PT * r + c][threadIdx.x]),
                                               mag_mul(mag_from_double(s[r][c], cen ? -ecen[gi] - fcen[gj] : 0), infl));
-                        mag_store(e, &eb[4 * r + c][threadIdx.x], &ef[4 * r + c][threadIdx.x]);
+                        mag_store(e, &eb[PT * r + c][threadIdx.x], &ef[PT * r + c][threadIdx.x]);
                     }
                     s[r][c] = 0.0;
                 }
         }
     }
 #pragma unroll
-    for (int r = 0; r < 4; r++)
+    for (int r = 0; r < PT; r++)
 #pragma unroll
-        for (int c = 0; c < 4; c++) {
-            const int64_t gi = i0 + ty * 4 + r, gj = j0 + tx * 4 + c;
+        for (int c = 0; c < PT; c++) {
+            const int64_t gi = i0 + ty * PT + r, gj = j0 + tx * PT + c;
             if (gi >= M || gj >= N) continue;
             const int64_t o = gi * N + gj;
-            Mag m = mag_load(eb[4 * r + c][threadIdx.x], ef[4 * r + c][threadIdx.x]);
+            Mag m = mag_load(eb[PT * r + c][threadIdx.x], ef[PT * r + c][threadIdx.x]);
             if (accumulate) {
                 if (m.kind == 0) continue;
                 m = mag_add(mag_load(rb[o], rf[o]), m);
@@ -1701,7 +1701,7 @@ __global__ void __launch_bounds__(64) rad_gemm_kernel(const double* __restrict__
                                                        int64_t N, int64_t w, const int64_t* ecen,
                                                        const int64_t* fcen, uint32_t* rb, int64_t* rf,
                                                        int accumulate, int a_trans, const long long* sel = nullptr) {
-    rad_gemm_body(da, db, M, N, w, ecen, fcen, rb, rf, accumulate, a_trans, sel, blockIdx.x, blockIdx.y);
+    rad_gemm_body<4>(da, db, M, N, w, ecen, fcen, rb, rf, accumulate, a_trans, sel, blockIdx.x, blockIdx.y);
 }
 
 
@@ -2174,14 +2174,21 @@ __global__ void __launch_bounds__(T) rad_sparse2_kernel(RadPair P) {
 #ifndef APB_RADG_MINB
 #define APB_RADG_MINB 4  // 8: 128 registers, 16 warps/SM -- 3% faster at N=2048, 5% slower at c2
 #endif
-__global__ void __launch_bounds__(64, APB_RADG_MINB) rad_gemm2_kernel(RadPair P) {
+template <int PT>
+APB_DEV void rad_gemm2_body(const RadPair& P) {
     if (blockIdx.z == 0)
-        rad_gemm_body(P.da1, P.db1, P.M, P.N, P.K, P.ec1, P.fc1, P.r1b, P.r1f, 0, 1, P.mw1, blockIdx.x, blockIdx.y,
-                      P.cflag);
+        rad_gemm_body<PT>(P.da1, P.db1, P.M, P.N, P.K, P.ec1, P.fc1, P.r1b, P.r1f, 0, 1, P.mw1, blockIdx.x,
+                          blockIdx.y, P.cflag);
     else
-        rad_gemm_body(P.da2, P.db2, P.M, P.N, P.K, P.ec2, P.fc2, P.r2b, P.r2f, 0, 0, P.mw2, blockIdx.x, blockIdx.y,
-                      P.cflag);
+        rad_gemm_body<PT>(P.da2, P.db2, P.M, P.N, P.K, P.ec2, P.fc2, P.r2b, P.r2f, 0, 0, P.mw2, blockIdx.x,
+                          blockIdx.y, P.cflag);
 }
+__global__ void __launch_bounds__(64, APB_RADG_MINB) rad_gemm2_kernel(RadPair P) { rad_gemm2_body<4>(P); }
+// small products (fewer 32 x 32 tiles than ~4 per SM): 2 x 2 outputs per thread,
+// 4x the warps for the same tiles (c2: rad products 73 us at ~2 warps per SM)
+__global__ void __launch_bounds__(256, 2) rad_gemm2s_kernel(RadPair P) { rad_gemm2_body<2>(P); }
+// tiles of both dense products below which the 2 x 2 variant runs
+constexpr int64_t RAD_SMALL_TILES = 4 * 148;
 
 // exact double planes of both sides in one launch: blocks [0, nA) A, the rest B
 __global__ void fused_planes2_kernel(BallsView A, BallsView B, RadPair P, int64_t nA) {
@@ -3223,7 +3230,14 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
                 cfg.numAttrs = 1;
                 cudaLaunchKernelEx(&cfg, rad_sparse2_kernel<2, 256>, rp);
             }
-            rad_gemm2_kernel<<<dim3(blocks_for(N, RT), blocks_for(M, RT), 2), RTHREADS, 0, ss>>>(rp);
+            {
+                const dim3 g2(blocks_for(N, RT), blocks_for(M, RT), 2);
+                static const bool no_small = std::getenv("APB_RAD_NO_SMALL") != nullptr;  // test hook
+                if (!no_small && (int64_t)g2.x * g2.y * 2 < RAD_SMALL_TILES)
+                    rad_gemm2s_kernel<<<g2, 256, 0, ss>>>(rp);
+                else
+                    rad_gemm2_kernel<<<g2, RTHREADS, 0, ss>>>(rp);
+            }
             prof_end(tk, ss);
             rec_event(ev_join, ss, capturing);
             count_launch(no_scan_planes ? 3 : 2);
