@@ -30,6 +30,55 @@ APB_DEV uint64_t funnel_r(uint64_t lo, uint64_t hi, unsigned rb) {
     return rb ? (lo >> rb) | (hi << (64 - rb)) : lo;
 }
 
+// s += c / s -= c modulo 2^(64 NS), one PTX carry chain (add.cc / addc) for
+// the small window widths of the dot kernels, a compare-and-carry loop otherwise
+template <int NS>
+APB_DEV void addn_mod(uint64_t (&s)[NS], const uint64_t (&c)[NS]) {
+    if constexpr (NS == 2) {
+        asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(s[0]), "+l"(s[1]) : "l"(c[0]), "l"(c[1]));
+    } else if constexpr (NS == 3) {
+        asm("add.cc.u64 %0, %0, %3;\n\taddc.cc.u64 %1, %1, %4;\n\taddc.u64 %2, %2, %5;"
+            : "+l"(s[0]), "+l"(s[1]), "+l"(s[2]) : "l"(c[0]), "l"(c[1]), "l"(c[2]));
+    } else if constexpr (NS == 5) {
+        asm("add.cc.u64 %0, %0, %5;\n\taddc.cc.u64 %1, %1, %6;\n\taddc.cc.u64 %2, %2, %7;\n\t"
+            "addc.cc.u64 %3, %3, %8;\n\taddc.u64 %4, %4, %9;"
+            : "+l"(s[0]), "+l"(s[1]), "+l"(s[2]), "+l"(s[3]), "+l"(s[4])
+            : "l"(c[0]), "l"(c[1]), "l"(c[2]), "l"(c[3]), "l"(c[4]));
+    } else {
+        uint64_t cy = 0;
+#pragma unroll
+        for (int j = 0; j < NS; j++) {
+            const uint64_t s1 = s[j] + c[j];
+            const uint64_t c1 = s1 < c[j];
+            const uint64_t s2 = s1 + cy;
+            cy = c1 | (s2 < cy);
+            s[j] = s2;
+        }
+    }
+}
+template <int NS>
+APB_DEV void subn_mod(uint64_t (&s)[NS], const uint64_t (&c)[NS]) {
+    if constexpr (NS == 2) {
+        asm("sub.cc.u64 %0, %0, %2;\n\tsubc.u64 %1, %1, %3;" : "+l"(s[0]), "+l"(s[1]) : "l"(c[0]), "l"(c[1]));
+    } else if constexpr (NS == 3) {
+        asm("sub.cc.u64 %0, %0, %3;\n\tsubc.cc.u64 %1, %1, %4;\n\tsubc.u64 %2, %2, %5;"
+            : "+l"(s[0]), "+l"(s[1]), "+l"(s[2]) : "l"(c[0]), "l"(c[1]), "l"(c[2]));
+    } else if constexpr (NS == 5) {
+        asm("sub.cc.u64 %0, %0, %5;\n\tsubc.cc.u64 %1, %1, %6;\n\tsubc.cc.u64 %2, %2, %7;\n\t"
+            "subc.cc.u64 %3, %3, %8;\n\tsubc.u64 %4, %4, %9;"
+            : "+l"(s[0]), "+l"(s[1]), "+l"(s[2]), "+l"(s[3]), "+l"(s[4])
+            : "l"(c[0]), "l"(c[1]), "l"(c[2]), "l"(c[3]), "l"(c[4]));
+    } else {
+        uint64_t bw = 0;
+#pragma unroll
+        for (int j = 0; j < NS; j++) {
+            const uint64_t x = s[j], y = c[j];
+            s[j] = x - y - bw;
+            bw = (x < y) || (x == y && bw);
+        }
+    }
+}
+
 // 64x64 -> 128
 APB_DEV void mul64(uint64_t a, uint64_t b, uint64_t& lo, uint64_t& hi) {
     lo = a * b;

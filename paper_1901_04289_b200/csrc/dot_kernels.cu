@@ -411,25 +411,10 @@ APB_DEV void acc_term(Acc<L, NS>& a, const Term<L>& t, const Plan& pl) {
             }
             Cl[j] = rb ? (hi << rb) | (lo >> (64 - rb)) : hi;
         }
-        if (!negate) {
-            uint64_t c = 0;
-#pragma unroll
-            for (int j = 0; j < NS; j++) {
-                const uint64_t s1 = a.s[j] + Cl[j];
-                const uint64_t c1 = s1 < Cl[j];
-                const uint64_t s2 = s1 + c;
-                c = c1 | (s2 < c);
-                a.s[j] = s2;
-            }
-        } else {
-            uint64_t bw = 0;
-#pragma unroll
-            for (int j = 0; j < NS; j++) {
-                const uint64_t x = a.s[j], y = Cl[j];
-                a.s[j] = x - y - bw;
-                bw = (x < y) || (x == y && bw);
-            }
-        }
+        if (!negate)
+            addn_mod<NS>(a.s, Cl);
+        else
+            subn_mod<NS>(a.s, Cl);
         return;
     }
     const int rl = r >> 6;
@@ -464,25 +449,10 @@ APB_DEV void acc_term(Acc<L, NS>& a, const Term<L>& t, const Plan& pl) {
         Cl[j] = funnel_r(lo, hi, rb);
     }
     // two's complement add / subtract mod 2^(64 NS) (add_signed_range)
-    if (!negate) {
-        uint64_t c = 0;
-#pragma unroll
-        for (int j = 0; j < NS; j++) {
-            const uint64_t s1 = a.s[j] + Cl[j];
-            const uint64_t c1 = s1 < Cl[j];
-            const uint64_t s2 = s1 + c;
-            c = c1 | (s2 < c);
-            a.s[j] = s2;
-        }
-    } else {
-        uint64_t bw = 0;
-#pragma unroll
-        for (int j = 0; j < NS; j++) {
-            const uint64_t x = a.s[j], y = Cl[j];
-            a.s[j] = x - y - bw;
-            bw = (x < y) || (x == y && bw);
-        }
-    }
+    if (!negate)
+        addn_mod<NS>(a.s, Cl);
+    else
+        subn_mod<NS>(a.s, Cl);
 }
 
 // radius_pass_term (src/dot.cpp:346-358)
