@@ -5,7 +5,10 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <condition_variable>
+#include <deque>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -397,15 +400,33 @@ int apb_matmul_host(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, 
 }
 
 // ---- pipelined matmul host entry: copy-in / compute / copy-out streams, two
-// device buffer sets (workspace slots 64 + 15 k: A, B, C)
+// device buffer sets (workspace slots 64 + 15 k: A, B, C).  The caller's thread
+// enqueues each product's copy-in and returns; a worker thread enqueues the
+// product itself and its copy-out.  apb_matmul blocks its thread until the
+// product's plan is read back (after the copy-in and the scan), so with the
+// worker the copy-in of product i+1 is already queued behind product i's
+// instead of waiting for that readback on the caller's thread.
 namespace {
+struct PipeJob {
+    apb_mat dA, dB, dC;
+    apb_balls hC;
+    int64_t prec;
+    int algo, k;
+};
 struct HostPipe {
     cudaStream_t in, comp, out;
     cudaEvent_t in_ready[2], comp_done[2], out_done[2];
     bool used[2] = {false, false};
     int next = 0;
     int err = APB_OK;
+    std::string msg;
+    int dev = 0;
+    std::mutex mu;
+    std::condition_variable cv_job, cv_done;
+    std::deque<PipeJob> jobs;
+    int64_t queued = 0, finished = 0;
     HostPipe() {
+        cudaGetDevice(&dev);
         cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking);
         cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking);
         cudaStreamCreateWithFlags(&out, cudaStreamNonBlocking);
@@ -414,11 +435,50 @@ struct HostPipe {
             cudaEventCreateWithFlags(&comp_done[k], cudaEventDisableTiming);
             cudaEventCreateWithFlags(&out_done[k], cudaEventDisableTiming);
         }
+        std::thread([this] { run(); }).detach();  // lives as long as the process
+    }
+    // worker: product and copy-out of each submission, in submission order
+    void run() {
+        cudaSetDevice(dev);
+        for (;;) {
+            PipeJob j;
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv_job.wait(lk, [&] { return !jobs.empty(); });
+                j = jobs.front();
+                jobs.pop_front();
+            }
+            int rc = APB_OK;
+            cudaStreamWaitEvent(comp, in_ready[j.k], 0);
+            if (used[j.k]) cudaStreamWaitEvent(comp, out_done[j.k], 0);  // set k's C has left
+            if ((rc = apb_matmul(&j.dA, &j.dB, j.prec, j.algo, &j.dC, comp)) == APB_OK) {
+                cudaEventRecord(comp_done[j.k], comp);
+                cudaStreamWaitEvent(out, comp_done[j.k], 0);
+                rc = to_host(&j.dC.b, &j.hC, out);
+                cudaEventRecord(out_done[j.k], out);
+            } else {
+                cudaEventRecord(comp_done[j.k], comp);
+                cudaEventRecord(out_done[j.k], out);
+            }
+            std::lock_guard<std::mutex> lk(mu);
+            used[j.k] = true;
+            if (rc && !err) {
+                err = rc;
+                msg = apb_last_error();
+            }
+            finished++;
+            cv_done.notify_all();
+        }
+    }
+    // block until the worker has enqueued submissions [0, n)
+    void wait_finished(int64_t n) {
+        std::unique_lock<std::mutex> lk(mu);
+        cv_done.wait(lk, [&] { return finished >= n; });
     }
 };
 HostPipe& host_pipe() {
-    static HostPipe p;
-    return p;
+    static HostPipe* p = new HostPipe;  // never destroyed: the worker thread outlives static teardown
+    return *p;
 }
 // would any buffer of set k have to grow (a reallocation must not race in-flight work)?
 bool pipe_grows(int k, const apb_mat* A, const apb_mat* B, const apb_mat* C) {
@@ -438,37 +498,50 @@ int apb_matmul_host_submit(const apb_mat* A, const apb_mat* B, int64_t prec, int
     HostPipe& P = host_pipe();
     const int k = P.next;
     P.next ^= 1;
-    if (pipe_grows(k, A, B, C)) cudaDeviceSynchronize();  // first use / larger operands
-    apb_mat dA = *A, dB = *B, dC = *C;
+    // submission i reuses set k of submission i-2: its product, comp_done[k] and
+    // out_done[k] must be enqueued (by the worker) before they are waited on here
+    P.wait_finished(P.queued - 1);
+    if (pipe_grows(k, A, B, C)) {  // first use / larger operands: nothing may be in flight
+        P.wait_finished(P.queued);
+        cudaDeviceSynchronize();
+    }
+    PipeJob j;
+    j.dA = *A;
+    j.dB = *B;
+    j.dC = *C;
+    j.hC = C->b;
+    j.prec = prec;
+    j.algo = algo;
+    j.k = k;
     int rc;
     // set k's inputs were last read by the product two submissions ago
     if (P.used[k]) cudaStreamWaitEvent(P.in, P.comp_done[k], 0);
-    if ((rc = to_device(&A->b, &dA.b, 64 + 15 * k, P.in, true))) return rc;
-    if ((rc = to_device(&B->b, &dB.b, 69 + 15 * k, P.in, true))) return rc;
-    if ((rc = to_device(&C->b, &dC.b, 74 + 15 * k, P.in, false))) return rc;
+    if ((rc = to_device(&A->b, &j.dA.b, 64 + 15 * k, P.in, true))) return rc;
+    if ((rc = to_device(&B->b, &j.dB.b, 69 + 15 * k, P.in, true))) return rc;
+    if ((rc = to_device(&C->b, &j.dC.b, 74 + 15 * k, P.in, false))) return rc;
     cudaEventRecord(P.in_ready[k], P.in);
-    cudaStreamWaitEvent(P.comp, P.in_ready[k], 0);
-    if (P.used[k]) cudaStreamWaitEvent(P.comp, P.out_done[k], 0);  // set k's C has left
-    if ((rc = apb_matmul(&dA, &dB, prec, algo, &dC, P.comp))) {
-        if (!P.err) P.err = rc;
-        return rc;
+    {
+        std::lock_guard<std::mutex> lk(P.mu);
+        P.jobs.push_back(j);
+        P.queued++;
     }
-    cudaEventRecord(P.comp_done[k], P.comp);
-    cudaStreamWaitEvent(P.out, P.comp_done[k], 0);
-    if ((rc = to_host(&dC.b, &C->b, P.out))) return rc;
-    cudaEventRecord(P.out_done[k], P.out);
-    P.used[k] = true;
+    P.cv_job.notify_one();
     return APB_OK;
 }
 
 int apb_matmul_host_drain(void) {
     HostPipe& P = host_pipe();
+    P.wait_finished(P.queued);
     cudaStreamSynchronize(P.in);
     cudaStreamSynchronize(P.out);
     int rc = apb_device_status(P.comp);
     if (!rc) rc = cuda_check(cudaGetLastError(), "host pipeline");
-    if (!rc && P.err) rc = P.err;
+    if (!rc && P.err) {
+        rc = P.err;
+        set_error(P.msg.c_str());
+    }
     P.err = APB_OK;
+    P.msg.clear();
     return rc;
 }
 
