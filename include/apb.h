@@ -255,6 +255,8 @@ int apb_matmul_complex_host(const apb_mat* Are, const apb_mat* Aim, const apb_ma
  * copy-in, compute, copy-out).  The host buffers of a submitted product
  * (pinned memory for overlap) must stay untouched until apb_matmul_host_drain
  * returns, which waits for every submitted product and returns the first error.
+ * A submission returns once its copy-in is queued; a library worker thread
+ * queues the product and its copy-out.  Drain before other library calls.
  * Results are identical to apb_matmul_host. */
 int apb_matmul_host_submit(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, apb_mat* C);
 int apb_matmul_host_drain(void);
