@@ -296,3 +296,41 @@ def test_complex_c4_shape_vs_reference():
     rre, rim = po.matmul_complex(*parts, n, n, n, p, which="ref", threads=os.cpu_count() or 8)
     assert cre.balls.to_host().identical(rre).all()
     assert cim.balls.to_host().identical(rim).all()
+
+
+def test_host_pipeline_growth_and_errors():
+    """pipelined entry with operands that grow between submissions (the buffer
+    sets reallocate while the worker thread holds earlier products), a
+    dimension mismatch mid-stream (drain returns APB_ERR_INVALID with the
+    library's message), and a clean stream afterwards"""
+    import ctypes as C
+    from paper_1901_04289_b200 import ops
+    from paper_1901_04289_b200.balls import BallArray, apb_mat, limbs_for
+    lib = ops._lib.lib()
+    jobs = []
+    for n, p, salt in [(64, 128, 0), (256, 128, 1), (128, 256, 2), (512, 256, 3)]:
+        a, b = (gen.config2_matrices(n=n, p=p, seed_salt=salt) if p == 128
+                else gen.config3_matrices(n=n, p=p, seed_salt=salt))
+        ha, hb = a.pinned(), b.pinned()
+        hc = BallArray.zeros(n * n, limbs_for(p)).pinned()
+        jobs.append((n, p, a, b, ha, hb, hc, apb_mat(ha.c(), n, n), apb_mat(hb.c(), n, n), apb_mat(hc.c(), n, n)))
+    for n, p, a, b, ha, hb, hc, am, bm, cm in jobs:
+        ops._lib.check(lib.apb_matmul_host_submit(C.byref(am), C.byref(bm), p, 1, C.byref(cm)), "submit")
+    ops._lib.check(lib.apb_matmul_host_drain(), "drain")
+    for n, p, a, b, ha, hb, hc, *_ in jobs:
+        ref, _ = po.matmul(a, b, n, n, n, p, which="ref", algo=1, threads=os.cpu_count() or 8)
+        assert hc.identical(ref).all(), (n, p)
+    # A (64 x 64) times B (128 x 128): invalid dimensions, reported by drain
+    bad_c = BallArray.zeros(64 * 128, limbs_for(128)).pinned()
+    bm_bad = jobs[2][8]
+    cm_bad = apb_mat(bad_c.c(), 64, 128)
+    assert lib.apb_matmul_host_submit(C.byref(jobs[0][7]), C.byref(bm_bad), 128, 1, C.byref(cm_bad)) == 0
+    rc = lib.apb_matmul_host_drain()
+    assert rc == 1, rc
+    assert b"dimension" in lib.apb_last_error()
+    # the pipeline recovers
+    n, p, a, b, ha, hb, hc, am, bm, cm = jobs[1]
+    ops._lib.check(lib.apb_matmul_host_submit(C.byref(am), C.byref(bm), p, 1, C.byref(cm)), "submit")
+    ops._lib.check(lib.apb_matmul_host_drain(), "drain")
+    ref, _ = po.matmul(a, b, n, n, n, p, which="ref", algo=1, threads=os.cpu_count() or 8)
+    assert hc.identical(ref).all()
