@@ -2172,7 +2172,7 @@ __global__ void __launch_bounds__(T) rad_sparse2_kernel(RadPair P) {
 
 // dense variants (stand down unless picked): blockIdx.z = product
 #ifndef APB_RADG_MINB
-#define APB_RADG_MINB 4  // 8: 128 registers, 16 warps/SM -- 3% faster at N=2048, 5% slower at c2
+#define APB_RADG_MINB 8  // 128 registers, 16 warps/SM: 2.5% faster than 4 at N=2048 (c2 runs the 2x2 kernel)
 #endif
 template <int PT>
 APB_DEV void rad_gemm2_body(const RadPair& P) {
