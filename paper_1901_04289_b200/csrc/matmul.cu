@@ -1613,18 +1613,27 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
     const Mag infl = mag_parts((1ull << 29) + 1, 1);
     double pa[PER], pb[PER];
     const bool rows_in = i0 + RT <= M && j0 + RT <= N;
+    // A tiles of a row-major plane (a_trans = 0, M x w) are read with consecutive
+    // threads along k (coalesced rows) and stored transposed into sA[k][i]
     auto fetch = [&](int64_t l0) {
-        if (rows_in && l0 + RK <= w && a_trans) {  // interior tile: strided pointers, no bounds tests
+        if (rows_in && l0 + RK <= w) {  // interior tile: strided pointers, no bounds tests
             // element u: kk = tid / 32 + (NT / 32) u, rr = tid % 32
             const int kk0 = threadIdx.x / RT, rr = threadIdx.x % RT;
-            const double* pA = da + (l0 + kk0) * M + i0 + rr;
             const double* pB = db + (l0 + kk0) * N + j0 + rr;
-            const int64_t sa = (int64_t)(NT / RT) * M, sb = (int64_t)(NT / RT) * N;
+            const int64_t sb = (int64_t)(NT / RT) * N;
+            if (a_trans) {
+                const double* pA = da + (l0 + kk0) * M + i0 + rr;
+                const int64_t sa = (int64_t)(NT / RT) * M;
 #pragma unroll
-            for (int u = 0; u < PER; u++) {
-                pa[u] = __ldg(pA + u * sa);
-                pb[u] = __ldg(pB + u * sb);
+                for (int u = 0; u < PER; u++) pa[u] = __ldg(pA + u * sa);
+            } else {  // element u: row i0 + tid / 32 + (NT / 32) u, k = l0 + tid % 32
+                const double* pA = da + (i0 + kk0) * w + l0 + rr;
+                const int64_t sa = (int64_t)(NT / RT) * w;
+#pragma unroll
+                for (int u = 0; u < PER; u++) pa[u] = __ldg(pA + u * sa);
             }
+#pragma unroll
+            for (int u = 0; u < PER; u++) pb[u] = __ldg(pB + u * sb);
             return;
         }
 #pragma unroll
@@ -1632,7 +1641,10 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
             const int q = threadIdx.x + NT * u;
             const int kk = q / RT, rr = q % RT;
             const int64_t gi = i0 + rr, gl = l0 + kk, gj = j0 + rr;
-            pa[u] = (gi < M && gl < w) ? (a_trans ? da[gl * M + gi] : da[gi * w + gl]) : 0.0;
+            if (a_trans)
+                pa[u] = (gi < M && gl < w) ? da[gl * M + gi] : 0.0;
+            else  // transposed roles: row i0 + kk, k l0 + rr
+                pa[u] = (i0 + kk < M && l0 + rr < w) ? da[(i0 + kk) * w + l0 + rr] : 0.0;
             pb[u] = (gj < N && gl < w) ? db[gl * N + gj] : 0.0;
         }
     };
@@ -1642,7 +1654,10 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
 #pragma unroll
         for (int u = 0; u < PER; u++) {
             const int q = threadIdx.x + NT * u;
-            sA[q / RT][q % RT] = pa[u];
+            if (a_trans)
+                sA[q / RT][q % RT] = pa[u];
+            else
+                sA[q % RT][q / RT] = pa[u];
             sB[q / RT][q % RT] = pb[u];
         }
         __syncthreads();
