@@ -37,6 +37,21 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+# headers included by one translation unit only (the rest rebuild everything)
+PRIVATE_HEADERS = {"dot_reg.cuh": "dot_kernels.cu"}
+
+
+def _stale(src: str, obj: str) -> bool:
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    deps = [src, os.path.join(ROOT, "include", "apb.h")]
+    for f in os.listdir(CSRC):
+        if f.endswith((".cuh", ".h")) and PRIVATE_HEADERS.get(f, os.path.basename(src)) == os.path.basename(src):
+            deps.append(os.path.join(CSRC, f))
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
@@ -44,6 +59,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     procs = []
     for src in sources():
         obj = os.path.join(CSRC, os.path.splitext(os.path.basename(src))[0] + ".o")
+        if not force and not _stale(src, obj):
+            objs.append(obj)
+            continue
         cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-dc" if False else "-c", src, "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

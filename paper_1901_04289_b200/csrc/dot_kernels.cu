@@ -834,6 +834,8 @@ __global__ void __launch_bounds__(128, APB_GRP_MINB) dot_grp_kernel(DotArgs A) {
     }
 }
 
+#include "dot_reg.cuh"
+
 // ------------------------------------------------- bulk-staged kernel
 // Contiguous batches (dot b = elements [b n, (b+1) n) of x and y, n even, 2-limb
 // operands, 16-byte aligned arrays -- config 1): a persistent CTA of 8 warps
@@ -2044,6 +2046,50 @@ static void launch_grp(DotArgs A, cudaStream_t st) {
     count_launch();
 }
 
+template <int TPD, int RS, bool UNIT, bool PF>
+static void launch_reg_u(const DotArgs& A, cudaStream_t st) {
+    constexpr int DPR = 32 / TPD;
+    static int occ = 0;
+    if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dot_reg_kernel<TPD, RS, UNIT, PF>, 128, 0);
+        if (occ < 1) occ = 1;
+    }
+    const int64_t ngroups = (A.batch + DPR - 1) / DPR;
+    const int64_t blocks = std::min<int64_t>((ngroups + 3) / 4, (int64_t)148 * occ);
+    dot_reg_kernel<TPD, RS, UNIT, PF><<<(unsigned)blocks, 128, 0, st>>>(A, ngroups);
+    count_launch();
+}
+template <int TPD, int RS>
+static void launch_reg(const DotArgs& A, cudaStream_t st) {
+    // L2 prefetch of the next group: opt-in (APB_REG_PF=1), measured slower on config 1
+    static const bool pf = std::getenv("APB_REG_PF") != nullptr;
+    const bool unit = A.idx.xstep == 1 && A.idx.ystep == 1;
+    const bool flat = unit && A.idx.bdiv == 1 && A.idx.xs1 == A.n && A.idx.ys1 == A.n && pf;
+    if (flat)
+        launch_reg_u<TPD, RS, true, true>(A, st);
+    else if (unit)
+        launch_reg_u<TPD, RS, true, false>(A, st);
+    else
+        launch_reg_u<TPD, RS, false, false>(A, st);
+}
+
+// register-resident kernel (dot_reg.cuh): <= 2-limb operands, n_s <= 3, no initial
+// value, 33 <= n <= 128 terms (RS = ceil(n / 32) slots); APB_DOT_NOREG=1 keeps the
+// lane-group / warp kernels
+static bool try_reg(const DotArgs& A, int Lin, int nsb, int64_t total, cudaStream_t st) {
+    static const bool off = std::getenv("APB_DOT_NOREG") != nullptr;
+    static const int env_tpd = std::getenv("APB_REG_TPD") ? std::atoi(std::getenv("APB_REG_TPD")) : 0;
+    if (off || Lin > 2 || nsb > 3 || A.has_init || A.palen > 0 || total > 128 || total <= 32) return false;
+    if (env_tpd == 16 && total > 96 && total <= 112) {
+        launch_reg<16, 7>(A, st);
+        return true;
+    }
+    if (total > 96) launch_reg<32, 4>(A, st);
+    else if (total > 64) launch_reg<32, 3>(A, st);
+    else launch_reg<32, 2>(A, st);
+    return true;
+}
+
 template <int L, int NS>
 static bool try_small_tpl(const DotArgs& A, int64_t total, cudaStream_t st) {
     if (L == 2 && A.batch >= 148 * BLK_DOTS * 4 && blk_ok(A, L)) {  // contiguous batch: bulk-staged
@@ -2123,7 +2169,8 @@ int dot_dispatch(DotArgs& A, int Lin, int64_t total, cudaStream_t st) {
     A.mant16 = A.x.L == 2 && A.y.L == 2 && ((uintptr_t)A.x.mant % 16) == 0 && ((uintptr_t)A.y.mant % 16) == 0;
     const int tok = prof_begin("dot", st);
     bool small = true;
-    if (Lin <= 1 && nsb <= 3) try_small_tpl<1, 3>(A, total, st);
+    if (try_reg(A, Lin, nsb, total, st)) {
+    } else if (Lin <= 1 && nsb <= 3) try_small_tpl<1, 3>(A, total, st);
     else if (Lin <= 2 && nsb <= 3) try_small_tpl<2, 3>(A, total, st);
     else if (Lin <= 2 && nsb <= 5) try_small_tpl<2, 5>(A, total, st);
     else if (Lin <= 4 && nsb <= 5) try_small_tpl<4, 5>(A, total, st);

@@ -118,14 +118,18 @@ def test_reference_shaped_dot_ball():
     assert got.identical(ref).all()
 
 
-@pytest.mark.parametrize("hook", ["APB_DOT_KEEP", "APB_DOT_STAGE", "APB_DOT_GENERIC", "APB_DOT_TPD", "APB_DOT_BULK"])
+@pytest.mark.parametrize("hook", ["APB_DOT_KEEP", "APB_DOT_STAGE", "APB_DOT_GENERIC", "APB_DOT_TPD", "APB_DOT_BULK",
+                                  "APB_DOT_NOREG", "APB_REG_TPD", "APB_REG_PF"])
 def test_dot_kernel_variants(hook):
     """the register-resident (KEEP) and cp.async-staged (STAGE) dot kernels,
     selected by their tuning hooks in a subprocess, on the golden and edge cases"""
     import os
     import subprocess
     import sys
-    env = dict(os.environ, **{hook: "32" if hook == "APB_DOT_TPD" else "1"})  # TPD 32: one warp per dot
+    val = {"APB_DOT_TPD": "32", "APB_REG_TPD": "16"}.get(hook, "1")  # TPD 32: one warp per dot
+    env = dict(os.environ, **{hook: val})
+    if hook in ("APB_DOT_KEEP", "APB_DOT_STAGE", "APB_DOT_TPD", "APB_DOT_BULK"):
+        env["APB_DOT_NOREG"] = "1"  # these select among the round-1 kernels
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-k",
                         "test_dot_golden_gpu or test_edge_random or test_host_entry or test_c1_full",
                         os.path.abspath(__file__)], env=env, capture_output=True, text=True, timeout=600)
