@@ -152,6 +152,23 @@ def dist_setup():
 
 # ------------------------------------------------------------ workloads
 
+L2_NOTE = ("GPU arm: L2 flushed before every step (256 MiB write, outside the timed events); "
+           "reference arm: host-resident inputs on the CPU")
+
+
+def matmul_config(cfg, n, p, world):
+    """the `config` object of both arms (identical, so the driver can pair them)"""
+    return {"workload": f"BASELINE config {cfg[1:]}: real ball matmul N={n}, p={p}",
+            "M": n, "N": n, "K": n, "prec": p, "l2": L2_NOTE,
+            "parallelism": f"row-block weak scaling x{world}"}
+
+
+def dots_config(batch, n, p, world):
+    return {"workload": f"BASELINE config 1: {batch:,} real ball dots, N={n}, p={p}",
+            "batch": batch, "n": n, "prec": p, "l2": L2_NOTE,
+            "parallelism": f"batch weak scaling x{world}"}
+
+
 def matmul_workload(cfg, rank, p_override=None):
     from paper_1901_04289_b200 import gen
     if cfg == "c2":
@@ -242,12 +259,9 @@ def run_matmul(torch, cfg, steps, warmup, world, rank, want_e2e=True, want_cpu=T
     res = {
         "metric": "ball matmul terms/s (N^3 multiply-adds of p-bit balls per second)",
         "value": value, "unit": "terms/s", "ms_per_step": ms,
-        "config": {"workload": f"BASELINE config {cfg[1:]}: real ball matmul N={n}, p={p}",
-                   "M": n, "N": n, "K": n, "prec": p, "blocks": stats["last_block_count"],
-                   "height_a": ha, "height_b": hb, "slices_a": stats["last_slices_a"],
-                   "slices_b": stats["last_slices_b"],
-                   "l2": "flushed before every step (256 MiB write, outside the timed events)",
-                   "parallelism": f"row-block weak scaling x{world}" if world > 1 else "single GPU"},
+        "config": matmul_config(cfg, n, p, world),
+        "plan": {"blocks": stats["last_block_count"], "height_a": ha, "height_b": hb,
+                 "slices_a": stats["last_slices_a"], "slices_b": stats["last_slices_b"]},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
                      "frac": achieved / peak, "traffic": ncu_traffic("band3_gemm"),
                      "kernel": "band3_gemm_kernel<256,2>", "kernel_ms": per_launch_ms,
@@ -407,12 +421,13 @@ def run_dots(torch, steps, warmup, world, rank, want_e2e=True, want_cpu=True):
     peak, src = hbm_peak()
     res = {"metric": "ball dot terms/s", "value": world * terms / (ms * 1e-3), "unit": "terms/s",
            "ms_per_step": ms,
-           "config": {"workload": "BASELINE config 1: 65,536 real ball dots, N=100, p=128",
-                      "batch": batch, "n": n, "prec": p},
+           "config": dots_config(batch, n, p, world),
            "roofline": {"bound": "hbm", "achieved": alg_bytes / (kms * 1e-3) / 1e9, "peak": peak,
                         "unit": "GB/s", "frac": alg_bytes / (kms * 1e-3) / 1e9 / peak,
-                        "traffic": ncu_traffic("dot_grp_kernel"), "kernel": "dot_grp_kernel<2,3,4>",
+                        "traffic": ncu_traffic("dot_reg_kernel"), "kernel": "dot_reg_kernel<32,4,1,0>",
                         "kernel_ms": kms, "work": f"{alg_bytes} algorithmic bytes per launch",
+                        "timing": "CUDA events around the library's dot launch sequence (dot_reg_kernel "
+                                  "+ the special-value pass) inside the timed steps",
                         "peak_source": src},
            "gpu_launches": launches, "clocks": clk.summary()}
     if want_e2e and rank == 0:
@@ -457,14 +472,13 @@ def reference_arm(args, world, rank):
         batch, n, p = 65536, 100, 128
         x, y = gen.config1_dots(batch=batch, n=n, p=p)
         meas = [cpu_dots(x, y, n, batch, p, threads=T) for _ in range(args.warmup + args.steps)][args.warmup:]
-        metric, cfg = "ball dot terms/s", {"workload": "BASELINE config 1: 65,536 real ball dots, N=100, p=128"}
+        metric, cfg = "ball dot terms/s", dots_config(batch, n, p, world)
     else:
         a, b, n, p = matmul_workload(args.config, 0, args.prec)
         rows = min(n, max(8, 8 * T)) if n >= 1024 else None
         meas = [cpu_matmul(a, b, n, p, rows=rows, threads=T) for _ in range(args.warmup + args.steps)][args.warmup:]
         metric = "ball matmul terms/s (N^3 multiply-adds of p-bit balls per second)"
-        cfg = {"workload": f"BASELINE config {args.config[1:]}: real ball matmul N={n}, p={p}",
-               "M": n, "N": n, "K": n, "prec": p}
+        cfg = matmul_config(args.config, n, p, world)
     v = statistics.median(m["value"] for m in meas)
     line = {"impl": "reference", "metric": metric, "value": v, "unit": "terms/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.median(m["seconds"] for m in meas) * 1e3,
@@ -534,7 +548,7 @@ def main():
                 "config": res["config"], "roofline": res["roofline"], "e2e": res.get("e2e"),
                 "cpu_baseline": res.get("cpu_baseline"), "gpu_launches": res["gpu_launches"],
                 "clocks": res["clocks"]}
-        for extra in ("kernel_ms_per_step", "stage_ms_profiled_pass"):
+        for extra in ("plan", "kernel_ms_per_step", "stage_ms_profiled_pass"):
             if extra in res:
                 line[extra] = res[extra]
         if also:

@@ -34,6 +34,30 @@ int cuda_check(cudaError_t e, const char* where) {
 
 static std::mutex g_ws_mu;
 
+// ---------------------------------------------------------- API lock
+static std::recursive_mutex g_api_mu;
+static thread_local int t_api_depth = 0;
+static bool pipe_busy();
+static void pipe_quiet_drain();
+
+ApiLock::ApiLock(NoDrain) {
+    g_api_mu.lock();
+    t_api_depth++;
+}
+ApiLock::ApiLock() {
+    for (;;) {
+        g_api_mu.lock();
+        if (t_api_depth > 0 || !pipe_busy()) break;  // nested calls never wait
+        g_api_mu.unlock();
+        pipe_quiet_drain();
+    }
+    t_api_depth++;
+}
+ApiLock::~ApiLock() {
+    t_api_depth--;
+    g_api_mu.unlock();
+}
+
 // ------------------------------------------------------------- profiling
 struct ProfRec {
     std::string name;
@@ -113,8 +137,14 @@ extern "C" {
 int apb_version(void) { return 1; }
 uint64_t apb_launch_count(void) { return g_launches.load(); }
 const char* apb_last_error(void) { return g_error.c_str(); }
-apb_matmul_stats* apb_matmul_stats_get(void) { return &g_stats; }
-void apb_matmul_stats_reset(void) { std::memset(&g_stats, 0, sizeof g_stats); }
+apb_matmul_stats* apb_matmul_stats_get(void) {
+    ApiLock api_lock;  // pending pipelined products have updated the counters
+    return &g_stats;
+}
+void apb_matmul_stats_reset(void) {
+    ApiLock api_lock;
+    std::memset(&g_stats, 0, sizeof g_stats);
+}
 
 void apb_profile_enable(int on) { g_prof_on = on != 0; }
 
@@ -169,6 +199,7 @@ int apb_profile_dump(char* buf, size_t cap) {
 }
 
 int apb_device_status(void* stream) {
+    ApiLock api_lock;
     cudaStream_t st = (cudaStream_t)stream;
     int rc = cuda_check(cudaStreamSynchronize(st), "apb_device_status");
     if (rc) return rc;
@@ -188,6 +219,7 @@ int apb_dot_batch(const apb_balls* x, const apb_balls* y, const apb_balls* initi
                   const apb_dot_index* idx, int64_t n, int64_t batch, int64_t prec, int mode,
                   const apb_dot_tuning* tuning, apb_balls* out, apb_dot_state* state,
                   uint64_t* acc_limbs, int64_t acc_stride, void* stream) {
+    ApiLock api_lock;
     if (batch < 0 || n < 0 || !idx || !out || !balls_ok(out) || idx->bdiv < 1) {
         set_error("apb_dot_batch: invalid arguments");
         return APB_ERR_INVALID;
@@ -216,6 +248,7 @@ int apb_dot_batch(const apb_balls* x, const apb_balls* y, const apb_balls* initi
 
 int apb_poly_mullow(const apb_balls* a, int64_t alen, const apb_balls* b, int64_t blen, int64_t len,
                     int64_t prec, apb_balls* out, void* stream) {
+    ApiLock api_lock;
     if (alen < 0 || blen < 0 || len < 0 || !out || !balls_ok(out) || (alen > 0 && (!balls_ok(a) || a->count < alen)) ||
         (blen > 0 && (!balls_ok(b) || b->count < blen))) {
         set_error("apb_poly_mullow: invalid arguments");
@@ -234,6 +267,7 @@ int apb_poly_mullow(const apb_balls* a, int64_t alen, const apb_balls* b, int64_
 }
 
 int apb_series_exp(const apb_balls* a, int64_t alen, int64_t len, int64_t prec, apb_balls* out, void* stream) {
+    ApiLock api_lock;
     if (alen < 0 || len < 0 || !out || !balls_ok(out) || (alen > 0 && (!balls_ok(a) || a->count < alen))) {
         set_error("apb_series_exp: invalid arguments");
         return APB_ERR_INVALID;
@@ -265,6 +299,7 @@ int apb_dot_complex_batch(const apb_balls* xre, const apb_balls* xim, const apb_
                           const apb_balls* yim, const apb_dot_index* idx, int64_t n, int64_t batch,
                           int64_t prec, int mode, const apb_dot_tuning* tuning, apb_balls* out_re,
                           apb_balls* out_im, uint64_t* threeprod_hits, void* stream) {
+    ApiLock api_lock;
     if (batch < 0 || n < 0 || !idx || !balls_ok(out_re) || !balls_ok(out_im) || idx->bdiv < 1) {
         set_error("apb_dot_complex_batch: invalid arguments");
         return APB_ERR_INVALID;
@@ -290,6 +325,7 @@ int apb_dot_complex_batch(const apb_balls* xre, const apb_balls* xim, const apb_
 
 int apb_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, apb_mat* C,
                void* stream) {
+    ApiLock api_lock;
     if (!A || !B || !C) {
         set_error("apb_matmul: null matrix");
         return APB_ERR_INVALID;
@@ -365,6 +401,7 @@ cudaStream_t host_stream() {
 int apb_dot_batch_host(const apb_balls* x, const apb_balls* y, const apb_balls* initial,
                        int subtract, const apb_dot_index* idx, int64_t n, int64_t batch,
                        int64_t prec, int mode, apb_balls* out) {
+    ApiLock api_lock;
     cudaStream_t st = host_stream();
     apb_balls dx{}, dy{}, di{}, dout{};
     int rc;
@@ -384,6 +421,7 @@ int apb_dot_batch_host(const apb_balls* x, const apb_balls* y, const apb_balls* 
 }
 
 int apb_matmul_host(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, apb_mat* C) {
+    ApiLock api_lock;
     cudaStream_t st = host_stream();
     apb_mat dA = *A, dB = *B, dC = *C;
     int rc;
@@ -405,7 +443,10 @@ int apb_matmul_host(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, 
 // product itself and its copy-out.  apb_matmul blocks its thread until the
 // product's plan is read back (after the copy-in and the scan), so with the
 // worker the copy-in of product i+1 is already queued behind product i's
-// instead of waiting for that readback on the caller's thread.
+// instead of waiting for that readback on the caller's thread.  The worker
+// holds the API lock while it runs a product; every other entry point waits
+// for the pipeline to empty first (ApiLock), and a device status raised by a
+// pipelined product is kept for apb_matmul_host_drain.
 namespace {
 struct PipeJob {
     apb_mat dA, dB, dC;
@@ -425,6 +466,7 @@ struct HostPipe {
     std::condition_variable cv_job, cv_done;
     std::deque<PipeJob> jobs;
     int64_t queued = 0, finished = 0;
+    std::atomic<int64_t> synced{0};  // submissions known complete on the device
     HostPipe() {
         cudaGetDevice(&dev);
         cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking);
@@ -435,7 +477,13 @@ struct HostPipe {
             cudaEventCreateWithFlags(&comp_done[k], cudaEventDisableTiming);
             cudaEventCreateWithFlags(&out_done[k], cudaEventDisableTiming);
         }
-        std::thread([this] { run(); }).detach();  // lives as long as the process
+        std::thread([this] { run(); }).detach();  // parked on cv_job when idle; drained at exit
+    }
+    void record_error(int rc, const char* m) {  // caller holds mu
+        if (rc && !err) {
+            err = rc;
+            msg = m ? m : "";
+        }
     }
     // worker: product and copy-out of each submission, in submission order
     void run() {
@@ -449,23 +497,25 @@ struct HostPipe {
                 jobs.pop_front();
             }
             int rc = APB_OK;
-            cudaStreamWaitEvent(comp, in_ready[j.k], 0);
-            if (used[j.k]) cudaStreamWaitEvent(comp, out_done[j.k], 0);  // set k's C has left
-            if ((rc = apb_matmul(&j.dA, &j.dB, j.prec, j.algo, &j.dC, comp)) == APB_OK) {
-                cudaEventRecord(comp_done[j.k], comp);
-                cudaStreamWaitEvent(out, comp_done[j.k], 0);
-                rc = to_host(&j.dC.b, &j.hC, out);
-                cudaEventRecord(out_done[j.k], out);
-            } else {
-                cudaEventRecord(comp_done[j.k], comp);
-                cudaEventRecord(out_done[j.k], out);
+            std::string m;
+            {
+                ApiLock api_lock{ApiLock::NoDrain{}};
+                cudaStreamWaitEvent(comp, in_ready[j.k], 0);
+                if (used[j.k]) cudaStreamWaitEvent(comp, out_done[j.k], 0);  // set k's C has left
+                if ((rc = apb_matmul(&j.dA, &j.dB, j.prec, j.algo, &j.dC, comp)) == APB_OK) {
+                    cudaEventRecord(comp_done[j.k], comp);
+                    cudaStreamWaitEvent(out, comp_done[j.k], 0);
+                    rc = to_host(&j.dC.b, &j.hC, out);
+                    cudaEventRecord(out_done[j.k], out);
+                } else {
+                    cudaEventRecord(comp_done[j.k], comp);
+                    cudaEventRecord(out_done[j.k], out);
+                }
+                if (rc) m = apb_last_error();
             }
             std::lock_guard<std::mutex> lk(mu);
             used[j.k] = true;
-            if (rc && !err) {
-                err = rc;
-                msg = apb_last_error();
-            }
+            record_error(rc, m.c_str());
             finished++;
             cv_done.notify_all();
         }
@@ -475,10 +525,37 @@ struct HostPipe {
         std::unique_lock<std::mutex> lk(mu);
         cv_done.wait(lk, [&] { return finished >= n; });
     }
+    int64_t n_queued() {
+        std::lock_guard<std::mutex> lk(mu);
+        return queued;
+    }
+    // every submission enqueued and complete on the device; the device status
+    // word (shared with the synchronous entries) is read under the API lock and
+    // kept as the pipeline's pending error
+    void settle() {
+        const int64_t n = n_queued();
+        wait_finished(n);
+        cudaStreamSynchronize(in);
+        cudaStreamSynchronize(comp);
+        cudaStreamSynchronize(out);
+        ApiLock api_lock{ApiLock::NoDrain{}};
+        const int rc = apb_device_status(comp);
+        std::lock_guard<std::mutex> lk(mu);
+        record_error(rc, rc ? apb_last_error() : nullptr);
+        if (synced.load() < n) synced.store(n);
+    }
 };
+HostPipe* g_pipe = nullptr;
+std::mutex g_pipe_init_mu;
 HostPipe& host_pipe() {
-    static HostPipe* p = new HostPipe;  // never destroyed: the worker thread outlives static teardown
-    return *p;
+    std::lock_guard<std::mutex> g(g_pipe_init_mu);
+    if (!g_pipe) {
+        g_pipe = new HostPipe;  // never destroyed: the worker thread outlives static teardown
+        std::atexit([] {        // no product may still be in flight when the CUDA runtime tears down
+            if (g_pipe) g_pipe->settle();
+        });
+    }
+    return *g_pipe;
 }
 // would any buffer of set k have to grow (a reallocation must not race in-flight work)?
 bool pipe_grows(int k, const apb_mat* A, const apb_mat* B, const apb_mat* C) {
@@ -494,15 +571,29 @@ bool pipe_grows(int k, const apb_mat* A, const apb_mat* B, const apb_mat* C) {
 }
 }  // namespace
 
+extern "C++" {
+namespace apb {
+static bool pipe_busy() { return g_pipe && g_pipe->synced.load() < g_pipe->n_queued(); }
+static void pipe_quiet_drain() {
+    if (g_pipe) g_pipe->settle();
+}
+}  // namespace apb
+}
+
 int apb_matmul_host_submit(const apb_mat* A, const apb_mat* B, int64_t prec, int algo, apb_mat* C) {
     HostPipe& P = host_pipe();
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != P.dev) {
+        set_error("apb_matmul_host_submit: the pipeline runs on the device of its first submission");
+        return APB_ERR_INVALID;
+    }
     const int k = P.next;
-    P.next ^= 1;
     // submission i reuses set k of submission i-2: its product, comp_done[k] and
     // out_done[k] must be enqueued (by the worker) before they are waited on here
-    P.wait_finished(P.queued - 1);
+    P.wait_finished(P.n_queued() - 1);
     if (pipe_grows(k, A, B, C)) {  // first use / larger operands: nothing may be in flight
-        P.wait_finished(P.queued);
+        P.settle();
         cudaDeviceSynchronize();
     }
     PipeJob j;
@@ -513,13 +604,22 @@ int apb_matmul_host_submit(const apb_mat* A, const apb_mat* B, int64_t prec, int
     j.prec = prec;
     j.algo = algo;
     j.k = k;
-    int rc;
-    // set k's inputs were last read by the product two submissions ago
-    if (P.used[k]) cudaStreamWaitEvent(P.in, P.comp_done[k], 0);
-    if ((rc = to_device(&A->b, &j.dA.b, 64 + 15 * k, P.in, true))) return rc;
-    if ((rc = to_device(&B->b, &j.dB.b, 69 + 15 * k, P.in, true))) return rc;
-    if ((rc = to_device(&C->b, &j.dC.b, 74 + 15 * k, P.in, false))) return rc;
-    cudaEventRecord(P.in_ready[k], P.in);
+    int rc = APB_OK;
+    {
+        ApiLock api_lock{ApiLock::NoDrain{}};
+        // set k's inputs were last read by the product two submissions ago
+        if (P.used[k]) cudaStreamWaitEvent(P.in, P.comp_done[k], 0);
+        if (!(rc = to_device(&A->b, &j.dA.b, 64 + 15 * k, P.in, true)) &&
+            !(rc = to_device(&B->b, &j.dB.b, 69 + 15 * k, P.in, true)))
+            rc = to_device(&C->b, &j.dC.b, 74 + 15 * k, P.in, false);
+        if (rc) {  // nothing queued: set k stays as it was; drain reports the error too
+            std::lock_guard<std::mutex> lk(P.mu);
+            P.record_error(rc, apb_last_error());
+            return rc;
+        }
+        cudaEventRecord(P.in_ready[k], P.in);
+    }
+    P.next = k ^ 1;
     {
         std::lock_guard<std::mutex> lk(P.mu);
         P.jobs.push_back(j);
@@ -531,11 +631,10 @@ int apb_matmul_host_submit(const apb_mat* A, const apb_mat* B, int64_t prec, int
 
 int apb_matmul_host_drain(void) {
     HostPipe& P = host_pipe();
-    P.wait_finished(P.queued);
-    cudaStreamSynchronize(P.in);
-    cudaStreamSynchronize(P.out);
-    int rc = apb_device_status(P.comp);
-    if (!rc) rc = cuda_check(cudaGetLastError(), "host pipeline");
+    P.settle();
+    ApiLock api_lock{ApiLock::NoDrain{}};
+    int rc = cuda_check(cudaGetLastError(), "host pipeline");
+    std::lock_guard<std::mutex> lk(P.mu);
     if (!rc && P.err) {
         rc = P.err;
         set_error(P.msg.c_str());
@@ -549,6 +648,7 @@ int apb_dot_complex_batch_host(const apb_balls* xre, const apb_balls* xim, const
                                const apb_balls* yim, const apb_dot_index* idx, int64_t n, int64_t batch,
                                int64_t prec, int mode, const apb_dot_tuning* tuning, apb_balls* out_re,
                                apb_balls* out_im, uint64_t* threeprod_hits) {
+    ApiLock api_lock;
     cudaStream_t st = host_stream();
     apb_balls d[6] = {};
     const apb_balls* h[4] = {xre, xim, yre, yim};
@@ -578,6 +678,7 @@ int apb_dot_complex_batch_host(const apb_balls* xre, const apb_balls* xim, const
 
 int apb_poly_mullow_host(const apb_balls* a, int64_t alen, const apb_balls* b, int64_t blen, int64_t len,
                          int64_t prec, apb_balls* out) {
+    ApiLock api_lock;
     cudaStream_t st = host_stream();
     apb_balls da{}, db{}, dout{};
     int rc;
@@ -591,6 +692,7 @@ int apb_poly_mullow_host(const apb_balls* a, int64_t alen, const apb_balls* b, i
 }
 
 int apb_series_exp_host(const apb_balls* a, int64_t alen, int64_t len, int64_t prec, apb_balls* out) {
+    ApiLock api_lock;
     cudaStream_t st = host_stream();
     apb_balls da{}, dout{};
     int rc;
@@ -603,6 +705,7 @@ int apb_series_exp_host(const apb_balls* a, int64_t alen, int64_t len, int64_t p
 
 int apb_matmul_complex_host(const apb_mat* Are, const apb_mat* Aim, const apb_mat* Bre,
                             const apb_mat* Bim, int64_t prec, int algo, apb_mat* Cre, apb_mat* Cim) {
+    ApiLock api_lock;
     cudaStream_t st = host_stream();
     apb_mat d[6] = {*Are, *Aim, *Bre, *Bim, *Cre, *Cim};
     const apb_mat* h[6] = {Are, Aim, Bre, Bim, Cre, Cim};

@@ -24,6 +24,23 @@ struct Workspace {
 };
 Workspace& workspace();
 
+// Library-wide serialization of the public entry points (a recursive lock; the
+// pipelined host entry's worker thread takes it around each product).  A
+// top-level entry first waits until every pipelined product has been enqueued
+// and has finished, folding a device status raised by one of them into the
+// pipeline's pending error (reported by apb_matmul_host_drain), so no other call
+// can observe or clear it and no host state (workspace, scratch tables, stats,
+// status word) is touched by two threads at once.
+struct ApiLock {
+    ApiLock();
+    ~ApiLock();
+    ApiLock(const ApiLock&) = delete;
+    ApiLock& operator=(const ApiLock&) = delete;
+    // for the pipeline itself: take the lock without waiting for the pipeline
+    struct NoDrain {};
+    explicit ApiLock(NoDrain);
+};
+
 void count_launch(uint64_t k = 1);
 void launch_count_adjust(int64_t d);  // graph replays: kernels counted at capture, added per launch
 

@@ -1578,6 +1578,7 @@ APB_DEV int rad_variant(const long long* mw, int64_t M, int64_t K, int64_t N, in
 }
 
 constexpr int RT = 32, RK = 32, RTHREADS = 64;
+static_assert(RT == RK, "the transposed A-tile fetch of rad_gemm_body maps k and row indices through RT");
 // PT x PT outputs per thread: PT = 4 (64 threads per 32 x 32 tile) for large
 // products, PT = 2 (256 threads) when the grid is too small to fill the SMs with
 // the 64-thread tiles (c2: 128 tiles, ~2 warps per SM, FP64 latency-bound)
@@ -1593,7 +1594,13 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
     // sums (__dmul_rn / __dadd_rn, no contraction) folded into the Mag bound at
     // every 1024-term chunk end (src/matmul.cpp:404-431); the folded Mags wait in
     // shared memory (they are touched once per chunk)
-    __shared__ __align__(16) double sA[RK][RT + 2];  // rows 16-byte aligned: 128-bit operand loads
+    // rows 16-byte aligned: 128-bit operand loads.  The once-per-tile transposed
+    // store sA[q % RT][q / RT] of a row-major A plane puts lanes r, r+8, r+16, r+24
+    // on one bank pair (4 wavefronts for 32 doubles instead of 2); with even row
+    // strides and pair-preserving swizzles every lane's double has the same slot
+    // parity, so the 2-wavefront minimum needs odd strides, which would break the
+    // double2 loads of the inner loop (the hot part) -- accepted.
+    __shared__ __align__(16) double sA[RK][RT + 2];
     __shared__ __align__(16) double sB[RK][RT];
     constexpr int NT = (RT / PT) * (RT / PT);  // threads per tile
     __shared__ uint32_t eb[PT * PT][NT];
@@ -3546,6 +3553,7 @@ extern "C" {
 
 int apb_matmul_complex(const apb_mat* Are, const apb_mat* Aim, const apb_mat* Bre, const apb_mat* Bim,
                        int64_t prec, int algo, apb_mat* Cre, apb_mat* Cim, void* stream) {
+    ApiLock api_lock;
     cudaStream_t st = (cudaStream_t)stream;
     if (!Are || !Aim || !Bre || !Bim || !Cre || !Cim || Are->cols != Bre->rows || Aim->cols != Bim->rows ||
         Are->rows != Aim->rows || Bre->cols != Bim->cols) {
@@ -3675,6 +3683,7 @@ int imad_block_product(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t h
 
 int apb_block_int_product(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int64_t* row_scale,
                           int64_t* col_scale, uint64_t* out, int64_t out_limbs, void* stream) {
+    ApiLock api_lock;
     if (!A || !B || A->cols != B->rows || lo < 0 || hi > A->cols || hi <= lo) {
         set_error("int_matmul: dimension mismatch");
         return APB_ERR_INVALID;
@@ -3685,6 +3694,7 @@ int apb_block_int_product(const apb_mat* A, const apb_mat* B, int64_t lo, int64_
 
 int apb_block_int_product_imad(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int64_t* row_scale,
                                int64_t* col_scale, uint64_t* out, int64_t out_limbs, float* gemm_ms, void* stream) {
+    ApiLock api_lock;
     if (!A || !B || A->cols != B->rows || lo < 0 || hi > A->cols || hi <= lo) {
         set_error("int_matmul: dimension mismatch");
         return APB_ERR_INVALID;
@@ -3694,6 +3704,7 @@ int apb_block_int_product_imad(const apb_mat* A, const apb_mat* B, int64_t lo, i
 
 int apb_plan_blocks(const apb_mat* A, const apb_mat* B, int64_t prec, int64_t* steps_out, int64_t max_steps,
                     int64_t* n_steps, void* stream) {
+    ApiLock api_lock;
     if (!A || !B || A->cols != B->rows) {
         set_error("plan_blocks: dimension mismatch");
         return APB_ERR_INVALID;
@@ -3709,6 +3720,7 @@ int apb_plan_blocks(const apb_mat* A, const apb_mat* B, int64_t prec, int64_t* s
 
 int apb_matmul_plan_info(const apb_mat* A, const apb_mat* B, int64_t prec, apb_plan_info* out,
                          void* stream) {
+    ApiLock api_lock;
     if (!A || !B || !out || A->cols != B->rows) {
         set_error("plan_info: dimension mismatch");
         return APB_ERR_INVALID;
@@ -3745,6 +3757,7 @@ int apb_matmul_plan_info(const apb_mat* A, const apb_mat* B, int64_t prec, apb_p
 int apb_radius_matmul_upper(const uint32_t* p_man, const int64_t* p_exp, const uint32_t* q_man,
                             const int64_t* q_exp, int64_t m, int64_t n, int64_t k, uint32_t* out_man,
                             int64_t* out_exp, void* stream) {
+    ApiLock api_lock;
     // P and Q are carried as the radius planes of ball matrices whose
     // midpoints are never read (operand kinds 1 and 2 of rad_operand)
     if (!p_man || !p_exp || !q_man || !q_exp || !out_man || !out_exp || m < 0 || n < 0 || k < 0) {

@@ -162,17 +162,7 @@ def sharded_matmul(A, B, M: int, K: int, N: int, prec: int, *, group=None, root:
                 parts.append(gathered[f][r][:(rh - rl) * N])
             out[f] = torch.cat(parts)
         return from_tensors(out, on_device)
-    # fallback: the root runs the full product
-    gathered = {f: [torch.zeros_like(mine[f]) for _ in range(world)] if rank == root else None for f in FIELDS}
-    for f in FIELDS:
-        dist.gather(mine[f], gathered[f], dst=root, group=group)
+    # fallback: the root runs the full product on the A it scattered (no gather)
     if rank != root:
         return None
-    full = {}
-    for f in FIELDS:
-        parts = []
-        for r in range(world):
-            rl, rh, _ = row_range(M, world, r)
-            parts.append(gathered[f][r][:(rh - rl) * K])
-        full[f] = torch.cat(parts)
     return compute(from_tensors(full, on_device), b_arr, M, K, N, prec)

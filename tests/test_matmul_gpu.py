@@ -334,3 +334,52 @@ def test_host_pipeline_growth_and_errors():
     ops._lib.check(lib.apb_matmul_host_drain(), "drain")
     ref, _ = po.matmul(a, b, n, n, n, p, which="ref", algo=1, threads=os.cpu_count() or 8)
     assert hc.identical(ref).all()
+
+
+def test_host_pipeline_interleaved_with_other_entries():
+    """other entry points called between submit and drain (same thread and a
+    second thread) wait for the pipelined products (library API lock): every
+    result is right, the stats see the pipelined products, and an error of a
+    pipelined product is still reported by drain after an intervening call"""
+    import ctypes as C
+    import threading
+    from paper_1901_04289_b200 import ops
+    from paper_1901_04289_b200.balls import BallArray, apb_mat, limbs_for
+    lib = ops._lib.lib()
+    n, p = 256, 128
+    a, b = gen.config2_matrices(n=n, p=p, seed_salt=7)
+    ha, hb = a.pinned(), b.pinned()
+    outs = [BallArray.zeros(n * n, limbs_for(p)).pinned() for _ in range(3)]
+    am, bm = apb_mat(ha.c(), n, n), apb_mat(hb.c(), n, n)
+    cms = [apb_mat(o.c(), n, n) for o in outs]
+    ref, _ = po.matmul(a, b, n, n, n, p, which="ref", algo=1, threads=os.cpu_count() or 8)
+    x, y = gen.config1_dots(batch=512)
+    dref = po.dot_batch(x, y, 100, 512, 128, which="ref")
+    errs = []
+
+    def other_thread():
+        try:
+            for _ in range(3):
+                got = ops.dot_batch(x.to_device(), y.to_device(), 100, 512, 128).to_host()
+                assert got.identical(dref).all()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = threading.Thread(target=other_thread)
+    th.start()
+    for cm in cms:
+        ops._lib.check(lib.apb_matmul_host_submit(C.byref(am), C.byref(bm), p, 1, C.byref(cm)), "submit")
+    # same thread, before drain: a synchronous product and a dot batch
+    dA, dB = _mat(a, n, n), _mat(b, n, n)
+    assert ops.block_matmul_ball(dA, dB, p).balls.to_host().identical(ref).all()
+    assert ops.dot_batch(x.to_device(), y.to_device(), 100, 512, 128).to_host().identical(dref).all()
+    th.join()
+    assert not errs, errs
+    ops._lib.check(lib.apb_matmul_host_drain(), "drain")
+    for o in outs:
+        assert o.identical(ref).all()
+    # a failing pipelined product, then another entry point, then drain: still reported
+    bad_c = BallArray.zeros(n * 2 * n, limbs_for(p)).pinned()
+    assert lib.apb_matmul_host_submit(C.byref(am), C.byref(bm), p, 1, C.byref(apb_mat(bad_c.c(), n, 2 * n))) == 0
+    assert ops.dot_batch(x.to_device(), y.to_device(), 100, 512, 128).to_host().identical(dref).all()
+    assert lib.apb_matmul_host_drain() == 1
