@@ -605,10 +605,17 @@ int apb_matmul_host_submit(const apb_mat* A, const apb_mat* B, int64_t prec, int
     j.algo = algo;
     j.k = k;
     int rc = APB_OK;
+    bool used_k;
     {
-        ApiLock api_lock{ApiLock::NoDrain{}};
+        std::lock_guard<std::mutex> lk(P.mu);
+        used_k = P.used[k];
+    }
+    {
+        // no API lock here: the copy-in touches only the pipeline's own workspace
+        // slots (64..93, allocation under the workspace mutex) and its own stream,
+        // so it is queued while the worker holds the lock for product i-1
         // set k's inputs were last read by the product two submissions ago
-        if (P.used[k]) cudaStreamWaitEvent(P.in, P.comp_done[k], 0);
+        if (used_k) cudaStreamWaitEvent(P.in, P.comp_done[k], 0);
         if (!(rc = to_device(&A->b, &j.dA.b, 64 + 15 * k, P.in, true)) &&
             !(rc = to_device(&B->b, &j.dB.b, 69 + 15 * k, P.in, true)))
             rc = to_device(&C->b, &j.dC.b, 74 + 15 * k, P.in, false);
