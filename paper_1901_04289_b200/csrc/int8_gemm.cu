@@ -619,8 +619,11 @@ __device__ __forceinline__ int item_kb_norm(const BandGemmParams& P, int pairs) 
 #endif
 // register cap (168 = the most 10 warps fit: 3 warps per SM sub-partition); 144 leaves room on every SM sub-partition for a co-resident 4-warp
 // radius block (APB_RAD_BESIDE schedule), at the price of epilogue spills
-template <int BNT, int BAND_W>
-__global__ void __maxnreg__(BNT == 256 ? APB_BAND_MAXNREG : 168)
+// RAW: raw-accumulator epilogue (P.raw), a pure TMEM -> global copy: 128 registers, which
+// leaves every SM sub-partition (3 of these warps each) room for one 128-register warp of the
+// radius kernel launched beside it
+template <int BNT, int BAND_W, bool RAW>
+__global__ void __maxnreg__(BNT == 256 ? (RAW ? 128 : APB_BAND_MAXNREG) : 168)
     band3_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       BandGemmParams P) {
     using Cfg = BandCfg<BNT, BAND_W>;
@@ -642,6 +645,9 @@ __global__ void __maxnreg__(BNT == 256 ? APB_BAND_MAXNREG : 168)
     const int it_begin = P.cta_begin[blockIdx.x], it_end = P.cta_begin[blockIdx.x + 1];
     if (P.dbg_ts && threadIdx.x == 0) P.dbg_ts[blockIdx.x * 32 + 31] = clock64();
     span_timer_enter(P.timer);
+    // a programmatic dependent (the sparse radius products, which do not read this grid's
+    // output) may be scheduled beside these CTAs once every one of them is resident
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < RA; i++) {
@@ -728,7 +734,7 @@ __global__ void __maxnreg__(BNT == 256 ? APB_BAND_MAXNREG : 168)
                 fence_after();
                 if (P.dbg_ts && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 1] = clock64();
                 uint32_t init_mask = 0;
-                const int kbn = item_kb_norm(P, s_hi - s_lo + 1);
+                const int kbn = RAW ? 0 : item_kb_norm(P, s_hi - s_lo + 1);
                 for (int kb = 0; kb < P.n_kb; kb++) {
                     const int t_first = max(0, d0 - s_hi);
                     const uint32_t b_first = bi;
@@ -775,7 +781,7 @@ __global__ void __maxnreg__(BNT == 256 ? APB_BAND_MAXNREG : 168)
             const int m0 = (W.x / P.n_tiles_n) * 128, n0 = (W.x % P.n_tiles_n) * BNT;
             const int d0 = BAND_W * W.y;
             const int row = m0 + 32 * q + lane;
-            const int kbn = item_kb_norm(P, min(P.S_A - 1, d0 + BAND_W - 1) - max(0, d0 - (P.S_B - 1)) + 1);
+            const int kbn = RAW ? 0 : item_kb_norm(P, min(P.S_A - 1, d0 + BAND_W - 1) - max(0, d0 - (P.S_B - 1)) + 1);
             const int n_norm = kbn ? (P.n_kb - 1) / kbn : 0;
             for (int ev = 0; ev < n_norm; ev++) {
                 // in-place normalisation: D_w = r_w + 256 q_w, r_w in [0, 256); q_w moves to
@@ -829,6 +835,41 @@ __global__ void __maxnreg__(BNT == 256 ? APB_BAND_MAXNREG : 168)
             mbar_wait(tfull, tph);
             fence_after();
             if (P.dbg_ts && warp == 2 && lane == 0 && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 3] = clock64();
+            if (RAW) {
+                // raw epilogue: the int32 accumulators go out as they are (plane Tw = the band's
+                // first diagonal, Tc = its second); the accumulators are free once the last
+                // chunk is in registers, so the next item's MMAs start under the final stores
+#pragma unroll 1
+                for (int h = 0; h < BNT / 64; h++) {
+                    uint32_t v[2][32];
+#pragma unroll
+                    for (int u = 0; u < 2; u++) {
+                        if (d0 + u < P.ND) {
+                            const uint32_t taddr =
+                                tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(u * BNT + col0 + 32 * h);
+                            TMEM_LD32(taddr, v[u]);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < 32; c++) v[u][c] = 0;
+                        }
+                    }
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (h == BNT / 64 - 1) {
+                        fence_before();
+                        mbar_arrive(tempty);
+                    }
+                    const size_t q0 = (size_t)W.y * (P.Np >> 2) + ((size_t)(n0 + col0 + 32 * h) >> 2);
+#pragma unroll
+                    for (int c = 0; c < 32; c += 4) {
+                        const size_t off = (((q0 + (c >> 2)) * P.Mp + row) << 2);
+                        *(uint4*)(P.Tw + off) = make_uint4(v[0][c], v[0][c + 1], v[0][c + 2], v[0][c + 3]);
+                        *(uint4*)(P.Tc + off) = make_uint4(v[1][c], v[1][c + 1], v[1][c + 2], v[1][c + 3]);
+                    }
+                }
+                if (P.dbg_ts && warp == 2 && lane == 0 && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 4] = clock64();
+                tph ^= 1;
+                continue;
+            }
             constexpr int WB = BAND_W == 2 ? 2 : 1;  // TMEM loads in flight per wait
 #pragma unroll 1
             for (int h = 0; h < BNT / 64; h++) {
@@ -972,9 +1013,11 @@ static int band_launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const Ban
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(band_gemm_kernel<BNT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-        cudaFuncSetAttribute(band3_gemm_kernel<BNT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        cudaFuncSetAttribute(band3_gemm_kernel<BNT, W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        cudaFuncSetAttribute(band3_gemm_kernel<BNT, W, W == 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         // full shared-memory carveout, so the SM keeps room for a co-resident radius block
-        cudaFuncSetAttribute(band3_gemm_kernel<BNT, W>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(band3_gemm_kernel<BNT, W, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(band3_gemm_kernel<BNT, W, W == 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr = true;
     }
     static const bool v2 = std::getenv("APB_BAND_V2") != nullptr;  // previous issue loop (A/B timing)
@@ -999,7 +1042,8 @@ static int band_launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const Ban
     at[0].val.priority = prio;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, band3_gemm_kernel<BNT, W>, ma, mb, P);
+    if (W == 2 && P.raw) cudaLaunchKernelEx(&cfg, band3_gemm_kernel<BNT, W, W == 2>, ma, mb, P);
+    else cudaLaunchKernelEx(&cfg, band3_gemm_kernel<BNT, W, false>, ma, mb, P);
     return APB_OK;
 }
 

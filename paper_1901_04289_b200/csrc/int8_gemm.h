@@ -31,6 +31,9 @@ struct BandGemmParams {
     const int* cta_begin;     // [n_ctas + 1] item ranges per CTA
     uint32_t* Tw;             // [n_bands][Mp][Np] result bytes of diagonals 4b..4b+3
     int32_t* Tc;              // [n_bands][Mp][Np] carry out of band b
+    // raw epilogue (no normalisations only): Tw[band] = diagonal 2b, Tc[band] = diagonal 2b+1 as
+    // the int32 accumulators themselves; recombine16 does the carry arithmetic (R.raw)
+    int raw = 0;
     int debug = 0;            // timing experiments only: 1 skip TMA refills, 2 skip epilogue stores
     long long* dbg_ts = nullptr;  // optional per-CTA clock64 trace (timing experiments)
     unsigned long long* timer = nullptr;  // device span timer (gemm_timer_*): [sum ns, launches, start, done, end]

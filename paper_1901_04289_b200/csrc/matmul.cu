@@ -579,6 +579,9 @@ struct RecombineArgs {
     int* status;
     int quad;  // band GEMM layout: plane[(j/4)][i][j%4] (coalesced epilogue stores), else [i][j]
     int digit_bits = 32;  // bits per Tw plane digit: 8 x diagonals per word
+    // raw band planes (recombine16 only): Tw[b] / Tc[b] are the int32 accumulators of
+    // diagonals 2b / 2b+1 (BandGemmParams::raw), band b contributes D0 + 256 D1 at digit b
+    int raw = 0;
     // optional fused radius combine (recombine16 only): C.rad = err (+) (r1 (+) r2), the
     // rad_combine_kernel step of src/matmul.cpp:512-513 folded into the store
     const uint32_t* r1b = nullptr;
@@ -882,15 +885,29 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
                 pc += plane;
             }
         }
+        if (R.raw) {
 #pragma unroll
-        for (int v = 0; v < RB; v++) {
-            const int k = kb + v;
-            if (k < ND) {
-                const int32_t d = run + (int32_t)w[v] + prev_c;
-                prev_c = c[v];
-                if (k == ND - 1) neg = d < 0;  // the arithmetic top digit carries the sign
-                else run = d >> 16;
-                Wd[k >> 1] |= ((uint32_t)d & 0xFFFFu) << (16 * (k & 1));
+            for (int v = 0; v < RB; v++) {
+                const int k = kb + v;
+                if (k < ND) {
+                    // |D| < 2^31: the band value needs 41 bits, the running carry stays below 2^26
+                    const int64_t d = (int64_t)c[v] * 256 + ((int64_t)run + (int64_t)(int32_t)w[v]);
+                    if (k == ND - 1) neg = d < 0;
+                    else run = (int32_t)(d >> 16);
+                    Wd[k >> 1] |= ((uint32_t)d & 0xFFFFu) << (16 * (k & 1));
+                }
+            }
+        } else {
+#pragma unroll
+            for (int v = 0; v < RB; v++) {
+                const int k = kb + v;
+                if (k < ND) {
+                    const int32_t d = run + (int32_t)w[v] + prev_c;
+                    prev_c = c[v];
+                    if (k == ND - 1) neg = d < 0;  // the arithmetic top digit carries the sign
+                    else run = d >> 16;
+                    Wd[k >> 1] |= ((uint32_t)d & 0xFFFFu) << (16 * (k & 1));
+                }
             }
         }
     }
@@ -1770,8 +1787,34 @@ __global__ void row_lists_kernel(const double* __restrict__ da, int64_t M, int64
     if (lane == 0) cnt[i] = base;
 }
 
+// mag_mul(mag_from_double(s, x), (1 + 2^-29)) for s > 0: Mag::from_double_upper
+// (src/mag.cpp:79-87: 53-bit mantissa -> top 30 bits rounded up) and mag_mul_up
+// (src/mag.cpp:132-145) on the double's bit fields; normal doubles and |x| < 2^40 take
+// the integer path, everything else the general routines (same results)
+APB_DEV Mag rad_fold_mag(double s, int64_t x) {
+    const uint64_t bits = (uint64_t)__double_as_longlong(s);
+    const int E = (int)(bits >> 52) & 0x7ff;
+    if (E == 0 || E == 0x7ff || (bits >> 63) || x > ((int64_t)1 << 40) || x < -((int64_t)1 << 40))
+        return mag_mul(mag_from_double(s, x), mag_parts((1ull << 29) + 1, 1));
+    const uint64_t m53 = (bits & ((1ull << 52) - 1)) | (1ull << 52);
+    uint64_t b = m53 >> 23;
+    if (m53 & ((1ull << 23) - 1)) b++;
+    int64_t f = x + (int64_t)(E - 1022);
+    if (b == kMagOne) {
+        b >>= 1;
+        f++;
+    }
+    uint64_t q = (b * ((1ull << 29) + 1) + (kMagOne - 1)) >> 30;
+    f += 1;
+    if (q < (kMagOne >> 1)) {
+        q <<= 1;
+        f--;
+    }
+    return mag_parts(q, f);
+}
+
 APB_DEV void rad_fold(Mag& ent, double& s, int64_t e_i, int64_t f_j) {
-    if (s != 0.0) ent = mag_add(ent, mag_mul(mag_from_double(s, -e_i - f_j), mag_parts((1ull << 29) + 1, 1)));
+    if (s != 0.0) ent = mag_add(ent, rad_fold_mag(s, -e_i - f_j));
     s = 0.0;
 }
 
@@ -2190,6 +2233,223 @@ __global__ void __launch_bounds__(T) rad_sparse2_kernel(RadPair P) {
     else
         rad_sprow_v3_body<R, T>(sm, (int64_t)blockIdx.x - P.N, P.da2, P.db2, P.M, P.N, P.K, P.ec2, P.fc2, P.r2b,
                                 P.r2f, P.mw2, P.cflag);
+}
+
+// ---- tiled sparse products (the speculative step's default).  rad_sparse2 gathers
+// every term's dense operand from L2 (26 terms x 8 B per output at config 3, ~109 MB of L2
+// reads for both products); here the sparse lines' (index, value) lists are compacted
+// once (rad_lists_kernel, warp per line, l order) and a CTA keeps a strip of TI dense
+// lines (TI x 1024 doubles per chunk) in shared memory, so a list entry read once
+// serves TI outputs: thread = sparse line, TI interleaved RN sums in the reference's
+// term order, chunk folds at the 1024-term boundaries (src/matmul.cpp:404-431).
+// Zero terms are skipped (s + a 0 = s for the nonnegative finite planes): same bits as
+// rad_sparse2 / rad_gemm2.
+struct RadLists {
+    int *cnt1, *idx1;  // product 1: column lists of db1 (K x N): cnt1[sub-chunk][N] cumulative, idx1[N][K]
+    double* val1;
+    int *cnt2, *idx2;  // product 2: row lists of da2 (M x K): cnt2[sub-chunk][M], idx2[M][K]
+    double* val2;
+};
+constexpr int RSUB = 256;     // list sub-chunk = dense strip depth in shared memory (RCH = 4 RSUB)
+constexpr int RQ_DL = 16;     // dense lines per strip (two per lane): 256 x 16 doubles = 32 KB
+constexpr int RQ_WARPS = 8;   // warps per CTA: 2 per SM sub-partition at 88 registers beside a raw band-GEMM CTA
+constexpr int RQ_T = 32 * RQ_WARPS;
+constexpr int RQ_QW = 4;      // line quads per warp and item
+constexpr int RQ_LINES = RQ_WARPS * 4 * RQ_QW;  // sparse lines per item: warps x RQ_QW quads x 4 lines
+constexpr int RQ_SMEM = RSUB * RQ_DL * (int)sizeof(double);
+
+__global__ void __launch_bounds__(256) rad_lists_kernel(RadPair P, RadLists L) {
+    const int64_t wl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wl >= P.N + P.M) return;
+    const bool first = wl < P.N;
+    if (first ? rad_variant(P.mw1, P.M, P.K, P.N, 1) != 0 : rad_variant(P.mw2, P.M, P.K, P.N, 0) != 1) return;
+    const int64_t line = first ? wl : wl - P.N;
+    const int64_t LN = first ? P.N : P.M;
+    const double* src = first ? P.db1 + line : P.da2 + line * P.K;
+    const int64_t stride = first ? P.N : 1;
+    int* cnt = first ? L.cnt1 : L.cnt2;
+    int* idx = first ? L.idx1 : L.idx2;
+    double* val = first ? L.val1 : L.val2;
+    int pos = 0;
+    for (int64_t c0 = 0; c0 < P.K; c0 += RSUB) {
+        const int64_t c1 = c0 + RSUB < P.K ? c0 + RSUB : P.K;
+        double v[RSUB / 32];
+#pragma unroll
+        for (int u = 0; u < RSUB / 32; u++) {
+            const int64_t l = c0 + 32 * u + lane;
+            v[u] = l < c1 ? src[l * stride] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < RSUB / 32; u++) {
+            const unsigned bal = __ballot_sync(0xffffffffu, v[u] != 0.0);
+            if (v[u] != 0.0) {
+                const int64_t q = pos + __popc(bal & ((1u << lane) - 1u));
+                idx[line * P.K + q] = (int)(c0 + 32 * u + lane);
+                val[line * P.K + q] = v[u];
+            }
+            pos += __popc(bal);
+        }
+        if (lane == 0) cnt[(c0 / RSUB) * LN + line] = pos;
+    }
+}
+
+// Work item = (strip of 16 dense lines, group of 128 sparse lines); 128-thread CTAs walk
+// the items round-robin.  The strip's 256-deep sub-chunk sits in shared memory as [l][16]
+// (32 KB: with 128 threads and <= 128 registers a CTA fits beside a raw-epilogue band-GEMM
+// CTA, where the speculative step runs it, launched as the GEMM's programmatic dependent).
+// A warp takes four sparse lines at a time: lane = (line g = lane / 8, dense lines 2r, 2r+1
+// with r = lane % 8); the line's list entries are loaded 8 at a time (lane r holds entry
+// p + r) and broadcast inside the 8-lane group, so a step is 3 shuffles, one 16-byte shared
+// load and two RN multiply-adds.  List padding has value 0 (s + a 0 = s exactly for the
+// finite nonnegative planes).  Chunk folds go straight to the output (first 1024-term chunk)
+// or are added into it (later chunks).  pdl_tail: wait for the grid this one was launched
+// beside before exiting, so stream successors are ordered after both.
+__global__ void __maxnreg__(88)
+    rad_quad_kernel(RadPair P, RadLists L, int nt1, int ngrp1, int nt2, int ngrp2, int pdl_tail) {
+    extern __shared__ __align__(16) double rq_ds[];  // [RSUB][RQ_DL]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 3, r = lane & 7;
+    const int K = (int)P.K;
+    const int nsub = (K + RSUB - 1) / RSUB;
+    const bool cen = !P.cflag || *P.cflag;  // uncentred planes (scan-written) unless flagged
+    const bool on1 = rad_variant(P.mw1, P.M, P.K, P.N, 1) == 0, on2 = rad_variant(P.mw2, P.M, P.K, P.N, 0) == 1;
+    const int n1 = nt1 * ngrp1, nitems = n1 + nt2 * ngrp2;
+    bool used = false;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+        const bool first = item < n1;
+        if (first ? !on1 : !on2) continue;
+        const int it = first ? item : item - n1;
+        const int ngrp = first ? ngrp1 : ngrp2;
+        const int t0 = (it / ngrp) * RQ_DL;
+        const int base = (it % ngrp) * RQ_LINES + warp * (4 * RQ_QW) + g;  // + 4 q
+        const int TD = (int)(first ? P.M : P.N);  // dense lines (the strip's dimension)
+        const int LN = (int)(first ? P.N : P.M);  // sparse lines
+        const double* dense = first ? P.da1 : P.db2;  // [K][TD]: |A| transposed / |B| + R_B
+        const int* cnt = first ? L.cnt1 : L.cnt2;
+        const int* idx = first ? L.idx1 : L.idx2;
+        const double* val = first ? L.val1 : L.val2;
+        uint32_t* rb = first ? P.r1b : P.r2b;
+        int64_t* rf = first ? P.r1f : P.r2f;
+        const int d0 = t0 + 2 * r;  // this lane's dense lines d0, d0 + 1
+        int64_t cd[2] = {0, 0};
+        if (cen) {
+#pragma unroll
+            for (int h = 0; h < 2; h++)
+                if (d0 + h < TD) cd[h] = first ? P.ec1[d0 + h] : P.fc2[d0 + h];
+        }
+        double acc[RQ_QW][2];
+        int pcur[RQ_QW];
+#pragma unroll
+        for (int q = 0; q < RQ_QW; q++) {
+            acc[q][0] = acc[q][1] = 0.0;
+            pcur[q] = 0;
+        }
+        for (int sc = 0; sc < nsub; sc++) {
+            const int c0 = sc * RSUB;
+            if (used) __syncthreads();  // the previous strip is fully consumed
+            used = true;
+            // this sub-chunk's list segments of the warp's 8 quads: end positions, then the first
+            // 8 entries of each (all loads issued before the strip copy is waited for)
+            int pe[RQ_QW], cl[RQ_QW];
+            double cv[RQ_QW];
+#pragma unroll
+            for (int q = 0; q < RQ_QW; q++) pe[q] = base + 4 * q < LN ? cnt[sc * LN + base + 4 * q] : 0;
+            if ((TD & 1) == 0) {  // strip sub-chunk by 16-byte async copies (zero-filled outside the planes)
+                const int c2 = 2 * (threadIdx.x & 7);
+                const double* src = dense + (int64_t)c0 * TD + t0 + c2;
+                const bool cok = t0 + c2 < TD;
+#pragma unroll
+                for (int u = 0; u < RSUB / (RQ_T / 8); u++) {
+                    const int row = (threadIdx.x >> 3) + (RQ_T / 8) * u;
+                    const bool ok = cok && c0 + row < K;
+                    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(rq_ds + row * RQ_DL + c2);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst),
+                                 "l"(ok ? src + (int64_t)row * TD : dense), "r"(ok ? 16 : 0)
+                                 : "memory");
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            } else {  // odd leading dimension: thread -> (row e / 16, column e % 16), 8 loads in flight
+                const int col = threadIdx.x & 15;
+                const bool cok = t0 + col < TD;
+                const double* src = dense + (int64_t)c0 * TD + t0 + col;
+#pragma unroll 1
+                for (int e0 = threadIdx.x; e0 < RSUB * RQ_DL; e0 += 8 * RQ_T) {
+                    double t[8];
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        const int row = (e0 >> 4) + (RQ_T / 16) * u;  // (e0 + RQ_T u) / 16
+                        t[u] = (cok && c0 + row < K) ? src[(int64_t)row * TD] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; u++) rq_ds[e0 + RQ_T * u] = t[u];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < RQ_QW; q++) {
+                const int line = base + 4 * q;
+                const bool in = pcur[q] + r < pe[q];
+                cl[q] = in ? idx[(int64_t)line * K + pcur[q] + r] : c0;
+                cv[q] = in ? val[(int64_t)line * K + pcur[q] + r] : 0.0;
+            }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+            const bool fold = ((sc + 1) * RSUB) % RCH == 0 || sc + 1 == nsub;
+            const bool later = (sc * RSUB) / RCH > 0;  // not the first 1024-term chunk
+            const double* strip = rq_ds + 2 * r - (int64_t)c0 * RQ_DL;
+#pragma unroll
+            for (int q = 0; q < RQ_QW; q++) {
+                const int line = base + 4 * q;
+                const bool live = line < LN;
+                const int pend = pe[q];
+                int p = pcur[q];
+                const int* li = idx + (int64_t)line * K;
+                const double* lv = val + (int64_t)line * K;
+                int rem = __reduce_max_sync(0xffffffffu, pend - p);
+                int cle = cl[q];
+                double cve = cv[q];
+                double a0 = acc[q][0], a1 = acc[q][1];
+                while (rem > 0) {
+                    const bool more = p + 8 + r < pend;
+                    const int nl = more ? li[p + 8 + r] : c0;  // next 8 entries while these are consumed
+                    const double nv = more ? lv[p + 8 + r] : 0.0;
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        const int l = __shfl_sync(0xffffffffu, cle, u, 8);
+                        const double v = __shfl_sync(0xffffffffu, cve, u, 8);
+                        const double2 x = *reinterpret_cast<const double2*>(strip + l * RQ_DL);
+                        a0 = __dadd_rn(a0, __dmul_rn(x.x, v));
+                        a1 = __dadd_rn(a1, __dmul_rn(x.y, v));
+                    }
+                    p += 8;
+                    rem -= 8;
+                    cle = nl;
+                    cve = nv;
+                }
+                pcur[q] = pend;
+                if (fold) {
+                    if (live) {
+                        const int64_t cs = cen ? (first ? P.fc1[line] : P.ec2[line]) : 0;
+#pragma unroll
+                        for (int h = 0; h < 2; h++) {
+                            const int d = d0 + h;
+                            if (d < TD) {
+                                const double a = h ? a1 : a0;
+                                const int64_t o = first ? (int64_t)d * P.N + line : (int64_t)line * P.N + d;
+                                Mag m = a != 0.0 ? rad_fold_mag(a, -cd[h] - cs) : mag_zero();
+                                if (later) m = mag_add(mag_load(rb[o], rf[o]), m);
+                                mag_store(m, &rb[o], &rf[o]);
+                            }
+                        }
+                    }
+                    a0 = a1 = 0.0;
+                }
+                acc[q][0] = a0;
+                acc[q][1] = a1;
+            }
+        }
+    }
+    if (pdl_tail) griddep_wait();
 }
 
 // dense variants (stand down unless picked): blockIdx.z = product
@@ -2732,6 +2992,14 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     }
     int rc;
     const int* d_group_d1 = (const int*)(dunits + off_d1);
+    // the recombine that will read the planes: recombine16 takes the band GEMM's raw
+    // accumulators (no epilogue arithmetic in the GEMM) when no normalisation is needed
+    static const bool slow_rc = std::getenv("APB_SLOW_RECOMBINE") != nullptr;  // test hook
+    static const bool r64_rc = std::getenv("APB_RECOMBINE64") != nullptr;      // test hook
+    static const bool no_raw = std::getenv("APB_NO_RAW_EPI") != nullptr ||     // test hook: carry epilogue
+                               std::getenv("APB_BAND_V2") != nullptr;         // (the v2 kernel has no raw mode)
+    const bool rc16 = band && first && !int_out && C && out_of(&C->b).mant && !slow_rc && band_w == 2 && NW <= 80 && !r64_rc;
+    const bool raw_epi = rc16 && kb_norm == 0 && !no_raw;
     if (band) {
         BandGemmParams P;
         P.S_A = SA;
@@ -2750,6 +3018,7 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         P.Tw = Tw;
         P.Tc = Tc;
         P.spec_maxw = spec_maxw;
+        P.raw = raw_epi ? 1 : 0;
         static const int dbg = std::getenv("APB_GEMM_DEBUG") ? std::atoi(std::getenv("APB_GEMM_DEBUG")) : 0;
         P.debug = dbg;  // timing experiments only (results are wrong when set)
         if (dbg & 4) {  // clock64 trace of the band kernel, dumped to stderr after the call
@@ -2816,6 +3085,7 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     R.status = workspace().status_dev;
     R.quad = band ? 1 : 0;
     R.digit_bits = band ? 8 * band_w : 32;
+    R.raw = raw_epi ? 1 : 0;
     R.spec_maxw = spec_maxw;
     R.spec_sa = SA;
     R.spec_sb = SB;
@@ -3082,6 +3352,39 @@ cudaEvent_t make_event() {
     return e;
 }
 
+// the tiled sparse radius products: standalone (one CTA per item), or beside the band GEMM
+// (pdl: launched as the GEMM's programmatic dependent on the GEMM's stream with at most one
+// CTA per SM -- each fits next to a GEMM CTA -- and a tail wait for the GEMM grid)
+struct RadDefer {
+    RadPair rp;
+    RadLists rl;
+    bool ready = false;
+};
+int rad_quad_launch(const RadPair& rp, const RadLists& rl, cudaStream_t ss, bool pdl) {
+    static const bool attr = [] {
+        cudaFuncSetAttribute(rad_quad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, RQ_SMEM);
+        cudaFuncSetAttribute(rad_quad_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        return true;
+    }();
+    (void)attr;
+    const int nt1 = (int)blocks_for(rp.M, RQ_DL), ngrp1 = (int)blocks_for(rp.N, RQ_LINES);
+    const int nt2 = (int)blocks_for(rp.N, RQ_DL), ngrp2 = (int)blocks_for(rp.M, RQ_LINES);
+    const int64_t nitems = (int64_t)nt1 * ngrp1 + (int64_t)nt2 * ngrp2;
+    cudaLaunchConfig_t cfg = {};
+    static const int grid_force = std::getenv("APB_RAD_GRID") ? std::atoi(std::getenv("APB_RAD_GRID")) : 0;  // timing hook
+    cfg.gridDim = dim3((unsigned)std::min<int64_t>(nitems, grid_force > 0 ? grid_force : pdl ? 148 : 148 * 7 * 2));
+    cfg.blockDim = dim3(RQ_T);
+    cfg.dynamicSmemBytes = RQ_SMEM;
+    cfg.stream = ss;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, rad_quad_kernel, rp, rl, nt1, ngrp1, nt2, ngrp2, pdl ? 1 : 0);
+    return cuda_check(cudaGetLastError(), "radius products");
+}
+
 int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, cudaStream_t st) {
     // one host synchronisation: fused scans of A and B (planner windows and both
     // radius products' windows), centring, exact double planes and nonzero counts
@@ -3224,7 +3527,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     };
     // speculative radius products (single radius block; sparse/dense chosen on the device)
     // `mid` (optional): a wait enqueued between the planes and the products
-    auto phaseR = [&](cudaStream_t ss, bool capturing, cudaEvent_t mid = nullptr) -> int {
+    auto phaseR = [&](cudaStream_t ss, bool capturing, cudaEvent_t mid = nullptr, RadDefer* defer = nullptr) -> int {
         const int tk = prof_begin("radius", ss);
         static const bool no_scan_planes = std::getenv("APB_NO_SCAN_PLANES") != nullptr;
         RadPair rp{M, K, N, da1, db1, da2, db2, ec1, fc1, ec2, fc2, r1b, r2b, r1f, r2f, mw1, mw2,
@@ -3250,7 +3553,34 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
                 at[0].val.priority = prio;
                 cfg.attrs = at;
                 cfg.numAttrs = 1;
-                cudaLaunchKernelEx(&cfg, rad_sparse2_kernel<2, 256>, rp);
+                // default: the per-line gather kernel (rad_sparse2); APB_RAD_QUAD=1: list
+                // compaction + strip products (rad_lists + rad_quad), measured slower at
+                // config 3 (6 + 23 us against 25 us, profiles/r2/radius_variants.txt)
+                static const bool gather = std::getenv("APB_RAD_QUAD") == nullptr;
+                const int64_t LNmax = std::max(M, N), nch = (K + RSUB - 1) / RSUB;
+                RadLists rl{};
+                if (!gather) {
+                    rl.cnt1 = sbuf<int>(kRad[0].lcnt, (size_t)nch * LNmax, ss);
+                    rl.idx1 = sbuf<int>(kRad[0].lidx, (size_t)K * LNmax, ss);
+                    rl.val1 = sbuf<double>(kRad[0].lval, (size_t)K * LNmax, ss);
+                    rl.cnt2 = sbuf<int>(kRad[1].lcnt, (size_t)nch * LNmax, ss);
+                    rl.idx2 = sbuf<int>(kRad[1].lidx, (size_t)K * LNmax, ss);
+                    rl.val2 = sbuf<double>(kRad[1].lval, (size_t)K * LNmax, ss);
+                }
+                if (!gather && rl.cnt1 && rl.idx1 && rl.val1 && rl.cnt2 && rl.idx2 && rl.val2) {
+                    cfg.gridDim = dim3(blocks_for(32 * (N + M), 256));
+                    cudaLaunchKernelEx(&cfg, rad_lists_kernel, rp, rl);
+                    if (defer) {  // the caller launches the products beside the GEMM
+                        defer->rp = rp;
+                        defer->rl = rl;
+                        defer->ready = true;
+                    } else {
+                        rad_quad_launch(rp, rl, ss, false);
+                    }
+                    count_launch(1);
+                } else {
+                    cudaLaunchKernelEx(&cfg, rad_sparse2_kernel<2, 256>, rp);
+                }
             }
             {
                 const dim3 g2(blocks_for(N, RT), blocks_for(M, RT), 2);
@@ -3434,13 +3764,23 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
                     static cudaEvent_t ev_packed = make_event();
                     cudaStreamWaitEvent(side, ev_fork, 0);  // the planes beside the pack
                     if (!rad_first) cudaEventRecord(ev_packed, cs);
-                    if ((r = phaseR(side, true, rad_first ? nullptr : ev_packed))) return r;
+                    // APB_RAD_QUAD=1 APB_RAD_QUAD_BESIDE=1: the sparse radius products leave the side
+                    // branch (which keeps the list compaction and the dense variants) and run beside
+                    // the GEMM, launched right behind it on its stream as a programmatic dependent.
+                    // Measured at config 3: the GEMM starts 20 us earlier but a GEMM CTA sharing its
+                    // SM slows from 92 to 107 us whatever the co-resident warps execute (shuffles and
+                    // shared loads go through the datapath the MMA operand fetch keeps ~75% busy),
+                    // net 193 -> 191 us; not the default
+                    static const bool beside = std::getenv("APB_RAD_QUAD_BESIDE") != nullptr && rad_first;
+                    RadDefer dfr;
+                    if ((r = phaseR(side, true, rad_first ? nullptr : ev_packed, beside ? &dfr : nullptr))) return r;
                     cudaEventRecord(ev_rdone, side);
                     if (rad_first) cudaStreamWaitEvent(cs, ev_rdone, 0);
                     RadFuse fz{r1b, r1f, r2b, r2f, ev_rdone, false, false};
+                    const std::function<int()> rad_hook = [&]() -> int { return rad_quad_launch(dfr.rp, dfr.rl, cs, true); };
                     r = scaled_block(A, B, 0, K, prec, C, true, P.maxw_a, P.maxw_b, RW.top[0], RW.bot[0],
-                                     CW.top[0], CW.bot[0], nullptr, 0, nullptr, nullptr, cs, nullptr, true, &fz,
-                                     &sum->maxw_a);
+                                     CW.top[0], CW.bot[0], nullptr, 0, nullptr, nullptr, cs,
+                                     dfr.ready ? &rad_hook : nullptr, true, &fz, &sum->maxw_a);
                     if (!r && !fz.used) r = APB_ERR_UNSUPPORTED;  // needs the fused recombine
                     cudaStreamWaitEvent(cs, ev_rdone, 0);           // rejoin the radius branch
                     return r;

@@ -83,7 +83,7 @@ def test_full_config_vs_reference(cfg):
                                   "APB_RECOMBINE64=1", "APB_NO_RAD_FUSE=1", "APB_NO_PDL=1",
                                   "APB_NO_SPEC_STEP=1", "APB_NO_PRIO=1", "APB_RAD_SPLIT=1", "APB_RAD_BESIDE=1",
                                   "APB_BAND_KBNORM=1", "APB_NO_SCAN_PLANES=1", "APB_RAD_MAIN=1",
-                                  "APB_RAD_NO_SMALL=1"])
+                                  "APB_RAD_NO_SMALL=1", "APB_NO_RAW_EPI=1", "APB_RAD_QUAD=1", "APB_RAD_QUAD=1,APB_RAD_QUAD_BESIDE=1"])
 def test_kernel_variants_golden(hook):
     """alternative kernels / schedules selected by the library's tuning hooks
     (unit GEMM used when a diagonal could overflow int32, byte-serial pack,
@@ -91,8 +91,7 @@ def test_kernel_variants_golden(hook):
     on the golden cases and configs 2 and 3 in a subprocess"""
     import subprocess
     import sys
-    k, v = hook.split("=")
-    env = dict(os.environ, **{k: v})
+    env = dict(os.environ, **dict(kv.split("=") for kv in hook.split(",")))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-k",
                         "test_matmul_golden_gpu or test_full_config_vs_reference or test_repeated_calls", os.path.abspath(__file__)],
                        env=env, capture_output=True, text=True, timeout=600)
