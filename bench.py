@@ -156,6 +156,20 @@ L2_NOTE = ("GPU arm: L2 flushed before every step (256 MiB write, outside the ti
            "reference arm: host-resident inputs on the CPU")
 
 
+def gemm_kernel_name(lib):
+    """the band GEMM instantiation of the last product (apb_gemm_last_config)"""
+    import ctypes as C
+    v = [C.c_int(0) for _ in range(4)]
+    lib.apb_gemm_last_config(*[C.byref(x) for x in v])
+    tn, bw, raw, ks = [x.value for x in v]
+    name = f"band3_gemm_kernel<{tn},{bw}>"
+    if raw:
+        name += " raw-accumulator epilogue"
+    if ks > 1:
+        name += f", K split {ks}"
+    return name
+
+
 def matmul_config(cfg, n, p, world):
     """the `config` object of both arms (identical, so the driver can pair them)"""
     return {"workload": f"BASELINE config {cfg[1:]}: real ball matmul N={n}, p={p}",
@@ -264,7 +278,7 @@ def run_matmul(torch, cfg, steps, warmup, world, rank, want_e2e=True, want_cpu=T
                  "slices_a": stats["last_slices_a"], "slices_b": stats["last_slices_b"]},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
                      "frac": achieved / peak, "traffic": ncu_traffic("band3_gemm"),
-                     "kernel": "band3_gemm_kernel<256,2>", "kernel_ms": per_launch_ms,
+                     "kernel": gemm_kernel_name(lib), "kernel_ms": per_launch_ms,
                      "kernel_launches_timed": gl.value,
                      "timing": "device span timer (%globaltimer) over the timed steps",
                      "work": f"2*M*N*K*ceil(h_A/8)*ceil(h_B/8) = {credited_ops:.4g} int8 ops per launch",
@@ -325,7 +339,7 @@ def run_complex(torch, steps, warmup):
     return {"metric": "complex ball matmul terms/s (N^3 complex multiply-adds per second)",
             "value": n ** 3 / (ms * 1e-3), "unit": "terms/s", "ms_per_step": ms,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
-                         "frac": achieved / peak, "kernel": "band3_gemm_kernel<256,2>",
+                         "frac": achieved / peak, "kernel": gemm_kernel_name(lib),
                          "kernel_ms": per_launch_ms, "kernel_launches_timed": gl.value,
                          "work": f"4 real products x 2*N^3*ceil(h/8)^2 = 4 x {credited:.4g} int8 ops"},
             "clocks": clk.summary(),

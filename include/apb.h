@@ -286,6 +286,9 @@ int apb_profile_dump(char* buf, size_t cap);
  * captured CUDA graphs, where per-call event regions are not recorded */
 int apb_gemm_timer_read(uint64_t* total_ns, uint64_t* launches);
 int apb_gemm_timer_reset(void);
+/* shape of the last band GEMM launched (measurement aid): output tile width (128 / 256),
+ * diagonals per band, raw-accumulator epilogue (0/1), K splits */
+int apb_gemm_last_config(int* tile_n, int* band_w, int* raw, int* ksplit);
 
 apb_matmul_stats* apb_matmul_stats_get(void);
 void apb_matmul_stats_reset(void);

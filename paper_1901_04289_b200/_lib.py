@@ -106,6 +106,8 @@ def lib():
     L.apb_profile_dump.restype = I
     L.apb_gemm_timer_read.argtypes = [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
     L.apb_gemm_timer_read.restype = I
+    L.apb_gemm_last_config.argtypes = [C.POINTER(C.c_int)] * 4
+    L.apb_gemm_last_config.restype = I
     L.apb_gemm_timer_reset.argtypes = []
     L.apb_gemm_timer_reset.restype = I
     _lib = L

@@ -622,7 +622,7 @@ __device__ __forceinline__ int item_kb_norm(const BandGemmParams& P, int pairs) 
 // RAW: raw-accumulator epilogue (P.raw), a pure TMEM -> global copy: 128 registers, which
 // leaves every SM sub-partition (3 of these warps each) room for one 128-register warp of the
 // radius kernel launched beside it
-template <int BNT, int BAND_W, bool RAW>
+template <int BNT, int BAND_W, bool RAW, bool SPLIT = false>
 __global__ void __maxnreg__(BNT == 256 ? (RAW ? 128 : APB_BAND_MAXNREG) : 168)
     band3_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       BandGemmParams P) {
@@ -682,9 +682,11 @@ __global__ void __maxnreg__(BNT == 256 ? (RAW ? 128 : APB_BAND_MAXNREG) : 168)
             for (int it = it_begin; it < it_end; it++) {
                 const int2 W = P.items[it];
                 const int m0 = (W.x / P.n_tiles_n) * 128, n0 = (W.x % P.n_tiles_n) * BNT;
-                const int d0 = BAND_W * W.y;
+                const int d0 = BAND_W * (SPLIT ? (W.y & 0xFFFF) : W.y);
+                const int kb0 = SPLIT ? (W.y >> 16) * P.kb_per : 0;
+                const int kb1 = SPLIT ? min(P.n_kb, kb0 + P.kb_per) : P.n_kb;
                 const int s_hi = min(P.S_A - 1, d0 + BAND_W - 1), s_lo = max(0, d0 - (P.S_B - 1));
-                for (int kb = 0; kb < P.n_kb; kb++) {
+                for (int kb = SPLIT ? kb0 : 0; kb < (SPLIT ? kb1 : P.n_kb); kb++) {
                     const int t_first = max(0, d0 - s_hi);
                     const uint32_t b_first = bi;
                     int tmax_prev = -1;
@@ -727,7 +729,9 @@ __global__ void __maxnreg__(BNT == 256 ? (RAW ? 128 : APB_BAND_MAXNREG) : 168)
             uint32_t bi = 0, tph = 0;
             for (int it = it_begin; it < it_end; it++) {
                 const int2 W = P.items[it];
-                const int d0 = BAND_W * W.y;
+                const int d0 = BAND_W * (SPLIT ? (W.y & 0xFFFF) : W.y);
+                const int kb0 = SPLIT ? (W.y >> 16) * P.kb_per : 0;
+                const int kb1 = SPLIT ? min(P.n_kb, kb0 + P.kb_per) : P.n_kb;
                 const int s_hi = min(P.S_A - 1, d0 + BAND_W - 1), s_lo = max(0, d0 - (P.S_B - 1));
                 if (P.dbg_ts && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 0] = clock64();
                 mbar_wait(tempty, tph ^ 1);
@@ -735,7 +739,7 @@ __global__ void __maxnreg__(BNT == 256 ? (RAW ? 128 : APB_BAND_MAXNREG) : 168)
                 if (P.dbg_ts && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 1] = clock64();
                 uint32_t init_mask = 0;
                 const int kbn = RAW ? 0 : item_kb_norm(P, s_hi - s_lo + 1);
-                for (int kb = 0; kb < P.n_kb; kb++) {
+                for (int kb = SPLIT ? kb0 : 0; kb < (SPLIT ? kb1 : P.n_kb); kb++) {
                     const int t_first = max(0, d0 - s_hi);
                     const uint32_t b_first = bi;
                     for (int s = s_hi; s >= s_lo; s--, j++) {
@@ -779,7 +783,7 @@ __global__ void __maxnreg__(BNT == 256 ? (RAW ? 128 : APB_BAND_MAXNREG) : 168)
         for (int it = it_begin; it < it_end; it++) {
             const int2 W = P.items[it];
             const int m0 = (W.x / P.n_tiles_n) * 128, n0 = (W.x % P.n_tiles_n) * BNT;
-            const int d0 = BAND_W * W.y;
+            const int d0 = BAND_W * (SPLIT ? (W.y & 0xFFFF) : W.y);
             const int row = m0 + 32 * q + lane;
             const int kbn = RAW ? 0 : item_kb_norm(P, min(P.S_A - 1, d0 + BAND_W - 1) - max(0, d0 - (P.S_B - 1)) + 1);
             const int n_norm = kbn ? (P.n_kb - 1) / kbn : 0;
@@ -858,7 +862,8 @@ __global__ void __maxnreg__(BNT == 256 ? (RAW ? 128 : APB_BAND_MAXNREG) : 168)
                         fence_before();
                         mbar_arrive(tempty);
                     }
-                    const size_t q0 = (size_t)W.y * (P.Np >> 2) + ((size_t)(n0 + col0 + 32 * h) >> 2);
+                    const size_t q0 = (size_t)(SPLIT ? (W.y & 0xFFFF) + (W.y >> 16) * P.n_bands : W.y) * (P.Np >> 2) +
+                                      ((size_t)(n0 + col0 + 32 * h) >> 2);
 #pragma unroll
                     for (int c = 0; c < 32; c += 4) {
                         const size_t off = (((q0 + (c >> 2)) * P.Mp + row) << 2);
@@ -1015,6 +1020,7 @@ static int band_launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const Ban
         cudaFuncSetAttribute(band_gemm_kernel<BNT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         cudaFuncSetAttribute(band3_gemm_kernel<BNT, W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         cudaFuncSetAttribute(band3_gemm_kernel<BNT, W, W == 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        cudaFuncSetAttribute(band3_gemm_kernel<BNT, W, W == 2, W == 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         // full shared-memory carveout, so the SM keeps room for a co-resident radius block
         cudaFuncSetAttribute(band3_gemm_kernel<BNT, W, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(band3_gemm_kernel<BNT, W, W == 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1042,7 +1048,8 @@ static int band_launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const Ban
     at[0].val.priority = prio;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (W == 2 && P.raw) cudaLaunchKernelEx(&cfg, band3_gemm_kernel<BNT, W, W == 2>, ma, mb, P);
+    if (W == 2 && P.raw && P.n_bands > 0) cudaLaunchKernelEx(&cfg, band3_gemm_kernel<BNT, W, W == 2, W == 2>, ma, mb, P);  // K split
+    else if (W == 2 && P.raw) cudaLaunchKernelEx(&cfg, band3_gemm_kernel<BNT, W, W == 2>, ma, mb, P);
     else cudaLaunchKernelEx(&cfg, band3_gemm_kernel<BNT, W, false>, ma, mb, P);
     return APB_OK;
 }
@@ -1058,9 +1065,15 @@ unsigned long long* gemm_timer() {
     return t;
 }
 
+static int g_last_cfg[4] = {0, 0, 0, 0};
+
 int band_gemm_launch(const int8_t* Apack, const int8_t* Bpack, const BandGemmParams& Pin, int n_ctas,
                      cudaStream_t st) {
     BandGemmParams P = Pin;
+    g_last_cfg[0] = P.bn;
+    g_last_cfg[1] = P.band_w;
+    g_last_cfg[2] = P.raw;
+    g_last_cfg[3] = P.n_bands > 0 ? (P.n_kb + P.kb_per - 1) / P.kb_per : 1;
     if (!P.timer) P.timer = gemm_timer();
     CUtensorMap ma, mb;
     int rc = make_map(&ma, Apack, (uint64_t)P.Kp, (uint64_t)P.S_A * P.Mp, BM);
@@ -1069,6 +1082,7 @@ int band_gemm_launch(const int8_t* Apack, const int8_t* Bpack, const BandGemmPar
     if (rc) return rc;
     const int tok = prof_begin("slice_gemm", st);
     if (P.bn == 256) band_launch_t<256, 2>(ma, mb, P, n_ctas, st);
+    else if (P.band_w == 2) band_launch_t<128, 2>(ma, mb, P, n_ctas, st);  // raw mode, small products
     else band_launch_t<128, 4>(ma, mb, P, n_ctas, st);
     prof_end(tok, st);
     count_launch();
@@ -1086,6 +1100,14 @@ int apb_gemm_timer_read(uint64_t* total_ns, uint64_t* launches) {
     if (cudaMemcpy(h, apb::gemm_timer(), sizeof h, cudaMemcpyDeviceToHost) != cudaSuccess) return APB_ERR_CUDA;
     if (total_ns) *total_ns = h[0];
     if (launches) *launches = h[1];
+    return APB_OK;
+}
+
+int apb_gemm_last_config(int* tile_n, int* band_w, int* raw, int* ksplit) {
+    if (tile_n) *tile_n = apb::g_last_cfg[0];
+    if (band_w) *band_w = apb::g_last_cfg[1];
+    if (raw) *raw = apb::g_last_cfg[2];
+    if (ksplit) *ksplit = apb::g_last_cfg[3];
     return APB_OK;
 }
 

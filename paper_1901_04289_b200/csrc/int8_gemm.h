@@ -34,6 +34,10 @@ struct BandGemmParams {
     // raw epilogue (no normalisations only): Tw[band] = diagonal 2b, Tc[band] = diagonal 2b+1 as
     // the int32 accumulators themselves; recombine16 does the carry arithmetic (R.raw)
     int raw = 0;
+    // raw mode only: K split.  item.y = band | ks << 16; split ks covers K blocks
+    // [ks * kb_per, min(n_kb, (ks + 1) * kb_per)) and writes its own planes (index band +
+    // n_bands * ks); the recombine adds the splits' accumulators
+    int n_bands = 0, kb_per = 1 << 30;
     int debug = 0;            // timing experiments only: 1 skip TMA refills, 2 skip epilogue stores
     long long* dbg_ts = nullptr;  // optional per-CTA clock64 trace (timing experiments)
     unsigned long long* timer = nullptr;  // device span timer (gemm_timer_*): [sum ns, launches, start, done, end]

@@ -582,6 +582,7 @@ struct RecombineArgs {
     // raw band planes (recombine16 only): Tw[b] / Tc[b] are the int32 accumulators of
     // diagonals 2b / 2b+1 (BandGemmParams::raw), band b contributes D0 + 256 D1 at digit b
     int raw = 0;
+    int nsplit = 1;  // raw mode: K splits (1 or 2), the second split's planes start at plane index nwords
     // optional fused radius combine (recombine16 only): C.rad = err (+) (r1 (+) r2), the
     // rad_combine_kernel step of src/matmul.cpp:512-513 folded into the store
     const uint32_t* r1b = nullptr;
@@ -841,7 +842,7 @@ __global__ void __launch_bounds__(128) recombine_fast_kernel(RecombineArgs R) {
 // shared memory (one padded row per thread) so the p-bit output window and
 // the truncation error are read with dynamic word indices instead of select
 // chains.  Same results as recombine_fast_kernel<*, 16>.
-template <int NBC>
+template <int NBC, bool SPLIT = false>
 __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
     constexpr int ND = NBC + 2;        // base-2^16 digits (band b: word digit b, carry digit b+1)
     constexpr int NW = (ND + 1) / 2;   // 32-bit magnitude words
@@ -870,6 +871,8 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
     // band planes by pointer stepping (one 64-bit add per band, no per-band multiply)
     const uint32_t* pw = R.Tw + off;
     const int32_t* pc = R.Tc + off;
+    const uint32_t* pw2 = pw + (size_t)NB * plane;  // SPLIT: planes of the second K split
+    const int32_t* pc2 = pc + (size_t)NB * plane;
 #pragma unroll
     for (int kb = 0; kb < ND; kb += RB) {
         uint32_t w[RB];
@@ -883,6 +886,27 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
             if (b < NBC) {
                 pw += plane;
                 pc += plane;
+            }
+        }
+        if (SPLIT) {  // raw mode with K split in two: the second split's accumulators, loaded in the
+                      // same batch (the sums are the unsplit diagonals, below 2^31 like them)
+            uint32_t w2[RB];
+            int32_t c2[RB];
+#pragma unroll
+            for (int v = 0; v < RB; v++) {
+                const int b = kb + v;
+                const bool live = b < NBC && b < NB;
+                w2[v] = live ? __ldcs(pw2) : 0u;
+                c2[v] = live ? __ldcs(pc2) : 0;
+                if (b < NBC) {
+                    pw2 += plane;
+                    pc2 += plane;
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < RB; v++) {
+                w[v] += w2[v];
+                c[v] += c2[v];
             }
         }
         if (R.raw) {
@@ -2856,7 +2880,7 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     }
     const int SA = slices_for(maxw_a), SB = slices_for(maxw_b);
     const BandGeom geo = band_geom(M, N, w);
-    const int bn = geo.bn, band_w = geo.band_w, Mp = geo.Mp, Np = geo.Np, Kp = geo.Kp;
+    const int Mp = geo.Mp, Np = geo.Np, Kp = geo.Kp;
     stats().int_gemm_products++;
     stats().last_height_a = (uint64_t)maxw_a;
     stats().last_height_b = (uint64_t)maxw_b;
@@ -2890,7 +2914,6 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     prof_end(tok, st);
     if (!prepacked) count_launch(2);
     htrace().mark("pack_launched");
-    const int tiles = (Mp / kSliceTile) * (Np / bn);
     const int ND = SA + SB - 1;
     // band kernel when every diagonal fits an int32 accumulator: pairs * w * 2^14 < 2^31
     static const bool force_unit = std::getenv("APB_FORCE_UNIT_GEMM") != nullptr;  // test hook
@@ -2904,6 +2927,66 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     int kb_norm = fits ? 0 : (((int64_t)1 << 17) - 1) / (pairs * kSliceBK) >= 1 ? 1 << 20 : 0;
     if (kb_force > 0) kb_norm = kb_force;  // test hook: an event every kb_force K blocks
     const bool band = !force_unit && (fits || (!no_norm && kb_norm > 0));
+    // the recombine that will read the planes: recombine16 takes the band GEMM's raw
+    // accumulators (no epilogue arithmetic in the GEMM) when no normalisation is needed
+    static const bool slow_rc = std::getenv("APB_SLOW_RECOMBINE") != nullptr;  // test hook
+    static const bool r64_rc = std::getenv("APB_RECOMBINE64") != nullptr;      // test hook
+    static const bool no_raw = std::getenv("APB_NO_RAW_EPI") != nullptr ||     // test hook: carry epilogue
+                               std::getenv("APB_BAND_V2") != nullptr;         // (the v2 kernel has no raw mode)
+    const bool raw_epi = band && first && !int_out && C && out_of(&C->b).mant && !slow_rc && !r64_rc && !no_raw &&
+                         kb_norm == 0 && (ND + 1) / 2 <= 80;
+    // raw mode always runs 2 diagonals per band (16-bit digits for recombine16); small products
+    // that leave most SMs without a 128 x 256 item may take 128-wide tiles and split K between
+    // CTAs (the raw planes of the splits are summed by the recombine): the (tile width, splits)
+    // pair with the smallest LPT makespan in the cost model below wins
+    const int band_w = raw_epi ? 2 : geo.band_w;
+    int bn = geo.bn, ksplit = 1;
+    const int n_kb_all = Kp / kSliceBK;
+    auto band_weights = [&](std::vector<int64_t>& bw) {
+        const int NB = (ND + band_w - 1) / band_w;
+        bw.assign(NB, 0);
+        for (int d = 0; d < ND; d++) bw[d / band_w] += std::min(d, SA - 1) - std::max(0, d - SB + 1) + 1;
+    };
+    // item cost in tensor-pipe clocks: MMAs of M=128, K=32 take 128 (N=256) / ~72 (N=128) clocks,
+    // 4 per slice pair and K block, plus the item's epilogue (~8300 / ~4300 clocks for a 128 x 256 /
+    // 128 x 128 tile, measured; the accumulators are single-buffered, so an epilogue is not hidden
+    // behind the next item's MMAs) and ~2500 clocks to fill the pipeline
+    auto item_cost = [&](int64_t pairs_b, int tile_n, int kbs) -> int64_t {
+        return pairs_b * kbs * (tile_n == 256 ? 512 : 288) + (tile_n == 256 ? 8300 : 4300) + 700;
+    };
+    auto makespan = [&](int tile_n, int ks) -> int64_t {
+        std::vector<int64_t> bw;
+        band_weights(bw);
+        const int kbs = (n_kb_all + ks - 1) / ks;
+        std::vector<int64_t> it;
+        const int nt = (Mp / kSliceTile) * (Np / tile_n);
+        for (int t = 0; t < nt * ks; t++)
+            for (int64_t x : bw) it.push_back(item_cost(x, tile_n, kbs));
+        std::sort(it.begin(), it.end(), std::greater<int64_t>());
+        std::vector<int64_t> load(std::min<size_t>(148, it.size()), 0);
+        for (int64_t c : it) *std::min_element(load.begin(), load.end()) += c;
+        return *std::max_element(load.begin(), load.end());
+    };
+    if (raw_epi) {
+        static const int bn_env = std::getenv("APB_BAND_BN") ? std::atoi(std::getenv("APB_BAND_BN")) : 0;
+        static const int ks_env = std::getenv("APB_BAND_KSPLIT") ? std::atoi(std::getenv("APB_BAND_KSPLIT")) : 0;
+        int64_t best = INT64_MAX;
+        for (int tn : {256, 128}) {
+            if (Np % tn || (bn_env && tn != bn_env)) continue;
+            for (int ks : {1, 2}) {
+                if (ks > n_kb_all || (ks - 1) * ((n_kb_all + ks - 1) / ks) >= n_kb_all || (ks_env && ks != ks_env))
+                    continue;  // (every split keeps at least one K block)
+                if (ks > 1 && (int64_t)(Mp / kSliceTile) * (Np / tn) * ((ND + 1) / 2) >= 148) continue;  // enough items
+                const int64_t m = makespan(tn, ks);
+                if (m < best) {
+                    best = m;
+                    bn = tn;
+                    ksplit = ks;
+                }
+            }
+        }
+    }
+    const int tiles = (Mp / kSliceTile) * (Np / bn);
     // work tables depend only on (band, S_A, S_B, w, tile grid): built once on the
     // host (LPT item assignment / unit groups), cached as device copies
     struct Tables {
@@ -2912,19 +2995,21 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         size_t off_items, off_begin, off_d1, n_ctas;
     };
     static std::map<std::vector<int64_t>, Tables> table_cache;
-    const std::vector<int64_t> key = {band ? bn : 0, SA, SB, w, Mp, Np};
+    const std::vector<int64_t> key = {band ? bn : 0, SA, SB, w, Mp, Np, band_w, ksplit};
     auto hit = table_cache.find(key);
     if (hit == table_cache.end()) {
         Tables T{};
         std::vector<char> host;
         if (band) {
             const int NB = (ND + band_w - 1) / band_w;
-            std::vector<int64_t> bw(NB, 0);
-            for (int d = 0; d < ND; d++)
-                bw[d / band_w] += std::min(d, SA - 1) - std::max(0, d - SB + 1) + 1;
+            std::vector<int64_t> bw;
+            band_weights(bw);
             std::vector<std::pair<int64_t, int2>> items;
+            const int kbs = (n_kb_all + ksplit - 1) / ksplit;
             for (int t = 0; t < tiles; t++)
-                for (int bnd = 0; bnd < NB; bnd++) items.push_back({bw[bnd], make_int2(t, bnd)});
+                for (int ks = 0; ks < ksplit; ks++)
+                    for (int bnd = 0; bnd < NB; bnd++)
+                        items.push_back({item_cost(bw[bnd], bn, std::min(kbs, n_kb_all - ks * kbs)), make_int2(t, bnd | (ks << 16))});
             std::stable_sort(items.begin(), items.end(),
                              [](const std::pair<int64_t, int2>& x, const std::pair<int64_t, int2>& y) {
                                  return x.first > y.first;
@@ -2984,22 +3069,14 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     const int G = TB.G, NW = TB.NW;
     char* dunits = TB.dev;
     const size_t off_items = TB.off_items, off_begin = TB.off_begin, off_d1 = TB.off_d1, n_ctas = TB.n_ctas;
-    uint32_t* Tw = sbuf<uint32_t>(S_TW, (size_t)NW * Mp * Np, st);
-    int32_t* Tc = sbuf<int32_t>(S_TC, (size_t)G * Mp * Np, st);
+    uint32_t* Tw = sbuf<uint32_t>(S_TW, (size_t)NW * ksplit * Mp * Np, st);
+    int32_t* Tc = sbuf<int32_t>(S_TC, (size_t)G * ksplit * Mp * Np, st);
     if (!Tw || !Tc) {
         set_error("out of device memory (product planes)");
         return APB_ERR_CUDA;
     }
     int rc;
     const int* d_group_d1 = (const int*)(dunits + off_d1);
-    // the recombine that will read the planes: recombine16 takes the band GEMM's raw
-    // accumulators (no epilogue arithmetic in the GEMM) when no normalisation is needed
-    static const bool slow_rc = std::getenv("APB_SLOW_RECOMBINE") != nullptr;  // test hook
-    static const bool r64_rc = std::getenv("APB_RECOMBINE64") != nullptr;      // test hook
-    static const bool no_raw = std::getenv("APB_NO_RAW_EPI") != nullptr ||     // test hook: carry epilogue
-                               std::getenv("APB_BAND_V2") != nullptr;         // (the v2 kernel has no raw mode)
-    const bool rc16 = band && first && !int_out && C && out_of(&C->b).mant && !slow_rc && band_w == 2 && NW <= 80 && !r64_rc;
-    const bool raw_epi = rc16 && kb_norm == 0 && !no_raw;
     if (band) {
         BandGemmParams P;
         P.S_A = SA;
@@ -3019,6 +3096,10 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         P.Tc = Tc;
         P.spec_maxw = spec_maxw;
         P.raw = raw_epi ? 1 : 0;
+        if (raw_epi && ksplit > 1) {
+            P.n_bands = (ND + band_w - 1) / band_w;
+            P.kb_per = (n_kb_all + ksplit - 1) / ksplit;
+        }
         static const int dbg = std::getenv("APB_GEMM_DEBUG") ? std::atoi(std::getenv("APB_GEMM_DEBUG")) : 0;
         P.debug = dbg;  // timing experiments only (results are wrong when set)
         if (dbg & 4) {  // clock64 trace of the band kernel, dumped to stderr after the call
@@ -3086,6 +3167,7 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     R.quad = band ? 1 : 0;
     R.digit_bits = band ? 8 * band_w : 32;
     R.raw = raw_epi ? 1 : 0;
+    R.nsplit = ksplit;
     R.spec_maxw = spec_maxw;
     R.spec_sa = SA;
     R.spec_sb = SB;
@@ -3110,6 +3192,8 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         if (fast && band_w == 4 && NW <= 20) recombine_fast_kernel<20, 32><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 4 && NW <= 40) recombine_fast_kernel<40, 32><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 4 && NW <= 72) recombine_fast_kernel<72, 32><<<gbq, 128, 0, st>>>(R);
+        else if (fast && band_w == 2 && NW <= 40 && !r64 && ksplit > 1) recombine16_kernel<40, true><<<gbq, 128, 0, st>>>(R);
+        else if (fast && band_w == 2 && NW <= 80 && !r64 && ksplit > 1) recombine16_kernel<80, true><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 2 && NW <= 40 && !r64) recombine16_kernel<40><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 2 && NW <= 80 && !r64) recombine16_kernel<80><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 2 && NW <= 40) recombine_fast_kernel<40, 16><<<gbq, 128, 0, st>>>(R);
