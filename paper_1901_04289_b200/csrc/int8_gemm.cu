@@ -864,11 +864,29 @@ __global__ void __maxnreg__(BNT == 256 ? (RAW ? 128 : APB_BAND_MAXNREG) : 168)
                     }
                     const size_t q0 = (size_t)(SPLIT ? (W.y & 0xFFFF) + (W.y >> 16) * P.n_bands : W.y) * (P.Np >> 2) +
                                       ((size_t)(n0 + col0 + 32 * h) >> 2);
+                    if (P.raw == 2) {
+                        // 40-bit band values V = D0 + 256 D1 (|V| < 2^39 on this path): low words in Tw,
+                        // the four high bytes of a column quad in one word of the byte plane Tc
 #pragma unroll
-                    for (int c = 0; c < 32; c += 4) {
-                        const size_t off = (((q0 + (c >> 2)) * P.Mp + row) << 2);
-                        *(uint4*)(P.Tw + off) = make_uint4(v[0][c], v[0][c + 1], v[0][c + 2], v[0][c + 3]);
-                        *(uint4*)(P.Tc + off) = make_uint4(v[1][c], v[1][c + 1], v[1][c + 2], v[1][c + 3]);
+                        for (int c = 0; c < 32; c += 4) {
+                            uint32_t lo[4], hi = 0;
+#pragma unroll
+                            for (int e = 0; e < 4; e++) {
+                                const int64_t V = (int64_t)(int32_t)v[1][c + e] * 256 + (int64_t)(int32_t)v[0][c + e];
+                                lo[e] = (uint32_t)V;
+                                hi |= ((uint32_t)(V >> 32) & 0xFFu) << (8 * e);
+                            }
+                            const size_t qe = (q0 + (c >> 2)) * P.Mp + row;
+                            *(uint4*)(P.Tw + (qe << 2)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                            ((uint32_t*)P.Tc)[qe] = hi;
+                        }
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 32; c += 4) {
+                            const size_t off = (((q0 + (c >> 2)) * P.Mp + row) << 2);
+                            *(uint4*)(P.Tw + off) = make_uint4(v[0][c], v[0][c + 1], v[0][c + 2], v[0][c + 3]);
+                            *(uint4*)(P.Tc + off) = make_uint4(v[1][c], v[1][c + 1], v[1][c + 2], v[1][c + 3]);
+                        }
                     }
                 }
                 if (P.dbg_ts && warp == 2 && lane == 0 && it - it_begin < 4) P.dbg_ts[blockIdx.x * 32 + 8 * (it - it_begin) + 4] = clock64();

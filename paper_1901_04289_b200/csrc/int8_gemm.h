@@ -31,8 +31,10 @@ struct BandGemmParams {
     const int* cta_begin;     // [n_ctas + 1] item ranges per CTA
     uint32_t* Tw;             // [n_bands][Mp][Np] result bytes of diagonals 4b..4b+3
     int32_t* Tc;              // [n_bands][Mp][Np] carry out of band b
-    // raw epilogue (no normalisations only): Tw[band] = diagonal 2b, Tc[band] = diagonal 2b+1 as
-    // the int32 accumulators themselves; recombine16 does the carry arithmetic (R.raw)
+    // raw epilogue (no normalisations only): 1: Tw[band] = diagonal 2b, Tc[band] = diagonal 2b+1 as
+    // the int32 accumulators themselves; 2 (when |D0 + 256 D1| < 2^39): Tw[band] = the low word of
+    // D0 + 256 D1 and Tc, as a byte plane [band][entry], its bits 32..39; recombine16 does the
+    // carry arithmetic (R.raw)
     int raw = 0;
     // raw mode only: K split.  item.y = band | ks << 16; split ks covers K blocks
     // [ks * kb_per, min(n_kb, (ks + 1) * kb_per)) and writes its own planes (index band +

@@ -579,8 +579,9 @@ struct RecombineArgs {
     int* status;
     int quad;  // band GEMM layout: plane[(j/4)][i][j%4] (coalesced epilogue stores), else [i][j]
     int digit_bits = 32;  // bits per Tw plane digit: 8 x diagonals per word
-    // raw band planes (recombine16 only): Tw[b] / Tc[b] are the int32 accumulators of
-    // diagonals 2b / 2b+1 (BandGemmParams::raw), band b contributes D0 + 256 D1 at digit b
+    // raw band planes (recombine16 only): 1: Tw[b] / Tc[b] are the int32 accumulators of
+    // diagonals 2b / 2b+1; 2: Tw[b] is the low word of D0 + 256 D1 and Tc a byte plane with its
+    // bits 32..39 (BandGemmParams::raw); band b contributes D0 + 256 D1 at digit b
     int raw = 0;
     int nsplit = 1;  // raw mode: K splits (1 or 2), the second split's planes start at plane index nwords
     // optional fused radius combine (recombine16 only): C.rad = err (+) (r1 (+) r2), the
@@ -873,6 +874,9 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
     const int32_t* pc = R.Tc + off;
     const uint32_t* pw2 = pw + (size_t)NB * plane;  // SPLIT: planes of the second K split
     const int32_t* pc2 = pc + (size_t)NB * plane;
+    const bool v40 = R.raw == 2;  // Tc is a byte plane: bits 32..39 of the band values
+    const int8_t* pb = (const int8_t*)R.Tc + off;
+    const int8_t* pb2 = pb + (size_t)NB * plane;
 #pragma unroll
     for (int kb = 0; kb < ND; kb += RB) {
         uint32_t w[RB];
@@ -882,10 +886,11 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
             const int b = kb + v;
             const bool live = b < NBC && b < NB;
             w[v] = live ? __ldcs(pw) : 0u;
-            c[v] = live ? __ldcs(pc) : 0;
+            c[v] = !live ? 0 : v40 ? (int32_t)(int8_t)__ldcs(pb) : __ldcs(pc);
             if (b < NBC) {
                 pw += plane;
                 pc += plane;
+                pb += plane;
             }
         }
         if (SPLIT) {  // raw mode with K split in two: the second split's accumulators, loaded in the
@@ -897,16 +902,23 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
                 const int b = kb + v;
                 const bool live = b < NBC && b < NB;
                 w2[v] = live ? __ldcs(pw2) : 0u;
-                c2[v] = live ? __ldcs(pc2) : 0;
+                c2[v] = !live ? 0 : v40 ? (int32_t)(int8_t)__ldcs(pb2) : __ldcs(pc2);
                 if (b < NBC) {
                     pw2 += plane;
                     pc2 += plane;
+                    pb2 += plane;
                 }
             }
 #pragma unroll
             for (int v = 0; v < RB; v++) {
-                w[v] += w2[v];
-                c[v] += c2[v];
+                if (v40) {  // low words add with a carry into the high parts
+                    const uint32_t t = w[v] + w2[v];
+                    c[v] += c2[v] + (t < w[v] ? 1 : 0);
+                    w[v] = t;
+                } else {
+                    w[v] += w2[v];
+                    c[v] += c2[v];
+                }
             }
         }
         if (R.raw) {
@@ -915,7 +927,8 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
                 const int k = kb + v;
                 if (k < ND) {
                     // |D| < 2^31: the band value needs 41 bits, the running carry stays below 2^26
-                    const int64_t d = (int64_t)c[v] * 256 + ((int64_t)run + (int64_t)(int32_t)w[v]);
+                    const int64_t d = v40 ? (int64_t)(((uint64_t)(uint32_t)c[v] << 32) | w[v]) + (int64_t)run
+                                          : (int64_t)c[v] * 256 + ((int64_t)run + (int64_t)(int32_t)w[v]);
                     if (k == ND - 1) neg = d < 0;
                     else run = (int32_t)(d >> 16);
                     Wd[k >> 1] |= ((uint32_t)d & 0xFFFFu) << (16 * (k & 1));
@@ -1610,7 +1623,7 @@ __global__ void rad_planes_kernel(BallsView X, int64_t rows, int64_t cols, int64
 // runs, decided on the device from the scan's nonzero counts mw[2] (A side)
 // and mw[3] (B side) with the host's rule (radius_compute): 0 sparse columns
 // of Q, 1 sparse rows of P, 2 dense.  Bit-identical results either way.
-APB_DEV int rad_variant(const long long* mw, int64_t M, int64_t K, int64_t N, int a_trans) {
+__host__ __device__ inline int rad_variant(const long long* mw, int64_t M, int64_t K, int64_t N, int a_trans) {
     const double dens_a = M * K ? (double)mw[2] / (double)(M * K) : 1.0;
     const double dens_b = K * N ? (double)mw[3] / (double)(K * N) : 1.0;
     if (a_trans && dens_b <= 0.25 && dens_b <= dens_a) return 0;
@@ -3076,6 +3089,7 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         return APB_ERR_CUDA;
     }
     int rc;
+    int raw_mode = 0;
     const int* d_group_d1 = (const int*)(dunits + off_d1);
     if (band) {
         BandGemmParams P;
@@ -3095,7 +3109,10 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         P.Tw = Tw;
         P.Tc = Tc;
         P.spec_maxw = spec_maxw;
-        P.raw = raw_epi ? 1 : 0;
+        // 40-bit band values when |D0 + 256 D1| <= 257 pairs K 2^14 stays below 2^39
+        static const bool no_v40 = std::getenv("APB_RAW32") != nullptr;  // test hook: two int32 planes
+        raw_mode = !raw_epi ? 0 : (!no_v40 && pairs * w <= 130560) ? 2 : 1;
+        P.raw = raw_mode;
         if (raw_epi && ksplit > 1) {
             P.n_bands = (ND + band_w - 1) / band_w;
             P.kb_per = (n_kb_all + ksplit - 1) / ksplit;
@@ -3166,7 +3183,7 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
     R.status = workspace().status_dev;
     R.quad = band ? 1 : 0;
     R.digit_bits = band ? 8 * band_w : 32;
-    R.raw = raw_epi ? 1 : 0;
+    R.raw = raw_mode;
     R.nsplit = ksplit;
     R.spec_maxw = spec_maxw;
     R.spec_sa = SA;
@@ -3611,7 +3628,9 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     };
     // speculative radius products (single radius block; sparse/dense chosen on the device)
     // `mid` (optional): a wait enqueued between the planes and the products
-    auto phaseR = [&](cudaStream_t ss, bool capturing, cudaEvent_t mid = nullptr, RadDefer* defer = nullptr) -> int {
+    // `which`: 1 sparse kernels, 2 dense kernels, 3 both (each stands down on the device unless picked)
+    auto phaseR = [&](cudaStream_t ss, bool capturing, cudaEvent_t mid = nullptr, RadDefer* defer = nullptr,
+                      int which = 3) -> int {
         const int tk = prof_begin("radius", ss);
         static const bool no_scan_planes = std::getenv("APB_NO_SCAN_PLANES") != nullptr;
         RadPair rp{M, K, N, da1, db1, da2, db2, ec1, fc1, ec2, fc2, r1b, r2b, r1f, r2f, mw1, mw2,
@@ -3622,7 +3641,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
             if (no_scan_planes)  // else the scan wrote uncentred planes (host redoes if flagged)
                 fused_planes2_kernel<<<(unsigned)(nA + blocks_for(K * N, 256)), 256, 0, ss>>>(av, bv, rp, nA);
             if (mid) cudaStreamWaitEvent(ss, mid, 0);
-            {  // highest priority: its blocks are dispatched ahead of the pack's
+            if (which & 1) {  // highest priority: its blocks are dispatched ahead of the pack's
                 static const int prio = [] {
                     int least = 0, greatest = 0;
                     cudaDeviceGetStreamPriorityRange(&least, &greatest);
@@ -3666,7 +3685,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
                     cudaLaunchKernelEx(&cfg, rad_sparse2_kernel<2, 256>, rp);
                 }
             }
-            {
+            if (which & 2) {
                 const dim3 g2(blocks_for(N, RT), blocks_for(M, RT), 2);
                 static const bool no_small = std::getenv("APB_RAD_NO_SMALL") != nullptr;  // test hook
                 if (!no_small && (int64_t)g2.x * g2.y * 2 < RAD_SMALL_TILES)
@@ -3676,7 +3695,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
             }
             prof_end(tk, ss);
             rec_event(ev_join, ss, capturing);
-            count_launch(no_scan_planes ? 3 : 2);
+            count_launch((no_scan_planes ? 1 : 0) + (which & 1) + ((which >> 1) & 1));
             return cuda_check(cudaGetLastError(), "radius");
         }
         fused_planes_kernel<<<blocks_for(M * K, 256), 256, 0, ss>>>(av, M, K, 1, ec1, ec2, da1, da2, nullptr, nullptr);
@@ -3770,7 +3789,14 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     // the speculative radius used the scan's uncentred planes: void if an operand
     // exponent was too far out (redo with centred planes, like a multi-block radius)
     static const bool no_scan_planes_h = std::getenv("APB_NO_SCAN_PLANES") != nullptr;
-    const bool rad_redo = rad_multi || (!no_scan_planes_h && hsum.rad_centred);
+    // which radius kernels the device picks for this call's operands (rad_variant on the host copy
+    // of the counts): the fused step's graph holds only those, so it is keyed on them too, and a
+    // replay whose graph lacks a kernel these operands need redoes the radius
+    static const bool rad_both = std::getenv("APB_RAD_BOTH") != nullptr;  // test hook: always launch both
+    const int rv1 = rad_variant(hw1, M, K, N, 1), rv2 = rad_variant(hw2, M, K, N, 0);
+    const int rad_which = rad_both ? 3 : ((rv1 == 0 || rv2 == 1) ? 1 : 0) | ((rv1 == 2 || rv2 == 2) ? 2 : 0);
+    const bool rad_missing = full_spec && k2_spec.size() > 2 && (rad_which & ~(int)k2_spec[2]) != 0;
+    const bool rad_redo = rad_multi || (!no_scan_planes_h && hsum.rad_centred) || rad_missing;
     const bool single = P.steps.size() == 3 && P.steps[0] == 0 && P.steps[1] == A->cols && P.steps[2] == 0;
     const bool prepacked =
         single && sncw && slices_for(P.maxw_a) <= 8 * sncw && slices_for(P.maxw_b) <= 8 * sncw;
@@ -3789,7 +3815,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         return cuda_check(cudaGetLastError(), "block matmul");
     };
     if (full_spec) {
-        const std::vector<int64_t> k2 = {slices_for(P.maxw_a), slices_for(P.maxw_b)};
+        const std::vector<int64_t> k2 = {slices_for(P.maxw_a), slices_for(P.maxw_b), rad_which};
         gs->k2s = k2;
         if (!rad_redo && prepacked && k2 == k2_spec) {  // the whole step already ran in G1S
             stats().int_gemm_products++;
@@ -3805,7 +3831,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         // continue below exactly as after G1 + GR (whose work G1S contains)
     }
     if (gs && spec && !rad_redo && prepacked) {  // the speculation held: G2
-        const std::vector<int64_t> k2 = {slices_for(P.maxw_a), slices_for(P.maxw_b)};
+        const std::vector<int64_t> k2 = {slices_for(P.maxw_a), slices_for(P.maxw_b), rad_which};
         auto it = gs->g2.find(k2);
         gs->k2s = k2;
         if (it != gs->g2.end() && !full_spec && !gs->g1s.count(k2) && !no_spec_step) {
@@ -3857,7 +3883,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
                     // net 193 -> 191 us; not the default
                     static const bool beside = std::getenv("APB_RAD_QUAD_BESIDE") != nullptr && rad_first;
                     RadDefer dfr;
-                    if ((r = phaseR(side, true, rad_first ? nullptr : ev_packed, beside ? &dfr : nullptr))) return r;
+                    if ((r = phaseR(side, true, rad_first ? nullptr : ev_packed, beside ? &dfr : nullptr, rad_which))) return r;
                     cudaEventRecord(ev_rdone, side);
                     if (rad_first) cudaStreamWaitEvent(cs, ev_rdone, 0);
                     RadFuse fz{r1b, r1f, r2b, r2f, ev_rdone, false, false};

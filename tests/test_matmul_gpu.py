@@ -85,7 +85,7 @@ def test_full_config_vs_reference(cfg):
                                   "APB_BAND_KBNORM=1", "APB_NO_SCAN_PLANES=1", "APB_RAD_MAIN=1",
                                   "APB_RAD_NO_SMALL=1", "APB_NO_RAW_EPI=1", "APB_RAD_QUAD=1", "APB_RAD_QUAD=1,APB_RAD_QUAD_BESIDE=1",
                                   "APB_BAND_BN=128,APB_NO_RAW_EPI=1", "APB_BAND_KSPLIT=2", "APB_BAND_BN=128,APB_BAND_KSPLIT=2",
-                                  "APB_BAND_BN=256,APB_BAND_KSPLIT=1"])
+                                  "APB_BAND_BN=256,APB_BAND_KSPLIT=1", "APB_RAW32=1", "APB_RAW32=1,APB_BAND_KSPLIT=2", "APB_RAD_BOTH=1"])
 def test_kernel_variants_golden(hook):
     """alternative kernels / schedules selected by the library's tuning hooks
     (unit GEMM used when a diagonal could overflow int32, byte-serial pack,
@@ -95,7 +95,7 @@ def test_kernel_variants_golden(hook):
     import sys
     env = dict(os.environ, **dict(kv.split("=") for kv in hook.split(",")))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-k",
-                        "test_matmul_golden_gpu or test_full_config_vs_reference or test_repeated_calls", os.path.abspath(__file__)],
+                        "test_matmul_golden_gpu or test_full_config_vs_reference or test_repeated_calls or test_graph_replay", os.path.abspath(__file__)],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:]
 
@@ -142,6 +142,31 @@ def test_graph_replay_tracks_new_inputs():
     got = ops.block_matmul_ball(A, B, p, out=out).balls.to_host()
     ref, _ = po.matmul(a2, b2, n, n, n, p, which="ref", algo=1, threads=os.cpu_count() or 8)
     assert got.identical(ref).all()
+
+
+def test_graph_replay_radius_variant_changes():
+    """same buffers and slice counts, but the radius density flips between calls: the fused
+    step's graph holds only the radius kernels of the last operands (sparse or dense), so a
+    replay whose operands need the other kind must redo the radius products"""
+    from paper_1901_04289_b200 import ops
+    n, p = 256, 128
+    rng = gen.rng_for(2, 123)
+    dense = [gen.random_balls(rng, n * n, p, e_lo=-4, e_hi=4, rad_k=130) for _ in range(2)]
+    sparse = [gen.random_balls(rng, n * n, p, e_lo=-4, e_hi=4, rad_k=130, rad_frac=0.04) for _ in range(2)]
+    refs = {}
+    for key, (a, b) in (("dense", dense), ("sparse", sparse)):
+        refs[key], _ = po.matmul(a, b, n, n, n, p, which="ref", algo=1, threads=os.cpu_count() or 8)
+    A, B = _mat(dense[0], n, n), _mat(dense[1], n, n)
+    out = ops.block_matmul_ball(A, B, p)
+    seq = ["dense"] * 4 + ["sparse"] * 4 + ["dense"] * 2 + ["sparse", "dense"]
+    for k, key in enumerate(seq):
+        a, b = dense if key == "dense" else sparse
+        for dst, src in ((A, a), (B, b)):
+            d = src.to_device()
+            for f in ("mant", "exp", "kind", "rad_man", "rad_exp"):
+                getattr(dst.balls, f).copy_(getattr(d, f))
+        got = ops.block_matmul_ball(A, B, p, out=out).balls.to_host()
+        assert got.identical(refs[key]).all(), f"call {k} ({key})"
 
 
 @pytest.mark.parametrize("path", MM, ids=[name(p) for p in MM])
