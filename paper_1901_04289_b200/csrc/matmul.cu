@@ -849,6 +849,7 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
     constexpr int NW = (ND + 1) / 2;   // 32-bit magnitude words
     constexpr int STR = NW + 3;        // smem row stride (odd for bank spread), 2 guard words
     __shared__ uint32_t sm[128 * STR];
+    griddep_wait();  // (launched as the band GEMM's programmatic dependent in the fused step)
     if (R.spec_maxw && ((int)((R.spec_maxw[0] + 9) / 8) != R.spec_sa || (int)((R.spec_maxw[1] + 9) / 8) != R.spec_sb))
         return;  // speculation void (the GEMM stood down too)
     uint32_t* row = sm + threadIdx.x * STR;
@@ -2855,6 +2856,7 @@ struct RadFuse {
     cudaEvent_t ready;
     bool capturing;
     bool used;  // out: the recombine took the radius (no rad_combine_kernel needed)
+    bool joined = false;  // the stream already waited for `ready` (before the GEMM): no second wait
 };
 void wait_event(cudaStream_t s, cudaEvent_t ev, bool capturing);
 
@@ -3199,20 +3201,29 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         if (fuse) {
             fuse->used = fast && band_w == 2 && NW <= 80 && !r64;  // recombine16 below
             if (fuse->used) {
-                wait_event(st, fuse->ready, fuse->capturing);
+                if (!fuse->joined) wait_event(st, fuse->ready, fuse->capturing);
                 R.r1b = fuse->r1b;
                 R.r1f = fuse->r1f;
                 R.r2b = fuse->r2b;
                 R.r2f = fuse->r2f;
             }
         }
+        // APB_RC_PDL=1: recombine16 as the raw-epilogue GEMM's programmatic dependent.  Measured at
+        // config 3: its blocks wait beside the GEMM CTAs from the GEMM's start and slow it from 91.5 to
+        // 97.4 us; the plain launch starts 0.1 us after the GEMM's end once no event wait sits between
+        // the two (RadFuse::joined), so it is the default
+        static const bool rc_pdl = std::getenv("APB_RC_PDL") && std::atoi(std::getenv("APB_RC_PDL")) == 1;
+        auto rc16_launch = [&](auto kern) {
+            if (rc_pdl && raw_mode && spec_maxw) launch_pdl(kern, dim3(gbq), dim3(128), 0, st, R);
+            else kern<<<gbq, 128, 0, st>>>(R);
+        };
         if (fast && band_w == 4 && NW <= 20) recombine_fast_kernel<20, 32><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 4 && NW <= 40) recombine_fast_kernel<40, 32><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 4 && NW <= 72) recombine_fast_kernel<72, 32><<<gbq, 128, 0, st>>>(R);
-        else if (fast && band_w == 2 && NW <= 40 && !r64 && ksplit > 1) recombine16_kernel<40, true><<<gbq, 128, 0, st>>>(R);
-        else if (fast && band_w == 2 && NW <= 80 && !r64 && ksplit > 1) recombine16_kernel<80, true><<<gbq, 128, 0, st>>>(R);
-        else if (fast && band_w == 2 && NW <= 40 && !r64) recombine16_kernel<40><<<gbq, 128, 0, st>>>(R);
-        else if (fast && band_w == 2 && NW <= 80 && !r64) recombine16_kernel<80><<<gbq, 128, 0, st>>>(R);
+        else if (fast && band_w == 2 && NW <= 40 && !r64 && ksplit > 1) rc16_launch(recombine16_kernel<40, true>);
+        else if (fast && band_w == 2 && NW <= 80 && !r64 && ksplit > 1) rc16_launch(recombine16_kernel<80, true>);
+        else if (fast && band_w == 2 && NW <= 40 && !r64) rc16_launch(recombine16_kernel<40>);
+        else if (fast && band_w == 2 && NW <= 80 && !r64) rc16_launch(recombine16_kernel<80>);
         else if (fast && band_w == 2 && NW <= 40) recombine_fast_kernel<40, 16><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 2 && NW <= 80) recombine_fast_kernel<80, 16><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 2 && NW <= 144) recombine_fast_kernel<144, 16><<<gbq, 128, 0, st>>>(R);
@@ -3887,6 +3898,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
                     cudaEventRecord(ev_rdone, side);
                     if (rad_first) cudaStreamWaitEvent(cs, ev_rdone, 0);
                     RadFuse fz{r1b, r1f, r2b, r2f, ev_rdone, false, false};
+                    fz.joined = rad_first;  // (the wait above; keeps the recombine right behind the GEMM)
                     const std::function<int()> rad_hook = [&]() -> int { return rad_quad_launch(dfr.rp, dfr.rl, cs, true); };
                     r = scaled_block(A, B, 0, K, prec, C, true, P.maxw_a, P.maxw_b, RW.top[0], RW.bot[0],
                                      CW.top[0], CW.bot[0], nullptr, 0, nullptr, nullptr, cs,

@@ -1,0 +1,8 @@
+timeout 600 python -m pytest tests/test_matmul_gpu.py -m gpu -x -q -k "golden or full_config or repeated or replay" > gpurun_out/gputests_mm.log 2>&1; tail -2 gpurun_out/gputests_mm.log
+timeout 120 python profiles/kineto_timeline.py c3 3 2>&1 | tail -9
+APB_RC_PDL=0 timeout 120 python profiles/kineto_timeline.py c3 3 2>&1 | grep -E "span|recombine|band3"
+timeout 300 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.log 2> gpurun_out/bench.err; python - <<'P'
+import json
+d=json.loads(open('gpurun_out/bench.log').read().strip().splitlines()[-1])
+print(d['ms_per_step'], d['roofline']['kernel_ms'], d['roofline']['frac'], d['e2e']['ms_per_step'], d['also']['c2']['ms_per_step'], d['also']['c2']['roofline']['kernel_ms'], d['also']['c4']['ms_per_step'], d['also']['c4']['roofline']['frac'])
+P
