@@ -500,7 +500,10 @@ struct PackAB {
 };
 
 template <int NCW>
-__global__ void __launch_bounds__(256) pack_ab_v2_kernel(PackAB P) {
+#ifndef APB_PACK_MINB
+#define APB_PACK_MINB 1
+#endif
+__global__ void __launch_bounds__(256, APB_PACK_MINB) pack_ab_v2_kernel(PackAB P) {
     griddep_wait();
     // the B blocks (4 entries per thread + a shared-memory transpose) are the long
     // ones: they take the low block indices so they are dispatched first
@@ -1360,7 +1363,10 @@ constexpr int SCAN_B_ROWS = 32;   // rows per B block: 32 columns x 8 warps x 4 
 
 // blocks [0, nbA): A rows; [nbA, nbA + nbB): B column tiles.  Partials land in
 // pa[f][c][i] (A, cA chunks per row) and pb[f][c][j] (B, cB chunks per column).
-__global__ void __launch_bounds__(256) scan_v2_kernel(BallsView A, BallsView B, int64_t M, int64_t K, int64_t N,
+#ifndef APB_SCAN_MINB
+#define APB_SCAN_MINB 1
+#endif
+__global__ void __launch_bounds__(256, APB_SCAN_MINB) scan_v2_kernel(BallsView A, BallsView B, int64_t M, int64_t K, int64_t N,
                                                       int cA, int cB, int64_t* pa, int64_t* pb, ScanSummary* sum,
                                                       long long* mw1, long long* mw2, double* da1T = nullptr,
                                                       double* da2 = nullptr, double* db1 = nullptr,
@@ -2982,9 +2988,19 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         for (int64_t c : it) *std::min_element(load.begin(), load.end()) += c;
         return *std::max_element(load.begin(), load.end());
     };
-    if (raw_epi) {
-        static const int bn_env = std::getenv("APB_BAND_BN") ? std::atoi(std::getenv("APB_BAND_BN")) : 0;
-        static const int ks_env = std::getenv("APB_BAND_KSPLIT") ? std::atoi(std::getenv("APB_BAND_KSPLIT")) : 0;
+    static const int bn_env = std::getenv("APB_BAND_BN") ? std::atoi(std::getenv("APB_BAND_BN")) : 0;
+    static const int ks_env = std::getenv("APB_BAND_KSPLIT") ? std::atoi(std::getenv("APB_BAND_KSPLIT")) : 0;
+    // (the model only matters while the 256-wide items are few; its answer is cached per shape)
+    static std::map<std::vector<int64_t>, std::pair<int, int>> shape_cache;
+    const std::vector<int64_t> shape_key = {SA, SB, Mp, Np, Kp};
+    const bool many_items = Np % 256 == 0 && (int64_t)(Mp / kSliceTile) * (Np / 256) * ((ND + 1) / 2) >= 4 * 148;
+    auto cached = shape_cache.find(shape_key);
+    if (raw_epi && many_items && !bn_env && !ks_env) {
+        bn = 256;
+    } else if (raw_epi && cached != shape_cache.end()) {
+        bn = cached->second.first;
+        ksplit = cached->second.second;
+    } else if (raw_epi) {
         int64_t best = INT64_MAX;
         for (int tn : {256, 128}) {
             if (Np % tn || (bn_env && tn != bn_env)) continue;
@@ -3000,6 +3016,8 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
                 }
             }
         }
+        if (shape_cache.size() > 1024) shape_cache.clear();
+        shape_cache[shape_key] = {bn, ksplit};
     }
     const int tiles = (Mp / kSliceTile) * (Np / bn);
     // work tables depend only on (band, S_A, S_B, w, tile grid): built once on the
@@ -3640,6 +3658,14 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     // speculative radius products (single radius block; sparse/dense chosen on the device)
     // `mid` (optional): a wait enqueued between the planes and the products
     // `which`: 1 sparse kernels, 2 dense kernels, 3 both (each stands down on the device unless picked)
+    // centred planes in the speculative radius branch: when the previous product's operand
+    // exponents were too far out for the scan's uncentred planes (config 4: radii near 2^-531),
+    // this one most likely needs them too, so fused_planes2_kernel joins the branch (it stands
+    // down on the device when the planes are fine) and the products are right the first time --
+    // otherwise they would run on invalid planes and the host would redo the radius after the
+    // midpoint product (at config 4: 0.45 ms wasted + 0.68 ms redone per real product)
+    static bool want_planes = false;  // (under the API lock)
+    const bool planes_used = want_planes;
     auto phaseR = [&](cudaStream_t ss, bool capturing, cudaEvent_t mid = nullptr, RadDefer* defer = nullptr,
                       int which = 3) -> int {
         const int tk = prof_begin("radius", ss);
@@ -3649,7 +3675,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         static const bool split = std::getenv("APB_RAD_SPLIT") != nullptr;  // previous 6-launch schedule
         if (!split) {
             const int64_t nA = blocks_for(M * K, 256);
-            if (no_scan_planes)  // else the scan wrote uncentred planes (host redoes if flagged)
+            if (no_scan_planes || planes_used)  // else the scan wrote uncentred planes (host redoes if flagged)
                 fused_planes2_kernel<<<(unsigned)(nA + blocks_for(K * N, 256)), 256, 0, ss>>>(av, bv, rp, nA);
             if (mid) cudaStreamWaitEvent(ss, mid, 0);
             if (which & 1) {  // highest priority: its blocks are dispatched ahead of the pack's
@@ -3706,7 +3732,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
             }
             prof_end(tk, ss);
             rec_event(ev_join, ss, capturing);
-            count_launch((no_scan_planes ? 1 : 0) + (which & 1) + ((which >> 1) & 1));
+            count_launch(((no_scan_planes || planes_used) ? 1 : 0) + (which & 1) + ((which >> 1) & 1));
             return cuda_check(cudaGetLastError(), "radius");
         }
         fused_planes_kernel<<<blocks_for(M * K, 256), 256, 0, ss>>>(av, M, K, 1, ec1, ec2, da1, da2, nullptr, nullptr);
@@ -3739,7 +3765,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     std::vector<int64_t> key;
     if (use_graphs) {
         const apb_balls* bs[3] = {&A->b, &B->b, &C->b};
-        key = {M, K, N, prec, sncw, (int64_t)scratch().gen};
+        key = {M, K, N, prec, sncw, (int64_t)scratch().gen, planes_used ? 1 : 0};
         for (const apb_balls* x : bs)
             key.insert(key.end(), {(int64_t)x->mant, (int64_t)x->exp, (int64_t)x->kind, (int64_t)x->rad_man,
                                    (int64_t)x->rad_exp, (int64_t)x->L});
@@ -3807,7 +3833,8 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     const int rv1 = rad_variant(hw1, M, K, N, 1), rv2 = rad_variant(hw2, M, K, N, 0);
     const int rad_which = rad_both ? 3 : ((rv1 == 0 || rv2 == 1) ? 1 : 0) | ((rv1 == 2 || rv2 == 2) ? 2 : 0);
     const bool rad_missing = full_spec && k2_spec.size() > 2 && (rad_which & ~(int)k2_spec[2]) != 0;
-    const bool rad_redo = rad_multi || (!no_scan_planes_h && hsum.rad_centred) || rad_missing;
+    const bool rad_redo = rad_multi || (!no_scan_planes_h && !planes_used && hsum.rad_centred) || rad_missing;
+    want_planes = hsum.rad_centred != 0 && !rad_multi;
     const bool single = P.steps.size() == 3 && P.steps[0] == 0 && P.steps[1] == A->cols && P.steps[2] == 0;
     const bool prepacked =
         single && sncw && slices_for(P.maxw_a) <= 8 * sncw && slices_for(P.maxw_b) <= 8 * sncw;

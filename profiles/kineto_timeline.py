@@ -23,20 +23,29 @@ elif which == "c2":
     a, b = gen.config2_matrices()
     n, p = 256, 128
 else:
-    a, b = gen.config4_matrices(n=1024)
+    parts = gen.config4_matrices(n=1024)
     n, p = 1024, 512
-A, B = ops.BallMatrix(a.to_device(), n, n), ops.BallMatrix(b.to_device(), n, n)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-out = ops.block_matmul_ball(A, B, p)
+if which == "c4":  # complex product: four real block products + ball_sub / ball_add
+    Ms = [ops.BallMatrix(x.to_device(), n, n) for x in parts]
+
+    def step():
+        ops.complex_matmul_ball(*Ms, p)
+else:
+    A, B = ops.BallMatrix(a.to_device(), n, n), ops.BallMatrix(b.to_device(), n, n)
+    out = ops.block_matmul_ball(A, B, p)
+
+    def step():
+        ops.block_matmul_ball(A, B, p, out=out)
 for _ in range(3):
-    ops.block_matmul_ball(A, B, p, out=out)
+    step()
 torch.cuda.synchronize()
 marks = []
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
     for s in range(steps):
         flush.zero_()
         torch.cuda.synchronize()
-        ops.block_matmul_ball(A, B, p, out=out)
+        step()
         torch.cuda.synchronize()
 path = os.path.join(tempfile.gettempdir(), "apb_trace.json")
 prof.export_chrome_trace(path)

@@ -144,6 +144,24 @@ def test_graph_replay_tracks_new_inputs():
     assert got.identical(ref).all()
 
 
+def test_repeated_calls_centred_radius_planes():
+    """config-4-like radii (2^-515 |m|: beyond the range of the scan's uncentred planes): the first
+    call redoes the radius with centred planes, later calls run the centred planes inside the
+    speculative branch; a product whose planes are in range follows; all bit-identical"""
+    from paper_1901_04289_b200 import ops
+    n, p = 192, 512
+    rng = gen.rng_for(4, 77)
+    far = [gen.random_balls(rng, n * n, p, e_lo=-16, e_hi=16, rad_k=515) for _ in range(2)]
+    near = [gen.random_balls(rng, n * n, p, e_lo=-16, e_hi=16, rad_k=300) for _ in range(2)]
+    refs = {}
+    for key, (a, b) in (("far", far), ("near", near)):
+        refs[key], _ = po.matmul(a, b, n, n, n, p, which="ref", algo=1, threads=os.cpu_count() or 8)
+    for k, key in enumerate(["far", "far", "far", "near", "near", "far"]):
+        a, b = far if key == "far" else near
+        got = ops.block_matmul_ball(_mat(a, n, n), _mat(b, n, n), p).balls.to_host()
+        assert got.identical(refs[key]).all(), f"call {k} ({key})"
+
+
 def test_graph_replay_radius_variant_changes():
     """same buffers and slice counts, but the radius density flips between calls: the fused
     step's graph holds only the radius kernels of the last operands (sparse or dense), so a
