@@ -2850,7 +2850,7 @@ BandGeom band_geom(int64_t M, int64_t N, int64_t w) {
 }
 
 // digit-word template (2, 5 or 8 words) of the byte-parallel pack for S slices; 0 = byte-serial
-inline int pack_ncw(int S) { return S <= 16 ? 2 : S <= 40 ? 5 : S <= 64 ? 8 : 0; }
+inline int pack_ncw(int S) { return S <= 16 ? 2 : S <= 40 ? 5 : S <= 64 ? 8 : S <= 72 ? 9 : 0; }
 
 // radius products to fold into the recombine (single block): the recombine waits
 // for `ready` (recorded by the radius stream) and stores C.rad = err (+) (r1 (+) r2)
@@ -2924,12 +2924,14 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         if (ca >= 1 && ca <= 2) pack_a_v2_kernel<2><<<ga, 256, 0, st>>>(a, M, K, lo, hi, rtop, rbot, SA, Mp, Kp, Ap, esc);
         else if (ca >= 3 && ca <= 5) pack_a_v2_kernel<5><<<ga, 256, 0, st>>>(a, M, K, lo, hi, rtop, rbot, SA, Mp, Kp, Ap, esc);
         else if (ca >= 6 && ca <= 8) pack_a_v2_kernel<8><<<ga, 256, 0, st>>>(a, M, K, lo, hi, rtop, rbot, SA, Mp, Kp, Ap, esc);
+        else if (ca == 9) pack_a_v2_kernel<9><<<ga, 256, 0, st>>>(a, M, K, lo, hi, rtop, rbot, SA, Mp, Kp, Ap, esc);  // (config 4: 69 slices)
         else pack_kernel<false><<<blocks_for((int64_t)Mp * Kp / 4, 256), 256, 0, st>>>(a, M, K, lo, hi, rtop, rbot, SA, Mp, Kp, Ap, esc);
         dim3 gb((unsigned)(Np / 32), (unsigned)(Kp / 32));
         const int cb = v1 ? 0 : (SB + 7) / 8;
         if (cb >= 1 && cb <= 2) pack_b_v2_kernel<2><<<gb, 256, 0, st>>>(b, N, lo, hi, ctop, cbot, SB, Np, Kp, Bp, fsc);
         else if (cb >= 3 && cb <= 5) pack_b_v2_kernel<5><<<gb, 256, 0, st>>>(b, N, lo, hi, ctop, cbot, SB, Np, Kp, Bp, fsc);
         else if (cb >= 6 && cb <= 8) pack_b_v2_kernel<8><<<gb, 256, 0, st>>>(b, N, lo, hi, ctop, cbot, SB, Np, Kp, Bp, fsc);
+        else if (cb == 9) pack_b_v2_kernel<9><<<gb, 256, 0, st>>>(b, N, lo, hi, ctop, cbot, SB, Np, Kp, Bp, fsc);
         else pack_b_tiled_kernel<<<gb, 256, 0, st>>>(b, N, lo, hi, ctop, cbot, SB, Np, Kp, Bp, fsc);
     }
     prof_end(tok, st);
@@ -3647,6 +3649,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
             };
             if (sncw == 2) lp(pack_ab_v2_kernel<2>);
             else if (sncw == 5) lp(pack_ab_v2_kernel<5>);
+            else if (sncw == 9) lp(pack_ab_v2_kernel<9>);
             else lp(pack_ab_v2_kernel<8>);
             prof_end(tk, s);
             count_launch(1);

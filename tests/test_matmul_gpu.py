@@ -160,6 +160,14 @@ def test_repeated_calls_centred_radius_planes():
         a, b = far if key == "far" else near
         got = ops.block_matmul_ball(_mat(a, n, n), _mat(b, n, n), p).balls.to_host()
         assert got.identical(refs[key]).all(), f"call {k} ({key})"
+    # the same buffers again and again: 69 slices take the 72-slice pack template, the speculative
+    # pack and the captured graphs (with the centred planes inside the radius branch)
+    A, B = _mat(far[0], n, n), _mat(far[1], n, n)
+    out = ops.block_matmul_ball(A, B, p)
+    assert ops.matmul_stats()["last_slices_a"] > 64
+    for k in range(4):
+        got = ops.block_matmul_ball(A, B, p, out=out).balls.to_host()
+        assert got.identical(refs["far"]).all(), f"replay {k}"
 
 
 def test_graph_replay_radius_variant_changes():
