@@ -2512,7 +2512,10 @@ APB_DEV void rad_gemm2_body(const RadPair& P) {
 __global__ void __launch_bounds__(64, APB_RADG_MINB) rad_gemm2_kernel(RadPair P) { rad_gemm2_body<4>(P); }
 // small products (fewer 32 x 32 tiles than ~4 per SM): 2 x 2 outputs per thread,
 // 4x the warps for the same tiles (c2: rad products 73 us at ~2 warps per SM)
-__global__ void __launch_bounds__(256, 2) rad_gemm2s_kernel(RadPair P) { rad_gemm2_body<2>(P); }
+// (88 registers: two of its warps fit on each SM sub-partition beside the 3 x 112-register warps of a
+// raw-epilogue band-GEMM CTA, and its 30 KB of shared memory in what that CTA leaves, so on small
+// products the dense radius runs next to the GEMM instead of in front of it)
+__global__ void __maxnreg__(88) rad_gemm2s_kernel(RadPair P) { rad_gemm2_body<2>(P); }
 // tiles of both dense products below which the 2 x 2 variant runs
 constexpr int64_t RAD_SMALL_TILES = 4 * 148;
 
@@ -3926,9 +3929,16 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
                     RadDefer dfr;
                     if ((r = phaseR(side, true, rad_first ? nullptr : ev_packed, beside ? &dfr : nullptr, rad_which))) return r;
                     cudaEventRecord(ev_rdone, side);
-                    if (rad_first) cudaStreamWaitEvent(cs, ev_rdone, 0);
+                    // small dense radius products (rad_gemm2s: config 2) fit beside the GEMM's CTAs
+                    // and take longer than the GEMM: the GEMM does not wait for them, the recombine does
+                    static const bool no_rad_along = std::getenv("APB_NO_RAD_ALONG") != nullptr;  // test hook
+                    const dim3 rg2(blocks_for(N, RT), blocks_for(M, RT), 2);
+                    const bool rad_along = !no_rad_along && rad_which == 2 && !std::getenv("APB_RAD_NO_SMALL") &&
+                                           (int64_t)rg2.x * rg2.y * 2 < RAD_SMALL_TILES && !planes_used;
+                    const bool join_first = rad_first && !rad_along;
+                    if (join_first) cudaStreamWaitEvent(cs, ev_rdone, 0);
                     RadFuse fz{r1b, r1f, r2b, r2f, ev_rdone, false, false};
-                    fz.joined = rad_first;  // (the wait above; keeps the recombine right behind the GEMM)
+                    fz.joined = join_first;  // (the wait above; keeps the recombine right behind the GEMM)
                     const std::function<int()> rad_hook = [&]() -> int { return rad_quad_launch(dfr.rp, dfr.rl, cs, true); };
                     r = scaled_block(A, B, 0, K, prec, C, true, P.maxw_a, P.maxw_b, RW.top[0], RW.bot[0],
                                      CW.top[0], CW.bot[0], nullptr, 0, nullptr, nullptr, cs,
