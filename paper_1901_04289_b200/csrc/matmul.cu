@@ -1639,6 +1639,10 @@ __host__ __device__ inline int rad_variant(const long long* mw, int64_t M, int64
 }
 
 constexpr int RT = 32, RK = 32, RTHREADS = 64;
+#ifndef APB_RADG_UNROLL
+#define APB_RADG_UNROLL 4
+#endif
+constexpr int RADG_UNROLL = APB_RADG_UNROLL;  // k steps of a full tile unrolled together
 static_assert(RT == RK, "the transposed A-tile fetch of rad_gemm_body maps k and row indices through RT");
 // PT x PT outputs per thread: PT = 4 (64 threads per 32 x 32 tile) for large
 // products, PT = 2 (256 threads) when the grid is too small to fill the SMs with
@@ -1731,7 +1735,7 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
         __syncthreads();
         if (l0 + RK < w) fetch(l0 + RK);
         const int kmax = (w - l0) < RK ? (int)(w - l0) : RK;
-        for (int kk = 0; kk < kmax; kk++) {
+        auto kstep = [&](int kk) {
             double a[PT], b[PT];
 #pragma unroll
             for (int h = 0; h < PT; h += 2) {
@@ -1746,6 +1750,12 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
             for (int r = 0; r < PT; r++)
 #pragma unroll
                 for (int c = 0; c < PT; c++) s[r][c] = __dadd_rn(s[r][c], __dmul_rn(a[r], b[c]));
+        };
+        if (kmax == RK) {  // full tile: unrolled so the shared loads of later steps are issued early
+#pragma unroll RADG_UNROLL
+            for (int kk = 0; kk < RK; kk++) kstep(kk);
+        } else {
+            for (int kk = 0; kk < kmax; kk++) kstep(kk);
         }
         const int64_t l = l0 + kmax;  // RK divides 1024: chunk ends fall on tile ends
         if ((l & 1023) == 0 || l == w) {
