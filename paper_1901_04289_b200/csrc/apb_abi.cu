@@ -353,6 +353,16 @@ struct DevBalls {
 };
 
 // copy a host ball array into workspace slots [slot0, slot0+5)
+// the five SoA arrays of a ball array, one asynchronous copy each
+int copy_arrays(const apb_balls* dst, const apb_balls* src, cudaMemcpyKind kind, cudaStream_t st) {
+    const size_t cnt = (size_t)src->count;
+    void* dsts[5] = {dst->mant, dst->exp, dst->kind, dst->rad_man, dst->rad_exp};
+    void* srcs[5] = {src->mant, src->exp, src->kind, src->rad_man, src->rad_exp};
+    size_t sizes[5] = {cnt * src->L * 8, cnt * 8, cnt, cnt * 4, cnt * 8};
+    for (int f = 0; f < 5; f++) cudaMemcpyAsync(dsts[f], srcs[f], sizes[f], kind, st);
+    return 0;
+}
+
 int to_device(const apb_balls* h, apb_balls* d, int slot0, cudaStream_t st, bool copy) {
     Workspace& ws = workspace();
     const size_t cnt = (size_t)h->count;
@@ -368,23 +378,13 @@ int to_device(const apb_balls* h, apb_balls* d, int slot0, cudaStream_t st, bool
         return APB_ERR_CUDA;
     }
     if (!copy || cnt == 0) return APB_OK;
-    cudaMemcpyAsync(d->mant, h->mant, cnt * h->L * 8, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(d->exp, h->exp, cnt * 8, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(d->kind, h->kind, cnt, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(d->rad_man, h->rad_man, cnt * 4, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(d->rad_exp, h->rad_exp, cnt * 8, cudaMemcpyHostToDevice, st);
-    return cuda_check(cudaGetLastError(), "h2d");
+    return copy_arrays(d, h, cudaMemcpyHostToDevice, st) ? APB_ERR_CUDA : cuda_check(cudaGetLastError(), "h2d");
 }
 
 int to_host(const apb_balls* d, apb_balls* h, cudaStream_t st) {
     const size_t cnt = (size_t)h->count;
     if (cnt == 0) return APB_OK;
-    cudaMemcpyAsync(h->mant, d->mant, cnt * h->L * 8, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(h->exp, d->exp, cnt * 8, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(h->kind, d->kind, cnt, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(h->rad_man, d->rad_man, cnt * 4, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(h->rad_exp, d->rad_exp, cnt * 8, cudaMemcpyDeviceToHost, st);
-    return cuda_check(cudaGetLastError(), "d2h");
+    return copy_arrays(h, d, cudaMemcpyDeviceToHost, st) ? APB_ERR_CUDA : cuda_check(cudaGetLastError(), "d2h");
 }
 
 cudaStream_t host_stream() {
