@@ -500,10 +500,11 @@ struct PackAB {
 };
 
 template <int NCW>
-#ifndef APB_PACK_MINB
-#define APB_PACK_MINB 1
-#endif
+#ifdef APB_PACK_MINB  // occupancy experiments (5 / 6 blocks per SM measured no faster: profiles/r2/README.md)
 __global__ void __launch_bounds__(256, APB_PACK_MINB) pack_ab_v2_kernel(PackAB P) {
+#else
+__global__ void __launch_bounds__(256) pack_ab_v2_kernel(PackAB P) {
+#endif
     griddep_wait();
     // the B blocks (4 entries per thread + a shared-memory transpose) are the long
     // ones: they take the low block indices so they are dispatched first
@@ -1363,10 +1364,11 @@ constexpr int SCAN_B_ROWS = 32;   // rows per B block: 32 columns x 8 warps x 4 
 
 // blocks [0, nbA): A rows; [nbA, nbA + nbB): B column tiles.  Partials land in
 // pa[f][c][i] (A, cA chunks per row) and pb[f][c][j] (B, cB chunks per column).
-#ifndef APB_SCAN_MINB
-#define APB_SCAN_MINB 1
-#endif
+#ifdef APB_SCAN_MINB  // occupancy experiments (6 blocks per SM: 16.7 -> 15.7 us at config 3, not adopted)
 __global__ void __launch_bounds__(256, APB_SCAN_MINB) scan_v2_kernel(BallsView A, BallsView B, int64_t M, int64_t K, int64_t N,
+#else
+__global__ void __launch_bounds__(256) scan_v2_kernel(BallsView A, BallsView B, int64_t M, int64_t K, int64_t N,
+#endif
                                                       int cA, int cB, int64_t* pa, int64_t* pb, ScanSummary* sum,
                                                       long long* mw1, long long* mw2, double* da1T = nullptr,
                                                       double* da2 = nullptr, double* db1 = nullptr,
