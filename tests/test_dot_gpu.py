@@ -97,6 +97,32 @@ def test_edge_random_vs_reference():
             assert ok.all(), (n, p, np.nonzero(~ok)[0][:5])
 
 
+def test_term_counts_just_past_a_multiple_of_32():
+    """dots of 32 k + (1..4) terms (config 1 has 100 = 96 + 4: the last register slot of the register
+    kernel is mostly padding): batches that are no multiple of 8, edge values (zeros, specials ->
+    Fallback, radii), window sizes 2 and 3, subtract, state / accumulator outputs"""
+    from paper_1901_04289_b200 import ops
+    rng = np.random.Generator(np.random.PCG64(4242))
+    for n in (33, 34, 36, 65, 67, 68, 97, 98, 100):
+        for p, batch in ((64, 70), (128, 203), (129, 64), (53, 97)):
+            x, y = gen.edge_dots(rng, batch, n, max_limbs=2, spread=40 if p > 64 else 6)
+            sub = bool(rng.integers(0, 2))
+            got = ops.dot_batch(x.to_device(), y.to_device(), n, batch, p, subtract=sub).to_host()
+            ref = po.dot_batch(x, y, n, batch, p, which="ref", subtract=sub)
+            ok = got.identical(ref)
+            assert ok.all(), (n, p, batch, np.nonzero(~ok)[0][:5])
+    # config-1 distributions at full length, accumulator limbs and plan checked against the reference
+    x, y = gen.config1_dots(batch=1000)
+    got, st, acc = ops.dot_batch(x.to_device(), y.to_device(), 100, 1000, 128, want_state=True, acc_stride=3)
+    ref = po.dot_batch(x, y, 100, 1000, 128, which="ref")
+    rst, racc = po.dot_state(x, y, 100, 1000, 128, which="ref", acc_stride=3)
+    assert got.to_host().identical(ref).all()
+    for f in ("status", "e_max", "e_rad", "n_nonzero", "p_eff", "n_s", "e_s", "err"):
+        np.testing.assert_array_equal(st[f], rst[f], err_msg=f)
+    proceed = rst["status"] == 0
+    np.testing.assert_array_equal(np.asarray(acc).reshape(1000, 3)[proceed], racc[proceed])
+
+
 def test_host_entry_matches_device_entry():
     from paper_1901_04289_b200 import ops
     x, y = gen.config1_dots(batch=512)
