@@ -379,13 +379,28 @@ APB_DEV void digit_words(const BallsView& X, int64_t e, bool valid, int64_t scal
     }
 }
 
+// window (top, bottom) of line `line` from the scan's chunk partials P[f][c][line]
+APB_DEV void partial_window(const int64_t* P, int nc, int64_t nlines, int64_t line, int64_t& top, int64_t& bot) {
+    top = INT64_MIN;
+    bot = INT64_MAX;
+    const int64_t stride = (int64_t)nc * nlines;
+    for (int c = 0; c < nc; c++) {
+        const int64_t t = P[(int64_t)c * nlines + line], b = P[stride + (int64_t)c * nlines + line];
+        top = t > top ? t : top;
+        bot = b < bot ? b : bot;
+    }
+}
+
 // A side: thread per entry (row r, inner kk), plane[s][r][kk] byte stores --
 // a warp writes one 32-byte segment per plane
 template <int NCW>
 APB_DEV void pack_a_v2_body(const BallsView& X, int64_t rows, int64_t ld, int64_t lo, int64_t hi,
                             const int64_t* top, const int64_t* bot, int S, int Rp, int Kp, int8_t* out,
-                            int64_t* scale_out, const long long* maxw_dev, int64_t blk) {
-    if (maxw_dev) {  // speculative launch: slice count from the scan, before the host knows it
+                            int64_t* scale_out, const long long* maxw_dev, int64_t blk,
+                            const int64_t* part = nullptr, int nc = 0) {
+    if (part) {  // early pack: all template planes
+        S = 8 * NCW;
+    } else if (maxw_dev) {  // speculative launch: slice count from the scan, before the host knows it
         S = (int)((*maxw_dev + 2 + 7) / 8);
         if (S > 8 * NCW) return;
     }
@@ -393,7 +408,11 @@ APB_DEV void pack_a_v2_body(const BallsView& X, int64_t rows, int64_t ld, int64_
     if (t >= (int64_t)Rp * Kp) return;
     const int64_t r = t / Kp, kk = t % Kp;
     int64_t sc = 0;
-    if (r < rows) sc = top[r] == INT64_MIN ? 0 : -bot[r];
+    if (r < rows && part) {
+        int64_t tp, bt;
+        partial_window(part, nc, rows, r, tp, bt);
+        sc = tp == INT64_MIN ? 0 : -bt;
+    } else if (r < rows) sc = top[r] == INT64_MIN ? 0 : -bot[r];
     if (r < rows && kk == 0) scale_out[r] = sc;
     const bool valid = r < rows && kk < hi - lo;
     uint64_t d[NCW];
@@ -421,8 +440,11 @@ __global__ void __launch_bounds__(256) pack_a_v2_kernel(BallsView X, int64_t row
 template <int NCW>
 APB_DEV void pack_b_v2_body(const BallsView& X, int64_t N, int64_t lo, int64_t hi, const int64_t* top,
                             const int64_t* bot, int S, int Np, int Kp, int8_t* out, int64_t* scale_out,
-                            const long long* maxw_dev, int64_t bx, int64_t by) {
-    if (maxw_dev) {
+                            const long long* maxw_dev, int64_t bx, int64_t by, const int64_t* part = nullptr,
+                            int nc = 0) {
+    if (part) {
+        S = 8 * NCW;
+    } else if (maxw_dev) {
         S = (int)((*maxw_dev + 2 + 7) / 8);
         if (S > 8 * NCW) return;
     }
@@ -431,7 +453,11 @@ APB_DEV void pack_b_v2_body(const BallsView& X, int64_t N, int64_t lo, int64_t h
     const int64_t j = bx * 32 + jl;
     const int64_t kk0 = by * 32 + 4 * kq;
     int64_t sc = 0;
-    if (j < N) sc = top[j] == INT64_MIN ? 0 : -bot[j];
+    if (j < N && part) {
+        int64_t tp, bt;
+        partial_window(part, nc, N, j, tp, bt);
+        sc = tp == INT64_MIN ? 0 : -bt;
+    } else if (j < N) sc = top[j] == INT64_MIN ? 0 : -bot[j];
     if (j < N && by == 0 && kq == 0) scale_out[j] = sc;
     uint64_t d[4][NCW];
 #pragma unroll
@@ -497,7 +523,13 @@ struct PackAB {
     int64_t *esc, *fsc;
     const long long *mwa, *mwb;
     int64_t ga, gbx;
+    // early pack (right after the scan, beside the finish kernel): the line windows come from the
+    // scan's chunk partials (fields 0 / 1 = top / bottom, cA chunks per row, cB per column) and
+    // every template plane is written (the slice counts are the finish kernel's to know)
+    const int64_t *pa = nullptr, *pb = nullptr;
+    int cA = 0, cB = 0;
 };
+
 
 template <int NCW>
 #ifdef APB_PACK_MINB  // occupancy experiments (5 / 6 blocks per SM measured no faster: profiles/r2/README.md)
@@ -512,10 +544,10 @@ __global__ void __launch_bounds__(256) pack_ab_v2_kernel(PackAB P) {
     if ((int64_t)blockIdx.x < nb) {
         const int64_t bb = blockIdx.x;
         pack_b_v2_body<NCW>(P.b, P.N, 0, P.K, P.ctop, P.cbot, 0, P.Np, P.Kp, P.Bp, P.fsc, P.mwb, bb % P.gbx,
-                            bb / P.gbx);
+                            bb / P.gbx, P.pb, P.cB);
     } else {
         pack_a_v2_body<NCW>(P.a, P.M, P.K, 0, P.K, P.rtop, P.rbot, 0, P.Mp, P.Kp, P.Ap, P.esc, P.mwa,
-                            (int64_t)blockIdx.x - nb);
+                            (int64_t)blockIdx.x - nb, P.pa, P.cA);
     }
 }
 
@@ -847,7 +879,9 @@ __global__ void __launch_bounds__(128) recombine_fast_kernel(RecombineArgs R) {
 // shared memory (one padded row per thread) so the p-bit output window and
 // the truncation error are read with dynamic word indices instead of select
 // chains.  Same results as recombine_fast_kernel<*, 16>.
-template <int NBC, bool SPLIT = false>
+// V40: the planes are the 40-bit raw format (R.raw == 2): only the word and byte pointers are
+// stepped (the three per-band 64-bit pointer steps were 23% of the kernel's instructions)
+template <int NBC, bool SPLIT = false, bool V40 = false>
 __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
     constexpr int ND = NBC + 2;        // base-2^16 digits (band b: word digit b, carry digit b+1)
     constexpr int NW = (ND + 1) / 2;   // 32-bit magnitude words
@@ -879,7 +913,7 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
     const int32_t* pc = R.Tc + off;
     const uint32_t* pw2 = pw + (size_t)NB * plane;  // SPLIT: planes of the second K split
     const int32_t* pc2 = pc + (size_t)NB * plane;
-    const bool v40 = R.raw == 2;  // Tc is a byte plane: bits 32..39 of the band values
+    constexpr bool v40 = V40;  // Tc is a byte plane: bits 32..39 of the band values
     const int8_t* pb = (const int8_t*)R.Tc + off;
     const int8_t* pb2 = pb + (size_t)NB * plane;
 #pragma unroll
@@ -894,8 +928,8 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
             c[v] = !live ? 0 : v40 ? (int32_t)(int8_t)__ldcs(pb) : __ldcs(pc);
             if (b < NBC) {
                 pw += plane;
-                pc += plane;
-                pb += plane;
+                if (v40) pb += plane;
+                else pc += plane;
             }
         }
         if (SPLIT) {  // raw mode with K split in two: the second split's accumulators, loaded in the
@@ -910,8 +944,8 @@ __global__ void __launch_bounds__(128) recombine16_kernel(RecombineArgs R) {
                 c2[v] = !live ? 0 : v40 ? (int32_t)(int8_t)__ldcs(pb2) : __ldcs(pc2);
                 if (b < NBC) {
                     pw2 += plane;
-                    pc2 += plane;
-                    pb2 += plane;
+                    if (v40) pb2 += plane;
+                    else pc2 += plane;
                 }
             }
 #pragma unroll
@@ -3255,8 +3289,12 @@ int scaled_block(const apb_mat* A, const apb_mat* B, int64_t lo, int64_t hi, int
         if (fast && band_w == 4 && NW <= 20) recombine_fast_kernel<20, 32><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 4 && NW <= 40) recombine_fast_kernel<40, 32><<<gbq, 128, 0, st>>>(R);
         else if (fast && band_w == 4 && NW <= 72) recombine_fast_kernel<72, 32><<<gbq, 128, 0, st>>>(R);
+        else if (fast && band_w == 2 && NW <= 40 && !r64 && ksplit > 1 && raw_mode == 2) rc16_launch(recombine16_kernel<40, true, true>);
+        else if (fast && band_w == 2 && NW <= 80 && !r64 && ksplit > 1 && raw_mode == 2) rc16_launch(recombine16_kernel<80, true, true>);
         else if (fast && band_w == 2 && NW <= 40 && !r64 && ksplit > 1) rc16_launch(recombine16_kernel<40, true>);
         else if (fast && band_w == 2 && NW <= 80 && !r64 && ksplit > 1) rc16_launch(recombine16_kernel<80, true>);
+        else if (fast && band_w == 2 && NW <= 40 && !r64 && raw_mode == 2) rc16_launch(recombine16_kernel<40, false, true>);
+        else if (fast && band_w == 2 && NW <= 80 && !r64 && raw_mode == 2) rc16_launch(recombine16_kernel<80, false, true>);
         else if (fast && band_w == 2 && NW <= 40 && !r64) rc16_launch(recombine16_kernel<40>);
         else if (fast && band_w == 2 && NW <= 80 && !r64) rc16_launch(recombine16_kernel<80>);
         else if (fast && band_w == 2 && NW <= 40) recombine_fast_kernel<40, 16><<<gbq, 128, 0, st>>>(R);
@@ -3585,6 +3623,12 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking);
         return t;
     }();
+    static cudaStream_t pks = [] {  // the early pack's branch
+        cudaStream_t t;
+        cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking);
+        return t;
+    }();
+    static cudaEvent_t ev_scan = make_event(), ev_packed1 = make_event();
     const bool spec = rad_order == 4;
     // speculative slice packing for the single-block plan of (almost) every
     // input, issued before the host round trip: the slice counts come from the
@@ -3607,8 +3651,56 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     ScanSummary* hs = pinned_summary();
     long long* hw = hs->mw;
 
+    // early pack: the speculative pack only needs the scan (line windows from the chunk partials,
+    // every template plane written), so it runs on its own branch right behind the scan, beside
+    // the finish kernel, instead of after it (APB_NO_EARLY_PACK=1: behind the finish kernel)
+    static const bool no_early = std::getenv("APB_NO_EARLY_PACK") != nullptr;
+    const bool early_ok = sncw && !no_early && !prof_enabled();
+    auto launch_pack = [&](cudaStream_t ps, bool from_partials) {
+        PackAB pk;
+        pk.a = av;
+        pk.b = bv;
+        pk.M = M;
+        pk.K = K;
+        pk.N = N;
+        pk.rtop = RW.top[0];
+        pk.rbot = RW.bot[0];
+        pk.ctop = CW.top[0];
+        pk.cbot = CW.bot[0];
+        pk.Mp = sgeo.Mp;
+        pk.Np = sgeo.Np;
+        pk.Kp = sgeo.Kp;
+        pk.Ap = sAp;
+        pk.Bp = sBp;
+        pk.esc = esc;
+        pk.fsc = fsc;
+        pk.mwa = &sum->maxw_a;
+        pk.mwb = &sum->maxw_b;
+        if (from_partials) {
+            pk.pa = pa;
+            pk.pb = pb;
+            pk.cA = cA;
+            pk.cB = cB;
+        }
+        pk.ga = blocks_for((int64_t)sgeo.Mp * sgeo.Kp, 256);
+        pk.gbx = sgeo.Np / 32;
+        const dim3 g((unsigned)(pk.ga + pk.gbx * (sgeo.Kp / 32)));
+        // plain launch (not PDL): early-resident pack blocks waiting on the scan
+        // would hold the SMs the radius products need right after it
+        static const bool pack_pdl = std::getenv("APB_PACK_PDL") != nullptr;
+        auto lp = [&](auto kern) {
+            if (pack_pdl && !from_partials) launch_pdl(kern, g, dim3(256), 0, ps, pk);
+            else kern<<<g, 256, 0, ps>>>(pk);
+        };
+        if (sncw == 2) lp(pack_ab_v2_kernel<2>);
+        else if (sncw == 5) lp(pack_ab_v2_kernel<5>);
+        else if (sncw == 9) lp(pack_ab_v2_kernel<9>);
+        else lp(pack_ab_v2_kernel<8>);
+        count_launch(1);
+    };
     // `mid` (optional): work enqueued on `s` between the scan and the pack
     auto phase1 = [&](cudaStream_t s, bool capturing, const std::function<int(cudaStream_t)>* mid = nullptr) -> int {
+        const bool early = early_ok && !mid;
         const int tk_scan = prof_begin("scan", s);
         const int64_t nblk = M * cA + ((N + 31) / 32) * cB;
         static const bool no_scan_planes = std::getenv("APB_NO_SCAN_PLANES") != nullptr;  // test hook
@@ -3617,8 +3709,33 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         else
             scan_v2_kernel<<<(unsigned)nblk, 256, 0, s>>>(av, bv, M, K, N, cA, cB, pa, pb, sum, mw1, mw2, da1, da2,
                                                           db1, db2);
-        launch_pdl(scan_v2_finish_kernel, dim3(blocks_for(32 * (M + N), 256)), dim3(256), 0, s, pa, pb, M, N, cA, cB,
-                   RW.top[0], RW.bot[0], CW.top[0], CW.bot[0], ec1, ec2, fc1, fc2, sum, mw1, mw2);
+        if (early) {
+            cudaEventRecord(ev_scan, s);
+            {  // launched before the pack, at the highest priority: its few blocks go ahead of the pack's
+                static const int prio = [] {
+                    int least = 0, greatest = 0;
+                    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+                    return greatest;
+                }();
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(blocks_for(32 * (M + N), 256));
+                cfg.blockDim = dim3(256);
+                cfg.stream = s;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributePriority;
+                at[0].val.priority = prio;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                cudaLaunchKernelEx(&cfg, scan_v2_finish_kernel, (const int64_t*)pa, (const int64_t*)pb, M, N, cA, cB,
+                                   RW.top[0], RW.bot[0], CW.top[0], CW.bot[0], ec1, ec2, fc1, fc2, sum, mw1, mw2);
+            }
+            cudaStreamWaitEvent(pks, ev_scan, 0);
+            launch_pack(pks, true);
+            cudaEventRecord(ev_packed1, pks);
+        } else {
+            launch_pdl(scan_v2_finish_kernel, dim3(blocks_for(32 * (M + N), 256)), dim3(256), 0, s, pa, pb, M, N, cA,
+                       cB, RW.top[0], RW.bot[0], CW.top[0], CW.bot[0], ec1, ec2, fc1, fc2, sum, mw1, mw2);
+        }
         count_launch(2);
         prof_end(tk_scan, s);
         rec_event(ev_fin, s, capturing);
@@ -3631,44 +3748,12 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
             const int r = (*mid)(s);
             if (r) return r;
         }
-        if (sncw) {
+        if (sncw && !early) {
             const int tk = prof_begin("pack", s);
-            PackAB pk;
-            pk.a = av;
-            pk.b = bv;
-            pk.M = M;
-            pk.K = K;
-            pk.N = N;
-            pk.rtop = RW.top[0];
-            pk.rbot = RW.bot[0];
-            pk.ctop = CW.top[0];
-            pk.cbot = CW.bot[0];
-            pk.Mp = sgeo.Mp;
-            pk.Np = sgeo.Np;
-            pk.Kp = sgeo.Kp;
-            pk.Ap = sAp;
-            pk.Bp = sBp;
-            pk.esc = esc;
-            pk.fsc = fsc;
-            pk.mwa = &sum->maxw_a;
-            pk.mwb = &sum->maxw_b;
-            pk.ga = blocks_for((int64_t)sgeo.Mp * sgeo.Kp, 256);
-            pk.gbx = sgeo.Np / 32;
-            const dim3 g((unsigned)(pk.ga + pk.gbx * (sgeo.Kp / 32)));
-            // plain launch (not PDL): early-resident pack blocks waiting on the scan
-            // would hold the SMs the radius products need right after it
-            static const bool pack_pdl = std::getenv("APB_PACK_PDL") != nullptr;
-            auto lp = [&](auto kern) {
-                if (pack_pdl) launch_pdl(kern, g, dim3(256), 0, s, pk);
-                else kern<<<g, 256, 0, s>>>(pk);
-            };
-            if (sncw == 2) lp(pack_ab_v2_kernel<2>);
-            else if (sncw == 5) lp(pack_ab_v2_kernel<5>);
-            else if (sncw == 9) lp(pack_ab_v2_kernel<9>);
-            else lp(pack_ab_v2_kernel<8>);
+            launch_pack(s, false);
             prof_end(tk, s);
-            count_launch(1);
         }
+        if (early) cudaStreamWaitEvent(s, ev_packed1, 0);  // everything after phase 1 sees the slice planes
         cudaEventRecord(ev_cjoin, cps);
         cudaStreamWaitEvent(s, ev_cjoin, 0);
         return cuda_check(cudaGetLastError(), "matmul scan");
