@@ -397,9 +397,9 @@ template <int NCW>
 APB_DEV void pack_a_v2_body(const BallsView& X, int64_t rows, int64_t ld, int64_t lo, int64_t hi,
                             const int64_t* top, const int64_t* bot, int S, int Rp, int Kp, int8_t* out,
                             int64_t* scale_out, const long long* maxw_dev, int64_t blk,
-                            const int64_t* part = nullptr, int nc = 0) {
-    if (part) {  // early pack: all template planes
-        S = 8 * NCW;
+                            const int64_t* part = nullptr, int nc = 0, int planes = 0) {
+    if (part) {  // early pack: the planes the caller asks for, else all of the template
+        S = planes > 0 && planes <= 8 * NCW ? planes : 8 * NCW;
     } else if (maxw_dev) {  // speculative launch: slice count from the scan, before the host knows it
         S = (int)((*maxw_dev + 2 + 7) / 8);
         if (S > 8 * NCW) return;
@@ -441,9 +441,9 @@ template <int NCW>
 APB_DEV void pack_b_v2_body(const BallsView& X, int64_t N, int64_t lo, int64_t hi, const int64_t* top,
                             const int64_t* bot, int S, int Np, int Kp, int8_t* out, int64_t* scale_out,
                             const long long* maxw_dev, int64_t bx, int64_t by, const int64_t* part = nullptr,
-                            int nc = 0) {
+                            int nc = 0, int planes = 0) {
     if (part) {
-        S = 8 * NCW;
+        S = planes > 0 && planes <= 8 * NCW ? planes : 8 * NCW;
     } else if (maxw_dev) {
         S = (int)((*maxw_dev + 2 + 7) / 8);
         if (S > 8 * NCW) return;
@@ -528,6 +528,7 @@ struct PackAB {
     // every template plane is written (the slice counts are the finish kernel's to know)
     const int64_t *pa = nullptr, *pb = nullptr;
     int cA = 0, cB = 0;
+    int planes_a = 0, planes_b = 0;  // early pack: planes to write (0 = all 8 NCW of the template)
 };
 
 
@@ -544,10 +545,10 @@ __global__ void __launch_bounds__(256) pack_ab_v2_kernel(PackAB P) {
     if ((int64_t)blockIdx.x < nb) {
         const int64_t bb = blockIdx.x;
         pack_b_v2_body<NCW>(P.b, P.N, 0, P.K, P.ctop, P.cbot, 0, P.Np, P.Kp, P.Bp, P.fsc, P.mwb, bb % P.gbx,
-                            bb / P.gbx, P.pb, P.cB);
+                            bb / P.gbx, P.pb, P.cB, P.planes_b);
     } else {
         pack_a_v2_body<NCW>(P.a, P.M, P.K, 0, P.K, P.rtop, P.rbot, 0, P.Mp, P.Kp, P.Ap, P.esc, P.mwa,
-                            (int64_t)blockIdx.x - nb, P.pa, P.cA);
+                            (int64_t)blockIdx.x - nb, P.pa, P.cA, P.planes_a);
     }
 }
 
@@ -3656,7 +3657,9 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     // the finish kernel, instead of after it (APB_NO_EARLY_PACK=1: behind the finish kernel)
     static const bool no_early = std::getenv("APB_NO_EARLY_PACK") != nullptr;
     const bool early_ok = sncw && !no_early && !prof_enabled();
-    auto launch_pack = [&](cudaStream_t ps, bool from_partials) {
+    // (Sa, Sb): planes the early pack writes -- the speculated slice counts in the fused step's graph
+    // (a product that needs more is re-packed by the host), else all template planes
+    auto launch_pack = [&](cudaStream_t ps, bool from_partials, int Sa = 0, int Sb = 0) {
         PackAB pk;
         pk.a = av;
         pk.b = bv;
@@ -3681,6 +3684,8 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
             pk.pb = pb;
             pk.cA = cA;
             pk.cB = cB;
+            pk.planes_a = Sa;
+            pk.planes_b = Sb;
         }
         pk.ga = blocks_for((int64_t)sgeo.Mp * sgeo.Kp, 256);
         pk.gbx = sgeo.Np / 32;
@@ -3699,7 +3704,8 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
         count_launch(1);
     };
     // `mid` (optional): work enqueued on `s` between the scan and the pack
-    auto phase1 = [&](cudaStream_t s, bool capturing, const std::function<int(cudaStream_t)>* mid = nullptr) -> int {
+    auto phase1 = [&](cudaStream_t s, bool capturing, const std::function<int(cudaStream_t)>* mid = nullptr,
+                      int Sa = 0, int Sb = 0) -> int {
         const bool early = early_ok && !mid;
         const int tk_scan = prof_begin("scan", s);
         const int64_t nblk = M * cA + ((N + 31) / 32) * cB;
@@ -3730,7 +3736,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
                                    RW.top[0], RW.bot[0], CW.top[0], CW.bot[0], ec1, ec2, fc1, fc2, sum, mw1, mw2);
             }
             cudaStreamWaitEvent(pks, ev_scan, 0);
-            launch_pack(pks, true);
+            launch_pack(pks, true, Sa, Sb);
             cudaEventRecord(ev_packed1, pks);
         } else {
             launch_pdl(scan_v2_finish_kernel, dim3(blocks_for(32 * (M + N), 256)), dim3(256), 0, s, pa, pb, M, N, cA,
@@ -3939,8 +3945,11 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     const bool rad_redo = rad_multi || (!no_scan_planes_h && !planes_used && hsum.rad_centred) || rad_missing;
     want_planes = hsum.rad_centred != 0 && !rad_multi;
     const bool single = P.steps.size() == 3 && P.steps[0] == 0 && P.steps[1] == A->cols && P.steps[2] == 0;
-    const bool prepacked =
-        single && sncw && slices_for(P.maxw_a) <= 8 * sncw && slices_for(P.maxw_b) <= 8 * sncw;
+    // slice planes the speculative pack of this call wrote: the fused step's graph writes the
+    // speculated counts (early pack), every other path all template planes
+    const int planes_a = (full_spec && early_ok) ? (int)k2_spec[0] : 8 * sncw;
+    const int planes_b = (full_spec && early_ok) ? (int)k2_spec[1] : 8 * sncw;
+    const bool prepacked = single && sncw && slices_for(P.maxw_a) <= planes_a && slices_for(P.maxw_b) <= planes_b;
     static const bool no_fuse = std::getenv("APB_NO_RAD_FUSE") != nullptr;  // test hook
     auto phase2 = [&](cudaStream_t s, bool capturing) -> int {
         RadFuse fz{r1b, r1f, r2b, r2f, ev_join, capturing, false};
@@ -4005,7 +4014,7 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
                         }
                         return r;
                     }
-                    int r = phase1(cs, true);
+                    int r = phase1(cs, true, nullptr, (int)k2[0], (int)k2[1]);  // (k2: this call's slice counts)
                     if (r) return r;
                     // radius branch: planes beside the pack, products before the GEMM, which
                     // waits for them (measured fastest: squeezed beside a GEMM CTA, one block

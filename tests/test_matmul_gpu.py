@@ -170,6 +170,32 @@ def test_repeated_calls_centred_radius_planes():
         assert got.identical(refs["far"]).all(), f"replay {k}"
 
 
+def test_graph_replay_slice_count_changes():
+    """same buffers, but the exponent spread (and with it the slice counts) grows and shrinks between
+    calls: the fused step's graph packs only the slices it speculates on, so a product that needs
+    more must be re-packed by the host; all bit-identical"""
+    from paper_1901_04289_b200 import ops
+    n, p = 256, 128
+    rng = gen.rng_for(2, 321)
+    narrow = [gen.random_balls(rng, n * n, p, e_lo=-2, e_hi=2, rad_k=130) for _ in range(2)]
+    wide = [gen.random_balls(rng, n * n, p, e_lo=-30, e_hi=30, rad_k=130) for _ in range(2)]
+    refs, slices = {}, {}
+    for key, (a, b) in (("narrow", narrow), ("wide", wide)):
+        refs[key], _ = po.matmul(a, b, n, n, n, p, which="ref", algo=1, threads=os.cpu_count() or 8)
+    A, B = _mat(narrow[0], n, n), _mat(narrow[1], n, n)
+    out = ops.block_matmul_ball(A, B, p)
+    for k, key in enumerate(["narrow"] * 4 + ["wide"] * 4 + ["narrow"] * 3 + ["wide", "narrow"]):
+        a, b = narrow if key == "narrow" else wide
+        for dst, src in ((A, a), (B, b)):
+            d = src.to_device()
+            for f in ("mant", "exp", "kind", "rad_man", "rad_exp"):
+                getattr(dst.balls, f).copy_(getattr(d, f))
+        got = ops.block_matmul_ball(A, B, p, out=out).balls.to_host()
+        assert got.identical(refs[key]).all(), f"call {k} ({key})"
+        slices[key] = ops.matmul_stats()["last_slices_a"]
+    assert slices["wide"] > slices["narrow"], slices
+
+
 def test_graph_replay_radius_variant_changes():
     """same buffers and slice counts, but the radius density flips between calls: the fused
     step's graph holds only the radius kernels of the last operands (sparse or dense), so a
