@@ -3773,7 +3773,9 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
     // down on the device when the planes are fine) and the products are right the first time --
     // otherwise they would run on invalid planes and the host would redo the radius after the
     // midpoint product (at config 4: 0.45 ms wasted + 0.68 ms redone per real product)
-    static bool want_planes = false;  // (under the API lock)
+    static std::map<std::vector<int64_t>, bool> want_planes_of;  // per (M, K, N, prec); under the API lock
+    if (want_planes_of.size() > 4096) want_planes_of.clear();
+    bool& want_planes = want_planes_of[{M, K, N, prec}];
     const bool planes_used = want_planes;
     auto phaseR = [&](cudaStream_t ss, bool capturing, cudaEvent_t mid = nullptr, RadDefer* defer = nullptr,
                       int which = 3) -> int {
