@@ -1704,6 +1704,11 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
     // double2 loads of the inner loop (the hot part) -- accepted.
     __shared__ __align__(16) double sA[RK][RT + 2];
     __shared__ __align__(16) double sB[RK][RT];
+    // column permutation of the B tile for PT = 4: a thread's four columns 4 tx .. 4 tx + 3 are read as
+    // two 16-byte loads; stored in place the 8 threads of a row would read 16-byte pieces 32 bytes apart
+    // (tx and tx + 4 on the same banks: ncu counted 2 extra wavefronts per shared load at N = 1024), so
+    // the pair (h / 2) of thread tx lives at 16-byte slot (h / 2) * 8 + tx: 8 threads x 16 B contiguous
+    auto bcol = [](int c) -> int { return PT == 4 ? ((((c & 3) >> 1) * 8 + (c >> 2)) << 1) | (c & 1) : c; };
     constexpr int NT = (RT / PT) * (RT / PT);  // threads per tile
     __shared__ uint32_t eb[PT * PT][NT];
     __shared__ int64_t ef[PT * PT][NT];
@@ -1767,7 +1772,7 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
                 sA[q / RT][q % RT] = pa[u];
             else
                 sA[q % RT][q / RT] = pa[u];
-            sB[q / RT][q % RT] = pb[u];
+            sB[q / RT][bcol(q % RT)] = pb[u];
         }
         __syncthreads();
         if (l0 + RK < w) fetch(l0 + RK);
@@ -1777,7 +1782,7 @@ APB_DEV void rad_gemm_body(const double* __restrict__ da, const double* __restri
 #pragma unroll
             for (int h = 0; h < PT; h += 2) {
                 const double2 av = *reinterpret_cast<const double2*>(&sA[kk][ty * PT + h]);
-                const double2 bv = *reinterpret_cast<const double2*>(&sB[kk][tx * PT + h]);
+                const double2 bv = *reinterpret_cast<const double2*>(&sB[kk][bcol(tx * PT + h)]);
                 a[h] = av.x;
                 a[h + 1] = av.y;
                 b[h] = bv.x;
