@@ -425,6 +425,63 @@ APB_DEV void pack_a_v2_body(const BallsView& X, int64_t rows, int64_t ld, int64_
     }
 }
 
+// A side, four consecutive inner indices per thread: the digit bytes of the four entries are merged
+// with byte permutes and leave as one 4-byte store per plane (a warp writes 128 contiguous bytes per
+// plane instead of 32: a quarter of the store instructions of pack_a_v2_body).  blk counts blocks of
+// 256 threads over Rp * Kp / 4 thread slots.
+template <int NCW>
+APB_DEV void pack_a_v4_body(const BallsView& X, int64_t rows, int64_t ld, int64_t lo, int64_t hi,
+                            const int64_t* top, const int64_t* bot, int S, int Rp, int Kp, int8_t* out,
+                            int64_t* scale_out, const long long* maxw_dev, int64_t blk,
+                            const int64_t* part = nullptr, int nc = 0, int planes = 0) {
+    if (part) {
+        S = planes > 0 && planes <= 8 * NCW ? planes : 8 * NCW;
+    } else if (maxw_dev) {
+        S = (int)((*maxw_dev + 2 + 7) / 8);
+        if (S > 8 * NCW) return;
+    }
+    const int64_t t = blk * blockDim.x + threadIdx.x;
+    const int64_t K4 = Kp >> 2;
+    if (t >= (int64_t)Rp * K4) return;
+    const int64_t r = t / K4, kk = 4 * (t % K4);
+    int64_t sc = 0;
+    if (r < rows && part) {
+        int64_t tp, bt;
+        partial_window(part, nc, rows, r, tp, bt);
+        sc = tp == INT64_MIN ? 0 : -bt;
+    } else if (r < rows) sc = top[r] == INT64_MIN ? 0 : -bot[r];
+    if (r < rows && kk == 0) scale_out[r] = sc;
+    uint64_t d[4][NCW];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const bool valid = r < rows && kk + q < hi - lo;
+        digit_words<NCW>(X, valid ? r * ld + lo + kk + q : 0, valid, sc, d[q]);
+    }
+    const size_t plane = (size_t)Rp * Kp;
+    uint32_t* dst = reinterpret_cast<uint32_t*>(out + (size_t)r * Kp + kk);
+#pragma unroll
+    for (int c = 0; c < NCW; c++) {
+        if (8 * c >= S) break;
+        const uint64_t w0 = d[0][c], w1 = d[1][c], w2 = d[2][c], w3 = d[3][c];
+        // byte b of (w0, w1, w2, w3) -> the word of digit 8 c + b (as pack_b_v2_body)
+        const uint32_t lo01 = __byte_perm((uint32_t)w0, (uint32_t)w1, 0x5140);
+        const uint32_t lo23 = __byte_perm((uint32_t)w2, (uint32_t)w3, 0x5140);
+        const uint32_t hi01 = __byte_perm((uint32_t)w0, (uint32_t)w1, 0x7362);
+        const uint32_t hi23 = __byte_perm((uint32_t)w2, (uint32_t)w3, 0x7362);
+        const uint32_t lo01b = __byte_perm((uint32_t)(w0 >> 32), (uint32_t)(w1 >> 32), 0x5140);
+        const uint32_t lo23b = __byte_perm((uint32_t)(w2 >> 32), (uint32_t)(w3 >> 32), 0x5140);
+        const uint32_t hi01b = __byte_perm((uint32_t)(w0 >> 32), (uint32_t)(w1 >> 32), 0x7362);
+        const uint32_t hi23b = __byte_perm((uint32_t)(w2 >> 32), (uint32_t)(w3 >> 32), 0x7362);
+        const uint32_t dg[8] = {__byte_perm(lo01, lo23, 0x5410),   __byte_perm(lo01, lo23, 0x7632),
+                                __byte_perm(hi01, hi23, 0x5410),   __byte_perm(hi01, hi23, 0x7632),
+                                __byte_perm(lo01b, lo23b, 0x5410), __byte_perm(lo01b, lo23b, 0x7632),
+                                __byte_perm(hi01b, hi23b, 0x5410), __byte_perm(hi01b, hi23b, 0x7632)};
+#pragma unroll
+        for (int b = 0; b < 8; b++)
+            if (8 * c + b < S) dst[((size_t)(8 * c + b) * plane) >> 2] = dg[b];
+    }
+}
+
 template <int NCW>
 __global__ void __launch_bounds__(256) pack_a_v2_kernel(BallsView X, int64_t rows, int64_t ld, int64_t lo, int64_t hi,
                                                         const int64_t* top, const int64_t* bot, int S, int Rp, int Kp,
@@ -529,6 +586,7 @@ struct PackAB {
     const int64_t *pa = nullptr, *pb = nullptr;
     int cA = 0, cB = 0;
     int planes_a = 0, planes_b = 0;  // early pack: planes to write (0 = all 8 NCW of the template)
+    int a4 = 0;  // A side: four inner indices per thread (ga counts blocks over Mp * Kp / 4 slots)
 };
 
 
@@ -547,8 +605,12 @@ __global__ void __launch_bounds__(256) pack_ab_v2_kernel(PackAB P) {
         pack_b_v2_body<NCW>(P.b, P.N, 0, P.K, P.ctop, P.cbot, 0, P.Np, P.Kp, P.Bp, P.fsc, P.mwb, bb % P.gbx,
                             bb / P.gbx, P.pb, P.cB, P.planes_b);
     } else {
-        pack_a_v2_body<NCW>(P.a, P.M, P.K, 0, P.K, P.rtop, P.rbot, 0, P.Mp, P.Kp, P.Ap, P.esc, P.mwa,
-                            (int64_t)blockIdx.x - nb, P.pa, P.cA, P.planes_a);
+        if (P.a4)
+            pack_a_v4_body<NCW>(P.a, P.M, P.K, 0, P.K, P.rtop, P.rbot, 0, P.Mp, P.Kp, P.Ap, P.esc, P.mwa,
+                                (int64_t)blockIdx.x - nb, P.pa, P.cA, P.planes_a);
+        else
+            pack_a_v2_body<NCW>(P.a, P.M, P.K, 0, P.K, P.rtop, P.rbot, 0, P.Mp, P.Kp, P.Ap, P.esc, P.mwa,
+                                (int64_t)blockIdx.x - nb, P.pa, P.cA, P.planes_a);
     }
 }
 
@@ -3694,7 +3756,9 @@ int block_matmul(const apb_mat* A, const apb_mat* B, int64_t prec, apb_mat* C, c
             pk.planes_a = Sa;
             pk.planes_b = Sb;
         }
-        pk.ga = blocks_for((int64_t)sgeo.Mp * sgeo.Kp, 256);
+        static const bool no_a4 = std::getenv("APB_PACK_A1") != nullptr;  // test hook: one entry per thread
+        pk.a4 = no_a4 ? 0 : 1;
+        pk.ga = blocks_for((int64_t)sgeo.Mp * sgeo.Kp / (pk.a4 ? 4 : 1), 256);
         pk.gbx = sgeo.Np / 32;
         const dim3 g((unsigned)(pk.ga + pk.gbx * (sgeo.Kp / 32)));
         // plain launch (not PDL): early-resident pack blocks waiting on the scan

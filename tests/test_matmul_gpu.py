@@ -85,7 +85,7 @@ def test_full_config_vs_reference(cfg):
                                   "APB_BAND_KBNORM=1", "APB_NO_SCAN_PLANES=1", "APB_RAD_MAIN=1",
                                   "APB_RAD_NO_SMALL=1", "APB_NO_RAW_EPI=1", "APB_RAD_QUAD=1", "APB_RAD_QUAD=1,APB_RAD_QUAD_BESIDE=1",
                                   "APB_BAND_BN=128,APB_NO_RAW_EPI=1", "APB_BAND_KSPLIT=2", "APB_BAND_BN=128,APB_BAND_KSPLIT=2",
-                                  "APB_BAND_BN=256,APB_BAND_KSPLIT=1", "APB_RAW32=1", "APB_RAW32=1,APB_BAND_KSPLIT=2", "APB_RAD_BOTH=1", "APB_RC_PDL=1", "APB_NO_RAD_ALONG=1", "APB_NO_EARLY_PACK=1"])
+                                  "APB_BAND_BN=256,APB_BAND_KSPLIT=1", "APB_RAW32=1", "APB_RAW32=1,APB_BAND_KSPLIT=2", "APB_RAD_BOTH=1", "APB_RC_PDL=1", "APB_NO_RAD_ALONG=1", "APB_NO_EARLY_PACK=1", "APB_PACK_A1=1"])
 def test_kernel_variants_golden(hook):
     """alternative kernels / schedules selected by the library's tuning hooks
     (unit GEMM used when a diagonal could overflow int32, byte-serial pack,
